@@ -1,0 +1,189 @@
+/*
+ * rama_b200.h -- C ABI of the B200-native RAMA primal-dual multicut solver.
+ *
+ * This is the drop-in boundary for the reference's hot path: each entry
+ * point replaces one `parcut` operator (file:line into
+ * /root/reference/pkg/src/parcut/, cited per function).  Plain pointers and
+ * sizes only.  Unless a parameter says "host", arrays are DEVICE pointers
+ * (CUDA global memory) and all work is ordered on `stream` (a cudaStream_t
+ * passed as void*, NULL = legacy default stream).
+ *
+ * Conventions
+ *   - node ids int32 in [0, n); n, m < 2^31.  Costs / multipliers fp64.
+ *   - A "canonical graph" is the reference WeightedGraph invariant
+ *     (graph.py:17-57): u < v, sorted by (u, v), unique pairs.
+ *   - Return value: RAMA_OK (0) or an error code; never throws.  The
+ *     message of the last failure on this thread: rama_last_error().
+ *   - Output arrays are caller-allocated with the capacity stated per
+ *     function; the produced count is written to a host int64.
+ */
+#ifndef RAMA_B200_H
+#define RAMA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RAMA_OK 0
+#define RAMA_ERR_INVALID 1  /* bad input -> ValueError (graph.py:31-42, solver.py:50-62) */
+#define RAMA_ERR_CUDA 2     /* CUDA runtime failure -> RuntimeError */
+#define RAMA_ERR_NOMEM 3    /* device allocation failed -> MemoryError */
+#define RAMA_ERR_INTERNAL 4
+
+/* solver modes: solver.py:22 MODES */
+#define RAMA_MODE_P 0
+#define RAMA_MODE_PD 1
+#define RAMA_MODE_PD_PLUS 2
+#define RAMA_MODE_D 3
+#define RAMA_MODE_GAEC 4
+
+/* round phases: RoundRecord.phase (solver.py:65-75) */
+#define RAMA_PHASE_CONTRACT 0
+#define RAMA_PHASE_PRIMAL_DUAL 1
+#define RAMA_PHASE_CLEANUP 2
+#define RAMA_PHASE_DUAL 3
+#define RAMA_PHASE_GAEC 4
+
+/* SolverConfig (solver.py:27-62); max_cycle_length already resolved */
+typedef struct rama_cfg {
+  int32_t mode;
+  int32_t mp_iterations;
+  int32_t max_cycle_length;
+  int32_t max_rounds;
+  int32_t separation_rounds;
+  int32_t reserved;
+  double matching_switch_fraction;
+} rama_cfg;
+
+/* RoundRecord (solver.py:65-75); lb is NaN where the reference has None */
+typedef struct rama_round {
+  int32_t round_index;
+  int32_t phase;
+  int64_t nodes;
+  int64_t edges;
+  int64_t triplets;
+  double lb;
+  int32_t lb_valid;
+  int32_t reserved;
+  int64_t contracted;
+  double time_ms;
+} rama_round;
+
+/* library version (major*10000 + minor*100 + patch) */
+int rama_version(void);
+/* message of the last failed call on this thread ("" if none) */
+const char* rama_last_error(void);
+/* number of kernels the last call on this thread launched */
+int64_t rama_last_launch_count(void);
+
+/* Live kernel-family timing for roofline reporting: when enabled, each
+ * kernel family is bracketed by CUDA events on the call's stream.
+ * Families (index): 0 separate, 1 triangulate, 2 message passing, 3 bound /
+ * reparam graph, 4 matching, 5 forest, 6 components, 7 contract, 8 cleanup
+ * (inclusive), 9 canonicalize.  rama_profile_read fills host arrays of
+ * RAMA_PROFILE_FAMILIES: summed device ms, summed algorithmic bytes
+ * (SURVEY.md 8(d) formulas), scope count.  Enabling resets the sums. */
+#define RAMA_PROFILE_FAMILIES 10
+int rama_profile_enable(int32_t on);
+int rama_profile_read(double* ms, double* bytes, int64_t* count);
+
+/* ---- solver (solver.py:243-252 solve) ------------------------------------ */
+
+/* Full solve on a canonical graph (non-canonical COO is canonicalised
+ * first, WeightedGraph semantics).  labels: device int32[n] (canonical
+ * labeling, Solution.labeling).  primal_lb: host double[2] =
+ * {primal_cost, lower_bound} (lower_bound = -inf for P / GAEC).  trace: host
+ * rama_round[max_trace] (may be NULL); *n_rounds (host) = records written. */
+int rama_solve(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m,
+               const rama_cfg* cfg, int32_t* labels, double* primal_lb, rama_round* trace,
+               int32_t max_trace, int32_t* n_rounds, void* stream);
+
+/* Same with HOST arrays (u, v, c, labels); copies in and out through pinned
+ * staging inside the call.  The end-to-end entry for non-CUDA callers. */
+int rama_solve_host(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m,
+                    const rama_cfg* cfg, int32_t* labels, double* primal_lb, rama_round* trace,
+                    int32_t max_trace, int32_t* n_rounds, void* stream);
+
+/* ---- graph core ----------------------------------------------------------- */
+
+/* WeightedGraph.__init__ (graph.py:29-57): validate, orient, sort, sum
+ * parallel edges (np.add.reduceat order).  out_*: capacity m. */
+int rama_canonicalize(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m,
+                      int32_t* out_u, int32_t* out_v, double* out_c, int64_t* out_m, void* stream);
+
+/* clustering_cost (graph.py:134-145); *cost is host */
+int rama_clustering_cost(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m,
+                         const int32_t* labels, double* cost, void* stream);
+
+/* ---- contraction (contraction.py) ---------------------------------------- */
+
+/* connected_components (contraction.py:101-111): canonical map[n]. */
+int rama_components(int64_t n, const int32_t* su, const int32_t* sv, int64_t k, int32_t* map,
+                    int64_t* num_targets, void* stream);
+
+/* contract_graph (contraction.py:142-163) on a canonical graph.  out_*:
+ * capacity m; *joined (host) = cost mass of merged edges. */
+int rama_contract(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m,
+                  const int32_t* map, int64_t n_targets, int32_t* out_u, int32_t* out_v, double* out_c,
+                  int64_t* out_m, double* joined, void* stream);
+
+/* select_matching (contraction.py:179-228): su/sv capacity n/2 + 1 */
+int rama_select_matching(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m,
+                         int32_t rounds, int32_t* su, int32_t* sv, int64_t* k, void* stream);
+
+/* select_max_edge (contraction.py:166-176): *edge (host) = index or -1 */
+int rama_select_max_edge(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m,
+                         int64_t* edge, void* stream);
+
+/* select_spanning_forest_no_conflicts (contraction.py:287-366):
+ * su/sv capacity n */
+int rama_select_forest(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m,
+                       int32_t* su, int32_t* sv, int64_t* k, void* stream);
+
+/* contraction_step (contraction.py:369-394); policy 0 gaec, 1 matching,
+ * 2 forest, 3 auto.  map: capacity n (identity when nothing selected);
+ * out_*: capacity m.  info (host int64[4]) = {num_targets, |S|, m_out,
+ * used_forest}; *joined host. */
+int rama_contraction_step(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m,
+                          int32_t policy, double switch_fraction, int32_t* map, int32_t* out_u,
+                          int32_t* out_v, double* out_c, int64_t* info, double* joined, void* stream);
+
+/* ---- dual (dual.py) -------------------------------------------------------- */
+
+/* _separate_arrays (dual.py:169-197): one row per repulsive edge in
+ * ascending (u, v) order.  out_len capacity m, out_nodes capacity m*L
+ * (row-major, width L, zero padded); *rows (host) = repulsive edge count.
+ * 3 <= L <= 5. */
+int rama_separate(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m, int32_t L,
+                  int32_t* out_len, int32_t* out_nodes, int64_t* rows, void* stream);
+
+/* _triangulate_arrays (dual.py:255-290).  Capacities: aug_u/aug_v/base/
+ * coverage m + rows*(L-3); tri_nodes/tri_edges 3*rows*(L-2).  Outputs the
+ * reference layout: augmented edges = originals then new chords (sorted),
+ * triplets sorted lexicographically, handles (ij, ik, jk). */
+int rama_triangulate(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m,
+                     const int32_t* len, const int32_t* nodes, int64_t rows, int32_t L, int32_t* aug_u,
+                     int32_t* aug_v, double* base, int64_t* m_aug, int32_t* tri_nodes, int32_t* tri_edges,
+                     int64_t* T, int32_t* coverage, void* stream);
+
+/* message passing on lam[3T] in place (dual.py:358-392).
+ * phases: 1 = mp_edge_to_triplets only, 2 = mp_triplets_to_edges only,
+ * 3 = message_passing_iteration; repeated `iters` times. */
+int rama_message_passing(int64_t m_aug, const double* base, int64_t T, const int32_t* tri_edges, double* lam,
+                         int32_t iters, int32_t phases, void* stream);
+
+/* reparametrized_edge_costs (dual.py:309-316): cl[m_aug] */
+int rama_reparam_costs(int64_t m_aug, const double* base, int64_t T, const int32_t* tri_edges, const double* lam,
+                       double* cl, void* stream);
+
+/* lower_bound (dual.py:395-405); *lb host */
+int rama_lower_bound(int64_t m_aug, const double* base, int64_t T, const int32_t* tri_edges, const double* lam,
+                     double* lb, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RAMA_B200_H */

@@ -1,0 +1,375 @@
+// extern "C" boundary (include/rama_b200.h).  Every entry point runs inside
+// `guarded`, which owns the per-call context, converts exceptions to status
+// codes and records the message for rama_last_error().
+#include "../../include/rama_b200.h"
+#include "internal.h"
+
+#include <cmath>
+#include <limits>
+#include <new>
+#include <string>
+#include <vector>
+
+using namespace rama;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int64_t g_launches = 0;
+
+template <class F>
+int guarded(void* stream, F&& f) {
+  g_err.clear();
+  g_launches = 0;
+  try {
+    int dev_count = 0;
+    if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0) {
+      cudaGetLastError();
+      throw Error(kCuda, "no CUDA device available (the B200 build has no CPU fallback)");
+    }
+    Ctx ctx((cudaStream_t)stream);
+    f(ctx);
+    ctx.sync();
+    RAMA_CUDA(cudaGetLastError());
+    g_launches = ctx.launches;
+    return RAMA_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return RAMA_ERR_NOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return RAMA_ERR_INTERNAL;
+  }
+}
+
+GraphView view_of(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m) {
+  GraphView g;
+  g.n = n; g.m = m; g.u = u; g.v = v; g.c = c;
+  return g;
+}
+
+void check_sizes(int64_t n, int64_t m) {
+  RAMA_REQUIRE(n >= 0 && m >= 0, "sizes must be non-negative");
+  RAMA_REQUIRE(n < (1LL << 31) && m < (1LL << 31), "graph too large for int32 ids");
+}
+
+void export_graph(Ctx& ctx, const Graph& g, int32_t* ou, int32_t* ov, double* oc, int64_t* om) {
+  copy_d2d(ctx, ou, g.u.p, g.m);
+  copy_d2d(ctx, ov, g.v.p, g.m);
+  copy_d2d(ctx, oc, g.c.p, g.m);
+  *om = g.m;
+}
+
+__global__ void k_is_canonical(const int32_t* __restrict__ u, const int32_t* __restrict__ v, int64_t m, int64_t n,
+                               int32_t* bad) {
+  GRID_STRIDE(i, m) {
+    bool ok = u[i] >= 0 && u[i] < v[i] && v[i] < n;
+    if (ok && i > 0) ok = u[i - 1] < u[i] || (u[i - 1] == u[i] && v[i - 1] < v[i]);
+    if (!ok) atomicOr(bad, 1);
+  }
+}
+
+SolveConfig to_cfg(const rama_cfg* cfg) {
+  RAMA_REQUIRE(cfg != nullptr, "cfg is NULL");
+  SolveConfig c;
+  c.mode = cfg->mode;
+  c.mp_iterations = cfg->mp_iterations;
+  c.max_cycle_length = cfg->max_cycle_length;
+  c.max_rounds = cfg->max_rounds;
+  c.separation_rounds = cfg->separation_rounds;
+  c.switch_fraction = cfg->matching_switch_fraction;
+  // SolverConfig.validate (solver.py:50-62)
+  RAMA_REQUIRE(c.mode >= 0 && c.mode <= 4, "unknown mode");
+  RAMA_REQUIRE(!(c.mode >= 1 && c.mode <= 3) || c.mp_iterations >= 1, "mp_iterations must be at least 1 for dual modes");
+  RAMA_REQUIRE(c.max_cycle_length >= 3, "max_cycle_length must be at least 3");
+  RAMA_REQUIRE(c.switch_fraction > 0.0 && c.switch_fraction <= 1.0, "matching_switch_fraction must be in (0, 1]");
+  RAMA_REQUIRE(c.max_rounds >= 1, "max_rounds must be at least 1");
+  RAMA_REQUIRE(c.separation_rounds >= 1, "separation_rounds must be at least 1");
+  return c;
+}
+
+void run_solve(Ctx& ctx, int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m,
+               const rama_cfg* cfg, int32_t* labels, double* primal_lb, rama_round* trace, int32_t max_trace,
+               int32_t* n_rounds) {
+  check_sizes(n, m);
+  SolveConfig sc = to_cfg(cfg);
+  GraphView g = view_of(n, u, v, c, m);
+  Graph canon;
+  if (m > 0) {
+    Buf<int32_t> bad(1, ctx);
+    bad.zero();
+    RAMA_KERNEL(ctx, k_is_canonical, m, u, v, m, n, bad.p);
+    if (read_scalar(ctx, bad.p)) {
+      canon = canonicalize(ctx, n, u, v, c, m);
+      g = canon.view();
+    }
+  }
+  std::vector<RoundInfo> tr(max_trace > 0 ? max_trace : 0);
+  SolveResult res;
+  solve(ctx, g, sc, labels, res, tr.data(), (int)tr.size());
+  primal_lb[0] = res.primal;
+  primal_lb[1] = res.lb_finite ? res.lb : -std::numeric_limits<double>::infinity();
+  int written = res.n_rounds < max_trace ? res.n_rounds : max_trace;
+  for (int i = 0; trace && i < written; i++) {
+    const RoundInfo& r = tr[i];
+    rama_round& o = trace[i];
+    o.round_index = r.round_index;
+    o.phase = r.phase;
+    o.nodes = r.nodes;
+    o.edges = r.edges;
+    o.triplets = r.triplets;
+    o.lb = r.lb;
+    o.lb_valid = r.lb_valid;
+    o.reserved = 0;
+    o.contracted = r.contracted;
+    o.time_ms = r.time_ms;
+  }
+  if (n_rounds) *n_rounds = res.n_rounds;
+}
+
+// DualState over caller arrays (copied; slot lists rebuilt)
+void load_state(Ctx& ctx, DualState& st, int64_t m_aug, const double* base, int64_t T, const int32_t* tri_edges,
+                const double* lam) {
+  st.m_aug = m_aug;
+  st.T = T;
+  st.base.alloc(m_aug > 0 ? m_aug : 1, ctx.s);
+  copy_d2d(ctx, st.base.p, base, m_aug);
+  st.tri_edges.alloc(T > 0 ? 3 * T : 1, ctx.s);
+  copy_d2d(ctx, st.tri_edges.p, tri_edges, 3 * T);
+  st.lam.alloc(T > 0 ? 3 * T : 1, ctx.s);
+  copy_d2d(ctx, st.lam.p, lam, 3 * T);
+  build_slot_lists(ctx, st);
+}
+
+__global__ void k_handle_check(const int32_t* __restrict__ te, int64_t S, int64_t m_aug, int32_t* bad) {
+  GRID_STRIDE(s, S) {
+    if (te[s] < 0 || te[s] >= m_aug) atomicOr(bad, 1);
+  }
+}
+
+void check_handles(Ctx& ctx, const int32_t* te, int64_t T, int64_t m_aug) {
+  if (T <= 0) return;
+  Buf<int32_t> bad(1, ctx);
+  bad.zero();
+  RAMA_KERNEL(ctx, k_handle_check, 3 * T, te, 3 * T, m_aug, bad.p);
+  RAMA_REQUIRE(read_scalar(ctx, bad.p) == 0, "triplet edge handle out of range");
+}
+
+}  // namespace
+
+extern "C" {
+
+int rama_version(void) { return 1 * 10000 + 0 * 100 + 0; }
+
+const char* rama_last_error(void) { return g_err.c_str(); }
+
+int64_t rama_last_launch_count(void) { return g_launches; }
+
+int rama_profile_enable(int32_t on) {
+  return guarded(nullptr, [&](Ctx&) { prof_set(on != 0); });
+}
+
+int rama_profile_read(double* ms, double* bytes, int64_t* count) {
+  return guarded(nullptr, [&](Ctx&) { prof_read(ms, bytes, count); });
+}
+
+int rama_solve(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m, const rama_cfg* cfg,
+               int32_t* labels, double* primal_lb, rama_round* trace, int32_t max_trace, int32_t* n_rounds,
+               void* stream) {
+  return guarded(stream, [&](Ctx& ctx) {
+    run_solve(ctx, n, u, v, c, m, cfg, labels, primal_lb, trace, max_trace, n_rounds);
+  });
+}
+
+int rama_solve_host(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m, const rama_cfg* cfg,
+                    int32_t* labels, double* primal_lb, rama_round* trace, int32_t max_trace, int32_t* n_rounds,
+                    void* stream) {
+  return guarded(stream, [&](Ctx& ctx) {
+    check_sizes(n, m);
+    Buf<int32_t> du(m > 0 ? m : 1, ctx), dv(m > 0 ? m : 1, ctx), dl(n > 0 ? n : 1, ctx);
+    Buf<double> dc(m > 0 ? m : 1, ctx);
+    if (m > 0) {
+      RAMA_CUDA(cudaMemcpyAsync(du.p, u, sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx.s));
+      RAMA_CUDA(cudaMemcpyAsync(dv.p, v, sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx.s));
+      RAMA_CUDA(cudaMemcpyAsync(dc.p, c, sizeof(double) * m, cudaMemcpyHostToDevice, ctx.s));
+    }
+    run_solve(ctx, n, du.p, dv.p, dc.p, m, cfg, dl.p, primal_lb, trace, max_trace, n_rounds);
+    if (n > 0) RAMA_CUDA(cudaMemcpyAsync(labels, dl.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx.s));
+  });
+}
+
+int rama_canonicalize(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m, int32_t* out_u,
+                      int32_t* out_v, double* out_c, int64_t* out_m, void* stream) {
+  return guarded(stream, [&](Ctx& ctx) {
+    check_sizes(n, m);
+    Graph g = canonicalize(ctx, n, u, v, c, m);
+    export_graph(ctx, g, out_u, out_v, out_c, out_m);
+  });
+}
+
+int rama_clustering_cost(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m,
+                         const int32_t* labels, double* cost, void* stream) {
+  return guarded(stream, [&](Ctx& ctx) {
+    check_sizes(n, m);
+    *cost = clustering_cost(ctx, view_of(n, u, v, c, m), labels);
+  });
+}
+
+int rama_components(int64_t n, const int32_t* su, const int32_t* sv, int64_t k, int32_t* map, int64_t* num_targets,
+                    void* stream) {
+  return guarded(stream, [&](Ctx& ctx) {
+    check_sizes(n, k);
+    *num_targets = components(ctx, n, su, sv, k, map);
+  });
+}
+
+int rama_contract(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m, const int32_t* map,
+                  int64_t n_targets, int32_t* out_u, int32_t* out_v, double* out_c, int64_t* out_m, double* joined,
+                  void* stream) {
+  return guarded(stream, [&](Ctx& ctx) {
+    check_sizes(n, m);
+    Graph g = contract(ctx, view_of(n, u, v, c, m), map, n_targets, joined);
+    export_graph(ctx, g, out_u, out_v, out_c, out_m);
+  });
+}
+
+int rama_select_matching(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m, int32_t rounds,
+                         int32_t* su, int32_t* sv, int64_t* k, void* stream) {
+  return guarded(stream, [&](Ctx& ctx) {
+    check_sizes(n, m);
+    Buf<int32_t> a, b;
+    *k = select_matching(ctx, view_of(n, u, v, c, m), rounds, a, b);
+    copy_d2d(ctx, su, a.p, *k);
+    copy_d2d(ctx, sv, b.p, *k);
+  });
+}
+
+int rama_select_max_edge(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m, int64_t* edge,
+                         void* stream) {
+  return guarded(stream, [&](Ctx& ctx) {
+    check_sizes(n, m);
+    *edge = select_max_edge(ctx, view_of(n, u, v, c, m));
+  });
+}
+
+int rama_select_forest(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m, int32_t* su,
+                       int32_t* sv, int64_t* k, void* stream) {
+  return guarded(stream, [&](Ctx& ctx) {
+    check_sizes(n, m);
+    Buf<int32_t> a, b;
+    *k = select_forest(ctx, view_of(n, u, v, c, m), a, b);
+    copy_d2d(ctx, su, a.p, *k);
+    copy_d2d(ctx, sv, b.p, *k);
+  });
+}
+
+int rama_contraction_step(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m, int32_t policy,
+                          double switch_fraction, int32_t* map, int32_t* out_u, int32_t* out_v, double* out_c,
+                          int64_t* info, double* joined, void* stream) {
+  return guarded(stream, [&](Ctx& ctx) {
+    check_sizes(n, m);
+    RAMA_REQUIRE(policy >= 0 && policy <= 3, "unknown contraction policy");
+    GraphView g = view_of(n, u, v, c, m);
+    StepResult st;
+    contraction_step(ctx, g, policy, switch_fraction, st, true);
+    info[1] = st.num_selected;
+    info[3] = st.used_forest ? 1 : 0;
+    *joined = st.joined;
+    if (st.identity) {
+      iota(ctx, map, n);
+      copy_d2d(ctx, out_u, u, m);
+      copy_d2d(ctx, out_v, v, m);
+      copy_d2d(ctx, out_c, c, m);
+      info[0] = n;
+      info[2] = m;
+    } else {
+      copy_d2d(ctx, map, st.map.p, n);
+      int64_t mo = 0;
+      export_graph(ctx, st.next, out_u, out_v, out_c, &mo);
+      info[0] = st.num_targets;
+      info[2] = mo;
+    }
+  });
+}
+
+int rama_separate(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m, int32_t L,
+                  int32_t* out_len, int32_t* out_nodes, int64_t* rows, void* stream) {
+  return guarded(stream, [&](Ctx& ctx) {
+    check_sizes(n, m);
+    CycleRows cyc;
+    separate(ctx, view_of(n, u, v, c, m), L, cyc);
+    copy_d2d(ctx, out_len, cyc.len.p, cyc.rows);
+    copy_d2d(ctx, out_nodes, cyc.nodes.p, cyc.rows * (int64_t)L);
+    *rows = cyc.rows;
+  });
+}
+
+int rama_triangulate(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m, const int32_t* len,
+                     const int32_t* nodes, int64_t rows, int32_t L, int32_t* aug_u, int32_t* aug_v, double* base,
+                     int64_t* m_aug, int32_t* tri_nodes, int32_t* tri_edges, int64_t* T, int32_t* coverage,
+                     void* stream) {
+  return guarded(stream, [&](Ctx& ctx) {
+    check_sizes(n, m);
+    RAMA_REQUIRE(L >= 3 && rows >= 0, "bad cycle rows");
+    CycleRows cyc;
+    cyc.rows = rows;
+    cyc.L = L;
+    cyc.len.alloc(rows > 0 ? rows : 1, ctx.s);
+    cyc.nodes.alloc(rows > 0 ? rows * L : 1, ctx.s);
+    copy_d2d(ctx, cyc.len.p, len, rows);
+    copy_d2d(ctx, cyc.nodes.p, nodes, rows * (int64_t)L);
+    DualState st;
+    triangulate(ctx, view_of(n, u, v, c, m), cyc, st);
+    copy_d2d(ctx, aug_u, st.eu.p, st.m_aug);
+    copy_d2d(ctx, aug_v, st.ev.p, st.m_aug);
+    copy_d2d(ctx, base, st.base.p, st.m_aug);
+    copy_d2d(ctx, coverage, st.coverage.p, st.m_aug);
+    copy_d2d(ctx, tri_nodes, st.tri_nodes.p, 3 * st.T);
+    copy_d2d(ctx, tri_edges, st.tri_edges.p, 3 * st.T);
+    *m_aug = st.m_aug;
+    *T = st.T;
+  });
+}
+
+int rama_message_passing(int64_t m_aug, const double* base, int64_t T, const int32_t* tri_edges, double* lam,
+                         int32_t iters, int32_t phases, void* stream) {
+  return guarded(stream, [&](Ctx& ctx) {
+    check_sizes(0, m_aug);
+    RAMA_REQUIRE(phases >= 1 && phases <= 3, "phases must be 1, 2 or 3");
+    check_handles(ctx, tri_edges, T, m_aug);
+    DualState st;
+    load_state(ctx, st, m_aug, base, T, tri_edges, lam);
+    for (int it = 0; it < iters; it++) {
+      if (phases == 3) message_passing(ctx, st, 1);
+      else mp_phases(ctx, st, phases == 1, phases == 2);
+    }
+    copy_d2d(ctx, lam, st.lam.p, 3 * T);
+  });
+}
+
+int rama_reparam_costs(int64_t m_aug, const double* base, int64_t T, const int32_t* tri_edges, const double* lam,
+                       double* cl, void* stream) {
+  return guarded(stream, [&](Ctx& ctx) {
+    check_sizes(0, m_aug);
+    check_handles(ctx, tri_edges, T, m_aug);
+    DualState st;
+    load_state(ctx, st, m_aug, base, T, tri_edges, lam);
+    reparam_costs(ctx, st, cl);
+  });
+}
+
+int rama_lower_bound(int64_t m_aug, const double* base, int64_t T, const int32_t* tri_edges, const double* lam,
+                     double* lb, void* stream) {
+  return guarded(stream, [&](Ctx& ctx) {
+    check_sizes(0, m_aug);
+    check_handles(ctx, tri_edges, T, m_aug);
+    DualState st;
+    load_state(ctx, st, m_aug, base, T, tri_edges, lam);
+    *lb = lower_bound(ctx, st);
+  });
+}
+
+}  // extern "C"

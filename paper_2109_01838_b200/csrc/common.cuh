@@ -1,0 +1,298 @@
+// Common device/host infrastructure for the RAMA B200 library.
+//
+// * Errors: internal code throws rama::Error; the C-ABI layer (capi.cu)
+//   converts it to a status code + rama_last_error() message.
+// * Memory: every scratch buffer is stream-ordered (cudaMallocAsync /
+//   cudaFreeAsync) from the device's default pool, whose release threshold
+//   is raised once so freed blocks are cached across rounds and solves.
+// * Ids are int32 (n, m < 2^31), costs and multipliers fp64 (the reference
+//   is fp64 throughout, graph.py:35).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <utility>
+
+namespace rama {
+
+enum Status : int {
+  kOk = 0,
+  kInvalid = 1,   // -> ValueError
+  kCuda = 2,      // -> RuntimeError
+  kNoMemory = 3,  // -> MemoryError
+  kInternal = 4,
+};
+
+struct Error : public std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define RAMA_CUDA(call)                                                                   \
+  do {                                                                                    \
+    cudaError_t _e = (call);                                                              \
+    if (_e != cudaSuccess) {                                                              \
+      throw ::rama::Error(_e == cudaErrorMemoryAllocation ? ::rama::kNoMemory              \
+                                                          : ::rama::kCuda,                 \
+                          std::string(#call) + ": " + cudaGetErrorString(_e) + " @" +     \
+                              __FILE__ + ":" + std::to_string(__LINE__));                 \
+    }                                                                                     \
+  } while (0)
+
+#define RAMA_LAUNCH_CHECK() RAMA_CUDA(cudaGetLastError())
+
+#define RAMA_REQUIRE(cond, msg)                                   \
+  do {                                                            \
+    if (!(cond)) throw ::rama::Error(::rama::kInvalid, (msg));    \
+  } while (0)
+
+// Per-call context: the stream everything is ordered on plus a small pinned
+// staging area for scalar read-backs (the only host syncs in a solve).
+struct Ctx {
+  cudaStream_t s = nullptr;
+  int64_t* pinned = nullptr;  // 64 int64 slots
+  int launches = 0;           // kernels launched through this context
+
+  explicit Ctx(cudaStream_t st);
+  ~Ctx();
+  Ctx(const Ctx&) = delete;
+  Ctx& operator=(const Ctx&) = delete;
+  void sync() { RAMA_CUDA(cudaStreamSynchronize(s)); }
+};
+
+void ensure_pool_configured();
+
+// ---- live kernel-family timing (bench.py roofline) ------------------------
+// When enabled (rama_profile_enable), each ProfScope records a CUDA event
+// pair on the context stream around one kernel family and the algorithmic
+// bytes it moves; rama_profile_read() sums elapsed time per family.
+enum Family : int {
+  kFamSeparate = 0,
+  kFamTriangulate = 1,
+  kFamMP = 2,
+  kFamBound = 3,
+  kFamMatching = 4,
+  kFamForest = 5,
+  kFamComponents = 6,
+  kFamContract = 7,
+  kFamCleanup = 8,
+  kFamCanon = 9,
+  kNumFamilies = 10
+};
+bool prof_enabled();
+void prof_set(bool on);
+void prof_push(int fam, cudaEvent_t a, cudaEvent_t b, double bytes);
+void prof_read(double* ms, double* bytes, int64_t* count);
+
+struct ProfScope {
+  cudaStream_t s;
+  int fam;
+  double bytes;
+  cudaEvent_t a = nullptr, b = nullptr;
+  ProfScope(cudaStream_t st, int f, double by = 0.0) : s(st), fam(f), bytes(by) {
+    if (prof_enabled()) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, s);
+    }
+  }
+  void add_bytes(double by) { bytes += by; }
+  ~ProfScope() {
+    if (a) {
+      cudaEventRecord(b, s);
+      prof_push(fam, a, b, bytes);
+    }
+  }
+};
+
+template <class T>
+struct Buf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+
+  Buf() = default;
+  Buf(size_t count, cudaStream_t st) { alloc(count, st); }
+  Buf(size_t count, const Ctx& c) { alloc(count, c.s); }
+  ~Buf() { release(); }
+  Buf(const Buf&) = delete;
+  Buf& operator=(const Buf&) = delete;
+  Buf(Buf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  Buf& operator=(Buf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p; n = o.n; s = o.s;
+      o.p = nullptr; o.n = 0;
+    }
+    return *this;
+  }
+  void alloc(size_t count, cudaStream_t st) {
+    release();
+    s = st;
+    n = count;
+    if (count) RAMA_CUDA(cudaMallocAsync((void**)&p, sizeof(T) * count, st));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  T* get() const { return p; }
+  operator T*() const { return p; }
+  size_t bytes() const { return n * sizeof(T); }
+  void zero() {
+    if (n) RAMA_CUDA(cudaMemsetAsync(p, 0, bytes(), s));
+  }
+  void fill_bytes(int v) {
+    if (n) RAMA_CUDA(cudaMemsetAsync(p, v, bytes(), s));
+  }
+};
+
+constexpr int kBlock = 256;
+
+inline unsigned grid_for(int64_t work, int block = kBlock) {
+  int64_t g = (work + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > 0x7fffffff) g = 0x7fffffff;
+  return (unsigned)g;
+}
+
+// Grid-stride launch helper: caps the grid at a multiple of the SM count.
+unsigned capped_grid(int64_t work, int block = kBlock);
+
+#define RAMA_KERNEL(ctx, kernel, work, ...)                                           \
+  do {                                                                                \
+    int64_t _w = (int64_t)(work);                                                     \
+    if (_w > 0) {                                                                     \
+      kernel<<<::rama::capped_grid(_w), ::rama::kBlock, 0, (ctx).s>>>(__VA_ARGS__);   \
+      RAMA_LAUNCH_CHECK();                                                            \
+      (ctx).launches++;                                                               \
+    }                                                                                 \
+  } while (0)
+
+#define GRID_STRIDE(i, n) \
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)(n); i += (int64_t)gridDim.x * blockDim.x)
+
+// ---- scalar read-back -----------------------------------------------------
+template <class T>
+T read_scalar(Ctx& ctx, const T* dev) {
+  static_assert(sizeof(T) <= 8, "scalar");
+  RAMA_CUDA(cudaMemcpyAsync(ctx.pinned, dev, sizeof(T), cudaMemcpyDeviceToHost, ctx.s));
+  ctx.sync();
+  T v;
+  memcpy(&v, ctx.pinned, sizeof(T));
+  return v;
+}
+
+template <class T>
+void copy_d2d(Ctx& ctx, T* dst, const T* src, int64_t count) {
+  if (count > 0) RAMA_CUDA(cudaMemcpyAsync(dst, src, sizeof(T) * count, cudaMemcpyDeviceToDevice, ctx.s));
+}
+
+template <class T>
+void set_scalar(Ctx& ctx, T* dev, T value) {
+  RAMA_CUDA(cudaMemcpyAsync(dev, &value, sizeof(T), cudaMemcpyHostToDevice, ctx.s));
+  ctx.sync();  // value lives on the host stack
+}
+
+// ---- primitives (prims.cu) --------------------------------------------------
+// exclusive prefix sum of n int32 counts; out has n+1 entries, out[n] = total.
+// Returns the total (one read-back) when want_total.
+int64_t exclusive_scan(Ctx& ctx, const int32_t* in, int32_t* out, int64_t n, bool want_total = true);
+// in-place variant on int64
+void exclusive_scan64(Ctx& ctx, const int64_t* in, int64_t* out, int64_t n);
+
+// Bucket ("segmented") sort: items i in [0, N) with row[i] in [0, R) and a
+// 64-bit key.  Produces row_ptr[R+1], and for each output slot p the row,
+// key and source index, grouped by row and ascending by key inside a row.
+// Keys are made unique by the caller (they embed an index) so the output is
+// deterministic although the scatter uses atomics.
+struct BucketSorted {
+  Buf<int32_t> row_ptr;  // R + 1
+  Buf<int32_t> row;      // N (row of slot p)
+  Buf<uint64_t> key;     // N
+  Buf<int32_t> src;      // N
+};
+// Only rows < sort_rows are sorted (default all); later rows keep scatter
+// order (used to park dropped items in a trailing bucket).
+void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint64_t* key, BucketSorted& out,
+                 bool want_row = true, int64_t sort_rows = -1);
+
+// stable compaction of indices [0, n) where flag != 0; returns the count.
+int64_t compact_indices(Ctx& ctx, const uint8_t* flags, int64_t n, Buf<int32_t>& out);
+
+// deterministic fp64 sum (fixed block order, not numpy's order)
+double device_sum(Ctx& ctx, const double* x, int64_t n);
+
+// row pointers of a (u, v)-sorted edge list: ptr[x] = first edge with u >= x
+void row_ptr_from_sorted(Ctx& ctx, const int32_t* u, int64_t m, int64_t n, int32_t* ptr);
+
+// numpy summation orders on device (see oracle/rama_oracle.c)
+__device__ __forceinline__ double pw_leaf(const double* a, int64_t n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int64_t i = 0; i < n; i++) r = __dadd_rn(r, a[i]);
+    return r;
+  }
+  double r0 = a[0], r1 = a[1], r2 = a[2], r3 = a[3], r4 = a[4], r5 = a[5], r6 = a[6], r7 = a[7];
+  int64_t i;
+  for (i = 8; i < n - (n % 8); i += 8) {
+    r0 = __dadd_rn(r0, a[i + 0]); r1 = __dadd_rn(r1, a[i + 1]);
+    r2 = __dadd_rn(r2, a[i + 2]); r3 = __dadd_rn(r3, a[i + 3]);
+    r4 = __dadd_rn(r4, a[i + 4]); r5 = __dadd_rn(r5, a[i + 5]);
+    r6 = __dadd_rn(r6, a[i + 6]); r7 = __dadd_rn(r7, a[i + 7]);
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)),
+                         __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
+  for (; i < n; i++) res = __dadd_rn(res, a[i]);
+  return res;
+}
+
+// numpy pairwise sum; iterative post-order walk of numpy's fixed recursion
+// tree (split at n/2 rounded down to a multiple of 8, leaves <= 128).
+__device__ __forceinline__ double pw_sum(const double* a, int64_t n) {
+  if (n <= 128) return pw_leaf(a, n);
+  int64_t fo[40], fl[40];
+  double fleft[40];
+  int fstage[40];
+  int sp = 0;
+  fo[0] = 0; fl[0] = n; fstage[0] = 0;
+  double ret = 0.0;
+  while (true) {
+    if (fl[sp] <= 128) {
+      ret = pw_leaf(a + fo[sp], fl[sp]);
+      sp--;
+    } else if (fstage[sp] == 0) {
+      int64_t n2 = fl[sp] / 2; n2 -= n2 % 8;
+      fstage[sp] = 1;
+      fo[sp + 1] = fo[sp]; fl[sp + 1] = n2; fstage[sp + 1] = 0;
+      sp++;
+      continue;
+    } else if (fstage[sp] == 1) {
+      int64_t n2 = fl[sp] / 2; n2 -= n2 % 8;
+      fleft[sp] = ret;
+      fstage[sp] = 2;
+      fo[sp + 1] = fo[sp] + n2; fl[sp + 1] = fl[sp] - n2; fstage[sp + 1] = 0;
+      sp++;
+      continue;
+    } else {
+      ret = __dadd_rn(fleft[sp], ret);
+      sp--;
+    }
+    if (sp < 0) return ret;
+  }
+}
+
+// one np.add.reduceat segment: x[0] + pairwise(x[1:])
+__device__ __forceinline__ double seg_sum(const double* a, int64_t n) {
+  if (n <= 0) return 0.0;
+  if (n == 1) return __dadd_rn(a[0], 0.0);
+  return __dadd_rn(a[0], pw_sum(a + 1, n - 1));
+}
+
+__device__ __forceinline__ uint64_t dbits(double x) { return (uint64_t)__double_as_longlong(x); }
+
+}  // namespace rama

@@ -1,0 +1,575 @@
+// Dual machinery.
+//
+// Separation (dual.py:109-197).  The reference runs one BFS per repulsive
+// edge (a, b), a < b, over the attractive subgraph with neighbours expanded
+// in ascending id order, and reports the BFS parent chain.  That parent
+// chain has a closed form over sorted CSR rows, which is what each thread
+// evaluates here (one thread per repulsive edge, no queues, no visited set):
+//   level 1  N(a);  px(y) = min(N(a) & N(y)) is the BFS parent of a level-2
+//   node y, and level-2 nodes are dequeued in (px(y), y) order;
+//   3-cycle: x* = min(N(a) & N(b));
+//   4-cycle: y* = argmin_(y in N(b), dist(y) = 2) (px(y), y);
+//   5-cycle: for level-3 z, py(z) = argmin_(y in N(z), dist 2) (px(y), y) and
+//            z* = argmin_(z in N(b), dist(z) = 3) (px(py), py, z).
+// This is the BFS tie-break exactly (checked against the reference on the
+// golden fixtures and by the oracle parity tests).
+//
+// Message passing (dual.py:309-392).  Per iteration two kernels:
+//   edge phase  : cl[e] = base[e] + sum of lam over e's slots in ascending
+//                 slot order (== np.bincount), delta[e] = cl[e] / cov[e];
+//   triplet pass: lam[t,s] -= delta[e(t,s)]; then the damped six-step
+//                 schedule in registers.
+// All arithmetic is explicitly rounded (__dadd_rn/__dmul_rn/__ddiv_rn), so
+// nvcc cannot contract into FMAs and lam is bit-identical to numpy's.
+#include "internal.h"
+
+namespace rama {
+
+// ---------------------------------------------------------------- CSR
+
+__global__ void k_pos_flag(const double* __restrict__ c, int64_t m, uint8_t* __restrict__ f) {
+  GRID_STRIDE(i, m) f[i] = c[i] > 0.0;
+}
+
+__global__ void k_pos_arcs(const int32_t* __restrict__ P, int64_t np, const int32_t* __restrict__ u,
+                           const int32_t* __restrict__ v, int32_t* __restrict__ row, uint64_t* __restrict__ key) {
+  GRID_STRIDE(i, np) {
+    int32_t e = P[i];
+    row[2 * i] = u[e];
+    key[2 * i] = (uint64_t)(uint32_t)v[e];
+    row[2 * i + 1] = v[e];
+    key[2 * i + 1] = (uint64_t)(uint32_t)u[e];
+  }
+}
+
+__global__ void k_key_lo(const uint64_t* __restrict__ key, int64_t n, int32_t* __restrict__ out) {
+  GRID_STRIDE(i, n) out[i] = (int32_t)(uint32_t)key[i];
+}
+
+struct PosCSR {
+  Buf<int32_t> ptr;  // n + 1
+  Buf<int32_t> adj;  // 2 m+
+  int64_t arcs = 0;
+};
+
+// _positive_csr (dual.py:155-166): symmetric CSR of E+ sorted by (head, tail)
+static void positive_csr(Ctx& ctx, const GraphView& g, PosCSR& out) {
+  Buf<uint8_t> flag(g.m > 0 ? g.m : 1, ctx);
+  RAMA_KERNEL(ctx, k_pos_flag, g.m, g.c, g.m, flag.p);
+  Buf<int32_t> P;
+  int64_t np = compact_indices(ctx, flag.p, g.m, P);
+  int64_t na = 2 * np;
+  Buf<int32_t> row(na > 0 ? na : 1, ctx);
+  Buf<uint64_t> key(na > 0 ? na : 1, ctx);
+  RAMA_KERNEL(ctx, k_pos_arcs, np, P.p, np, g.u, g.v, row.p, key.p);
+  BucketSorted bs;
+  bucket_sort(ctx, g.n, na, row.p, key.p, bs, false);
+  out.ptr = std::move(bs.row_ptr);
+  out.adj.alloc(na > 0 ? na : 1, ctx.s);
+  RAMA_KERNEL(ctx, k_key_lo, na, bs.key.p, na, out.adj.p);
+  out.arcs = na;
+}
+
+// ----------------------------------------------------------- separation
+
+__device__ __forceinline__ bool in_sorted(const int32_t* a, int32_t len, int32_t y) {
+  int32_t lo = 0, hi = len;
+  while (lo < hi) {
+    int32_t mid = (lo + hi) >> 1;
+    int32_t x = a[mid];
+    if (x < y) lo = mid + 1;
+    else if (x > y) hi = mid;
+    else return true;
+  }
+  return false;
+}
+
+// smallest common element of two ascending lists, or -1
+__device__ __forceinline__ int32_t first_common(const int32_t* a, int32_t la, const int32_t* b, int32_t lb) {
+  int32_t i = 0, j = 0;
+  while (i < la && j < lb) {
+    int32_t x = a[i], y = b[j];
+    if (x == y) return x;
+    if (x < y) i++; else j++;
+  }
+  return -1;
+}
+
+__global__ void k_flag_neg(const double* __restrict__ c, int64_t m, uint8_t* __restrict__ f) {
+  GRID_STRIDE(i, m) f[i] = c[i] < 0.0;
+}
+
+__global__ void k_separate(const int32_t* __restrict__ NQ, int64_t nq, const int32_t* __restrict__ u,
+                           const int32_t* __restrict__ v, const int32_t* __restrict__ ptr,
+                           const int32_t* __restrict__ adj, int L, int32_t* __restrict__ out_len,
+                           int32_t* __restrict__ out_nodes) {
+  GRID_STRIDE(q, nq) {
+    int32_t e = NQ[q];
+    int32_t a = u[e], b = v[e];
+    const int32_t* Na = adj + ptr[a];
+    int32_t la = ptr[a + 1] - ptr[a];
+    const int32_t* Nb = adj + ptr[b];
+    int32_t lb = ptr[b + 1] - ptr[b];
+    int32_t* row = out_nodes + q * (int64_t)L;
+    int len = 0;
+    int32_t p1 = -1, p2 = -1, p3 = -1;
+    if (la > 0 && lb > 0) {
+      int32_t x = first_common(Na, la, Nb, lb);
+      if (x >= 0) {
+        len = 3;
+        p1 = x;
+      } else if (L >= 4) {
+        // 4-cycle: best level-2 neighbour of b by (px(y), y)
+        int32_t bp = 0x7fffffff, by = 0x7fffffff;
+        for (int32_t i = 0; i < lb; i++) {
+          int32_t y = Nb[i];
+          if (y == a || in_sorted(Na, la, y)) continue;
+          int32_t py = first_common(Na, la, adj + ptr[y], ptr[y + 1] - ptr[y]);
+          if (py < 0) continue;
+          if (py < bp || (py == bp && y < by)) { bp = py; by = y; }
+        }
+        if (bp != 0x7fffffff) {
+          len = 4;
+          p1 = bp;
+          p2 = by;
+        } else if (L >= 5) {
+          // 5-cycle: level-3 neighbours z of b ranked by (px(py(z)), py(z), z)
+          int32_t bx = 0x7fffffff, byy = 0x7fffffff, bz = 0x7fffffff;
+          for (int32_t i = 0; i < lb; i++) {
+            int32_t z = Nb[i];
+            if (z == a || in_sorted(Na, la, z)) continue;
+            const int32_t* Nz = adj + ptr[z];
+            int32_t lz = ptr[z + 1] - ptr[z];
+            if (first_common(Na, la, Nz, lz) >= 0) continue;  // z at distance 2
+            int32_t zx = 0x7fffffff, zy = 0x7fffffff;
+            for (int32_t j = 0; j < lz; j++) {
+              int32_t y = Nz[j];
+              if (y == a || in_sorted(Na, la, y)) continue;
+              int32_t py = first_common(Na, la, adj + ptr[y], ptr[y + 1] - ptr[y]);
+              if (py < 0) continue;
+              if (py < zx || (py == zx && y < zy)) { zx = py; zy = y; }
+            }
+            if (zx == 0x7fffffff) continue;
+            if (zx < bx || (zx == bx && (zy < byy || (zy == byy && z < bz)))) {
+              bx = zx; byy = zy; bz = z;
+            }
+          }
+          if (bx != 0x7fffffff) {
+            len = 5;
+            p1 = bx;
+            p2 = byy;
+            p3 = bz;
+          }
+        }
+      }
+    }
+    out_len[q] = len;
+    for (int j = 0; j < L; j++) row[j] = 0;
+    if (len >= 3) {
+      row[0] = a;
+      row[1] = p1;
+      if (len == 3) row[2] = b;
+      if (len >= 4) { row[2] = p2; }
+      if (len == 4) row[3] = b;
+      if (len == 5) { row[3] = p3; row[4] = b; }
+    }
+  }
+}
+
+void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
+  ProfScope prof(ctx.s, kFamSeparate);
+  RAMA_REQUIRE(L >= 3, "max_len must be at least 3");
+  RAMA_REQUIRE(L <= 5, "max_cycle_length > 5 (PD+) is not implemented in the B200 build yet");
+  Buf<uint8_t> flag(g.m > 0 ? g.m : 1, ctx);
+  RAMA_KERNEL(ctx, k_flag_neg, g.m, g.c, g.m, flag.p);
+  Buf<int32_t> NQ;
+  int64_t nq = compact_indices(ctx, flag.p, g.m, NQ);
+  out.rows = nq;
+  out.L = L;
+  out.len.alloc(nq > 0 ? nq : 1, ctx.s);
+  out.nodes.alloc(nq > 0 ? nq * L : 1, ctx.s);
+  if (nq == 0) return;
+  PosCSR csr;
+  positive_csr(ctx, g, csr);
+  if (csr.arcs == 0) {
+    out.len.zero();
+    out.nodes.zero();
+    return;
+  }
+  RAMA_KERNEL(ctx, k_separate, nq, NQ.p, nq, g.u, g.v, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p);
+}
+
+// --------------------------------------------------------- triangulation
+
+__global__ void k_fan_counts(const int32_t* __restrict__ len, int64_t rows, int32_t* __restrict__ nt,
+                             int32_t* __restrict__ nc) {
+  GRID_STRIDE(r, rows) {
+    int32_t l = len[r];
+    nt[r] = l >= 3 ? l - 2 : 0;
+    nc[r] = l >= 4 ? l - 3 : 0;
+  }
+}
+
+// _fan_arrays (dual.py:228-252): triplets {v0, v_j, v_j+1} and chords (v0, v_j)
+__global__ void k_fan_emit(const int32_t* __restrict__ len, const int32_t* __restrict__ nodes, int64_t rows, int L,
+                           const int32_t* __restrict__ toff, const int32_t* __restrict__ coff,
+                           int32_t* __restrict__ trow, uint64_t* __restrict__ tkey, int32_t* __restrict__ crow,
+                           uint64_t* __restrict__ ckey) {
+  GRID_STRIDE(r, rows) {
+    int32_t l = len[r];
+    if (l < 3) continue;
+    const int32_t* row = nodes + r * (int64_t)L;
+    int32_t v0 = row[0];
+    int32_t t = toff[r];
+    for (int j = 1; j < l - 1; j++) {
+      int32_t a = v0, b = row[j], c = row[j + 1], s;
+      if (a > b) { s = a; a = b; b = s; }
+      if (b > c) { s = b; b = c; c = s; }
+      if (a > b) { s = a; a = b; b = s; }
+      trow[t] = a;
+      tkey[t] = ((uint64_t)(uint32_t)b << 32) | (uint64_t)(uint32_t)c;
+      t++;
+    }
+    int32_t h = coff[r];
+    for (int j = 2; j < l - 1; j++) {
+      int32_t a = v0 < row[j] ? v0 : row[j];
+      int32_t b = v0 < row[j] ? row[j] : v0;
+      crow[h] = a;
+      ckey[h] = (uint64_t)(uint32_t)b;
+      h++;
+    }
+  }
+}
+
+__global__ void k_uniq_heads(const int32_t* __restrict__ row, const uint64_t* __restrict__ key, int64_t n,
+                             uint8_t* __restrict__ head) {
+  GRID_STRIDE(p, n) head[p] = (p == 0) || row[p] != row[p - 1] || key[p] != key[p - 1];
+}
+
+__device__ __forceinline__ int32_t find_in_row(const int32_t* __restrict__ rptr, const int32_t* __restrict__ ev,
+                                               int32_t a, int32_t b) {
+  int32_t lo = rptr[a], hi = rptr[a + 1];
+  while (lo < hi) {
+    int32_t mid = (lo + hi) >> 1;
+    int32_t x = ev[mid];
+    if (x < b) lo = mid + 1;
+    else if (x > b) hi = mid;
+    else return mid;
+  }
+  return -1;
+}
+
+// unique chords that are not already edges of g
+__global__ void k_chord_new(const int32_t* __restrict__ heads, int64_t nh, const int32_t* __restrict__ row,
+                            const uint64_t* __restrict__ key, const int32_t* __restrict__ rptr,
+                            const int32_t* __restrict__ gv, uint8_t* __restrict__ is_new) {
+  GRID_STRIDE(i, nh) {
+    int32_t p = heads[i];
+    is_new[i] = find_in_row(rptr, gv, row[p], (int32_t)key[p]) < 0;
+  }
+}
+
+__global__ void k_chord_out(const int32_t* __restrict__ sel, int64_t C, const int32_t* __restrict__ heads,
+                            const int32_t* __restrict__ row, const uint64_t* __restrict__ key, int64_t m,
+                            int32_t* __restrict__ eu, int32_t* __restrict__ ev, double* __restrict__ base,
+                            uint64_t* __restrict__ ckeys) {
+  GRID_STRIDE(i, C) {
+    int32_t p = heads[sel[i]];
+    int32_t a = row[p], b = (int32_t)key[p];
+    eu[m + i] = a;
+    ev[m + i] = b;
+    base[m + i] = 0.0;
+    ckeys[i] = ((uint64_t)(uint32_t)a << 32) | (uint64_t)(uint32_t)b;
+  }
+}
+
+__global__ void k_tri_out(const int32_t* __restrict__ heads, int64_t T, const int32_t* __restrict__ row,
+                          const uint64_t* __restrict__ key, int32_t* __restrict__ tn) {
+  GRID_STRIDE(t, T) {
+    int32_t p = heads[t];
+    tn[3 * t] = row[p];
+    tn[3 * t + 1] = (int32_t)(key[p] >> 32);
+    tn[3 * t + 2] = (int32_t)(uint32_t)key[p];
+  }
+}
+
+__device__ __forceinline__ int32_t edge_handle(const int32_t* rptr, const int32_t* gv, const uint64_t* ckeys,
+                                               int64_t C, int64_t m, int32_t a, int32_t b) {
+  int32_t e = find_in_row(rptr, gv, a, b);
+  if (e >= 0) return e;
+  uint64_t k = ((uint64_t)(uint32_t)a << 32) | (uint64_t)(uint32_t)b;
+  int64_t lo = 0, hi = C;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (ckeys[mid] < k) lo = mid + 1; else hi = mid;
+  }
+  return (int32_t)(m + lo);  // present by construction
+}
+
+__global__ void k_tri_handles(const int32_t* __restrict__ tn, int64_t T, const int32_t* __restrict__ rptr,
+                              const int32_t* __restrict__ gv, const uint64_t* __restrict__ ckeys, int64_t C,
+                              int64_t m, int32_t* __restrict__ te) {
+  GRID_STRIDE(t, T) {
+    int32_t i = tn[3 * t], j = tn[3 * t + 1], k = tn[3 * t + 2];
+    te[3 * t] = edge_handle(rptr, gv, ckeys, C, m, i, j);
+    te[3 * t + 1] = edge_handle(rptr, gv, ckeys, C, m, i, k);
+    te[3 * t + 2] = edge_handle(rptr, gv, ckeys, C, m, j, k);
+  }
+}
+
+__global__ void k_slot_items(const int32_t* __restrict__ te, int64_t S, uint64_t* __restrict__ key) {
+  GRID_STRIDE(s, S) key[s] = (uint64_t)s;
+}
+
+__global__ void k_coverage(const int32_t* __restrict__ ptr, int64_t m, int32_t* __restrict__ cov) {
+  GRID_STRIDE(e, m) cov[e] = ptr[e + 1] - ptr[e];
+}
+
+void build_slot_lists(Ctx& ctx, DualState& st) {
+  int64_t S = 3 * st.T;
+  st.coverage.alloc(st.m_aug > 0 ? st.m_aug : 1, ctx.s);
+  st.slots.alloc(S > 0 ? S : 1, ctx.s);
+  Buf<uint64_t> key(S > 0 ? S : 1, ctx);
+  RAMA_KERNEL(ctx, k_slot_items, S, st.tri_edges.p, S, key.p);
+  BucketSorted bs;
+  bucket_sort(ctx, st.m_aug, S, st.tri_edges.p, key.p, bs, false);
+  st.slot_ptr = std::move(bs.row_ptr);
+  RAMA_KERNEL(ctx, k_key_lo, S, bs.key.p, S, st.slots.p);
+  RAMA_KERNEL(ctx, k_coverage, st.m_aug, st.slot_ptr.p, st.m_aug, st.coverage.p);
+}
+
+void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& st) {
+  ProfScope prof(ctx.s, kFamTriangulate);
+  int64_t rows = cyc.rows, m = g.m, n = g.n;
+  st.n = n;
+  st.m_orig = m;
+  Buf<int32_t> nt(rows > 0 ? rows : 1, ctx), nc(rows > 0 ? rows : 1, ctx);
+  Buf<int32_t> toff(rows + 1, ctx), coff(rows + 1, ctx);
+  RAMA_KERNEL(ctx, k_fan_counts, rows, cyc.len.p, rows, nt.p, nc.p);
+  int64_t traw = exclusive_scan(ctx, nt.p, toff.p, rows, true);
+  int64_t craw = exclusive_scan(ctx, nc.p, coff.p, rows, true);
+  Buf<int32_t> trow(traw > 0 ? traw : 1, ctx), crow(craw > 0 ? craw : 1, ctx);
+  Buf<uint64_t> tkey(traw > 0 ? traw : 1, ctx), ckey(craw > 0 ? craw : 1, ctx);
+  RAMA_KERNEL(ctx, k_fan_emit, rows, cyc.len.p, cyc.nodes.p, rows, cyc.L, toff.p, coff.p, trow.p, tkey.p, crow.p,
+              ckey.p);
+
+  // chords: dedupe, drop existing edges
+  Buf<int32_t> rptr(n + 1, ctx);
+  row_ptr_from_sorted(ctx, g.u, m, n, rptr.p);
+  int64_t C = 0;
+  Buf<uint64_t> ckeys(1, ctx);
+  st.eu.alloc(m + craw > 0 ? m + craw : 1, ctx.s);
+  st.ev.alloc(m + craw > 0 ? m + craw : 1, ctx.s);
+  st.base.alloc(m + craw > 0 ? m + craw : 1, ctx.s);
+  copy_d2d(ctx, st.eu.p, g.u, m);
+  copy_d2d(ctx, st.ev.p, g.v, m);
+  copy_d2d(ctx, st.base.p, g.c, m);
+  if (craw > 0) {
+    BucketSorted cs;
+    bucket_sort(ctx, n, craw, crow.p, ckey.p, cs, true);
+    Buf<uint8_t> head(craw, ctx);
+    RAMA_KERNEL(ctx, k_uniq_heads, craw, cs.row.p, cs.key.p, craw, head.p);
+    Buf<int32_t> hp;
+    int64_t nh = compact_indices(ctx, head.p, craw, hp);
+    Buf<uint8_t> isnew(nh > 0 ? nh : 1, ctx);
+    RAMA_KERNEL(ctx, k_chord_new, nh, hp.p, nh, cs.row.p, cs.key.p, rptr.p, g.v, isnew.p);
+    Buf<int32_t> sel;
+    C = compact_indices(ctx, isnew.p, nh, sel);
+    ckeys.alloc(C > 0 ? C : 1, ctx.s);
+    RAMA_KERNEL(ctx, k_chord_out, C, sel.p, C, hp.p, cs.row.p, cs.key.p, m, st.eu.p, st.ev.p, st.base.p, ckeys.p);
+  }
+  st.m_aug = m + C;
+
+  // triplets: dedupe (lexicographic), handles
+  int64_t T = 0;
+  if (traw > 0) {
+    BucketSorted ts;
+    bucket_sort(ctx, n, traw, trow.p, tkey.p, ts, true);
+    Buf<uint8_t> head(traw, ctx);
+    RAMA_KERNEL(ctx, k_uniq_heads, traw, ts.row.p, ts.key.p, traw, head.p);
+    Buf<int32_t> hp;
+    T = compact_indices(ctx, head.p, traw, hp);
+    st.tri_nodes.alloc(3 * T, ctx.s);
+    st.tri_edges.alloc(3 * T, ctx.s);
+    RAMA_KERNEL(ctx, k_tri_out, T, hp.p, T, ts.row.p, ts.key.p, st.tri_nodes.p);
+    RAMA_KERNEL(ctx, k_tri_handles, T, st.tri_nodes.p, T, rptr.p, g.v, ckeys.p, C, m, st.tri_edges.p);
+  } else {
+    st.tri_nodes.alloc(1, ctx.s);
+    st.tri_edges.alloc(1, ctx.s);
+  }
+  st.T = T;
+  st.lam.alloc(T > 0 ? 3 * T : 1, ctx.s);
+  st.lam.zero();
+  build_slot_lists(ctx, st);
+}
+
+// ------------------------------------------------------ message passing
+
+__device__ __forceinline__ double mn2(double a, double b) { return a < b ? a : b; }  // np.minimum
+
+__device__ __forceinline__ double edge_sum(const int32_t* __restrict__ ptr, const int32_t* __restrict__ slots,
+                                           const double* __restrict__ lam, int64_t e, int32_t* cov) {
+  int32_t b = ptr[e], en = ptr[e + 1];
+  double acc = 0.0;
+  for (int32_t p = b; p < en; p++) acc = __dadd_rn(acc, lam[slots[p]]);
+  *cov = en - b;
+  return acc;
+}
+
+__global__ void k_mp_edge(int64_t m, const double* __restrict__ base, const int32_t* __restrict__ ptr,
+                          const int32_t* __restrict__ slots, const double* __restrict__ lam,
+                          double* __restrict__ delta) {
+  GRID_STRIDE(e, m) {
+    int32_t cov;
+    double acc = edge_sum(ptr, slots, lam, e, &cov);
+    if (cov == 0) continue;
+    double cl = __dadd_rn(base[e], acc);
+    delta[e] = __ddiv_rn(cl, (double)cov);
+  }
+}
+
+__device__ __forceinline__ double slot_marginal(double l0, double l1, double l2, int slot) {
+  double c110 = -__dadd_rn(l0, l1);
+  double c101 = -__dadd_rn(l0, l2);
+  double c011 = -__dadd_rn(l1, l2);
+  double c111 = -__dadd_rn(__dadd_rn(l0, l1), l2);
+  if (slot == 0) return __dsub_rn(mn2(mn2(c110, c101), c111), mn2(0.0, c011));
+  if (slot == 1) return __dsub_rn(mn2(mn2(c110, c011), c111), mn2(0.0, c101));
+  return __dsub_rn(mn2(mn2(c101, c011), c111), mn2(0.0, c110));
+}
+
+__device__ __forceinline__ void triplet_schedule(double& l0, double& l1, double& l2) {
+  // _SCHEDULE (dual.py:371): (0,1/3) (1,1/2) (2,1) (0,1/2) (1,1) (0,1)
+  l0 = __dadd_rn(l0, __dmul_rn(1.0 / 3.0, slot_marginal(l0, l1, l2, 0)));
+  l1 = __dadd_rn(l1, __dmul_rn(0.5, slot_marginal(l0, l1, l2, 1)));
+  l2 = __dadd_rn(l2, __dmul_rn(1.0, slot_marginal(l0, l1, l2, 2)));
+  l0 = __dadd_rn(l0, __dmul_rn(0.5, slot_marginal(l0, l1, l2, 0)));
+  l1 = __dadd_rn(l1, __dmul_rn(1.0, slot_marginal(l0, l1, l2, 1)));
+  l0 = __dadd_rn(l0, __dmul_rn(1.0, slot_marginal(l0, l1, l2, 0)));
+}
+
+__global__ void k_mp_triplet(int64_t T, const int32_t* __restrict__ te, const double* __restrict__ delta,
+                             double* __restrict__ lam, int do_edge, int do_tri) {
+  GRID_STRIDE(t, T) {
+    double l0 = lam[3 * t], l1 = lam[3 * t + 1], l2 = lam[3 * t + 2];
+    if (do_edge) {
+      l0 = __dsub_rn(l0, delta[te[3 * t]]);
+      l1 = __dsub_rn(l1, delta[te[3 * t + 1]]);
+      l2 = __dsub_rn(l2, delta[te[3 * t + 2]]);
+    }
+    if (do_tri) triplet_schedule(l0, l1, l2);
+    lam[3 * t] = l0;
+    lam[3 * t + 1] = l1;
+    lam[3 * t + 2] = l2;
+  }
+}
+
+void mp_phases(Ctx& ctx, DualState& st, bool edge_phase, bool triplet_phase) {
+  if (st.T == 0) return;
+  Buf<double> delta;
+  if (edge_phase) {
+    delta.alloc(st.m_aug, ctx.s);
+    RAMA_KERNEL(ctx, k_mp_edge, st.m_aug, st.m_aug, st.base.p, st.slot_ptr.p, st.slots.p, st.lam.p, delta.p);
+  }
+  RAMA_KERNEL(ctx, k_mp_triplet, st.T, st.T, st.tri_edges.p, delta.p, st.lam.p, edge_phase ? 1 : 0,
+              triplet_phase ? 1 : 0);
+}
+
+void message_passing(Ctx& ctx, DualState& st, int iters) {
+  if (st.T == 0) return;
+  // algorithmic bytes per iteration: 132 T + 20 m_aug
+  ProfScope prof(ctx.s, kFamMP, (double)iters * (132.0 * (double)st.T + 20.0 * (double)st.m_aug));
+  Buf<double> delta(st.m_aug, ctx);
+  for (int it = 0; it < iters; it++) {
+    RAMA_KERNEL(ctx, k_mp_edge, st.m_aug, st.m_aug, st.base.p, st.slot_ptr.p, st.slots.p, st.lam.p, delta.p);
+    RAMA_KERNEL(ctx, k_mp_triplet, st.T, st.T, st.tri_edges.p, delta.p, st.lam.p, 1, 1);
+  }
+}
+
+__global__ void k_reparam(int64_t m, const double* __restrict__ base, const int32_t* __restrict__ ptr,
+                          const int32_t* __restrict__ slots, const double* __restrict__ lam,
+                          double* __restrict__ cl, double* __restrict__ negpart) {
+  GRID_STRIDE(e, m) {
+    int32_t cov;
+    double acc = (ptr != nullptr) ? edge_sum(ptr, slots, lam, e, &cov) : 0.0;
+    double x = __dadd_rn(base[e], acc);
+    if (cl) cl[e] = x;
+    if (negpart) negpart[e] = mn2(x, 0.0);
+  }
+}
+
+void reparam_costs(Ctx& ctx, const DualState& st, double* cl) {
+  RAMA_KERNEL(ctx, k_reparam, st.m_aug, st.m_aug, st.base.p, st.T ? st.slot_ptr.p : (const int32_t*)nullptr,
+              st.slots.p, st.lam.p, cl, (double*)nullptr);
+}
+
+__global__ void k_tri_min(int64_t T, const double* __restrict__ lam, double* __restrict__ out) {
+  GRID_STRIDE(t, T) {
+    double l0 = lam[3 * t], l1 = lam[3 * t + 1], l2 = lam[3 * t + 2];
+    double c110 = -__dadd_rn(l0, l1);
+    double c101 = -__dadd_rn(l0, l2);
+    double c011 = -__dadd_rn(l1, l2);
+    double c111 = -__dadd_rn(__dadd_rn(l0, l1), l2);
+    out[t] = mn2(mn2(mn2(c110, c101), mn2(c011, c111)), 0.0);
+  }
+}
+
+double lower_bound(Ctx& ctx, const DualState& st) {
+  ProfScope prof(ctx.s, kFamBound);
+  double total = 0.0;
+  if (st.m_aug > 0) {
+    Buf<double> neg(st.m_aug, ctx);
+    RAMA_KERNEL(ctx, k_reparam, st.m_aug, st.m_aug, st.base.p, st.T ? st.slot_ptr.p : (const int32_t*)nullptr,
+                st.slots.p, st.lam.p, (double*)nullptr, neg.p);
+    total = device_sum(ctx, neg.p, st.m_aug);
+  }
+  if (st.T > 0) {
+    Buf<double> tm(st.T, ctx);
+    RAMA_KERNEL(ctx, k_tri_min, st.T, st.T, st.lam.p, tm.p);
+    total += device_sum(ctx, tm.p, st.T);
+  }
+  return total;
+}
+
+// --------------------------------------------------- reparametrized graph
+
+// merge position of originals [0, m) and chords [m, m_aug) (both sorted)
+__global__ void k_merge_scatter(int64_t m, int64_t C, const int32_t* __restrict__ eu, const int32_t* __restrict__ ev,
+                                const double* __restrict__ cl, int32_t* __restrict__ ou, int32_t* __restrict__ ov,
+                                double* __restrict__ oc) {
+  GRID_STRIDE(i, m + C) {
+    int32_t a = eu[i], b = ev[i];
+    int64_t lo, hi, self;
+    if (i < m) { lo = m; hi = m + C; self = i; }
+    else { lo = 0; hi = m; self = i - m; }
+    int64_t l0 = lo;
+    while (lo < hi) {  // count of other-list keys < (a, b)
+      int64_t mid = (lo + hi) >> 1;
+      int32_t x = eu[mid], y = ev[mid];
+      if (x < a || (x == a && y < b)) lo = mid + 1; else hi = mid;
+    }
+    int64_t pos = self + (lo - l0);
+    ou[pos] = a;
+    ov[pos] = b;
+    oc[pos] = __dadd_rn(cl[i], 0.0);  // WeightedGraph ctor: x0 + pairwise([]) per unique pair
+  }
+}
+
+Graph reparametrized_graph(Ctx& ctx, const DualState& st) {
+  ProfScope prof(ctx.s, kFamBound);
+  Graph g;
+  g.n = st.n;
+  g.m = st.m_aug;
+  int64_t ma = st.m_aug > 0 ? st.m_aug : 1;
+  g.u.alloc(ma, ctx.s);
+  g.v.alloc(ma, ctx.s);
+  g.c.alloc(ma, ctx.s);
+  if (st.m_aug == 0) return g;
+  Buf<double> cl(st.m_aug, ctx);
+  reparam_costs(ctx, st, cl.p);
+  RAMA_KERNEL(ctx, k_merge_scatter, st.m_aug, st.m_orig, st.m_aug - st.m_orig, st.eu.p, st.ev.p, cl.p, g.u.p, g.v.p,
+              g.c.p);
+  return g;
+}
+
+}  // namespace rama

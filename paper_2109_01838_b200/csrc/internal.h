@@ -1,0 +1,131 @@
+// Host-side internal API of the RAMA B200 library (one function per hot
+// path operator of SURVEY.md section 8(a)).  Everything takes device
+// pointers and is ordered on ctx.s.
+#pragma once
+
+#include "common.cuh"
+
+namespace rama {
+
+struct GraphView {
+  int64_t n = 0, m = 0;
+  const int32_t* u = nullptr;
+  const int32_t* v = nullptr;
+  const double* c = nullptr;
+};
+
+// owning canonical graph: u < v, sorted by (u, v), unique pairs
+struct Graph {
+  int64_t n = 0, m = 0;
+  Buf<int32_t> u, v;
+  Buf<double> c;
+  GraphView view() const {
+    GraphView g;
+    g.n = n; g.m = m; g.u = u.p; g.v = v.p; g.c = c.p;
+    return g;
+  }
+};
+
+// ---- graph core (graph.cu) --------------------------------------------------
+// a3  WeightedGraph.__init__ (graph.py:29-57)
+Graph canonicalize(Ctx& ctx, int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m);
+// a17 connected_components (contraction.py:101-111); returns num_targets
+int64_t components(Ctx& ctx, int64_t n, const int32_t* su, const int32_t* sv, int64_t k, int32_t* map);
+// a18 contract_graph (contraction.py:142-163); *joined (host) may be null
+Graph contract(Ctx& ctx, const GraphView& g, const int32_t* map, int64_t n_targets, double* joined);
+// a19 ContractionMapping.then (contraction.py:45-52): f_total = f[f_total]
+void compose(Ctx& ctx, int32_t* f_total, int64_t n0, const int32_t* f);
+// a21 clustering_cost (graph.py:134-145)
+double clustering_cost(Ctx& ctx, const GraphView& g, const int32_t* labels);
+void iota(Ctx& ctx, int32_t* x, int64_t n);
+
+// ---- contraction-set selection (select.cu) ---------------------------------
+// a14 select_matching (contraction.py:179-228); pairs sorted by u
+int64_t select_matching(Ctx& ctx, const GraphView& g, int rounds, Buf<int32_t>& su, Buf<int32_t>& sv);
+// select_max_edge (contraction.py:166-176); returns edge index or -1
+int64_t select_max_edge(Ctx& ctx, const GraphView& g);
+// a15/a16 select_spanning_forest_no_conflicts (contraction.py:287-366)
+int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_t>& sv);
+
+struct StepResult {
+  Graph next;            // contracted graph (empty if identity)
+  Buf<int32_t> map;      // f (size g.n) unless identity
+  int64_t num_targets = 0;
+  int64_t num_selected = 0;
+  bool identity = true;
+  bool used_forest = false;
+  double joined = 0.0;
+};
+// a13 contraction_step (contraction.py:369-394); policy: 0 gaec, 1 matching,
+// 2 forest, 3 auto
+void contraction_step(Ctx& ctx, const GraphView& g, int policy, double switch_fraction, StepResult& out,
+                      bool want_joined = false);
+
+// ---- dual (dual.cu) ---------------------------------------------------------
+struct CycleRows {
+  int64_t rows = 0;  // one row per repulsive edge (ascending (u, v))
+  int L = 0;
+  Buf<int32_t> len;    // rows
+  Buf<int32_t> nodes;  // rows * L
+};
+// a4/a5 _separate_arrays (dual.py:155-197)
+void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out);
+
+struct DualState {
+  int64_t n = 0, m_orig = 0, m_aug = 0, T = 0;
+  Buf<int32_t> eu, ev;      // augmented edges: originals then new chords
+  Buf<double> base;         // m_aug
+  Buf<int32_t> tri_nodes;   // T*3 sorted (i<j<k), rows sorted lexicographically
+  Buf<int32_t> tri_edges;   // T*3 handles (ij, ik, jk)
+  Buf<int32_t> coverage;    // m_aug
+  Buf<int32_t> slot_ptr;    // m_aug + 1 : edge -> ascending slot list
+  Buf<int32_t> slots;       // 3T
+  Buf<double> lam;          // 3T
+};
+// a6/a7 _triangulate_arrays (dual.py:216-290)
+void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& st);
+// a8 reparametrized_edge_costs (dual.py:309-316)
+void reparam_costs(Ctx& ctx, const DualState& st, double* cl);
+// a9/a10 message_passing_iteration x iters (dual.py:358-392)
+void message_passing(Ctx& ctx, DualState& st, int iters);
+// mp_edge_to_triplets / mp_triplets_to_edges individually (dual.py:358, 374)
+void mp_phases(Ctx& ctx, DualState& st, bool edge_phase, bool triplet_phase);
+// a11 lower_bound (dual.py:395-405)
+double lower_bound(Ctx& ctx, const DualState& st);
+// a12 reparametrized_graph (dual.py:408-411): canonical merge of originals
+// and chords carrying c^lambda
+Graph reparametrized_graph(Ctx& ctx, const DualState& st);
+// edge -> slot CSR + coverage for an existing tri_edges array
+void build_slot_lists(Ctx& ctx, DualState& st);
+
+// ---- driver (solver.cu) -----------------------------------------------------
+struct SolveConfig {
+  int mode = 1;  // 0 P, 1 PD, 2 PD+, 3 D, 4 GAEC
+  int mp_iterations = 5;
+  int max_cycle_length = 5;
+  double switch_fraction = 0.1;
+  int max_rounds = 100;
+  int separation_rounds = 1;
+};
+
+struct RoundInfo {
+  int32_t round_index;
+  int32_t phase;  // 0 contract, 1 primal-dual, 2 cleanup, 3 dual, 4 gaec
+  int64_t nodes, edges, triplets;
+  double lb;
+  int32_t lb_valid;
+  int64_t contracted;
+  double time_ms;
+};
+
+struct SolveResult {
+  double primal = 0.0;
+  double lb = 0.0;
+  bool lb_finite = false;
+  int n_rounds = 0;
+};
+
+void solve(Ctx& ctx, const GraphView& g, const SolveConfig& cfg, int32_t* labels, SolveResult& res,
+           RoundInfo* trace, int max_trace);
+
+}  // namespace rama

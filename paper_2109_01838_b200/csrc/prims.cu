@@ -1,0 +1,310 @@
+// Generic device primitives: prefix scans, compaction, deterministic sums,
+// and the bucket sort that every canonical-order step of the solver is
+// built on (canonicalisation, contraction, positive CSR, triplet and chord
+// dedupe, edge->slot lists).
+//
+// Bucket sort = counting sort on a 32-bit row id (atomic histogram + scan +
+// atomic scatter) followed by an in-row sort on a unique 64-bit key.  Rows
+// in this solver are short (grid degrees), so the in-row sort is a
+// thread-per-row insertion sort in registers-through-L1; the rare long
+// rows (power-law hubs) go through CUB's segmented sort.  CUB is used only
+// for generic scans/selection/segmented sorting, never for domain logic.
+#include "common.cuh"
+
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include <vector>
+
+namespace rama {
+
+static int g_num_sms = 0;
+
+Ctx::Ctx(cudaStream_t st) : s(st) {
+  ensure_pool_configured();
+  RAMA_CUDA(cudaMallocHost((void**)&pinned, 64 * sizeof(int64_t)));
+}
+
+Ctx::~Ctx() {
+  if (pinned) cudaFreeHost(pinned);
+}
+
+void ensure_pool_configured() {
+  static bool done = false;
+  if (done) return;
+  int dev = 0;
+  RAMA_CUDA(cudaGetDevice(&dev));
+  cudaMemPool_t pool;
+  RAMA_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t thr = UINT64_MAX;
+  RAMA_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  RAMA_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+  done = true;
+}
+
+// ------------------------------------------------------------- profiling
+
+namespace {
+struct ProfRec {
+  int fam;
+  cudaEvent_t a, b;
+  double bytes;
+};
+bool g_prof = false;
+std::vector<ProfRec> g_prof_recs;
+double g_prof_ms[kNumFamilies] = {0};
+double g_prof_bytes[kNumFamilies] = {0};
+int64_t g_prof_count[kNumFamilies] = {0};
+
+void prof_drain() {
+  for (auto& r : g_prof_recs) {
+    float ms = 0.f;
+    cudaEventSynchronize(r.b);
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    g_prof_ms[r.fam] += ms;
+    g_prof_bytes[r.fam] += r.bytes;
+    g_prof_count[r.fam] += 1;
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_prof_recs.clear();
+}
+}  // namespace
+
+bool prof_enabled() { return g_prof; }
+
+void prof_set(bool on) {
+  prof_drain();
+  for (int f = 0; f < kNumFamilies; f++) {
+    g_prof_ms[f] = 0.0;
+    g_prof_bytes[f] = 0.0;
+    g_prof_count[f] = 0;
+  }
+  g_prof = on;
+}
+
+void prof_push(int fam, cudaEvent_t a, cudaEvent_t b, double bytes) {
+  g_prof_recs.push_back(ProfRec{fam, a, b, bytes});
+  if (g_prof_recs.size() > 4096) prof_drain();
+}
+
+void prof_read(double* ms, double* bytes, int64_t* count) {
+  prof_drain();
+  for (int f = 0; f < kNumFamilies; f++) {
+    ms[f] = g_prof_ms[f];
+    bytes[f] = g_prof_bytes[f];
+    count[f] = g_prof_count[f];
+  }
+}
+
+unsigned capped_grid(int64_t work, int block) {
+  int64_t g = (work + block - 1) / block;
+  int64_t cap = (int64_t)(g_num_sms > 0 ? g_num_sms : 148) * 16;  // 16 x 256 threads per SM
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (unsigned)g;
+}
+
+// ---------------------------------------------------------------- scans
+
+__global__ void k_scan_tail(const int32_t* in, int32_t* out, int64_t n) {
+  out[n] = n ? out[n - 1] + in[n - 1] : 0;
+}
+
+int64_t exclusive_scan(Ctx& ctx, const int32_t* in, int32_t* out, int64_t n, bool want_total) {
+  if (n > 0) {
+    size_t tb = 0;
+    RAMA_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, (int)n, ctx.s));
+    Buf<uint8_t> tmp(tb, ctx);
+    RAMA_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, in, out, (int)n, ctx.s));
+    ctx.launches++;
+  }
+  k_scan_tail<<<1, 1, 0, ctx.s>>>(in, out, n);
+  RAMA_LAUNCH_CHECK();
+  ctx.launches++;
+  if (!want_total) return -1;
+  return read_scalar(ctx, out + n);
+}
+
+void exclusive_scan64(Ctx& ctx, const int64_t* in, int64_t* out, int64_t n) {
+  if (n <= 0) return;
+  size_t tb = 0;
+  RAMA_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, (int)n, ctx.s));
+  Buf<uint8_t> tmp(tb, ctx);
+  RAMA_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, in, out, (int)n, ctx.s));
+  ctx.launches++;
+}
+
+// ----------------------------------------------------------- compaction
+
+int64_t compact_indices(Ctx& ctx, const uint8_t* flags, int64_t n, Buf<int32_t>& out) {
+  out.alloc(n > 0 ? n : 1, ctx.s);
+  if (n <= 0) return 0;
+  Buf<int32_t> nsel(1, ctx);
+  thrust::counting_iterator<int32_t> it(0);
+  size_t tb = 0;
+  RAMA_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, flags, out.p, nsel.p, (int)n, ctx.s));
+  Buf<uint8_t> tmp(tb, ctx);
+  RAMA_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, it, flags, out.p, nsel.p, (int)n, ctx.s));
+  ctx.launches++;
+  return read_scalar(ctx, nsel.p);
+}
+
+// -------------------------------------------------- deterministic sum
+
+constexpr int kSumBlocks = 592;  // 4 x 148 SMs, fixed => deterministic order
+
+__global__ void k_partial_sum(const double* __restrict__ x, int64_t n, double* __restrict__ part) {
+  __shared__ double sh[kBlock];
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    acc += x[i];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+__global__ void k_final_sum(const double* part, int np, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < np; i++) s += part[i];
+    *out = s;
+  }
+}
+
+double device_sum(Ctx& ctx, const double* x, int64_t n) {
+  if (n <= 0) return 0.0;
+  Buf<double> part(kSumBlocks + 1, ctx);
+  k_partial_sum<<<kSumBlocks, kBlock, 0, ctx.s>>>(x, n, part.p);
+  RAMA_LAUNCH_CHECK();
+  k_final_sum<<<1, 1, 0, ctx.s>>>(part.p, kSumBlocks, part.p + kSumBlocks);
+  RAMA_LAUNCH_CHECK();
+  ctx.launches += 2;
+  return read_scalar(ctx, part.p + kSumBlocks);
+}
+
+// ----------------------------------------------------------- row ptrs
+
+__global__ void k_row_ptr(const int32_t* __restrict__ u, int64_t m, int64_t n, int32_t* __restrict__ ptr) {
+  GRID_STRIDE(x, n + 1) {
+    int64_t lo = 0, hi = m;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (u[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    ptr[x] = (int32_t)lo;
+  }
+}
+
+void row_ptr_from_sorted(Ctx& ctx, const int32_t* u, int64_t m, int64_t n, int32_t* ptr) {
+  RAMA_KERNEL(ctx, k_row_ptr, n + 1, u, m, n, ptr);
+}
+
+// ---------------------------------------------------------- bucket sort
+
+__global__ void k_bucket_count(const int32_t* __restrict__ row, int64_t N, int32_t* __restrict__ cnt) {
+  GRID_STRIDE(i, N) atomicAdd(&cnt[row[i]], 1);
+}
+
+__global__ void k_bucket_scatter(const int32_t* __restrict__ row, const uint64_t* __restrict__ key, int64_t N,
+                                 int32_t* __restrict__ cursor, uint64_t* __restrict__ okey,
+                                 int32_t* __restrict__ osrc, int32_t* __restrict__ orow) {
+  GRID_STRIDE(i, N) {
+    int32_t r = row[i];
+    int32_t p = atomicAdd(&cursor[r], 1);
+    okey[p] = key[i];
+    osrc[p] = (int32_t)i;
+    if (orow) orow[p] = r;
+  }
+}
+
+constexpr int kSmallRow = 32;
+
+// insertion sort of each short row; long rows are flagged for CUB
+__global__ void k_sort_rows_small(const int32_t* __restrict__ ptr, int64_t R, uint64_t* __restrict__ key,
+                                  int32_t* __restrict__ src, uint8_t* __restrict__ big) {
+  GRID_STRIDE(r, R) {
+    int32_t b = ptr[r], e = ptr[r + 1];
+    int32_t len = e - b;
+    big[r] = len > kSmallRow;
+    if (len < 2 || len > kSmallRow) continue;
+    for (int32_t i = b + 1; i < e; i++) {
+      uint64_t k = key[i];
+      int32_t s = src[i];
+      int32_t j = i - 1;
+      while (j >= b && key[j] > k) {
+        key[j + 1] = key[j];
+        src[j + 1] = src[j];
+        j--;
+      }
+      key[j + 1] = k;
+      src[j + 1] = s;
+    }
+  }
+}
+
+__global__ void k_big_lens(const int32_t* __restrict__ rows, int64_t nb, const int32_t* __restrict__ ptr,
+                           int32_t* __restrict__ len) {
+  GRID_STRIDE(i, nb) len[i] = ptr[rows[i] + 1] - ptr[rows[i]];
+}
+
+// move big rows to / from a contiguous staging area
+__global__ void k_big_move(const int32_t* __restrict__ rows, int64_t nb, const int32_t* __restrict__ ptr,
+                           const int32_t* __restrict__ off, uint64_t* __restrict__ key, int32_t* __restrict__ src,
+                           uint64_t* __restrict__ skey, int32_t* __restrict__ ssrc, bool to_stage) {
+  // one block per big row
+  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    int32_t r = rows[b];
+    int32_t base = ptr[r], len = ptr[r + 1] - base, o = off[b];
+    for (int32_t j = threadIdx.x; j < len; j += blockDim.x) {
+      if (to_stage) { skey[o + j] = key[base + j]; ssrc[o + j] = src[base + j]; }
+      else { key[base + j] = skey[o + j]; src[base + j] = ssrc[o + j]; }
+    }
+  }
+}
+
+void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint64_t* key, BucketSorted& out,
+                 bool want_row, int64_t sort_rows) {
+  if (sort_rows < 0 || sort_rows > R) sort_rows = R;
+  out.row_ptr.alloc(R + 1, ctx.s);
+  out.key.alloc(N > 0 ? N : 1, ctx.s);
+  out.src.alloc(N > 0 ? N : 1, ctx.s);
+  if (want_row) out.row.alloc(N > 0 ? N : 1, ctx.s);
+  Buf<int32_t> cnt(R > 0 ? R : 1, ctx);
+  cnt.zero();
+  RAMA_KERNEL(ctx, k_bucket_count, N, row, N, cnt.p);
+  exclusive_scan(ctx, cnt.p, out.row_ptr.p, R, false);
+  if (N == 0 || R == 0) return;
+  copy_d2d(ctx, cnt.p, out.row_ptr.p, R);  // cursor
+  RAMA_KERNEL(ctx, k_bucket_scatter, N, row, key, N, cnt.p, out.key.p, out.src.p,
+              want_row ? out.row.p : (int32_t*)nullptr);
+  if (sort_rows == 0) return;
+  Buf<uint8_t> big(sort_rows, ctx);
+  RAMA_KERNEL(ctx, k_sort_rows_small, sort_rows, out.row_ptr.p, sort_rows, out.key.p, out.src.p, big.p);
+  Buf<int32_t> brows;
+  int64_t nb = compact_indices(ctx, big.p, sort_rows, brows);
+  if (nb == 0) return;
+  Buf<int32_t> blen(nb, ctx), boff(nb + 1, ctx);
+  RAMA_KERNEL(ctx, k_big_lens, nb, brows.p, nb, out.row_ptr.p, blen.p);
+  int64_t tot = exclusive_scan(ctx, blen.p, boff.p, nb, true);
+  Buf<uint64_t> k1(tot, ctx), k2(tot, ctx);
+  Buf<int32_t> s1(tot, ctx), s2(tot, ctx);
+  unsigned g = (unsigned)std::min<int64_t>(nb, 4096);
+  k_big_move<<<g, kBlock, 0, ctx.s>>>(brows.p, nb, out.row_ptr.p, boff.p, out.key.p, out.src.p, k1.p, s1.p, true);
+  RAMA_LAUNCH_CHECK();
+  size_t tb = 0;
+  RAMA_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, tb, k1.p, k2.p, s1.p, s2.p, (int)tot, (int)nb, boff.p,
+                                                boff.p + 1, ctx.s));
+  Buf<uint8_t> tmp(tb, ctx);
+  RAMA_CUDA(cub::DeviceSegmentedSort::SortPairs(tmp.p, tb, k1.p, k2.p, s1.p, s2.p, (int)tot, (int)nb, boff.p,
+                                                boff.p + 1, ctx.s));
+  k_big_move<<<g, kBlock, 0, ctx.s>>>(brows.p, nb, out.row_ptr.p, boff.p, out.key.p, out.src.p, k2.p, s2.p, false);
+  RAMA_LAUNCH_CHECK();
+  ctx.launches += 3;
+}
+
+}  // namespace rama

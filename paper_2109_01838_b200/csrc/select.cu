@@ -1,0 +1,632 @@
+// Contraction-set selection.
+//
+// Matching (contraction.py:179-228): each handshake round is two atomic
+// vote passes over the positive edges -- atomicMax of the cost bits (positive
+// fp64 orders like its uint64 bit pattern), then atomicMin of the neighbour
+// id among edges attaining the max -- which reproduces the reference's
+// lexsort((nbr, -cost, node)) target exactly.  Mutual pairs match.  A round
+// that adds nothing leaves the state unchanged, so running all rounds
+// without a host check is equivalent to the reference's early exit.
+//
+// Forest (contraction.py:287-366): GPU Boruvka under the strict order
+// (cost desc, u asc, v asc) gives the unique maximum spanning forest, i.e.
+// the reference's forest bit for bit.  The conflict pass
+// (_remove_conflict_edges, contraction.py:231-284) is order dependent in
+// the reference (one repulsive edge at a time, ascending (u, v)); here it is
+// resolved EXACTLY in parallel:
+//   * every repulsive edge q inside one tree has a fixed tree path P_q and a
+//     fixed cheapest edge e_q on it (Euler tour + list ranking roots the
+//     forest; binary lifting answers LCA / path-min queries);
+//   * q cuts e_q iff no earlier cutting q' < q has e_q' on P_q (a cut
+//     disconnects, and a forest path is unique);
+//   * passes decide candidates whose earlier dependencies are decided (a
+//     path-min over "earliest cutting candidate per edge" and "earliest
+//     undecided candidate per edge"); each pass decides at least the
+//     smallest undecided candidate.
+#include "internal.h"
+
+#include <cub/cub.cuh>
+
+namespace rama {
+
+__device__ __forceinline__ int32_t sf_find(int32_t* p, int32_t x) {
+  while (true) {
+    int32_t px = __ldcg(p + x);
+    if (px == x) return x;
+    int32_t gp = __ldcg(p + px);
+    if (gp != px) p[x] = gp;
+    x = px;
+  }
+}
+
+__device__ __forceinline__ void sf_union(int32_t* p, int32_t a, int32_t b) {
+  while (true) {
+    a = sf_find(p, a);
+    b = sf_find(p, b);
+    if (a == b) return;
+    int32_t lo = a < b ? a : b, hi = a < b ? b : a;
+    int32_t old = atomicCAS(p + hi, hi, lo);
+    if (old == hi) return;
+    a = lo;
+    b = old;
+  }
+}
+
+__global__ void k_flag_positive(const double* __restrict__ c, int64_t m, uint8_t* __restrict__ f) {
+  GRID_STRIDE(i, m) f[i] = c[i] > 0.0;
+}
+
+// ----------------------------------------------------------------- matching
+
+__global__ void k_match_vote1(const int32_t* __restrict__ P, int64_t np, const int32_t* __restrict__ u,
+                              const int32_t* __restrict__ v, const double* __restrict__ c,
+                              const uint8_t* __restrict__ matched, unsigned long long* __restrict__ bc) {
+  GRID_STRIDE(i, np) {
+    int32_t e = P[i];
+    int32_t a = u[e], b = v[e];
+    if (matched[a] | matched[b]) continue;
+    unsigned long long bits = dbits(c[e]);
+    atomicMax(bc + a, bits);
+    atomicMax(bc + b, bits);
+  }
+}
+
+__global__ void k_match_vote2(const int32_t* __restrict__ P, int64_t np, const int32_t* __restrict__ u,
+                              const int32_t* __restrict__ v, const double* __restrict__ c,
+                              const uint8_t* __restrict__ matched, const unsigned long long* __restrict__ bc,
+                              int32_t* __restrict__ bn) {
+  GRID_STRIDE(i, np) {
+    int32_t e = P[i];
+    int32_t a = u[e], b = v[e];
+    if (matched[a] | matched[b]) continue;
+    unsigned long long bits = dbits(c[e]);
+    if (bits == bc[a]) atomicMin(bn + a, b);
+    if (bits == bc[b]) atomicMin(bn + b, a);
+  }
+}
+
+__global__ void k_match_pair(int64_t n, const unsigned long long* __restrict__ bc, const int32_t* __restrict__ bn,
+                             uint8_t* __restrict__ matched, int32_t* __restrict__ partner) {
+  GRID_STRIDE(x, n) {
+    if (bc[x] == 0ULL) continue;
+    int32_t t = bn[x];
+    if ((int32_t)x < t && bn[t] == (int32_t)x) {
+      partner[x] = t;
+      matched[x] = 1;
+      matched[t] = 1;
+    }
+  }
+}
+
+__global__ void k_match_out(const int32_t* __restrict__ idx, int64_t k, const int32_t* __restrict__ partner,
+                            int32_t* __restrict__ su, int32_t* __restrict__ sv) {
+  GRID_STRIDE(i, k) {
+    int32_t x = idx[i];
+    su[i] = x;
+    sv[i] = partner[x];
+  }
+}
+
+__global__ void k_flag_lower(const int32_t* __restrict__ partner, int64_t n, uint8_t* __restrict__ f) {
+  GRID_STRIDE(x, n) f[x] = partner[x] > (int32_t)x;
+}
+
+int64_t select_matching(Ctx& ctx, const GraphView& g, int rounds, Buf<int32_t>& su, Buf<int32_t>& sv) {
+  ProfScope prof(ctx.s, kFamMatching);
+  int64_t n = g.n, m = g.m;
+  su.alloc(1, ctx.s);
+  sv.alloc(1, ctx.s);
+  if (n == 0 || m == 0) return 0;
+  Buf<uint8_t> flag(m, ctx);
+  RAMA_KERNEL(ctx, k_flag_positive, m, g.c, m, flag.p);
+  Buf<int32_t> P;
+  int64_t np = compact_indices(ctx, flag.p, m, P);
+  if (np == 0) return 0;
+  Buf<uint8_t> matched(n, ctx);
+  matched.zero();
+  Buf<unsigned long long> bc(n, ctx);
+  Buf<int32_t> bn(n, ctx), partner(n, ctx);
+  partner.fill_bytes(0xff);
+  for (int r = 0; r < rounds; r++) {
+    bc.zero();
+    bn.fill_bytes(0x7f);
+    RAMA_KERNEL(ctx, k_match_vote1, np, P.p, np, g.u, g.v, g.c, matched.p, bc.p);
+    RAMA_KERNEL(ctx, k_match_vote2, np, P.p, np, g.u, g.v, g.c, matched.p, bc.p, bn.p);
+    RAMA_KERNEL(ctx, k_match_pair, n, n, bc.p, bn.p, matched.p, partner.p);
+  }
+  Buf<uint8_t> lf(n, ctx);
+  RAMA_KERNEL(ctx, k_flag_lower, n, partner.p, n, lf.p);
+  Buf<int32_t> idx;
+  int64_t k = compact_indices(ctx, lf.p, n, idx);
+  su.alloc(k > 0 ? k : 1, ctx.s);
+  sv.alloc(k > 0 ? k : 1, ctx.s);
+  RAMA_KERNEL(ctx, k_match_out, k, idx.p, k, partner.p, su.p, sv.p);
+  return k;
+}
+
+// ----------------------------------------------------------------- max edge
+
+__global__ void k_max_bits(const double* __restrict__ c, int64_t m, unsigned long long* best) {
+  GRID_STRIDE(i, m) {
+    if (c[i] > 0.0) atomicMax(best, dbits(c[i]));
+  }
+}
+
+__global__ void k_argmax(const double* __restrict__ c, int64_t m, const unsigned long long* best, int32_t* idx) {
+  GRID_STRIDE(i, m) {
+    if (c[i] > 0.0 && dbits(c[i]) == *best) atomicMin(idx, (int32_t)i);
+  }
+}
+
+int64_t select_max_edge(Ctx& ctx, const GraphView& g) {
+  if (g.m == 0) return -1;
+  Buf<unsigned long long> best(1, ctx);
+  Buf<int32_t> idx(1, ctx);
+  best.zero();
+  idx.fill_bytes(0x7f);
+  RAMA_KERNEL(ctx, k_max_bits, g.m, g.c, g.m, best.p);
+  RAMA_KERNEL(ctx, k_argmax, g.m, g.c, g.m, best.p, idx.p);
+  int32_t i = read_scalar(ctx, idx.p);
+  return i == 0x7f7f7f7f ? -1 : (int64_t)i;
+}
+
+// ------------------------------------------------------------------- forest
+
+__global__ void k_neg_bits(const int32_t* __restrict__ P, int64_t np, const double* __restrict__ c,
+                           uint64_t* __restrict__ key, int32_t* __restrict__ val) {
+  GRID_STRIDE(i, np) {
+    key[i] = ~dbits(c[P[i]]);  // descending cost
+    val[i] = (int32_t)i;
+  }
+}
+
+__global__ void k_scatter_rank(const int32_t* __restrict__ sorted_val, int64_t np, int32_t* __restrict__ rank) {
+  GRID_STRIDE(r, np) rank[sorted_val[r]] = (int32_t)r;
+}
+
+__global__ void k_bv_vote(const int32_t* __restrict__ P, int64_t np, const int32_t* __restrict__ u,
+                          const int32_t* __restrict__ v, const int32_t* __restrict__ rank, int32_t* comp,
+                          uint32_t* __restrict__ best, int32_t* __restrict__ any) {
+  GRID_STRIDE(i, np) {
+    int32_t e = P[i];
+    int32_t a = sf_find(comp, u[e]), b = sf_find(comp, v[e]);
+    if (a == b) continue;
+    uint32_t r = (uint32_t)rank[i];
+    atomicMin(best + a, r);
+    atomicMin(best + b, r);
+    *any = 1;
+  }
+}
+
+__global__ void k_bv_hook(int64_t n, const uint32_t* __restrict__ best, const int32_t* __restrict__ order,
+                          const int32_t* __restrict__ P, const int32_t* __restrict__ u,
+                          const int32_t* __restrict__ v, int32_t* comp, uint8_t* __restrict__ in_forest) {
+  GRID_STRIDE(x, n) {
+    uint32_t r = best[x];
+    if (r == 0xffffffffu) continue;
+    int32_t pi = order[r];
+    in_forest[pi] = 1;
+    int32_t e = P[pi];
+    sf_union(comp, u[e], v[e]);
+  }
+}
+
+__global__ void k_flatten(int32_t* comp, int64_t n) {
+  GRID_STRIDE(x, n) comp[x] = sf_find(comp, (int32_t)x);
+}
+
+// repulsive edges whose endpoints share a tree
+__global__ void k_flag_conflicts(const int32_t* __restrict__ u, const int32_t* __restrict__ v,
+                                 const double* __restrict__ c, int64_t m, const int32_t* __restrict__ comp,
+                                 uint8_t* __restrict__ f) {
+  GRID_STRIDE(i, m) f[i] = (c[i] < 0.0) && comp[u[i]] == comp[v[i]];
+}
+
+__global__ void k_forest_edges(const int32_t* __restrict__ Fi, int64_t kf, const int32_t* __restrict__ P,
+                               const int32_t* __restrict__ u, const int32_t* __restrict__ v,
+                               const double* __restrict__ c, int32_t* __restrict__ fu, int32_t* __restrict__ fv,
+                               uint64_t* __restrict__ fkey_bits, int32_t* __restrict__ fval) {
+  GRID_STRIDE(i, kf) {
+    int32_t e = P[Fi[i]];
+    fu[i] = u[e];
+    fv[i] = v[e];
+    fkey_bits[i] = dbits(c[e]);  // ascending cost, ties keep (u, v) order
+    fval[i] = (int32_t)i;
+  }
+}
+
+__global__ void k_arcs(const int32_t* __restrict__ fu, const int32_t* __restrict__ fv, int64_t kf,
+                       int32_t* __restrict__ row, uint64_t* __restrict__ key) {
+  GRID_STRIDE(a, 2 * kf) {
+    int32_t f = (int32_t)(a >> 1);
+    int32_t s = (a & 1) ? fv[f] : fu[f];
+    int32_t d = (a & 1) ? fu[f] : fv[f];
+    row[a] = s;
+    key[a] = ((uint64_t)(uint32_t)d << 32) | (uint64_t)a;
+  }
+}
+
+__global__ void k_arc_pos(const int32_t* __restrict__ arc_at, int64_t na, int32_t* __restrict__ pos) {
+  GRID_STRIDE(p, na) pos[arc_at[p]] = (int32_t)p;
+}
+
+// Euler successor: after arc (x->y) comes the arc following (y->x) in y's
+// cyclic adjacency list; the tour of each tree starts at its root's first
+// arc and is cut before returning to it.
+__global__ void k_euler_succ(int64_t na, const int32_t* __restrict__ arc_at, const int32_t* __restrict__ pos,
+                             const int32_t* __restrict__ arow, const int32_t* __restrict__ ptr,
+                             const int32_t* __restrict__ comp, int32_t* __restrict__ succ) {
+  GRID_STRIDE(a, na) {
+    int32_t t = (int32_t)a ^ 1;
+    int32_t pt = pos[t];
+    int32_t y = arow[pt];
+    int32_t p = pt + 1;
+    if (p == ptr[y + 1]) p = ptr[y];
+    int32_t nx = arc_at[p];
+    // cut: the arc whose successor is the root's first arc ends the tour
+    int32_t r = comp[y];
+    if (y == r && p == ptr[y]) nx = -1;
+    succ[a] = nx;
+  }
+}
+
+__global__ void k_rank_init(const int32_t* __restrict__ succ, int64_t na, int32_t* __restrict__ d) {
+  GRID_STRIDE(a, na) d[a] = succ[a] < 0 ? 0 : 1;
+}
+
+__global__ void k_rank_step(int64_t na, const int32_t* __restrict__ d, const int32_t* __restrict__ nx,
+                            int32_t* __restrict__ d2, int32_t* __restrict__ nx2) {
+  GRID_STRIDE(a, na) {
+    int32_t s = nx[a];
+    if (s >= 0) {
+      d2[a] = d[a] + d[s];
+      nx2[a] = nx[s];
+    } else {
+      d2[a] = d[a];
+      nx2[a] = -1;
+    }
+  }
+}
+
+__global__ void k_root_init(int64_t n, int32_t* __restrict__ par, int32_t* __restrict__ pedge,
+                            int32_t* __restrict__ enter, int32_t* __restrict__ exit_) {
+  GRID_STRIDE(x, n) {
+    par[x] = (int32_t)x;
+    pedge[x] = -1;
+    enter[x] = 0x7fffffff;
+    exit_[x] = -1;
+  }
+}
+
+// a down arc (x->y) precedes its twin in the tour (larger remaining distance)
+__global__ void k_orient(int64_t na, const int32_t* __restrict__ dist, const int32_t* __restrict__ fu,
+                         const int32_t* __restrict__ fv, int32_t* __restrict__ par, int32_t* __restrict__ pedge,
+                         int32_t* __restrict__ enter, int32_t* __restrict__ exit_) {
+  GRID_STRIDE(a, na) {
+    int32_t da = dist[a], dt = dist[a ^ 1];
+    if (da > dt) {
+      int32_t f = (int32_t)(a >> 1);
+      int32_t x = (a & 1) ? fv[f] : fu[f];
+      int32_t y = (a & 1) ? fu[f] : fv[f];
+      par[y] = x;
+      pedge[y] = f;
+      enter[y] = da;
+      exit_[y] = dt;
+    }
+  }
+}
+
+__device__ __forceinline__ bool is_anc(const int32_t* enter, const int32_t* exit_, int32_t x, int32_t w) {
+  if (x == w) return true;
+  int32_t ew = enter[w];
+  return exit_[x] < ew && ew < enter[x];
+}
+
+__global__ void k_lift0(int64_t n, const int32_t* __restrict__ par, const int32_t* __restrict__ pedge,
+                        const int32_t* __restrict__ edge_val, int32_t* __restrict__ up0, int32_t* __restrict__ mn0) {
+  GRID_STRIDE(x, n) {
+    if (up0) up0[x] = par[x];
+    int32_t f = pedge[x];
+    mn0[x] = f < 0 ? 0x7fffffff : edge_val[f];
+  }
+}
+
+__global__ void k_lift_up(int64_t n, const int32_t* __restrict__ upj, int32_t* __restrict__ upn) {
+  GRID_STRIDE(x, n) upn[x] = upj[upj[x]];
+}
+
+__global__ void k_lift_min(int64_t n, const int32_t* __restrict__ upj, const int32_t* __restrict__ mnj,
+                           int32_t* __restrict__ mnn) {
+  GRID_STRIDE(x, n) {
+    int32_t a = mnj[x], b = mnj[upj[x]];
+    mnn[x] = a < b ? a : b;
+  }
+}
+
+struct Lift {
+  int LOG = 0;
+  int64_t n = 0;
+  Buf<int32_t> up;  // LOG * n
+};
+
+__device__ __forceinline__ int32_t climb_min(const int32_t* up, const int32_t* mn, int LOG, int64_t n,
+                                             const int32_t* enter, const int32_t* exit_, int32_t x, int32_t l) {
+  int32_t acc = 0x7fffffff;
+  for (int j = LOG - 1; j >= 0; j--) {
+    int32_t y = up[(int64_t)j * n + x];
+    if (x != l && is_anc(enter, exit_, l, y)) {
+      int32_t v = mn[(int64_t)j * n + x];
+      acc = v < acc ? v : acc;
+      x = y;
+    }
+  }
+  return acc;
+}
+
+__device__ __forceinline__ int32_t lca(const int32_t* up, int LOG, int64_t n, const int32_t* enter,
+                                       const int32_t* exit_, int32_t a, int32_t b) {
+  if (is_anc(enter, exit_, a, b)) return a;
+  if (is_anc(enter, exit_, b, a)) return b;
+  int32_t x = a;
+  for (int j = LOG - 1; j >= 0; j--) {
+    int32_t y = up[(int64_t)j * n + x];
+    if (!is_anc(enter, exit_, y, b)) x = y;
+  }
+  return up[x];
+}
+
+__global__ void k_cand_paths(const int32_t* __restrict__ Q, int64_t nq, const int32_t* __restrict__ u,
+                             const int32_t* __restrict__ v, const int32_t* __restrict__ up,
+                             const int32_t* __restrict__ mn, int LOG, int64_t n, const int32_t* __restrict__ enter,
+                             const int32_t* __restrict__ exit_, const int32_t* __restrict__ key_inv,
+                             int32_t* __restrict__ qa, int32_t* __restrict__ qb, int32_t* __restrict__ ql,
+                             int32_t* __restrict__ qe) {
+  GRID_STRIDE(q, nq) {
+    int32_t e = Q[q];
+    int32_t a = u[e], b = v[e];
+    int32_t l = lca(up, LOG, n, enter, exit_, a, b);
+    int32_t m1 = climb_min(up, mn, LOG, n, enter, exit_, a, l);
+    int32_t m2 = climb_min(up, mn, LOG, n, enter, exit_, b, l);
+    int32_t mk = m1 < m2 ? m1 : m2;
+    qa[q] = a;
+    qb[q] = b;
+    ql[q] = l;
+    qe[q] = key_inv[mk];
+  }
+}
+
+__global__ void k_fill_i32(int32_t* x, int64_t n, int32_t v) {
+  GRID_STRIDE(i, n) x[i] = v;
+}
+
+// state: 0 undecided, 1 cuts, 2 does not cut
+__global__ void k_earliest(const int32_t* __restrict__ qe, const uint8_t* __restrict__ state, int64_t nq,
+                           int32_t* __restrict__ rf, int32_t* __restrict__ ru) {
+  GRID_STRIDE(q, nq) {
+    uint8_t s = state[q];
+    if (s == 1) atomicMin(rf + qe[q], (int32_t)q);
+    else if (s == 0) atomicMin(ru + qe[q], (int32_t)q);
+  }
+}
+
+__global__ void k_resolve(int64_t nq, const int32_t* __restrict__ qa, const int32_t* __restrict__ qb,
+                          const int32_t* __restrict__ ql, const int32_t* __restrict__ up,
+                          const int32_t* __restrict__ mf, const int32_t* __restrict__ mu, int LOG, int64_t n,
+                          const int32_t* __restrict__ enter, const int32_t* __restrict__ exit_,
+                          uint8_t* __restrict__ state, int32_t* __restrict__ left) {
+  GRID_STRIDE(q, nq) {
+    if (state[q] != 0) continue;
+    int32_t a = qa[q], b = qb[q], l = ql[q];
+    int32_t pf = min(climb_min(up, mf, LOG, n, enter, exit_, a, l), climb_min(up, mf, LOG, n, enter, exit_, b, l));
+    if (pf < (int32_t)q) {
+      state[q] = 2;
+      continue;
+    }
+    int32_t pu = min(climb_min(up, mu, LOG, n, enter, exit_, a, l), climb_min(up, mu, LOG, n, enter, exit_, b, l));
+    if (pu < (int32_t)q) {
+      atomicAdd(left, 1);
+      continue;
+    }
+    state[q] = 1;
+  }
+}
+
+__global__ void k_mark_removed(const int32_t* __restrict__ qe, const uint8_t* __restrict__ state, int64_t nq,
+                               uint8_t* __restrict__ removed) {
+  GRID_STRIDE(q, nq) {
+    if (state[q] == 1) removed[qe[q]] = 1;
+  }
+}
+
+__global__ void k_forest_keep(const int32_t* __restrict__ Fi, int64_t kf, const uint8_t* __restrict__ removed,
+                              uint8_t* __restrict__ keep_pos) {
+  GRID_STRIDE(i, kf) keep_pos[Fi[i]] = !removed[i];
+}
+
+__global__ void k_gather_pairs(const int32_t* __restrict__ idx, int64_t k, const int32_t* __restrict__ P,
+                               const int32_t* __restrict__ u, const int32_t* __restrict__ v,
+                               int32_t* __restrict__ su, int32_t* __restrict__ sv) {
+  GRID_STRIDE(i, k) {
+    int32_t e = P[idx[i]];
+    su[i] = u[e];
+    sv[i] = v[e];
+  }
+}
+
+static void build_min_table(Ctx& ctx, int64_t n, int LOG, const int32_t* up, const int32_t* par,
+                            const int32_t* pedge, const int32_t* edge_val, Buf<int32_t>& mn) {
+  mn.alloc((size_t)LOG * n, ctx.s);
+  RAMA_KERNEL(ctx, k_lift0, n, n, par, pedge, edge_val, (int32_t*)nullptr, mn.p);
+  for (int j = 1; j < LOG; j++)
+    RAMA_KERNEL(ctx, k_lift_min, n, n, up + (int64_t)(j - 1) * n, mn.p + (int64_t)(j - 1) * n, mn.p + (int64_t)j * n);
+}
+
+static void radix_sort_u64(Ctx& ctx, Buf<uint64_t>& k_in, Buf<int32_t>& v_in, Buf<uint64_t>& k_out,
+                           Buf<int32_t>& v_out, int64_t N) {
+  size_t tb = 0;
+  RAMA_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k_in.p, k_out.p, v_in.p, v_out.p, (int)N, 0, 64, ctx.s));
+  Buf<uint8_t> tmp(tb, ctx);
+  RAMA_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, k_in.p, k_out.p, v_in.p, v_out.p, (int)N, 0, 64, ctx.s));
+  ctx.launches++;
+}
+
+int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_t>& sv) {
+  ProfScope prof(ctx.s, kFamForest);
+  int64_t n = g.n, m = g.m;
+  su.alloc(1, ctx.s);
+  sv.alloc(1, ctx.s);
+  if (n == 0 || m == 0) return 0;
+  Buf<uint8_t> flag(m, ctx);
+  RAMA_KERNEL(ctx, k_flag_positive, m, g.c, m, flag.p);
+  Buf<int32_t> P;
+  int64_t np = compact_indices(ctx, flag.p, m, P);
+  if (np == 0) return 0;
+
+  // strict rank: cost desc, (u, v) asc == stable sort of the canonical order
+  Buf<uint64_t> k1(np, ctx), k2(np, ctx);
+  Buf<int32_t> v1(np, ctx), order(np, ctx), rank(np, ctx);
+  RAMA_KERNEL(ctx, k_neg_bits, np, P.p, np, g.c, k1.p, v1.p);
+  radix_sort_u64(ctx, k1, v1, k2, order, np);
+  RAMA_KERNEL(ctx, k_scatter_rank, np, order.p, np, rank.p);
+
+  // Boruvka
+  Buf<int32_t> comp(n, ctx), any(1, ctx);
+  Buf<uint32_t> best(n, ctx);
+  Buf<uint8_t> in_forest(np, ctx);
+  in_forest.zero();
+  iota(ctx, comp.p, n);
+  while (true) {
+    best.fill_bytes(0xff);
+    any.zero();
+    RAMA_KERNEL(ctx, k_bv_vote, np, P.p, np, g.u, g.v, rank.p, comp.p, best.p, any.p);
+    if (read_scalar(ctx, any.p) == 0) break;
+    RAMA_KERNEL(ctx, k_bv_hook, n, n, best.p, order.p, P.p, g.u, g.v, comp.p, in_forest.p);
+    RAMA_KERNEL(ctx, k_flatten, n, comp.p, n);
+  }
+  RAMA_KERNEL(ctx, k_flatten, n, comp.p, n);
+
+  Buf<int32_t> Fi;
+  int64_t kf = compact_indices(ctx, in_forest.p, np, Fi);
+  Buf<uint8_t> keep(np, ctx);
+  keep.zero();
+
+  // repulsive edges inside one tree, ascending (u, v) order
+  Buf<uint8_t> cflag(m, ctx);
+  RAMA_KERNEL(ctx, k_flag_conflicts, m, g.u, g.v, g.c, m, comp.p, cflag.p);
+  Buf<int32_t> Q;
+  int64_t nq = compact_indices(ctx, cflag.p, m, Q);
+
+  Buf<uint8_t> removed(kf > 0 ? kf : 1, ctx);
+  removed.zero();
+  if (nq > 0 && kf > 0) {
+    Buf<int32_t> fu(kf, ctx), fv(kf, ctx), fval(kf, ctx), fsorted(kf, ctx), fkey(kf, ctx);
+    Buf<uint64_t> fbits(kf, ctx), fbits2(kf, ctx);
+    RAMA_KERNEL(ctx, k_forest_edges, kf, Fi.p, kf, P.p, g.u, g.v, g.c, fu.p, fv.p, fbits.p, fval.p);
+    radix_sort_u64(ctx, fbits, fval, fbits2, fsorted, kf);  // key_inv: rank -> forest edge
+    RAMA_KERNEL(ctx, k_scatter_rank, kf, fsorted.p, kf, fkey.p);  // fkey: forest edge -> rank
+
+    // arcs, sorted adjacency, Euler tour
+    int64_t na = 2 * kf;
+    Buf<int32_t> arow(na, ctx);
+    Buf<uint64_t> akey(na, ctx);
+    RAMA_KERNEL(ctx, k_arcs, na, fu.p, fv.p, kf, arow.p, akey.p);
+    BucketSorted bs;
+    bucket_sort(ctx, n, na, arow.p, akey.p, bs, true);
+    Buf<int32_t> pos(na, ctx), succ(na, ctx);
+    RAMA_KERNEL(ctx, k_arc_pos, na, bs.src.p, na, pos.p);
+    RAMA_KERNEL(ctx, k_euler_succ, na, na, bs.src.p, pos.p, bs.row.p, bs.row_ptr.p, comp.p, succ.p);
+    Buf<int32_t> d1(na, ctx), d2(na, ctx), n1(na, ctx), n2(na, ctx);
+    RAMA_KERNEL(ctx, k_rank_init, na, succ.p, na, d1.p);
+    copy_d2d(ctx, n1.p, succ.p, na);
+    int steps = 0;
+    while ((1LL << steps) < na) steps++;
+    for (int s = 0; s <= steps; s++) {
+      RAMA_KERNEL(ctx, k_rank_step, na, na, d1.p, n1.p, d2.p, n2.p);
+      std::swap(d1, d2);
+      std::swap(n1, n2);
+    }
+    Buf<int32_t> par(n, ctx), pedge(n, ctx), enter(n, ctx), exit_(n, ctx);
+    RAMA_KERNEL(ctx, k_root_init, n, n, par.p, pedge.p, enter.p, exit_.p);
+    RAMA_KERNEL(ctx, k_orient, na, na, d1.p, fu.p, fv.p, par.p, pedge.p, enter.p, exit_.p);
+
+    // binary lifting tables (depth <= kf)
+    int LOG = 1;
+    while ((1LL << LOG) <= kf) LOG++;
+    Buf<int32_t> up((size_t)LOG * n, ctx);
+    copy_d2d(ctx, up.p, par.p, n);
+    for (int j = 1; j < LOG; j++) RAMA_KERNEL(ctx, k_lift_up, n, n, up.p + (int64_t)(j - 1) * n, up.p + (int64_t)j * n);
+    Buf<int32_t> mn;
+    build_min_table(ctx, n, LOG, up.p, par.p, pedge.p, fkey.p, mn);
+
+    Buf<int32_t> qa(nq, ctx), qb(nq, ctx), ql(nq, ctx), qe(nq, ctx);
+    RAMA_KERNEL(ctx, k_cand_paths, nq, Q.p, nq, g.u, g.v, up.p, mn.p, LOG, n, enter.p, exit_.p, fsorted.p, qa.p,
+                qb.p, ql.p, qe.p);
+    mn.release();
+
+    Buf<uint8_t> state(nq, ctx);
+    state.zero();
+    Buf<int32_t> rf(kf, ctx), ru(kf, ctx), left(1, ctx), mf, mu;
+    while (true) {
+      RAMA_KERNEL(ctx, k_fill_i32, kf, rf.p, kf, 0x7fffffff);
+      RAMA_KERNEL(ctx, k_fill_i32, kf, ru.p, kf, 0x7fffffff);
+      RAMA_KERNEL(ctx, k_earliest, nq, qe.p, state.p, nq, rf.p, ru.p);
+      build_min_table(ctx, n, LOG, up.p, par.p, pedge.p, rf.p, mf);
+      build_min_table(ctx, n, LOG, up.p, par.p, pedge.p, ru.p, mu);
+      left.zero();
+      RAMA_KERNEL(ctx, k_resolve, nq, nq, qa.p, qb.p, ql.p, up.p, mf.p, mu.p, LOG, n, enter.p, exit_.p, state.p,
+                  left.p);
+      if (read_scalar(ctx, left.p) == 0) break;
+    }
+    RAMA_KERNEL(ctx, k_mark_removed, nq, qe.p, state.p, nq, removed.p);
+  }
+  RAMA_KERNEL(ctx, k_forest_keep, kf, Fi.p, kf, removed.p, keep.p);
+  Buf<int32_t> idx;
+  int64_t k = compact_indices(ctx, keep.p, np, idx);
+  su.alloc(k > 0 ? k : 1, ctx.s);
+  sv.alloc(k > 0 ? k : 1, ctx.s);
+  RAMA_KERNEL(ctx, k_gather_pairs, k, idx.p, k, P.p, g.u, g.v, su.p, sv.p);
+  return k;
+}
+
+// ------------------------------------------------------- contraction step
+
+void contraction_step(Ctx& ctx, const GraphView& g, int policy, double switch_fraction, StepResult& out,
+                      bool want_joined) {
+  Buf<int32_t> su, sv;
+  int64_t k = 0;
+  out.used_forest = false;
+  if (policy == 0) {
+    int64_t e = select_max_edge(ctx, g);
+    if (e >= 0) {
+      su.alloc(1, ctx.s);
+      sv.alloc(1, ctx.s);
+      copy_d2d(ctx, su.p, g.u + e, 1);
+      copy_d2d(ctx, sv.p, g.v + e, 1);
+      k = 1;
+    }
+  } else if (policy == 1) {
+    k = select_matching(ctx, g, 5, su, sv);
+  } else if (policy == 2) {
+    k = select_forest(ctx, g, su, sv);
+    out.used_forest = true;
+  } else {
+    k = select_matching(ctx, g, 5, su, sv);
+    if ((double)k < switch_fraction * (double)g.n) {
+      k = select_forest(ctx, g, su, sv);
+      out.used_forest = true;
+    }
+  }
+  out.num_selected = k;
+  out.joined = 0.0;
+  if (k == 0) {
+    out.identity = true;
+    out.num_targets = g.n;
+    return;
+  }
+  out.identity = false;
+  out.map.alloc(g.n, ctx.s);
+  out.num_targets = components(ctx, g.n, su.p, sv.p, k, out.map.p);
+  out.next = contract(ctx, g, out.map.p, out.num_targets, want_joined ? &out.joined : nullptr);
+}
+
+}  // namespace rama

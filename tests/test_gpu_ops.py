@@ -1,0 +1,210 @@
+"""GPU operator parity: every hot-path operator through the C ABI against
+(a) golden vectors produced by the reference itself and (b) the CPU oracle
+on larger seeded inputs.  Integer outputs bit-exact; fp64 outputs bit-exact
+where the reference's summation order is reproduced (contracted costs,
+multipliers, reparametrized costs), else within the stated tolerance
+(lower bound and joined cost: 1e-12 relative, different reduction order)."""
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2109_01838_b200 as P
+from paper_2109_01838_b200 import instances
+from tests._golden import load
+
+pytestmark = pytest.mark.gpu
+
+RTOL_SUM = 1e-12
+
+
+def _pg(fx, i):
+    n, u, v, c = fx.graph_arrays(i)
+    return P.WeightedGraph._from_canonical(n, u, v, c)
+
+
+@pytest.fixture(scope="module")
+def ops():
+    return load("ops_small.npz")
+
+
+def close_sum(a, b):
+    return abs(a - b) <= RTOL_SUM * max(1.0, abs(b))
+
+
+# ------------------------------------------------------------ golden ops
+
+def test_canonicalize_golden(ops):
+    for i in range(ops.count("edges")):
+        n, u, v, c = ops.graph_arrays(i)
+        rng = np.random.default_rng(i)
+        perm = rng.permutation(u.size)
+        flip = rng.random(u.size) < 0.5
+        uu = np.where(flip, v, u)[perm]
+        vv = np.where(flip, u, v)[perm]
+        # duplicate a few edges with split costs: sums must follow reduceat order
+        dup = perm[: max(1, u.size // 4)]
+        uu = np.concatenate([uu, u[dup]])
+        vv = np.concatenate([vv, v[dup]])
+        cc = np.concatenate([c[perm], -0.25 * c[dup]])
+        g = P.WeightedGraph(n, uu, vv, cc)
+        ref = O.Graph(n, uu, vv, cc)
+        assert np.array_equal(g.edges_u, ref.edges_u) and np.array_equal(g.edges_v, ref.edges_v)
+        assert np.array_equal(g.costs, ref.costs)
+
+
+def test_components_contract_golden(ops):
+    for i in range(ops.count("edges")):
+        g = _pg(ops, i)
+        S = ops.get("S", i).reshape(-1, 2)
+        f = P.connected_components(g.num_nodes, S)
+        assert np.array_equal(f.map, ops.vec("cc_map", i))
+        gq, joined = P.contract_graph(g, f)
+        assert np.array_equal(np.stack([gq.edges_u, gq.edges_v], 1).reshape(-1), ops.vec("contract_edges", i))
+        assert np.array_equal(gq.costs, ops.vec("contract_costs", i))
+        assert close_sum(joined, ops.scalar("contract_joined", i))
+
+
+def test_selection_golden(ops):
+    for i in range(ops.count("edges")):
+        g = _pg(ops, i)
+        assert np.array_equal(P.select_matching(g).reshape(-1), ops.vec("matching", i)), i
+        assert np.array_equal(P.select_spanning_forest_no_conflicts(g).reshape(-1), ops.vec("forest", i)), i
+        assert np.array_equal(P.select_max_edge(g).reshape(-1), ops.vec("max_edge", i)), i
+
+
+def test_separation_golden(ops):
+    for i in range(ops.count("edges")):
+        g = _pg(ops, i)
+        for L in (3, 4, 5):
+            lengths, nodes = P.dual._separate(g, L)
+            assert np.array_equal(lengths, ops.vec("sep%d_len" % L, i)), (i, L)
+            assert np.array_equal(nodes.reshape(-1), ops.vec("sep%d_nodes" % L, i)), (i, L)
+
+
+def test_triangulation_mp_golden(ops):
+    for i in range(ops.count("edges")):
+        g = _pg(ops, i)
+        st = P.dual._triangulate_arrays(g, *P.dual._separate(g, 5))
+        assert np.array_equal(np.stack([st.edges_u, st.edges_v], 1).reshape(-1), ops.vec("tri_aug", i))
+        assert np.array_equal(st.base_costs, ops.vec("tri_base", i))
+        assert np.array_equal(st.tri_nodes.reshape(-1), ops.vec("tri_nodes", i))
+        assert np.array_equal(st.tri_edges.reshape(-1), ops.vec("tri_edges", i))
+        assert np.array_equal(st.coverage, ops.vec("tri_cov", i))
+        assert close_sum(P.lower_bound(st), ops.scalar("lb0", i))
+        P.message_passing(st, 5)
+        assert np.array_equal(st.lam.reshape(-1), ops.vec("lam5", i)), i  # bit-exact multipliers
+        assert np.array_equal(P.reparametrized_edge_costs(st), ops.vec("cl5", i))
+        assert close_sum(P.lower_bound(st), ops.scalar("lb5", i))
+
+
+# ----------------------------------------------- reference unit vectors
+
+def tri():
+    return P.WeightedGraph.from_edges(3, [(0, 1, 1.0), (1, 2, 1.0), (0, 2, -2.0)])
+
+
+def test_reference_unit_vectors():
+    # test_contraction.py:97-101, 192-196, 212-219, 242-246
+    g = P.WeightedGraph.from_edges(3, [(0, 1, 2.0), (1, 2, 3.0), (0, 2, -1.0)])
+    res = P.contract(P.build_adjacency(g), P.connected_components(3, [(1, 2)]))
+    assert res.contracted.entries() == [(0, 1, 1.0), (1, 0, 1.0)] and res.joined_cost == 3.0
+    sq = P.WeightedGraph.from_edges(4, [(0, 1, 1.0), (1, 2, 1.0), (2, 3, 1.0), (0, 3, 1.0)])
+    assert P.select_matching(sq).tolist() == [[0, 1], [2, 3]]
+    assert P.select_spanning_forest_no_conflicts(tri()).tolist() == [[1, 2]]
+    g2, f, joined = P.contraction_step(tri(), "forest")
+    assert f.map.tolist() == [0, 1, 1] and g2.edges == [(0, 1, -1.0)] and joined == 1.0
+    star = P.WeightedGraph.from_edges(21, [(0, i, float(i)) for i in range(1, 21)])
+    g2, f, joined = P.contraction_step(star, "auto")
+    assert f.num_targets == 1 and joined == sum(range(1, 21))
+    # test_dual.py:61-82, 204-235
+    assert [c.nodes for c in P.separate_conflicted_cycles(tri(), 3)] == [(0, 1, 2)]
+    tie = P.WeightedGraph.from_edges(4, [(0, 1, 1.0), (0, 2, 1.0), (1, 3, 1.0), (2, 3, 1.0), (0, 3, -1.0)])
+    assert [c.nodes for c in P.separate_conflicted_cycles(tie, 5)] == [(0, 1, 3)]
+    st = P.triangulate(P.separate_conflicted_cycles(tri(), 3), tri())
+    st.lam[0] = (-1.0, 2.0, -1.0)
+    P.mp_triplets_to_edges(st)
+    assert np.allclose(st.lam[0], [-1.0, 1.0, -1.0], atol=1e-12)
+    st = P.triangulate(P.separate_conflicted_cycles(tri(), 3), tri())
+    P.message_passing_iteration(st)
+    assert np.allclose(P.reparametrized_edge_costs(st), [0.0, -1.0, 0.0], atol=1e-12)
+    assert P.lower_bound(st) == pytest.approx(-1.0, abs=1e-12)
+    g = P.WeightedGraph.from_edges(4, [(0, 1, 4.0), (0, 2, -2.0), (0, 3, 1.0), (1, 2, 1.0), (1, 3, 1.0), (2, 3, 7.0)])
+    st = P.DualState(g, g.edges_u, g.edges_v, g.costs, g.num_edges, [[0, 1, 2], [0, 1, 3]], [[0, 1, 3], [0, 2, 4]])
+    P.mp_edge_to_triplets(st)
+    assert st.lam[0, 0] == -2.0 and st.lam[1, 0] == -2.0 and st.lam[0, 1] == 2.0
+    assert P.reparametrized_edge_costs(st)[5] == 7.0
+
+
+def test_errors_raise_before_work():
+    with pytest.raises(ValueError):
+        P.WeightedGraph(3, [0], [0], [1.0])
+    with pytest.raises(ValueError):
+        P.WeightedGraph(3, [0], [3], [1.0])
+    with pytest.raises(ValueError):
+        P.connected_components(3, [(0, 5)])
+    with pytest.raises(ValueError):
+        P.separate_conflicted_cycles(tri(), 2)
+    with pytest.raises(ValueError):
+        P.contraction_step(tri(), "steepest")
+
+
+# ------------------------------------------------ oracle parity at size
+
+def _both(n, u, v, c):
+    return P.WeightedGraph(n, u, v, c), O.Graph(n, u, v, c)
+
+
+@pytest.mark.parametrize("shape", [("grid", 200, 300, 3), ("grid8", 160, 200, 0), ("er", 3000, 0.002, 0)])
+def test_ops_oracle_parity(shape):
+    kind, a, b, s = shape
+    if kind == "grid":
+        n, u, v, c = instances.grid_coo(a, b, s, seed=11)
+    elif kind == "grid8":
+        n, u, v, c = instances.grid8_coo(a, b, strides=(2, 3), seed=11)
+    else:
+        n, u, v, c = instances.random_coo(a, b, seed=11)
+    g, og = _both(n, u, v, c)
+    assert np.array_equal(g.costs, og.costs)
+    assert np.array_equal(P.select_matching(g), O.select_matching(og))
+    assert np.array_equal(P.select_spanning_forest_no_conflicts(g), O.select_spanning_forest_no_conflicts(og))
+    for L in (3, 4, 5):
+        a1, b1 = P.dual._separate(g, L)
+        a2, b2 = O.separate(og, L)
+        assert np.array_equal(a1, a2) and np.array_equal(b1, b2)
+    lengths, nodes = O.separate(og, 5)
+    st = P.dual._triangulate_arrays(g, lengths, nodes)
+    ost = O.triangulate(og, lengths, nodes)
+    assert np.array_equal(st.tri_edges, ost.tri_edges) and np.array_equal(st.edges_u, ost.edges_u)
+    P.message_passing(st, 5)
+    O.message_passing(ost, 5)
+    assert np.array_equal(st.lam, ost.lam)
+    assert close_sum(P.lower_bound(st), O.lower_bound(ost))
+    rep = P.reparametrized_graph(st)
+    orep = O.reparametrized_graph(ost)
+    assert np.array_equal(rep.costs, orep.costs)
+    # contraction on the reparametrized graph
+    g2, f, _ = P.contraction_step(rep, "auto")
+    og2, of, ont, _, _ = O.contraction_step(orep, "auto")
+    assert np.array_equal(f.map, of) and f.num_targets == ont
+    assert np.array_equal(g2.edges_u, og2.edges_u) and np.array_equal(g2.costs, og2.costs)
+
+
+def test_forest_conflict_resolution_exact():
+    # dense positive trees with many in-tree repulsive edges: the sequential
+    # conflict pass (contraction.py:231-284) must be reproduced exactly
+    for seed in range(12):
+        n, u, v, c = instances.random_coo(400, 0.02, seed=seed)
+        c = c + 0.6  # mostly attractive -> big trees, many conflicts
+        g, og = _both(n, u, v, c)
+        assert np.array_equal(P.select_spanning_forest_no_conflicts(g), O.select_spanning_forest_no_conflicts(og))
+    n, u, v, c = instances.grid_coo(120, 150, 2, seed=3)
+    g, og = _both(n, u, v, c + 0.8)
+    assert np.array_equal(P.select_spanning_forest_no_conflicts(g), O.select_spanning_forest_no_conflicts(og))
+
+
+def test_clustering_cost_matches_oracle():
+    n, u, v, c = instances.grid_coo(300, 300, 0, seed=2)
+    g, og = _both(n, u, v, c)
+    lab = np.random.default_rng(0).integers(0, 50, n)
+    assert close_sum(P.clustering_cost(g, lab), O.clustering_cost(og, lab))
