@@ -1,0 +1,353 @@
+"""Benchmark: RAMA primal-dual multicut solve on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--workload c2|c3|c4|c5|c1]
+
+One step = one full PD solve (separation, triangulation, 5 MP iterations,
+contraction rounds, cleanup, objective) of one synthetic instance of the
+named shape.  Default workload: C2 (8-connected 1024x2048 grid + lattice
+strides 2, 3; 2,097,152 nodes / 9,892,581 edges), BASELINE.json configs[1].
+
+* value : edges/s with the canonical COO resident in HBM (rama_solve on
+          device buffers), CUDA events on the solving stream, L2 flushed
+          (256 MiB write) between steps outside the events.
+* e2e   : edges/s through the C ABI with HOST buffers (rama_solve_host:
+          H2D of u, v, c + solve + D2H of labels inside the timed region).
+* N > 1 : one process per GPU (torchrun), each rank solves its own
+          independent instance (seed = rank) and the labels/objectives are
+          gathered over NCCL every step -- weak scaling, no other exchange.
+* --impl reference : the CPU oracle port of the reference solver
+          (oracle/, single-threaded like the reference) on a bounded sample.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CPU_SAMPLE_ROWS = 256  # C2 crop for the CPU baseline: 256 x 2048 (~2.4M edges, ~11 s oracle)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+WORKLOAD_DESC = {
+    "c1": "C1: 4-connected 64x64 grid, N(0,1) costs",
+    "c2": "C2: 8-connected 1024x2048 grid + lattice strides 2,3 (Cityscapes-like), N(0,1) costs",
+    "c3": "C3: 6-connected 3D grid 128x256x256 + stride-2 lattice (connectomics-like), N(0,1) costs",
+    "c4": "C4: Chung-Lu power-law graph, 1M nodes, alpha 2.1, mixed-sign costs",
+    "c5": "C5: one 512x512 4-connected grid instance",
+}
+
+
+def mode_of(workload):
+    return "P" if workload == "c1" else "PD"
+
+
+# ------------------------------------------------------------ CPU oracle
+
+def cpu_sample(workload):
+    """Bounded sample of the workload for the single-threaded CPU oracle."""
+    from paper_2109_01838_b200 import instances
+
+    if workload == "c2":
+        n, u, v, c = instances.grid8_coo(CPU_SAMPLE_ROWS, 2048, strides=(2, 3), seed=0)
+        desc = "C2-shaped crop %dx2048 (+strides 2,3), seed 0, %d edges, full PD solve" % (CPU_SAMPLE_ROWS, u.size)
+    elif workload == "c3":
+        n, u, v, c = instances.grid3d_coo(16, 256, 256, stride=2, seed=0)
+        desc = "C3-shaped crop 16x256x256 (+stride 2), seed 0, %d edges, full PD solve" % u.size
+    elif workload == "c4":
+        n, u, v, c = instances.chung_lu_coo(10_000, 2.1, 260_000, seed=0)
+        desc = "C4-shaped Chung-Lu n=10k (m target 20n), seed 0, full PD solve"
+    else:
+        return instances.make(workload), "full %s instance" % workload
+    return (n, u, v, c), desc
+
+
+def run_oracle(sample, mode):
+    import oracle
+
+    n, u, v, c = sample
+    g = oracle.Graph(n, u, v, c)
+    t0 = time.perf_counter()
+    sol = oracle.solve(g, mode=mode)
+    return time.perf_counter() - t0, g.num_edges, sol
+
+
+def cpu_baseline(workload):
+    sample, desc = cpu_sample(workload)
+    secs, m, _ = run_oracle(sample, mode_of(workload))
+    return {"value": m / secs, "unit": "edges/s", "cores": 1, "kind": "port",
+            "sample": desc + "; %.2f s on 1 host core (oracle/rama_oracle.c, the reference is single-threaded too)"
+            % secs}
+
+
+# --------------------------------------------------------------- clocks
+
+class ClockSampler:
+    def __init__(self, index):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                clk, mx, util = float(f[0]), float(f[1]), float(f[7])
+            except ValueError:
+                continue
+            smax = mx
+            if util > 0:
+                sm.append(clk)
+            for nm, val in zip(names, f[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples_under_load": len(sm)}
+
+
+def peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def traffic_from_profiles(family):
+    """dram bytes per launch of the dominant family from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        d = json.load(fh)
+    return d.get("traffic_bytes_per_call", {}).get(family)
+
+
+# ---------------------------------------------------------------- arms
+
+def reference_arm(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    sample, desc = cpu_sample(args.workload)
+    mode = mode_of(args.workload)
+    import oracle
+    from paper_2109_01838_b200 import instances
+
+    small = instances.grid_coo(64, 64, 0, seed=0)
+    for _ in range(args.warmup):  # warm caches / page in the library
+        oracle.solve(oracle.Graph(*small), mode=mode)
+    times, m = [], 0
+    for _ in range(args.steps):
+        secs, m, _ = run_oracle(sample, mode)
+        times.append(secs)
+    total = sum(times)
+    value = m * args.steps / total
+    line = {
+        "impl": "reference", "metric": "multicut solve throughput (edges/s)", "value": value, "unit": "edges/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD_DESC[args.workload], "mode": mode, "sample": desc},
+        "cpu_baseline": {"value": value, "unit": "edges/s", "cores": 1, "kind": "port", "sample": desc},
+        "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def b200_arm(args):
+    import torch
+
+    rank, local, world = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2109_01838_b200 as P
+    from paper_2109_01838_b200 import _lib, instances
+
+    mode = mode_of(args.workload)
+    cfg = P.SolverConfig(mode=mode)
+    n, u, v, c = instances.make(args.workload, seed=rank)
+    g = P.WeightedGraph(n, u, v, c)  # canonicalised on the GPU (not timed)
+    m = g.num_edges
+    du, dv, dc = g.device()
+    labels = torch.empty(n, dtype=torch.int32, device="cuda")
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    gathered = None
+    if world > 1:
+        gathered = torch.empty(world * n, dtype=torch.int32, device="cuda")
+        objs = torch.empty(world * 2, dtype=torch.float64, device="cuda")
+
+    def step():
+        _, primal, lb, trace = P.solve_device(n, du, dv, dc, m, cfg, labels)
+        if world > 1:  # NCCL gather of labels and objectives (the only exchange)
+            torch.distributed.all_gather_into_tensor(gathered, labels)
+            mine = torch.tensor([primal, lb], dtype=torch.float64, device="cuda")
+            torch.distributed.all_gather_into_tensor(objs, mine)
+        return primal, lb, trace
+
+    for _ in range(args.warmup):
+        step()
+        flush.zero_()
+    barrier()
+    clocks = ClockSampler(local)
+    _lib.profile_enable(True)
+    launches0 = _lib.launches
+    ms = []
+    for _ in range(args.steps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        primal, lb, trace = step()
+        e1.record(stream)
+        e1.synchronize()
+        ms.append(e0.elapsed_time(e1))
+        flush.zero_()
+    barrier()
+    fam = _lib.profile_read()
+    _lib.profile_enable(False)
+    launches = _lib.launches - launches0  # our kernels in the timed region (all steps)
+    clk = clocks.stop()
+    t_local = sum(ms)
+    t = torch.tensor([t_local], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    t_max = float(t.item())
+    value = world * m * args.steps / (t_max / 1e3)
+
+    # end to end through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        hu = torch.from_numpy(g.edges_u.astype(np.int32)).pin_memory().numpy()
+        hv = torch.from_numpy(g.edges_v.astype(np.int32)).pin_memory().numpy()
+        hc = torch.from_numpy(g.costs.astype(np.float64)).pin_memory().numpy()
+        for _ in range(max(1, args.warmup)):
+            P.solve_host(n, hu, hv, hc, cfg)
+        barrier()
+        e_ms = []
+        for _ in range(args.steps):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            lab_h, _, _, _ = P.solve_host(n, hu, hv, hc, cfg)
+            e1.record(stream)
+            e1.synchronize()
+            e_ms.append(e0.elapsed_time(e1))
+            flush.zero_()
+        barrier()
+        te = torch.tensor([sum(e_ms)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+        e2e = {"value": world * m * args.steps / (float(te.item()) / 1e3), "unit": "edges/s",
+               "h2d_bytes_per_step": int(m * (4 + 4 + 8)), "d2h_bytes_per_step": int(n * 4 + 16),
+               "ms_per_step": float(te.item()) / args.steps}
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+
+    # roofline of the dominant kernel family with defined algorithmic bytes
+    peak, peak_src = peak_hbm()
+    cands = {k: vv for k, vv in fam.items() if vv[1] > 0 and vv[0] > 0}
+    dom = max(cands, key=lambda k: cands[k][0]) if cands else None
+    roof = None
+    if dom:
+        f_ms, f_bytes, f_cnt = fam[dom]
+        achieved = f_bytes / (f_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "peak_source": peak_src,
+                "traffic": traffic_from_profiles(dom),
+                "algorithmic_bytes_per_step": f_bytes / args.steps, "ms_per_step": f_ms / args.steps,
+                "share_of_step": f_ms / t_local}
+    families = {k: {"ms_per_step": vv[0] / args.steps, "alg_GB_per_step": vv[1] / args.steps / 1e9,
+                    "scopes_per_step": vv[2] / args.steps} for k, vv in fam.items() if vv[2]}
+
+    gap = None
+    refp = os.path.join(ROOT, "tests", "golden", "c2_reference.json")
+    if args.workload == "c2" and rank == 0 and os.path.exists(refp):
+        with open(refp) as fh:
+            ref = json.load(fh)
+        gap = {"primal_pct": 100.0 * (primal - ref["primal"]) / abs(ref["primal"]),
+               "lb_pct": 100.0 * (lb - ref["lower_bound"]) / abs(ref["lower_bound"]),
+               "reference_primal": ref["primal"], "reference_lb": ref["lower_bound"]}
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.workload)
+
+    line = {
+        "metric": "multicut solve throughput (edges/s)", "value": value, "unit": "edges/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD_DESC[args.workload], "nodes": n, "edges": m, "mode": mode,
+                   "instances_per_step": world, "seed": "rank",
+                   "l2": "inputs %.0f MB > 126 MB L2, and a 256 MiB buffer is written between steps" % (m * 16 / 1e6),
+                   "parallelism": "independent instance per GPU" if world > 1 else "single GPU"},
+        "solve_time_s": t_max / args.steps / 1e3,
+        "objective": {"primal": primal, "lower_bound": lb, "rounds": len(trace), "gap_vs_cpu_reference": gap},
+        "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": launches,
+        "kernel_families": families,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        b200_arm(args)
+
+
+if __name__ == "__main__":
+    main()

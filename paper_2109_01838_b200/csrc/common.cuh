@@ -86,6 +86,7 @@ bool prof_enabled();
 void prof_set(bool on);
 void prof_push(int fam, cudaEvent_t a, cudaEvent_t b, double bytes);
 void prof_read(double* ms, double* bytes, int64_t* count);
+cudaEvent_t prof_event();  // from a recycled pool (no per-scope cudaEventCreate)
 
 struct ProfScope {
   cudaStream_t s;
@@ -94,8 +95,8 @@ struct ProfScope {
   cudaEvent_t a = nullptr, b = nullptr;
   ProfScope(cudaStream_t st, int f, double by = 0.0) : s(st), fam(f), bytes(by) {
     if (prof_enabled()) {
-      cudaEventCreate(&a);
-      cudaEventCreate(&b);
+      a = prof_event();
+      b = prof_event();
       cudaEventRecord(a, s);
     }
   }

@@ -99,79 +99,106 @@ __global__ void k_flag_neg(const double* __restrict__ c, int64_t m, uint8_t* __r
   GRID_STRIDE(i, m) f[i] = c[i] < 0.0;
 }
 
-__global__ void k_separate(const int32_t* __restrict__ NQ, int64_t nq, const int32_t* __restrict__ u,
-                           const int32_t* __restrict__ v, const int32_t* __restrict__ ptr,
-                           const int32_t* __restrict__ adj, int L, int32_t* __restrict__ out_len,
-                           int32_t* __restrict__ out_nodes) {
+__global__ void k_gather_i32(const int32_t* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
+                             int32_t* __restrict__ dst) {
+  GRID_STRIDE(i, n) dst[i] = src[idx[i]];
+}
+
+// Three convergent passes instead of one divergent kernel: every repulsive
+// edge tries the 3-cycle; the misses are compacted and try the 4-cycle; the
+// remaining misses try the 5-cycle.  (One fused kernel made nearly every
+// warp wait for its slowest 5-cycle lane.)
+__global__ void k_sep3(const int32_t* __restrict__ NQ, int64_t nq, const int32_t* __restrict__ u,
+                       const int32_t* __restrict__ v, const int32_t* __restrict__ ptr,
+                       const int32_t* __restrict__ adj, int L, int32_t* __restrict__ out_len,
+                       int32_t* __restrict__ out_nodes, uint8_t* __restrict__ miss) {
   GRID_STRIDE(q, nq) {
+    int32_t e = NQ[q];
+    int32_t a = u[e], b = v[e];
+    int32_t pa = ptr[a], pb = ptr[b];
+    int32_t x = first_common(adj + pa, ptr[a + 1] - pa, adj + pb, ptr[b + 1] - pb);
+    int32_t* row = out_nodes + q * (int64_t)L;
+    if (x >= 0) {
+      out_len[q] = 3;
+      row[0] = a; row[1] = x; row[2] = b;
+      for (int j = 3; j < L; j++) row[j] = 0;
+    } else {
+      out_len[q] = 0;
+      for (int j = 0; j < L; j++) row[j] = 0;
+    }
+    if (miss) miss[q] = (x < 0);
+  }
+}
+
+// px(y) for a level-2 candidate y (y not a, not in N(a)); -1 if y is not at distance 2
+__device__ __forceinline__ int32_t level2_parent(const int32_t* __restrict__ ptr, const int32_t* __restrict__ adj,
+                                                 int32_t a, const int32_t* Na, int32_t la, int32_t y) {
+  if (y == a || in_sorted(Na, la, y)) return -1;
+  return first_common(Na, la, adj + ptr[y], ptr[y + 1] - ptr[y]);
+}
+
+__global__ void k_sep4(const int32_t* __restrict__ Q, int64_t nq, const int32_t* __restrict__ NQ,
+                       const int32_t* __restrict__ u, const int32_t* __restrict__ v,
+                       const int32_t* __restrict__ ptr, const int32_t* __restrict__ adj, int L,
+                       int32_t* __restrict__ out_len, int32_t* __restrict__ out_nodes, uint8_t* __restrict__ miss) {
+  GRID_STRIDE(i, nq) {
+    int32_t q = Q[i];
     int32_t e = NQ[q];
     int32_t a = u[e], b = v[e];
     const int32_t* Na = adj + ptr[a];
     int32_t la = ptr[a + 1] - ptr[a];
-    const int32_t* Nb = adj + ptr[b];
-    int32_t lb = ptr[b + 1] - ptr[b];
-    int32_t* row = out_nodes + q * (int64_t)L;
-    int len = 0;
-    int32_t p1 = -1, p2 = -1, p3 = -1;
-    if (la > 0 && lb > 0) {
-      int32_t x = first_common(Na, la, Nb, lb);
-      if (x >= 0) {
-        len = 3;
-        p1 = x;
-      } else if (L >= 4) {
-        // 4-cycle: best level-2 neighbour of b by (px(y), y)
-        int32_t bp = 0x7fffffff, by = 0x7fffffff;
-        for (int32_t i = 0; i < lb; i++) {
-          int32_t y = Nb[i];
-          if (y == a || in_sorted(Na, la, y)) continue;
-          int32_t py = first_common(Na, la, adj + ptr[y], ptr[y + 1] - ptr[y]);
-          if (py < 0) continue;
-          if (py < bp || (py == bp && y < by)) { bp = py; by = y; }
-        }
-        if (bp != 0x7fffffff) {
-          len = 4;
-          p1 = bp;
-          p2 = by;
-        } else if (L >= 5) {
-          // 5-cycle: level-3 neighbours z of b ranked by (px(py(z)), py(z), z)
-          int32_t bx = 0x7fffffff, byy = 0x7fffffff, bz = 0x7fffffff;
-          for (int32_t i = 0; i < lb; i++) {
-            int32_t z = Nb[i];
-            if (z == a || in_sorted(Na, la, z)) continue;
-            const int32_t* Nz = adj + ptr[z];
-            int32_t lz = ptr[z + 1] - ptr[z];
-            if (first_common(Na, la, Nz, lz) >= 0) continue;  // z at distance 2
-            int32_t zx = 0x7fffffff, zy = 0x7fffffff;
-            for (int32_t j = 0; j < lz; j++) {
-              int32_t y = Nz[j];
-              if (y == a || in_sorted(Na, la, y)) continue;
-              int32_t py = first_common(Na, la, adj + ptr[y], ptr[y + 1] - ptr[y]);
-              if (py < 0) continue;
-              if (py < zx || (py == zx && y < zy)) { zx = py; zy = y; }
-            }
-            if (zx == 0x7fffffff) continue;
-            if (zx < bx || (zx == bx && (zy < byy || (zy == byy && z < bz)))) {
-              bx = zx; byy = zy; bz = z;
-            }
-          }
-          if (bx != 0x7fffffff) {
-            len = 5;
-            p1 = bx;
-            p2 = byy;
-            p3 = bz;
-          }
-        }
+    int32_t pb = ptr[b], lb = ptr[b + 1] - pb;
+    int32_t bp = 0x7fffffff, by = 0x7fffffff;
+    for (int32_t k = 0; k < lb; k++) {
+      int32_t y = adj[pb + k];
+      int32_t py = level2_parent(ptr, adj, a, Na, la, y);
+      if (py < 0) continue;
+      if (py < bp || (py == bp && y < by)) { bp = py; by = y; }
+    }
+    bool found = bp != 0x7fffffff;
+    if (found) {
+      int32_t* row = out_nodes + q * (int64_t)L;
+      out_len[q] = 4;
+      row[0] = a; row[1] = bp; row[2] = by; row[3] = b;
+    }
+    if (miss) miss[i] = !found;
+  }
+}
+
+__global__ void k_sep5(const int32_t* __restrict__ Q, int64_t nq, const int32_t* __restrict__ NQ,
+                       const int32_t* __restrict__ u, const int32_t* __restrict__ v,
+                       const int32_t* __restrict__ ptr, const int32_t* __restrict__ adj, int L,
+                       int32_t* __restrict__ out_len, int32_t* __restrict__ out_nodes) {
+  GRID_STRIDE(i, nq) {
+    int32_t q = Q[i];
+    int32_t e = NQ[q];
+    int32_t a = u[e], b = v[e];
+    const int32_t* Na = adj + ptr[a];
+    int32_t la = ptr[a + 1] - ptr[a];
+    int32_t pb = ptr[b], lb = ptr[b + 1] - pb;
+    // level-3 neighbours z of b ranked by (px(py(z)), py(z), z)
+    int32_t bx = 0x7fffffff, byy = 0x7fffffff, bz = 0x7fffffff;
+    for (int32_t k = 0; k < lb; k++) {
+      int32_t z = adj[pb + k];
+      if (z == a || in_sorted(Na, la, z)) continue;
+      int32_t pz = ptr[z], lz = ptr[z + 1] - pz;
+      if (first_common(Na, la, adj + pz, lz) >= 0) continue;  // z at distance 2
+      int32_t zx = 0x7fffffff, zy = 0x7fffffff;
+      for (int32_t j = 0; j < lz; j++) {
+        int32_t y = adj[pz + j];
+        int32_t py = level2_parent(ptr, adj, a, Na, la, y);
+        if (py < 0) continue;
+        if (py < zx || (py == zx && y < zy)) { zx = py; zy = y; }
+      }
+      if (zx == 0x7fffffff) continue;
+      if (zx < bx || (zx == bx && (zy < byy || (zy == byy && z < bz)))) {
+        bx = zx; byy = zy; bz = z;
       }
     }
-    out_len[q] = len;
-    for (int j = 0; j < L; j++) row[j] = 0;
-    if (len >= 3) {
-      row[0] = a;
-      row[1] = p1;
-      if (len == 3) row[2] = b;
-      if (len >= 4) { row[2] = p2; }
-      if (len == 4) row[3] = b;
-      if (len == 5) { row[3] = p3; row[4] = b; }
+    if (bx != 0x7fffffff) {
+      int32_t* row = out_nodes + q * (int64_t)L;
+      out_len[q] = 5;
+      row[0] = a; row[1] = bx; row[2] = byy; row[3] = bz; row[4] = b;
     }
   }
 }
@@ -196,7 +223,22 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
     out.nodes.zero();
     return;
   }
-  RAMA_KERNEL(ctx, k_separate, nq, NQ.p, nq, g.u, g.v, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p);
+  Buf<uint8_t> miss(nq, ctx);
+  RAMA_KERNEL(ctx, k_sep3, nq, NQ.p, nq, g.u, g.v, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p,
+              L >= 4 ? miss.p : (uint8_t*)nullptr);
+  if (L < 4) return;
+  Buf<int32_t> Q2;
+  int64_t n2 = compact_indices(ctx, miss.p, nq, Q2);
+  if (n2 == 0) return;
+  RAMA_KERNEL(ctx, k_sep4, n2, Q2.p, n2, NQ.p, g.u, g.v, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p,
+              L >= 5 ? miss.p : (uint8_t*)nullptr);
+  if (L < 5) return;
+  Buf<int32_t> I3;
+  int64_t n3 = compact_indices(ctx, miss.p, n2, I3);
+  if (n3 == 0) return;
+  Buf<int32_t> Q3(n3, ctx);
+  RAMA_KERNEL(ctx, k_gather_i32, n3, Q2.p, I3.p, n3, Q3.p);
+  RAMA_KERNEL(ctx, k_sep5, n3, Q3.p, n3, NQ.p, g.u, g.v, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p);
 }
 
 // --------------------------------------------------------- triangulation

@@ -141,9 +141,20 @@ __global__ void k_cc_hook(const int32_t* __restrict__ su, const int32_t* __restr
   GRID_STRIDE(i, k) uf_union(parent, su[i], sv[i]);
 }
 
+// read-only find: a flatten pass must not path-halve, or another thread's
+// halving store can land after `parent[x] = root` and leave x pointing at a
+// non-root ancestor.
+__device__ __forceinline__ int32_t uf_root(const int32_t* p, int32_t x) {
+  while (true) {
+    int32_t px = __ldcg(p + x);
+    if (px == x) return x;
+    x = px;
+  }
+}
+
 __global__ void k_cc_flatten(int32_t* parent, int64_t n, int32_t* __restrict__ is_root) {
   GRID_STRIDE(x, n) {
-    int32_t r = uf_find(parent, (int32_t)x);
+    int32_t r = uf_root(parent, (int32_t)x);
     parent[x] = r;
     is_root[x] = (r == x);
   }

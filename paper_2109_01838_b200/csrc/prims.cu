@@ -56,6 +56,8 @@ double g_prof_ms[kNumFamilies] = {0};
 double g_prof_bytes[kNumFamilies] = {0};
 int64_t g_prof_count[kNumFamilies] = {0};
 
+std::vector<cudaEvent_t> g_event_pool;
+
 void prof_drain() {
   for (auto& r : g_prof_recs) {
     float ms = 0.f;
@@ -64,12 +66,25 @@ void prof_drain() {
     g_prof_ms[r.fam] += ms;
     g_prof_bytes[r.fam] += r.bytes;
     g_prof_count[r.fam] += 1;
-    cudaEventDestroy(r.a);
-    cudaEventDestroy(r.b);
+    g_event_pool.push_back(r.a);
+    g_event_pool.push_back(r.b);
   }
   g_prof_recs.clear();
 }
 }  // namespace
+
+cudaEvent_t prof_event() {
+  if (g_event_pool.empty()) {
+    for (int i = 0; i < 256; i++) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      g_event_pool.push_back(e);
+    }
+  }
+  cudaEvent_t e = g_event_pool.back();
+  g_event_pool.pop_back();
+  return e;
+}
 
 bool prof_enabled() { return g_prof; }
 
@@ -225,13 +240,19 @@ __global__ void k_bucket_scatter(const int32_t* __restrict__ row, const uint64_t
 constexpr int kSmallRow = 32;
 
 // insertion sort of each short row; long rows are flagged for CUB
+// Rows <= kSmallRow: one thread, insertion sort.  Longer rows are appended
+// to a work list (atomic order does not matter: each row is sorted on its
+// own unique keys).
 __global__ void k_sort_rows_small(const int32_t* __restrict__ ptr, int64_t R, uint64_t* __restrict__ key,
-                                  int32_t* __restrict__ src, uint8_t* __restrict__ big) {
+                                  int32_t* __restrict__ src, int32_t* __restrict__ big_list,
+                                  int32_t* __restrict__ counters) {
   GRID_STRIDE(r, R) {
     int32_t b = ptr[r], e = ptr[r + 1];
     int32_t len = e - b;
-    big[r] = len > kSmallRow;
-    if (len < 2 || len > kSmallRow) continue;
+    if (len > kSmallRow) {
+      big_list[atomicAdd(counters, 1)] = (int32_t)r;
+      continue;
+    }
     for (int32_t i = b + 1; i < e; i++) {
       uint64_t k = key[i];
       int32_t s = src[i];
@@ -247,16 +268,64 @@ __global__ void k_sort_rows_small(const int32_t* __restrict__ ptr, int64_t R, ui
   }
 }
 
+constexpr int kBlockRow = 4096;  // bitonic sort in shared memory: 4096 x 12 B = 48 KB
+
+// one block per listed row: bitonic sort of (key, src) in shared memory;
+// rows longer than kBlockRow go to the huge list (CUB)
+__global__ void __launch_bounds__(512) k_sort_rows_block(const int32_t* __restrict__ ptr,
+                                                         const int32_t* __restrict__ big_list,
+                                                         int32_t* __restrict__ counters, uint64_t* __restrict__ key,
+                                                         int32_t* __restrict__ src, int32_t* __restrict__ huge_list) {
+  __shared__ uint64_t sk[kBlockRow];
+  __shared__ int32_t ss[kBlockRow];
+  int32_t nbig = counters[0];
+  for (int32_t bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
+    int32_t r = big_list[bi];
+    int32_t b = ptr[r], len = ptr[r + 1] - b;
+    if (len > kBlockRow) {
+      if (threadIdx.x == 0) huge_list[atomicAdd(counters + 1, 1)] = r;
+      continue;
+    }
+    int32_t P = 64;
+    while (P < len) P <<= 1;
+    for (int32_t i = threadIdx.x; i < P; i += blockDim.x) {
+      if (i < len) { sk[i] = key[b + i]; ss[i] = src[b + i]; }
+      else { sk[i] = ~0ULL; ss[i] = 0x7fffffff; }
+    }
+    __syncthreads();
+    for (int32_t k = 2; k <= P; k <<= 1) {
+      for (int32_t j = k >> 1; j > 0; j >>= 1) {
+        for (int32_t i = threadIdx.x; i < P; i += blockDim.x) {
+          int32_t ixj = i ^ j;
+          if (ixj > i) {
+            bool up = (i & k) == 0;
+            uint64_t a = sk[i], c = sk[ixj];
+            if ((a > c) == up) {
+              sk[i] = c; sk[ixj] = a;
+              int32_t t = ss[i]; ss[i] = ss[ixj]; ss[ixj] = t;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (int32_t i = threadIdx.x; i < len; i += blockDim.x) {
+      key[b + i] = sk[i];
+      src[b + i] = ss[i];
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void k_big_lens(const int32_t* __restrict__ rows, int64_t nb, const int32_t* __restrict__ ptr,
                            int32_t* __restrict__ len) {
   GRID_STRIDE(i, nb) len[i] = ptr[rows[i] + 1] - ptr[rows[i]];
 }
 
-// move big rows to / from a contiguous staging area
+// move huge rows to / from a contiguous staging area
 __global__ void k_big_move(const int32_t* __restrict__ rows, int64_t nb, const int32_t* __restrict__ ptr,
                            const int32_t* __restrict__ off, uint64_t* __restrict__ key, int32_t* __restrict__ src,
                            uint64_t* __restrict__ skey, int32_t* __restrict__ ssrc, bool to_stage) {
-  // one block per big row
   for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
     int32_t r = rows[b];
     int32_t base = ptr[r], len = ptr[r + 1] - base, o = off[b];
@@ -283,18 +352,26 @@ void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint6
   RAMA_KERNEL(ctx, k_bucket_scatter, N, row, key, N, cnt.p, out.key.p, out.src.p,
               want_row ? out.row.p : (int32_t*)nullptr);
   if (sort_rows == 0) return;
-  Buf<uint8_t> big(sort_rows, ctx);
-  RAMA_KERNEL(ctx, k_sort_rows_small, sort_rows, out.row_ptr.p, sort_rows, out.key.p, out.src.p, big.p);
-  Buf<int32_t> brows;
-  int64_t nb = compact_indices(ctx, big.p, sort_rows, brows);
+  Buf<int32_t> lists(2 * sort_rows + 2, ctx);  // big list | huge list | counters
+  int32_t* big_list = lists.p;
+  int32_t* huge_list = lists.p + sort_rows;
+  int32_t* counters = lists.p + 2 * sort_rows;
+  RAMA_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(int32_t), ctx.s));
+  RAMA_KERNEL(ctx, k_sort_rows_small, sort_rows, out.row_ptr.p, sort_rows, out.key.p, out.src.p, big_list, counters);
+  unsigned gb = (unsigned)std::min<int64_t>(std::max<int64_t>(sort_rows / 64, 1), 148 * 4);
+  k_sort_rows_block<<<gb, 512, 0, ctx.s>>>(out.row_ptr.p, big_list, counters, out.key.p, out.src.p, huge_list);
+  RAMA_LAUNCH_CHECK();
+  ctx.launches++;
+  int32_t nb = read_scalar(ctx, counters + 1);
   if (nb == 0) return;
+  // rare (power-law hubs): CUB segmented sort of the rows > kBlockRow
   Buf<int32_t> blen(nb, ctx), boff(nb + 1, ctx);
-  RAMA_KERNEL(ctx, k_big_lens, nb, brows.p, nb, out.row_ptr.p, blen.p);
+  RAMA_KERNEL(ctx, k_big_lens, nb, huge_list, nb, out.row_ptr.p, blen.p);
   int64_t tot = exclusive_scan(ctx, blen.p, boff.p, nb, true);
   Buf<uint64_t> k1(tot, ctx), k2(tot, ctx);
   Buf<int32_t> s1(tot, ctx), s2(tot, ctx);
   unsigned g = (unsigned)std::min<int64_t>(nb, 4096);
-  k_big_move<<<g, kBlock, 0, ctx.s>>>(brows.p, nb, out.row_ptr.p, boff.p, out.key.p, out.src.p, k1.p, s1.p, true);
+  k_big_move<<<g, kBlock, 0, ctx.s>>>(huge_list, nb, out.row_ptr.p, boff.p, out.key.p, out.src.p, k1.p, s1.p, true);
   RAMA_LAUNCH_CHECK();
   size_t tb = 0;
   RAMA_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, tb, k1.p, k2.p, s1.p, s2.p, (int)tot, (int)nb, boff.p,
@@ -302,7 +379,7 @@ void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint6
   Buf<uint8_t> tmp(tb, ctx);
   RAMA_CUDA(cub::DeviceSegmentedSort::SortPairs(tmp.p, tb, k1.p, k2.p, s1.p, s2.p, (int)tot, (int)nb, boff.p,
                                                 boff.p + 1, ctx.s));
-  k_big_move<<<g, kBlock, 0, ctx.s>>>(brows.p, nb, out.row_ptr.p, boff.p, out.key.p, out.src.p, k2.p, s2.p, false);
+  k_big_move<<<g, kBlock, 0, ctx.s>>>(huge_list, nb, out.row_ptr.p, boff.p, out.key.p, out.src.p, k2.p, s2.p, false);
   RAMA_LAUNCH_CHECK();
   ctx.launches += 3;
 }

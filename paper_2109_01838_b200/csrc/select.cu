@@ -211,8 +211,17 @@ __global__ void k_bv_hook(int64_t n, const uint32_t* __restrict__ best, const in
   }
 }
 
+// read-only find for flattening (no path halving, see graph.cu k_cc_flatten)
 __global__ void k_flatten(int32_t* comp, int64_t n) {
-  GRID_STRIDE(x, n) comp[x] = sf_find(comp, (int32_t)x);
+  GRID_STRIDE(x, n) {
+    int32_t r = (int32_t)x;
+    while (true) {
+      int32_t p = __ldcg(comp + r);
+      if (p == r) break;
+      r = p;
+    }
+    comp[x] = r;
+  }
 }
 
 // repulsive edges whose endpoints share a tree
