@@ -164,13 +164,23 @@ inline unsigned grid_for(int64_t work, int block = kBlock) {
 // Grid-stride launch helper: caps the grid at a multiple of the SM count.
 unsigned capped_grid(int64_t work, int block = kBlock);
 
+// RAMA_TRACE=1 in the environment: print every launch and synchronise after
+// it (debugging hangs / faults; never set for timing)
+bool trace_enabled();   // RAMA_TRACE=1: print + sync after every launch
+bool trace_print();     // RAMA_TRACE=1 or 2: print launches and sync points
+
 #define RAMA_KERNEL(ctx, kernel, work, ...)                                           \
   do {                                                                                \
     int64_t _w = (int64_t)(work);                                                     \
     if (_w > 0) {                                                                     \
+      if (::rama::trace_print()) {                                                    \
+        fprintf(stderr, "[rama] %s work=%lld\n", #kernel, (long long)_w);             \
+        fflush(stderr);                                                               \
+      }                                                                               \
       kernel<<<::rama::capped_grid(_w), ::rama::kBlock, 0, (ctx).s>>>(__VA_ARGS__);   \
       RAMA_LAUNCH_CHECK();                                                            \
       (ctx).launches++;                                                               \
+      if (::rama::trace_enabled()) (ctx).sync();                                      \
     }                                                                                 \
   } while (0)
 
@@ -181,6 +191,10 @@ unsigned capped_grid(int64_t work, int block = kBlock);
 template <class T>
 T read_scalar(Ctx& ctx, const T* dev) {
   static_assert(sizeof(T) <= 8, "scalar");
+  if (trace_print()) {
+    fprintf(stderr, "[rama] sync\n");
+    fflush(stderr);
+  }
   RAMA_CUDA(cudaMemcpyAsync(ctx.pinned, dev, sizeof(T), cudaMemcpyDeviceToHost, ctx.s));
   ctx.sync();
   T v;
@@ -217,8 +231,8 @@ struct BucketSorted {
   Buf<uint64_t> key;     // N
   Buf<int32_t> src;      // N
 };
-// Only rows < sort_rows are sorted (default all); later rows keep scatter
-// order (used to park dropped items in a trailing bucket).
+// Items with row < 0 are dropped.  Only rows < sort_rows are sorted
+// (default all); later rows keep scatter order.
 void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint64_t* key, BucketSorted& out,
                  bool want_row = true, int64_t sort_rows = -1);
 

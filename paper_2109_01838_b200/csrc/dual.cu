@@ -137,31 +137,70 @@ __device__ __forceinline__ int32_t level2_parent(const int32_t* __restrict__ ptr
   return first_common(Na, la, adj + ptr[y], ptr[y + 1] - ptr[y]);
 }
 
+// 4- and 5-cycle passes: a group of kSepLanes lanes per repulsive edge; the
+// lanes split the candidate neighbours and the group takes the
+// lexicographic argmin with shuffles (keys packed as (parent << 32 | node)).
+constexpr int kSepLanes = 8;
+
+__device__ __forceinline__ uint64_t group_min(uint64_t x) {
+#pragma unroll
+  for (int o = kSepLanes / 2; o > 0; o >>= 1) {
+    uint64_t y = __shfl_xor_sync(0xffffffffu, x, o, kSepLanes);
+    x = y < x ? y : x;
+  }
+  return x;
+}
+
+__device__ __forceinline__ int32_t warp_max(int32_t x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = max(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
+
+__device__ __forceinline__ uint64_t pack2(int32_t hi, int32_t lo) {
+  return ((uint64_t)(uint32_t)hi << 32) | (uint64_t)(uint32_t)lo;
+}
+
 __global__ void k_sep4(const int32_t* __restrict__ Q, int64_t nq, const int32_t* __restrict__ NQ,
                        const int32_t* __restrict__ u, const int32_t* __restrict__ v,
                        const int32_t* __restrict__ ptr, const int32_t* __restrict__ adj, int L,
                        int32_t* __restrict__ out_len, int32_t* __restrict__ out_nodes, uint8_t* __restrict__ miss) {
-  GRID_STRIDE(i, nq) {
-    int32_t q = Q[i];
-    int32_t e = NQ[q];
-    int32_t a = u[e], b = v[e];
-    const int32_t* Na = adj + ptr[a];
-    int32_t la = ptr[a + 1] - ptr[a];
-    int32_t pb = ptr[b], lb = ptr[b + 1] - pb;
-    int32_t bp = 0x7fffffff, by = 0x7fffffff;
-    for (int32_t k = 0; k < lb; k++) {
-      int32_t y = adj[pb + k];
-      int32_t py = level2_parent(ptr, adj, a, Na, la, y);
-      if (py < 0) continue;
-      if (py < bp || (py == bp && y < by)) { bp = py; by = y; }
+  const int g = threadIdx.x % kSepLanes;
+  const int64_t per_warp = 32 / kSepLanes;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = warp * per_warp; base < nq; base += nwarps * per_warp) {  // warp-uniform
+    const int64_t i = base + (threadIdx.x & 31) / kSepLanes;
+    bool live = i < nq;
+    uint64_t best = ~0ULL;
+    int32_t a = 0, b = 0, q = 0;
+    if (live) {
+      q = Q[i];
+      int32_t e = NQ[q];
+      a = u[e];
+      b = v[e];
+      const int32_t* Na = adj + ptr[a];
+      int32_t la = ptr[a + 1] - ptr[a];
+      int32_t pb = ptr[b], lb = ptr[b + 1] - pb;
+      for (int32_t k = g; k < lb; k += kSepLanes) {
+        int32_t y = adj[pb + k];
+        int32_t py = level2_parent(ptr, adj, a, Na, la, y);
+        if (py >= 0) {
+          uint64_t key = pack2(py, y);
+          best = key < best ? key : best;
+        }
+      }
     }
-    bool found = bp != 0x7fffffff;
-    if (found) {
-      int32_t* row = out_nodes + q * (int64_t)L;
-      out_len[q] = 4;
-      row[0] = a; row[1] = bp; row[2] = by; row[3] = b;
+    best = group_min(best);
+    if (live && g == 0) {
+      bool found = best != ~0ULL;
+      if (found) {
+        int32_t* row = out_nodes + q * (int64_t)L;
+        out_len[q] = 4;
+        row[0] = a; row[1] = (int32_t)(best >> 32); row[2] = (int32_t)(uint32_t)best; row[3] = b;
+      }
+      if (miss) miss[i] = !found;
     }
-    if (miss) miss[i] = !found;
   }
 }
 
@@ -169,36 +208,66 @@ __global__ void k_sep5(const int32_t* __restrict__ Q, int64_t nq, const int32_t*
                        const int32_t* __restrict__ u, const int32_t* __restrict__ v,
                        const int32_t* __restrict__ ptr, const int32_t* __restrict__ adj, int L,
                        int32_t* __restrict__ out_len, int32_t* __restrict__ out_nodes) {
-  GRID_STRIDE(i, nq) {
-    int32_t q = Q[i];
-    int32_t e = NQ[q];
-    int32_t a = u[e], b = v[e];
-    const int32_t* Na = adj + ptr[a];
-    int32_t la = ptr[a + 1] - ptr[a];
-    int32_t pb = ptr[b], lb = ptr[b + 1] - pb;
-    // level-3 neighbours z of b ranked by (px(py(z)), py(z), z)
-    int32_t bx = 0x7fffffff, byy = 0x7fffffff, bz = 0x7fffffff;
-    for (int32_t k = 0; k < lb; k++) {
-      int32_t z = adj[pb + k];
-      if (z == a || in_sorted(Na, la, z)) continue;
-      int32_t pz = ptr[z], lz = ptr[z + 1] - pz;
-      if (first_common(Na, la, adj + pz, lz) >= 0) continue;  // z at distance 2
-      int32_t zx = 0x7fffffff, zy = 0x7fffffff;
-      for (int32_t j = 0; j < lz; j++) {
-        int32_t y = adj[pz + j];
-        int32_t py = level2_parent(ptr, adj, a, Na, la, y);
-        if (py < 0) continue;
-        if (py < zx || (py == zx && y < zy)) { zx = py; zy = y; }
+  const int g = threadIdx.x % kSepLanes;
+  const int64_t per_warp = 32 / kSepLanes;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = warp * per_warp; base < nq; base += nwarps * per_warp) {  // warp-uniform
+    const int64_t i = base + (threadIdx.x & 31) / kSepLanes;
+    bool live = i < nq;
+    int32_t a = 0, b = 0, q = 0, la = 0, pb = 0, lb = 0;
+    const int32_t* Na = adj;
+    if (live) {
+      q = Q[i];
+      int32_t e = NQ[q];
+      a = u[e];
+      b = v[e];
+      Na = adj + ptr[a];
+      la = ptr[a + 1] - ptr[a];
+      pb = ptr[b];
+      lb = ptr[b + 1] - pb;
+    }
+    // level-3 neighbours z of b ranked by (px(py(z)), py(z), z); each z's
+    // best level-2 neighbour py(z) is a group argmin over N(z)
+    uint64_t bx_y = ~0ULL;
+    int32_t bz = 0x7fffffff;
+    // trip counts are warp-uniform: the group shuffles below use the full mask
+    int32_t lbmax = warp_max(lb);
+    for (int32_t k = 0; k < lbmax; k++) {
+      bool zok = live && k < lb;
+      int32_t z = zok ? adj[pb + k] : 0;
+      int32_t pz = 0, lz = 0;
+      if (zok) {
+        if (z == a || in_sorted(Na, la, z)) zok = false;
       }
-      if (zx == 0x7fffffff) continue;
-      if (zx < bx || (zx == bx && (zy < byy || (zy == byy && z < bz)))) {
-        bx = zx; byy = zy; bz = z;
+      if (zok) {
+        pz = ptr[z];
+        lz = ptr[z + 1] - pz;
+        if (first_common(Na, la, adj + pz, lz) >= 0) zok = false;  // z at distance 2
+      }
+      uint64_t zbest = ~0ULL;
+      int32_t lzmax = warp_max(zok ? lz : 0);
+      for (int32_t j0 = 0; j0 < lzmax; j0 += kSepLanes) {
+        int32_t j = j0 + g;
+        if (zok && j < lz) {
+          int32_t y = adj[pz + j];
+          int32_t py = level2_parent(ptr, adj, a, Na, la, y);
+          if (py >= 0) {
+            uint64_t key = pack2(py, y);
+            zbest = key < zbest ? key : zbest;
+          }
+        }
+      }
+      zbest = group_min(zbest);
+      if (zok && zbest != ~0ULL && (zbest < bx_y || (zbest == bx_y && z < bz))) {
+        bx_y = zbest;
+        bz = z;
       }
     }
-    if (bx != 0x7fffffff) {
+    if (live && g == 0 && bx_y != ~0ULL) {
       int32_t* row = out_nodes + q * (int64_t)L;
       out_len[q] = 5;
-      row[0] = a; row[1] = bx; row[2] = byy; row[3] = bz; row[4] = b;
+      row[0] = a; row[1] = (int32_t)(bx_y >> 32); row[2] = (int32_t)(uint32_t)bx_y; row[3] = bz; row[4] = b;
     }
   }
 }
@@ -230,7 +299,7 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
   Buf<int32_t> Q2;
   int64_t n2 = compact_indices(ctx, miss.p, nq, Q2);
   if (n2 == 0) return;
-  RAMA_KERNEL(ctx, k_sep4, n2, Q2.p, n2, NQ.p, g.u, g.v, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p,
+  RAMA_KERNEL(ctx, k_sep4, n2 * kSepLanes, Q2.p, n2, NQ.p, g.u, g.v, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p,
               L >= 5 ? miss.p : (uint8_t*)nullptr);
   if (L < 5) return;
   Buf<int32_t> I3;
@@ -238,7 +307,7 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
   if (n3 == 0) return;
   Buf<int32_t> Q3(n3, ctx);
   RAMA_KERNEL(ctx, k_gather_i32, n3, Q2.p, I3.p, n3, Q3.p);
-  RAMA_KERNEL(ctx, k_sep5, n3, Q3.p, n3, NQ.p, g.u, g.v, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p);
+  RAMA_KERNEL(ctx, k_sep5, n3 * kSepLanes, Q3.p, n3, NQ.p, g.u, g.v, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p);
 }
 
 // --------------------------------------------------------- triangulation

@@ -6,7 +6,7 @@
 // segment by source edge index reproduces numpy's stable lexsort, and the
 // segment sum reproduces np.add.reduceat's x0 + pairwise(x[1:]) order, so
 // contracted costs are bit-identical to the reference (contraction.py:155-162).
-// Merged (f(u) == f(v)) edges go to an extra bucket R = n' and are skipped,
+// Merged (f(u) == f(v)) edges get row -1 and are dropped by the bucket sort,
 // which avoids a separate compaction pass.
 #include "internal.h"
 
@@ -192,7 +192,7 @@ __global__ void k_contract_prep(const int32_t* __restrict__ u, const int32_t* __
   GRID_STRIDE(i, m) {
     int32_t a = f[u[i]], b = f[v[i]];
     if (a == b) {
-      row[i] = n_out;  // parked in the extra bucket
+      row[i] = -1;  // merged edge: dropped by the bucket sort, joined mass
       key[i] = (uint64_t)i;
       if (jc) jc[i] = c[i];
     } else {
@@ -222,11 +222,8 @@ Graph contract(Ctx& ctx, const GraphView& g, const int32_t* map, int64_t n_targe
               joined ? jc.p : (double*)nullptr);
   if (joined) *joined = device_sum(ctx, jc.p, m);
   BucketSorted bs;
-  bucket_sort(ctx, n_targets + 1, m, row.p, key.p, bs, true, n_targets);
-  int64_t limit = 0;
-  RAMA_CUDA(cudaMemcpyAsync(ctx.pinned, bs.row_ptr.p + n_targets, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx.s));
-  ctx.sync();
-  limit = *(int32_t*)ctx.pinned;
+  bucket_sort(ctx, n_targets, m, row.p, key.p, bs, true);
+  int64_t limit = read_scalar(ctx, bs.row_ptr.p + n_targets);
   Graph out = reduce_sorted(ctx, n_targets, limit, bs, g.c);
   prof.add_bytes(16.0 * (double)out.m);
   return out;

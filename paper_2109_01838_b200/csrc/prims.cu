@@ -112,6 +112,18 @@ void prof_read(double* ms, double* bytes, int64_t* count) {
   }
 }
 
+static int trace_level() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RAMA_TRACE");
+    v = (e && e[0] >= '1' && e[0] <= '9') ? e[0] - '0' : 0;
+  }
+  return v;
+}
+
+bool trace_enabled() { return trace_level() == 1; }
+bool trace_print() { return trace_level() >= 1; }
+
 unsigned capped_grid(int64_t work, int block) {
   int64_t g = (work + block - 1) / block;
   int64_t cap = (int64_t)(g_num_sms > 0 ? g_num_sms : 148) * 16;  // 16 x 256 threads per SM
@@ -221,16 +233,36 @@ void row_ptr_from_sorted(Ctx& ctx, const int32_t* u, int64_t m, int64_t n, int32
 
 // ---------------------------------------------------------- bucket sort
 
-__global__ void k_bucket_count(const int32_t* __restrict__ row, int64_t N, int32_t* __restrict__ cnt) {
-  GRID_STRIDE(i, N) atomicAdd(&cnt[row[i]], 1);
+// Warp-aggregated histogram: lanes of a warp that hit the same row share
+// one atomicAdd (__match_any_sync), and every item records its offset
+// inside its row so the scatter pass needs no atomics.  Items with row < 0
+// are dropped (used by contraction for merged edges).
+__global__ void k_bucket_count(const int32_t* __restrict__ row, int64_t N, int32_t* __restrict__ cnt,
+                               int32_t* __restrict__ off) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < N; base += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = base + threadIdx.x;
+    int32_t r = i < N ? row[i] : -1;
+    unsigned active = __ballot_sync(0xffffffffu, r >= 0);
+    if (r >= 0) {
+      unsigned peers = __match_any_sync(active, r);
+      int leader = __ffs(peers) - 1;
+      int rank = __popc(peers & ((1u << lane) - 1u));
+      int32_t b = 0;
+      if (lane == leader) b = atomicAdd(&cnt[r], __popc(peers));
+      b = __shfl_sync(peers, b, leader);
+      off[i] = b + rank;
+    }
+  }
 }
 
-__global__ void k_bucket_scatter(const int32_t* __restrict__ row, const uint64_t* __restrict__ key, int64_t N,
-                                 int32_t* __restrict__ cursor, uint64_t* __restrict__ okey,
-                                 int32_t* __restrict__ osrc, int32_t* __restrict__ orow) {
+__global__ void k_bucket_scatter(const int32_t* __restrict__ row, const uint64_t* __restrict__ key,
+                                 const int32_t* __restrict__ off, int64_t N, const int32_t* __restrict__ ptr,
+                                 uint64_t* __restrict__ okey, int32_t* __restrict__ osrc, int32_t* __restrict__ orow) {
   GRID_STRIDE(i, N) {
     int32_t r = row[i];
-    int32_t p = atomicAdd(&cursor[r], 1);
+    if (r < 0) continue;
+    int32_t p = ptr[r] + off[i];
     okey[p] = key[i];
     osrc[p] = (int32_t)i;
     if (orow) orow[p] = r;
@@ -239,7 +271,34 @@ __global__ void k_bucket_scatter(const int32_t* __restrict__ row, const uint64_t
 
 constexpr int kSmallRow = 32;
 
-// insertion sort of each short row; long rows are flagged for CUB
+#define RAMA_CE(i, j)                                    \
+  if (k[j] < k[i]) {                                     \
+    uint64_t tk = k[i]; k[i] = k[j]; k[j] = tk;          \
+    int32_t ts = sv[i]; sv[i] = sv[j]; sv[j] = ts;       \
+  }
+
+// rows of 2..8 items: Batcher odd-even merge network in registers
+__device__ __forceinline__ void sort8_regs(uint64_t* __restrict__ key, int32_t* __restrict__ src, int32_t b,
+                                           int32_t len) {
+  uint64_t k[8];
+  int32_t sv[8];
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    k[i] = i < len ? key[b + i] : ~0ULL;
+    sv[i] = i < len ? src[b + i] : 0;
+  }
+  RAMA_CE(0, 1) RAMA_CE(2, 3) RAMA_CE(4, 5) RAMA_CE(6, 7)
+  RAMA_CE(0, 2) RAMA_CE(1, 3) RAMA_CE(4, 6) RAMA_CE(5, 7)
+  RAMA_CE(1, 2) RAMA_CE(5, 6)
+  RAMA_CE(0, 4) RAMA_CE(1, 5) RAMA_CE(2, 6) RAMA_CE(3, 7)
+  RAMA_CE(2, 4) RAMA_CE(3, 5)
+  RAMA_CE(1, 2) RAMA_CE(3, 4) RAMA_CE(5, 6)
+#pragma unroll
+  for (int i = 0; i < 8; i++)
+    if (i < len) { key[b + i] = k[i]; src[b + i] = sv[i]; }
+}
+#undef RAMA_CE
+
 // Rows <= kSmallRow: one thread, insertion sort.  Longer rows are appended
 // to a work list (atomic order does not matter: each row is sorted on its
 // own unique keys).
@@ -251,6 +310,11 @@ __global__ void k_sort_rows_small(const int32_t* __restrict__ ptr, int64_t R, ui
     int32_t len = e - b;
     if (len > kSmallRow) {
       big_list[atomicAdd(counters, 1)] = (int32_t)r;
+      continue;
+    }
+    if (len < 2) continue;
+    if (len <= 8) {
+      sort8_regs(key, src, b, len);
       continue;
     }
     for (int32_t i = b + 1; i < e; i++) {
@@ -343,13 +407,12 @@ void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint6
   out.key.alloc(N > 0 ? N : 1, ctx.s);
   out.src.alloc(N > 0 ? N : 1, ctx.s);
   if (want_row) out.row.alloc(N > 0 ? N : 1, ctx.s);
-  Buf<int32_t> cnt(R > 0 ? R : 1, ctx);
+  Buf<int32_t> cnt(R > 0 ? R : 1, ctx), off(N > 0 ? N : 1, ctx);
   cnt.zero();
-  RAMA_KERNEL(ctx, k_bucket_count, N, row, N, cnt.p);
+  RAMA_KERNEL(ctx, k_bucket_count, N, row, N, cnt.p, off.p);
   exclusive_scan(ctx, cnt.p, out.row_ptr.p, R, false);
   if (N == 0 || R == 0) return;
-  copy_d2d(ctx, cnt.p, out.row_ptr.p, R);  // cursor
-  RAMA_KERNEL(ctx, k_bucket_scatter, N, row, key, N, cnt.p, out.key.p, out.src.p,
+  RAMA_KERNEL(ctx, k_bucket_scatter, N, row, key, off.p, N, out.row_ptr.p, out.key.p, out.src.p,
               want_row ? out.row.p : (int32_t*)nullptr);
   if (sort_rows == 0) return;
   Buf<int32_t> lists(2 * sort_rows + 2, ctx);  // big list | huge list | counters
