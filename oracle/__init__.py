@@ -221,19 +221,19 @@ def gaec_exhaustive(g):
     return out, nt.value, joined.value
 
 
-def handshake_cleanup(g):
-    """The B200 build's parallel cleanup (deviation D1): one
-    handshake round, contract, repeat until no mutual pair remains."""
-    fmap = np.arange(g.num_nodes, dtype=np.int64)
-    cur = g
-    while True:
-        S = select_matching(cur, rounds=1)
-        if S.shape[0] == 0:
-            break
-        f, nt = connected_components(cur.num_nodes, S)
-        cur, _ = contract_graph(cur, f, nt)
-        fmap = f[fmap]
-    return fmap, cur.num_nodes
+def handshake_cleanup(g, with_rounds=False):
+    """The B200 build's parallel cleanup (deviation D1): repeated
+    handshake rounds on the quotient under its own costs, merged pairs keep
+    the smaller id, parallel edges fold into the smallest edge slot with a
+    sequential sum (rama_oracle.c orc_cleanup_handshake)."""
+    out = np.empty(g.num_nodes, np.int64)
+    nt = ctypes.c_int64()
+    rounds = ctypes.c_int64()
+    lib().orc_cleanup_handshake(ctypes.c_int64(g.num_nodes), ctypes.c_int64(g.num_edges), _p64(g.edges_u),
+                                _p64(g.edges_v), _pf(g.costs), _p64(out), ctypes.byref(nt), ctypes.byref(rounds))
+    if with_rounds:
+        return out, nt.value, rounds.value
+    return out, nt.value
 
 
 # -------------------------------------------------------------------- dual

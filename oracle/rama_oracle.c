@@ -831,3 +831,90 @@ int orc_gaec(i64 n, i64 m, const i64 *u, const i64 *v, const double *c, i64 *map
     pm_free(&pm);
     return ORC_OK;
 }
+
+/* ------------------------------------------------- handshake cleanup (D1)
+ *
+ * The B200 build's replacement for the sequential GAEC cleanup
+ * (solver.py:187-194 -> contraction.py:397-452); DESIGN.md deviation D1.
+ * Each round is one handshake on the current quotient: every node targets
+ * its live positive neighbour of maximum cost (ties -> smaller id, the
+ * select_matching rule, contraction.py:207), mutual pairs (x < t) merge
+ * into the smaller id.  Node ids are never renumbered; an edge with a
+ * merged endpoint (either side of a pair) is relabelled, dropped if it became internal, and
+ * parallel relabelled edges fold into the smallest edge slot with a
+ * sequential sum in ascending slot order.  Repeats until no pair forms;
+ * the labelling is the canonical component map of all merged pairs. */
+typedef struct { u64 key; i64 idx; } tkey_t;
+
+static int cmp_tkey(const void *pa, const void *pb) {
+    const tkey_t *a = (const tkey_t *)pa, *b = (const tkey_t *)pb;
+    if (a->key != b->key) return a->key < b->key ? -1 : 1;
+    return a->idx < b->idx ? -1 : (a->idx > b->idx);
+}
+
+int orc_cleanup_handshake(i64 n, i64 m, const i64 *u, const i64 *v, const double *c, i64 *map,
+                          i64 *num_targets, i64 *rounds_out) {
+    i64 *eu = (i64 *)xmalloc(sizeof(i64) * (m ? m : 1));
+    i64 *ev = (i64 *)xmalloc(sizeof(i64) * (m ? m : 1));
+    double *ec = (double *)xmalloc(sizeof(double) * (m ? m : 1));
+    char *alive = (char *)xmalloc(m ? m : 1);
+    for (i64 i = 0; i < m; i++) { eu[i] = u[i]; ev[i] = v[i]; ec[i] = c[i]; alive[i] = 1; }
+    i64 *tgt = (i64 *)xmalloc(sizeof(i64) * (n ? n : 1));
+    double *bc = (double *)xmalloc(sizeof(double) * (n ? n : 1));
+    i64 *rep = (i64 *)xmalloc(sizeof(i64) * (n ? n : 1));
+    i64 *par = (i64 *)xmalloc(sizeof(i64) * (n ? n : 1));
+    tkey_t *tk = (tkey_t *)xmalloc(sizeof(tkey_t) * (m ? m : 1));
+    for (i64 x = 0; x < n; x++) { par[x] = x; rep[x] = x; }
+    i64 rounds = 0;
+    while (1) {
+        for (i64 x = 0; x < n; x++) tgt[x] = -1;
+        for (i64 i = 0; i < m; i++) {
+            if (!alive[i] || !(ec[i] > 0.0)) continue;
+            for (int side = 0; side < 2; side++) {
+                i64 a = side ? ev[i] : eu[i], b = side ? eu[i] : ev[i];
+                if (tgt[a] < 0 || ec[i] > bc[a] || (ec[i] == bc[a] && b < tgt[a])) { tgt[a] = b; bc[a] = ec[i]; }
+            }
+        }
+        i64 pairs = 0;
+        for (i64 x = 0; x < n; x++) {
+            i64 t = tgt[x];
+            if (t >= 0 && x < t && tgt[t] == x) { rep[t] = x; par[t] = x; pairs++; }
+        }
+        /* mark merged nodes (tgt = -2 - partner keeps tgt[] readable above) */
+        for (i64 x = 0; x < n; x++)
+            if (rep[x] != x) { tgt[x] = -2; tgt[rep[x]] = -2; }
+        if (!pairs) break;
+        rounds++;
+        i64 nt = 0;
+        for (i64 i = 0; i < m; i++) {
+            if (!alive[i]) continue;
+            if (tgt[eu[i]] < -1 || tgt[ev[i]] < -1) {} else continue;  /* no endpoint merged */
+            i64 a = rep[eu[i]], b = rep[ev[i]];
+            if (a == b) { alive[i] = 0; continue; }
+            eu[i] = a < b ? a : b;
+            ev[i] = a < b ? b : a;
+            tk[nt].key = ((u64)eu[i] << 32) | (u64)ev[i];
+            tk[nt].idx = i;
+            nt++;
+        }
+        qsort(tk, nt, sizeof(tkey_t), cmp_tkey);
+        for (i64 j = 0; j < nt;) {
+            i64 first = tk[j].idx, e = j + 1;
+            double acc = ec[first];
+            while (e < nt && tk[e].key == tk[j].key) { acc += ec[tk[e].idx]; alive[tk[e].idx] = 0; e++; }
+            ec[first] = acc;
+            j = e;
+        }
+        for (i64 x = 0; x < n; x++) rep[x] = x;
+    }
+    i64 t = 0;
+    for (i64 x = 0; x < n; x++) {
+        i64 r = uf_find(par, x);
+        if (r == x) map[x] = t++;
+        else map[x] = map[r];
+    }
+    *num_targets = t;
+    if (rounds_out) *rounds_out = rounds;
+    free(eu); free(ev); free(ec); free(alive); free(tgt); free(bc); free(rep); free(par); free(tk);
+    return ORC_OK;
+}

@@ -4,7 +4,10 @@
 #include "../../include/rama_b200.h"
 #include "internal.h"
 
+#include <atomic>
 #include <cmath>
+#include <mutex>
+#include <thread>
 #include <limits>
 #include <new>
 #include <string>
@@ -222,7 +225,7 @@ int rama_components(int64_t n, const int32_t* su, const int32_t* sv, int64_t k, 
                     void* stream) {
   return guarded(stream, [&](Ctx& ctx) {
     check_sizes(n, k);
-    *num_targets = components(ctx, n, su, sv, k, map);
+    *num_targets = components(ctx, n, su, sv, k, map, true);
   });
 }
 
@@ -369,6 +372,75 @@ int rama_lower_bound(int64_t m_aug, const double* base, int64_t T, const int32_t
     DualState st;
     load_state(ctx, st, m_aug, base, T, tri_edges, lam);
     *lb = lower_bound(ctx, st);
+  });
+}
+
+int rama_solve_batch(int64_t count, const int64_t* node_off, const int64_t* edge_off, const int32_t* u,
+                     const int32_t* v, const double* c, const rama_cfg* cfg, int32_t* labels, double* primal_lb,
+                     int32_t workers, void* stream) {
+  return guarded(stream, [&](Ctx& ctx) {
+    RAMA_REQUIRE(count >= 0, "count must be non-negative");
+    if (count == 0) return;
+    RAMA_REQUIRE(node_off && edge_off && primal_lb, "offset / result arrays must not be NULL");
+    to_cfg(cfg);
+    for (int64_t i = 0; i < count; i++) {
+      RAMA_REQUIRE(node_off[i + 1] >= node_off[i] && edge_off[i + 1] >= edge_off[i], "offsets must be non-decreasing");
+      check_sizes(node_off[i + 1] - node_off[i], edge_off[i + 1] - edge_off[i]);
+    }
+    int dev = 0;
+    RAMA_CUDA(cudaGetDevice(&dev));
+    int W = workers > 0 ? workers : 8;
+    if (W > count) W = (int)count;
+    cudaEvent_t start;
+    RAMA_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    RAMA_CUDA(cudaEventRecord(start, ctx.s));
+    std::vector<cudaStream_t> streams(W);
+    for (int w = 0; w < W; w++) {
+      RAMA_CUDA(cudaStreamCreateWithFlags(&streams[w], cudaStreamNonBlocking));
+      RAMA_CUDA(cudaStreamWaitEvent(streams[w], start, 0));
+    }
+    std::atomic<int64_t> next(0), launches(0);
+    std::mutex mu;
+    int err_code = 0;
+    std::string err_msg;
+    auto worker = [&](int w) {
+      try {
+        RAMA_CUDA(cudaSetDevice(dev));
+        Ctx wc(streams[w]);
+        while (true) {
+          int64_t i = next.fetch_add(1);
+          if (i >= count) break;
+          int64_t no = node_off[i], eo = edge_off[i];
+          run_solve(wc, node_off[i + 1] - no, u + eo, v + eo, c + eo, edge_off[i + 1] - eo, cfg, labels + no,
+                    primal_lb + 2 * i, nullptr, 0, nullptr);
+        }
+        wc.sync();
+        launches += wc.launches;
+      } catch (const Error& e) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!err_code) { err_code = e.code; err_msg = e.what(); }
+        next = count;
+      } catch (const std::exception& e) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!err_code) { err_code = kInternal; err_msg = e.what(); }
+        next = count;
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int w = 1; w < W; w++) pool.emplace_back(worker, w);
+    worker(0);
+    for (auto& t : pool) t.join();
+    for (int w = 0; w < W; w++) {
+      cudaEvent_t done;
+      RAMA_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+      RAMA_CUDA(cudaEventRecord(done, streams[w]));
+      RAMA_CUDA(cudaStreamWaitEvent(ctx.s, done, 0));
+      cudaEventDestroy(done);
+      cudaStreamDestroy(streams[w]);
+    }
+    cudaEventDestroy(start);
+    ctx.launches += (int)launches.load();
+    if (err_code) throw Error(err_code, "batch instance failed: " + err_msg);
   });
 }
 

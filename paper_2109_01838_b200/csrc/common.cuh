@@ -230,11 +230,17 @@ struct BucketSorted {
   Buf<int32_t> row;      // N (row of slot p)
   Buf<uint64_t> key;     // N
   Buf<int32_t> src;      // N
+  int64_t total = 0;     // kept items (row >= 0) = row_ptr[R]
 };
 // Items with row < 0 are dropped.  Only rows < sort_rows are sorted
 // (default all); later rows keep scatter order.
 void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint64_t* key, BucketSorted& out,
                  bool want_row = true, int64_t sort_rows = -1);
+
+// stable LSD radix sort of (key, value) pairs on key bits [begin_bit, end_bit)
+// (CUB onesweep): equal keys keep their input order
+void radix_sort_pairs(Ctx& ctx, const uint64_t* k_in, const int32_t* v_in, uint64_t* k_out, int32_t* v_out,
+                      int64_t N, int begin_bit = 0, int end_bit = 64);
 
 // stable compaction of indices [0, n) where flag != 0; returns the count.
 int64_t compact_indices(Ctx& ctx, const uint8_t* flags, int64_t n, Buf<int32_t>& out);

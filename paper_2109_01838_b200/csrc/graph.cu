@@ -165,10 +165,10 @@ __global__ void k_cc_label(const int32_t* __restrict__ parent, const int32_t* __
   GRID_STRIDE(x, n) map[x] = rank[parent[x]];
 }
 
-int64_t components(Ctx& ctx, int64_t n, const int32_t* su, const int32_t* sv, int64_t k, int32_t* map) {
+int64_t components(Ctx& ctx, int64_t n, const int32_t* su, const int32_t* sv, int64_t k, int32_t* map, bool check) {
   ProfScope prof(ctx.s, kFamComponents);
   if (n == 0) return 0;
-  if (k > 0) {
+  if (check && k > 0) {
     Buf<int32_t> err(1, ctx);
     err.zero();
     RAMA_KERNEL(ctx, k_cc_check, k, su, sv, k, n, err.p);
@@ -223,7 +223,7 @@ Graph contract(Ctx& ctx, const GraphView& g, const int32_t* map, int64_t n_targe
   if (joined) *joined = device_sum(ctx, jc.p, m);
   BucketSorted bs;
   bucket_sort(ctx, n_targets, m, row.p, key.p, bs, true);
-  int64_t limit = read_scalar(ctx, bs.row_ptr.p + n_targets);
+  int64_t limit = bs.total;
   Graph out = reduce_sorted(ctx, n_targets, limit, bs, g.c);
   prof.add_bytes(16.0 * (double)out.m);
   return out;

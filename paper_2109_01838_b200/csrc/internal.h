@@ -30,7 +30,10 @@ struct Graph {
 // a3  WeightedGraph.__init__ (graph.py:29-57)
 Graph canonicalize(Ctx& ctx, int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m);
 // a17 connected_components (contraction.py:101-111); returns num_targets
-int64_t components(Ctx& ctx, int64_t n, const int32_t* su, const int32_t* sv, int64_t k, int32_t* map);
+// (check: validate endpoint ranges first -- the C ABI entry; internal callers
+// pass edges that are valid by construction)
+int64_t components(Ctx& ctx, int64_t n, const int32_t* su, const int32_t* sv, int64_t k, int32_t* map,
+                   bool check = false);
 // a18 contract_graph (contraction.py:142-163); *joined (host) may be null
 Graph contract(Ctx& ctx, const GraphView& g, const int32_t* map, int64_t n_targets, double* joined);
 // a19 ContractionMapping.then (contraction.py:45-52): f_total = f[f_total]

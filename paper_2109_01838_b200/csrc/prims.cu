@@ -3,17 +3,19 @@
 // built on (canonicalisation, contraction, positive CSR, triplet and chord
 // dedupe, edge->slot lists).
 //
-// Bucket sort = counting sort on a 32-bit row id (atomic histogram + scan +
-// atomic scatter) followed by an in-row sort on a unique 64-bit key.  Rows
-// in this solver are short (grid degrees), so the in-row sort is a
-// thread-per-row insertion sort in registers-through-L1; the rare long
-// rows (power-law hubs) go through CUB's segmented sort.  CUB is used only
+// Bucket sort = counting sort on a 32-bit row id (warp-aggregated atomic
+// histogram + scan + scatter) followed by an in-row sort on a 64-bit key.
+// Rows in this solver are short (grid degrees), so the in-row order comes
+// from a thread-per-item rank over the row (warp-broadcast loads); rows
+// longer than 64 use a shared-memory bitonic sort per block, and the rare
+// huge rows (power-law hubs) CUB's segmented sort.  CUB is used only
 // for generic scans/selection/segmented sorting, never for domain logic.
 #include "common.cuh"
 
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
+#include <mutex>
 #include <vector>
 
 namespace rama {
@@ -30,16 +32,16 @@ Ctx::~Ctx() {
 }
 
 void ensure_pool_configured() {
-  static bool done = false;
-  if (done) return;
-  int dev = 0;
-  RAMA_CUDA(cudaGetDevice(&dev));
-  cudaMemPool_t pool;
-  RAMA_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
-  uint64_t thr = UINT64_MAX;
-  RAMA_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-  RAMA_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-  done = true;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    RAMA_CUDA(cudaGetDevice(&dev));
+    cudaMemPool_t pool;
+    RAMA_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thr = UINT64_MAX;
+    RAMA_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    RAMA_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+  });
 }
 
 // ------------------------------------------------------------- profiling
@@ -57,6 +59,7 @@ double g_prof_bytes[kNumFamilies] = {0};
 int64_t g_prof_count[kNumFamilies] = {0};
 
 std::vector<cudaEvent_t> g_event_pool;
+std::mutex g_prof_mu;  // batch solves profile from several host threads
 
 void prof_drain() {
   for (auto& r : g_prof_recs) {
@@ -74,6 +77,7 @@ void prof_drain() {
 }  // namespace
 
 cudaEvent_t prof_event() {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
   if (g_event_pool.empty()) {
     for (int i = 0; i < 256; i++) {
       cudaEvent_t e;
@@ -89,6 +93,7 @@ cudaEvent_t prof_event() {
 bool prof_enabled() { return g_prof; }
 
 void prof_set(bool on) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
   prof_drain();
   for (int f = 0; f < kNumFamilies; f++) {
     g_prof_ms[f] = 0.0;
@@ -99,11 +104,13 @@ void prof_set(bool on) {
 }
 
 void prof_push(int fam, cudaEvent_t a, cudaEvent_t b, double bytes) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
   g_prof_recs.push_back(ProfRec{fam, a, b, bytes});
   if (g_prof_recs.size() > 4096) prof_drain();
 }
 
 void prof_read(double* ms, double* bytes, int64_t* count) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
   prof_drain();
   for (int f = 0; f < kNumFamilies; f++) {
     ms[f] = g_prof_ms[f];
@@ -113,11 +120,10 @@ void prof_read(double* ms, double* bytes, int64_t* count) {
 }
 
 static int trace_level() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {
     const char* e = getenv("RAMA_TRACE");
-    v = (e && e[0] >= '1' && e[0] <= '9') ? e[0] - '0' : 0;
-  }
+    return (e && e[0] >= '1' && e[0] <= '9') ? e[0] - '0' : 0;
+  }();
   return v;
 }
 
@@ -175,6 +181,16 @@ int64_t compact_indices(Ctx& ctx, const uint8_t* flags, int64_t n, Buf<int32_t>&
   RAMA_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, it, flags, out.p, nsel.p, (int)n, ctx.s));
   ctx.launches++;
   return read_scalar(ctx, nsel.p);
+}
+
+void radix_sort_pairs(Ctx& ctx, const uint64_t* k_in, const int32_t* v_in, uint64_t* k_out, int32_t* v_out,
+                      int64_t N, int begin_bit, int end_bit) {
+  if (N <= 0) return;
+  size_t tb = 0;
+  RAMA_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k_in, k_out, v_in, v_out, (int)N, begin_bit, end_bit, ctx.s));
+  Buf<uint8_t> tmp(tb, ctx);
+  RAMA_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, k_in, k_out, v_in, v_out, (int)N, begin_bit, end_bit, ctx.s));
+  ctx.launches++;
 }
 
 // -------------------------------------------------- deterministic sum
@@ -258,87 +274,62 @@ __global__ void k_bucket_count(const int32_t* __restrict__ row, int64_t N, int32
 
 __global__ void k_bucket_scatter(const int32_t* __restrict__ row, const uint64_t* __restrict__ key,
                                  const int32_t* __restrict__ off, int64_t N, const int32_t* __restrict__ ptr,
-                                 uint64_t* __restrict__ okey, int32_t* __restrict__ osrc, int32_t* __restrict__ orow) {
+                                 uint64_t* __restrict__ tkey, int32_t* __restrict__ tsrc, int32_t* __restrict__ orow) {
   GRID_STRIDE(i, N) {
     int32_t r = row[i];
     if (r < 0) continue;
     int32_t p = ptr[r] + off[i];
-    okey[p] = key[i];
-    osrc[p] = (int32_t)i;
-    if (orow) orow[p] = r;
+    tkey[p] = key[i];
+    tsrc[p] = (int32_t)i;
+    orow[p] = r;
   }
 }
 
-constexpr int kSmallRow = 32;
+// Rows of at most kSmallRow items are ordered by ranking: the thread of
+// slot p counts the row's keys below its own (ties by scatter slot, so the
+// result is a permutation even for duplicate keys) and writes its item to
+// row_start + rank.  Neighbouring threads read the same row, so the key
+// loads are warp broadcasts.  Longer rows are listed for the block sort.
+constexpr int kSmallRow = 64;
 
-#define RAMA_CE(i, j)                                    \
-  if (k[j] < k[i]) {                                     \
-    uint64_t tk = k[i]; k[i] = k[j]; k[j] = tk;          \
-    int32_t ts = sv[i]; sv[i] = sv[j]; sv[j] = ts;       \
-  }
-
-// rows of 2..8 items: Batcher odd-even merge network in registers
-__device__ __forceinline__ void sort8_regs(uint64_t* __restrict__ key, int32_t* __restrict__ src, int32_t b,
-                                           int32_t len) {
-  uint64_t k[8];
-  int32_t sv[8];
-#pragma unroll
-  for (int i = 0; i < 8; i++) {
-    k[i] = i < len ? key[b + i] : ~0ULL;
-    sv[i] = i < len ? src[b + i] : 0;
-  }
-  RAMA_CE(0, 1) RAMA_CE(2, 3) RAMA_CE(4, 5) RAMA_CE(6, 7)
-  RAMA_CE(0, 2) RAMA_CE(1, 3) RAMA_CE(4, 6) RAMA_CE(5, 7)
-  RAMA_CE(1, 2) RAMA_CE(5, 6)
-  RAMA_CE(0, 4) RAMA_CE(1, 5) RAMA_CE(2, 6) RAMA_CE(3, 7)
-  RAMA_CE(2, 4) RAMA_CE(3, 5)
-  RAMA_CE(1, 2) RAMA_CE(3, 4) RAMA_CE(5, 6)
-#pragma unroll
-  for (int i = 0; i < 8; i++)
-    if (i < len) { key[b + i] = k[i]; src[b + i] = sv[i]; }
-}
-#undef RAMA_CE
-
-// Rows <= kSmallRow: one thread, insertion sort.  Longer rows are appended
-// to a work list (atomic order does not matter: each row is sorted on its
-// own unique keys).
-__global__ void k_sort_rows_small(const int32_t* __restrict__ ptr, int64_t R, uint64_t* __restrict__ key,
-                                  int32_t* __restrict__ src, int32_t* __restrict__ big_list,
-                                  int32_t* __restrict__ counters) {
-  GRID_STRIDE(r, R) {
+__global__ void k_rank_rows(const int32_t* __restrict__ row, const int32_t* __restrict__ ptr, int64_t N,
+                            int64_t sort_rows, const uint64_t* __restrict__ tkey, const int32_t* __restrict__ tsrc,
+                            uint64_t* __restrict__ okey, int32_t* __restrict__ osrc, int32_t* __restrict__ big_list,
+                            int32_t* __restrict__ counters) {
+  GRID_STRIDE(p, N) {
+    int32_t r = row[p];
     int32_t b = ptr[r], e = ptr[r + 1];
-    int32_t len = e - b;
-    if (len > kSmallRow) {
-      big_list[atomicAdd(counters, 1)] = (int32_t)r;
+    uint64_t k = tkey[p];
+    int32_t s = tsrc[p];
+    if (e - b == 1 || r >= sort_rows) {
+      okey[p] = k;
+      osrc[p] = s;
       continue;
     }
-    if (len < 2) continue;
-    if (len <= 8) {
-      sort8_regs(key, src, b, len);
+    if (e - b > kSmallRow) {
+      if (p == b) big_list[atomicAdd(counters, 1)] = r;
       continue;
     }
-    for (int32_t i = b + 1; i < e; i++) {
-      uint64_t k = key[i];
-      int32_t s = src[i];
-      int32_t j = i - 1;
-      while (j >= b && key[j] > k) {
-        key[j + 1] = key[j];
-        src[j + 1] = src[j];
-        j--;
-      }
-      key[j + 1] = k;
-      src[j + 1] = s;
+    int32_t rank = 0;
+    for (int32_t q = b; q < e; q++) {
+      uint64_t x = tkey[q];
+      rank += (x < k) || (x == k && q < (int32_t)p);
     }
+    okey[b + rank] = k;
+    osrc[b + rank] = s;
   }
 }
 
 constexpr int kBlockRow = 4096;  // bitonic sort in shared memory: 4096 x 12 B = 48 KB
 
-// one block per listed row: bitonic sort of (key, src) in shared memory;
-// rows longer than kBlockRow go to the huge list (CUB)
+// one block per listed row: bitonic sort of (key, src) in shared memory,
+// from the scatter buffers into the output; rows longer than kBlockRow go
+// to the huge list (CUB segmented sort)
 __global__ void __launch_bounds__(512) k_sort_rows_block(const int32_t* __restrict__ ptr,
                                                          const int32_t* __restrict__ big_list,
-                                                         int32_t* __restrict__ counters, uint64_t* __restrict__ key,
+                                                         int32_t* __restrict__ counters,
+                                                         const uint64_t* __restrict__ tkey,
+                                                         const int32_t* __restrict__ tsrc, uint64_t* __restrict__ key,
                                                          int32_t* __restrict__ src, int32_t* __restrict__ huge_list) {
   __shared__ uint64_t sk[kBlockRow];
   __shared__ int32_t ss[kBlockRow];
@@ -353,7 +344,7 @@ __global__ void __launch_bounds__(512) k_sort_rows_block(const int32_t* __restri
     int32_t P = 64;
     while (P < len) P <<= 1;
     for (int32_t i = threadIdx.x; i < P; i += blockDim.x) {
-      if (i < len) { sk[i] = key[b + i]; ss[i] = src[b + i]; }
+      if (i < len) { sk[i] = tkey[b + i]; ss[i] = tsrc[b + i]; }
       else { sk[i] = ~0ULL; ss[i] = 0x7fffffff; }
     }
     __syncthreads();
@@ -386,16 +377,17 @@ __global__ void k_big_lens(const int32_t* __restrict__ rows, int64_t nb, const i
   GRID_STRIDE(i, nb) len[i] = ptr[rows[i] + 1] - ptr[rows[i]];
 }
 
-// move huge rows to / from a contiguous staging area
+// move huge rows between the row layout and a contiguous staging area
 __global__ void k_big_move(const int32_t* __restrict__ rows, int64_t nb, const int32_t* __restrict__ ptr,
-                           const int32_t* __restrict__ off, uint64_t* __restrict__ key, int32_t* __restrict__ src,
-                           uint64_t* __restrict__ skey, int32_t* __restrict__ ssrc, bool to_stage) {
+                           const int32_t* __restrict__ off, const uint64_t* __restrict__ key_in,
+                           const int32_t* __restrict__ src_in, uint64_t* __restrict__ key_out,
+                           int32_t* __restrict__ src_out, bool to_stage) {
   for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
     int32_t r = rows[b];
     int32_t base = ptr[r], len = ptr[r + 1] - base, o = off[b];
     for (int32_t j = threadIdx.x; j < len; j += blockDim.x) {
-      if (to_stage) { skey[o + j] = key[base + j]; ssrc[o + j] = src[base + j]; }
-      else { key[base + j] = skey[o + j]; src[base + j] = ssrc[o + j]; }
+      if (to_stage) { key_out[o + j] = key_in[base + j]; src_out[o + j] = src_in[base + j]; }
+      else { key_out[base + j] = key_in[o + j]; src_out[base + j] = src_in[o + j]; }
     }
   }
 }
@@ -406,23 +398,33 @@ void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint6
   out.row_ptr.alloc(R + 1, ctx.s);
   out.key.alloc(N > 0 ? N : 1, ctx.s);
   out.src.alloc(N > 0 ? N : 1, ctx.s);
-  if (want_row) out.row.alloc(N > 0 ? N : 1, ctx.s);
+  out.row.alloc(N > 0 ? N : 1, ctx.s);
   Buf<int32_t> cnt(R > 0 ? R : 1, ctx), off(N > 0 ? N : 1, ctx);
   cnt.zero();
   RAMA_KERNEL(ctx, k_bucket_count, N, row, N, cnt.p, off.p);
-  exclusive_scan(ctx, cnt.p, out.row_ptr.p, R, false);
-  if (N == 0 || R == 0) return;
-  RAMA_KERNEL(ctx, k_bucket_scatter, N, row, key, off.p, N, out.row_ptr.p, out.key.p, out.src.p,
-              want_row ? out.row.p : (int32_t*)nullptr);
-  if (sort_rows == 0) return;
+  int64_t total = exclusive_scan(ctx, cnt.p, out.row_ptr.p, R, true);  // kept items (row >= 0)
+  out.total = total;
+  if (total == 0 || R == 0) {
+    if (!want_row) out.row.release();
+    return;
+  }
+  Buf<uint64_t> tkey(total, ctx);
+  Buf<int32_t> tsrc(total, ctx);
+  RAMA_KERNEL(ctx, k_bucket_scatter, N, row, key, off.p, N, out.row_ptr.p, tkey.p, tsrc.p, out.row.p);
+  off.release();
+  cnt.release();
   Buf<int32_t> lists(2 * sort_rows + 2, ctx);  // big list | huge list | counters
   int32_t* big_list = lists.p;
   int32_t* huge_list = lists.p + sort_rows;
   int32_t* counters = lists.p + 2 * sort_rows;
   RAMA_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(int32_t), ctx.s));
-  RAMA_KERNEL(ctx, k_sort_rows_small, sort_rows, out.row_ptr.p, sort_rows, out.key.p, out.src.p, big_list, counters);
-  unsigned gb = (unsigned)std::min<int64_t>(std::max<int64_t>(sort_rows / 64, 1), 148 * 4);
-  k_sort_rows_block<<<gb, 512, 0, ctx.s>>>(out.row_ptr.p, big_list, counters, out.key.p, out.src.p, huge_list);
+  RAMA_KERNEL(ctx, k_rank_rows, total, out.row.p, out.row_ptr.p, total, sort_rows, tkey.p, tsrc.p, out.key.p,
+              out.src.p, big_list, counters);
+  if (!want_row) out.row.release();
+  if (sort_rows == 0) return;
+  unsigned gb = (unsigned)std::min<int64_t>(std::max<int64_t>(total / 256, 1), 148 * 4);
+  k_sort_rows_block<<<gb, 512, 0, ctx.s>>>(out.row_ptr.p, big_list, counters, tkey.p, tsrc.p, out.key.p, out.src.p,
+                                           huge_list);
   RAMA_LAUNCH_CHECK();
   ctx.launches++;
   int32_t nb = read_scalar(ctx, counters + 1);
@@ -434,7 +436,7 @@ void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint6
   Buf<uint64_t> k1(tot, ctx), k2(tot, ctx);
   Buf<int32_t> s1(tot, ctx), s2(tot, ctx);
   unsigned g = (unsigned)std::min<int64_t>(nb, 4096);
-  k_big_move<<<g, kBlock, 0, ctx.s>>>(huge_list, nb, out.row_ptr.p, boff.p, out.key.p, out.src.p, k1.p, s1.p, true);
+  k_big_move<<<g, kBlock, 0, ctx.s>>>(huge_list, nb, out.row_ptr.p, boff.p, tkey.p, tsrc.p, k1.p, s1.p, true);
   RAMA_LAUNCH_CHECK();
   size_t tb = 0;
   RAMA_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, tb, k1.p, k2.p, s1.p, s2.p, (int)tot, (int)nb, boff.p,
@@ -442,7 +444,7 @@ void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint6
   Buf<uint8_t> tmp(tb, ctx);
   RAMA_CUDA(cub::DeviceSegmentedSort::SortPairs(tmp.p, tb, k1.p, k2.p, s1.p, s2.p, (int)tot, (int)nb, boff.p,
                                                 boff.p + 1, ctx.s));
-  k_big_move<<<g, kBlock, 0, ctx.s>>>(huge_list, nb, out.row_ptr.p, boff.p, out.key.p, out.src.p, k2.p, s2.p, false);
+  k_big_move<<<g, kBlock, 0, ctx.s>>>(huge_list, nb, out.row_ptr.p, boff.p, k2.p, s2.p, out.key.p, out.src.p, false);
   RAMA_LAUNCH_CHECK();
   ctx.launches += 3;
 }

@@ -470,15 +470,6 @@ static void build_min_table(Ctx& ctx, int64_t n, int LOG, const int32_t* up, con
     RAMA_KERNEL(ctx, k_lift_min, n, n, up + (int64_t)(j - 1) * n, mn.p + (int64_t)(j - 1) * n, mn.p + (int64_t)j * n);
 }
 
-static void radix_sort_u64(Ctx& ctx, Buf<uint64_t>& k_in, Buf<int32_t>& v_in, Buf<uint64_t>& k_out,
-                           Buf<int32_t>& v_out, int64_t N) {
-  size_t tb = 0;
-  RAMA_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k_in.p, k_out.p, v_in.p, v_out.p, (int)N, 0, 64, ctx.s));
-  Buf<uint8_t> tmp(tb, ctx);
-  RAMA_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, k_in.p, k_out.p, v_in.p, v_out.p, (int)N, 0, 64, ctx.s));
-  ctx.launches++;
-}
-
 int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_t>& sv) {
   ProfScope prof(ctx.s, kFamForest);
   int64_t n = g.n, m = g.m;
@@ -495,7 +486,7 @@ int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_
   Buf<uint64_t> k1(np, ctx), k2(np, ctx);
   Buf<int32_t> v1(np, ctx), order(np, ctx), rank(np, ctx);
   RAMA_KERNEL(ctx, k_neg_bits, np, P.p, np, g.c, k1.p, v1.p);
-  radix_sort_u64(ctx, k1, v1, k2, order, np);
+  radix_sort_pairs(ctx, k1.p, v1.p, k2.p, order.p, np);
   RAMA_KERNEL(ctx, k_scatter_rank, np, order.p, np, rank.p);
 
   // Boruvka
@@ -531,7 +522,7 @@ int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_
     Buf<int32_t> fu(kf, ctx), fv(kf, ctx), fval(kf, ctx), fsorted(kf, ctx), fkey(kf, ctx);
     Buf<uint64_t> fbits(kf, ctx), fbits2(kf, ctx);
     RAMA_KERNEL(ctx, k_forest_edges, kf, Fi.p, kf, P.p, g.u, g.v, g.c, fu.p, fv.p, fbits.p, fval.p);
-    radix_sort_u64(ctx, fbits, fval, fbits2, fsorted, kf);  // key_inv: rank -> forest edge
+    radix_sort_pairs(ctx, fbits.p, fval.p, fbits2.p, fsorted.p, kf);  // key_inv: rank -> forest edge
     RAMA_KERNEL(ctx, k_scatter_rank, kf, fsorted.p, kf, fkey.p);  // fkey: forest edge -> rank
 
     // arcs, sorted adjacency, Euler tour

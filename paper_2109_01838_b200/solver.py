@@ -155,3 +155,50 @@ def dual_bound(g, cfg):
     if cfg.mode != "D":
         raise ValueError("dual_bound requires mode D")
     return solve(g, cfg).lower_bound
+
+
+def solve_batch(graphs, cfg, workers=8):
+    """Solve independent instances concurrently on one GPU (SURVEY.md 8(e),
+    config C5): one ``rama_solve_batch`` call, ``workers`` streams.
+
+    ``graphs``: WeightedGraph list.  Returns a list of Solution (trace
+    omitted: batch solves record no per-round trace).
+    """
+    cfg.validate()
+    t = L.torch()
+    count = len(graphs)
+    if count == 0:
+        return []
+    node_off = np.zeros(count + 1, np.int64)
+    edge_off = np.zeros(count + 1, np.int64)
+    for i, g in enumerate(graphs):
+        node_off[i + 1] = node_off[i] + g.num_nodes
+        edge_off[i + 1] = edge_off[i] + g.num_edges
+    parts = [g.device() for g in graphs if g.num_edges]
+    if parts:
+        du, dv, dc = (t.cat([p[j] for p in parts]) for j in range(3))
+    else:
+        du = dv = L.empty_i32(1)
+        dc = L.empty_f64(1)
+    labels, out = solve_batch_device(node_off, edge_off, du, dv, dc, cfg, workers)
+    lab = labels.cpu().numpy().astype(np.int64)
+    return [Solution(lab[node_off[i]:node_off[i + 1]], float(out[2 * i]), float(out[2 * i + 1]), [])
+            for i in range(count)]
+
+
+def solve_batch_device(node_off, edge_off, du, dv, dc, cfg, workers=8, labels=None):
+    """Device entry of the batch solve: concatenated canonical COO slices
+    (int32 u, v; float64 c CUDA tensors) with host offset arrays.  Returns
+    (labels int32 CUDA tensor, numpy float64[2 * count] of (primal, lb))."""
+    cfg.validate()
+    node_off = np.ascontiguousarray(node_off, np.int64)
+    edge_off = np.ascontiguousarray(edge_off, np.int64)
+    count = node_off.size - 1
+    if labels is None:
+        labels = L.empty_i32(int(node_off[-1]))
+    out = np.zeros(max(2 * count, 1), np.float64)
+    c = cfg.to_c()
+    L.call("rama_solve_batch", count, node_off.ctypes.data_as(L._I64P), edge_off.ctypes.data_as(L._I64P), L.ptr(du),
+           L.ptr(dv), L.ptr(dc), L.ctypes.byref(c), L.ptr(labels), out.ctypes.data_as(L._F64P), int(workers),
+           L.stream())
+    return labels, out

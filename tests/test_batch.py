@@ -1,0 +1,91 @@
+"""Batch / multi-GPU plumbing.
+
+CPU: shard arithmetic and the label/objective all-gather over gloo with
+world_size 2 (the same code runs over NCCL on the GPU box).
+GPU: the concurrent batch solve equals one solve per instance, bit for bit.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2109_01838_b200 import batch
+
+
+def test_shard_range_covers_batch():
+    for count in (0, 1, 5, 64, 65):
+        for world in (1, 2, 3, 4, 8):
+            spans = [batch.shard_range(count, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == count
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            sizes = [hi - lo for lo, hi in spans]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        batch.shard_range(4, 2, 2)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _gather_worker(rank, world, port, count, n, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lo, hi = batch.shard_range(count, rank, world)
+        # instance i's labels are all i, its objectives (i, -i)
+        lab = torch.cat([torch.full((n,), i, dtype=torch.int32) for i in range(lo, hi)]) if hi > lo else \
+            torch.empty(0, dtype=torch.int32)
+        obj = torch.tensor([[float(i), -float(i)] for i in range(lo, hi)], dtype=torch.float64).reshape(-1, 2)
+        L, O = batch.gather_results(lab, obj, n, count)
+        out[rank] = (L.numpy().copy(), O.numpy().copy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("count", [5, 64])
+def test_gather_results_gloo_world2(count):
+    world, n = 2, 7
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_gather_worker, args=(world, _free_port(), count, n, out), nprocs=world, join=True)
+    for r in range(world):
+        L, O = out[r]
+        assert L.shape == (count, n) and O.shape == (count, 2)
+        assert np.array_equal(L, np.repeat(np.arange(count, dtype=np.int32)[:, None], n, axis=1))
+        assert np.array_equal(O[:, 0], np.arange(count)) and np.array_equal(O[:, 1], -np.arange(count))
+
+
+@pytest.mark.gpu
+def test_batch_solve_equals_single_solves():
+    import paper_2109_01838_b200 as P
+    from paper_2109_01838_b200 import instances
+
+    graphs = [P.WeightedGraph(*instances.grid_coo(96, 128, 0, seed=s)) for s in range(6)]
+    graphs.append(P.WeightedGraph(*instances.grid8_coo(40, 50, strides=(2, 3), seed=9)))
+    graphs.append(P.WeightedGraph(5))  # no edges
+    for mode in ("PD", "P"):
+        cfg = P.SolverConfig(mode=mode)
+        got = P.solve_batch(graphs, cfg, workers=3)
+        for g, b in zip(graphs, got):
+            a = P.solve(g, cfg)
+            assert np.array_equal(a.labeling, b.labeling)
+            assert a.primal_cost == b.primal_cost and a.lower_bound == b.lower_bound
+
+
+@pytest.mark.gpu
+def test_batch_solve_reports_bad_instance():
+    import paper_2109_01838_b200 as P
+
+    cfg = P.SolverConfig(mode="PD")
+    with pytest.raises(ValueError):
+        P.solve_batch_device(np.array([0, 4, 2]), np.array([0, 0, 0]), P._lib.empty_i32(1), P._lib.empty_i32(1),
+                             P._lib.empty_f64(1), cfg)

@@ -191,3 +191,28 @@ def test_golden_grids():
     assert np.array_equal(sol.labeling, fx.vec("s3_labels", 0))
     assert sol.primal_cost == fx.scalar("s3_primal", 0)
     assert sol.lower_bound == fx.scalar("s3_lb", 0)
+
+
+def test_handshake_cleanup_equals_contraction_rounds():
+    """D1: the oracle's in-place handshake cleanup equals the
+    plain definition -- one select_matching round, connected_components,
+    contract_graph, repeat -- on seeded random graphs and grids."""
+    from paper_2109_01838_b200 import instances
+
+    def by_contraction(g):
+        fmap = np.arange(g.num_nodes, dtype=np.int64)
+        cur = g
+        while True:
+            S = O.select_matching(cur, rounds=1)
+            if S.shape[0] == 0:
+                return fmap, cur.num_nodes
+            f, nt = O.connected_components(cur.num_nodes, S)
+            cur, _ = O.contract_graph(cur, f, nt)
+            fmap = f[fmap]
+
+    graphs = [O.Graph(*instances.random_coo(8 + s % 40, 0.3, seed=s)) for s in range(60)]
+    graphs += [O.grid_graph(64, 64, 0, 0), O.grid_graph(48, 64, 3, 7)]
+    for g in graphs:
+        a, na = by_contraction(g)
+        b, nb = O.handshake_cleanup(g)
+        assert na == nb and np.array_equal(a, b)

@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q --timeout 600 2>&1 | tail -30 > gpurun_out/pytest_gpu.log
+timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1
+for c in c5 c3; do echo "== $c"; timeout 300 python tools/probe_configs.py $c 3 2>&1 | tail -30; done > gpurun_out/probe_configs.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c3.csv python tools/probe_configs.py c3 1 > /dev/null 2>&1
