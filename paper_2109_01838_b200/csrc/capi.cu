@@ -436,6 +436,7 @@ int rama_solve_batch(int64_t count, const int64_t* node_off, const int64_t* edge
       RAMA_CUDA(cudaEventRecord(done, streams[w]));
       RAMA_CUDA(cudaStreamWaitEvent(ctx.s, done, 0));
       cudaEventDestroy(done);
+      dev_release_stream(streams[w]);
       cudaStreamDestroy(streams[w]);
     }
     cudaEventDestroy(start);

@@ -10,6 +10,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <chrono>
 #include <cstdint>
 #include <cstdio>
 #include <stdexcept>
@@ -64,6 +65,9 @@ struct Ctx {
 };
 
 void ensure_pool_configured();
+// grow the stream-ordered pool to at least `bytes` up front (one mapping
+// instead of many growth steps in the middle of a solve)
+void reserve_pool(Ctx& ctx, size_t bytes);
 
 // ---- live kernel-family timing (bench.py roofline) ------------------------
 // When enabled (rama_profile_enable), each ProfScope records a CUDA event
@@ -109,6 +113,26 @@ struct ProfScope {
   }
 };
 
+// host-side accounting (RAMA_HOST_STATS=1): time in stream-ordered
+// allocation calls and in scalar read-back waits, per thread
+struct HostStats {
+  double alloc_ms = 0, sync_ms = 0;
+  int64_t allocs = 0, syncs = 0;
+};
+HostStats& host_stats();
+inline double host_ms_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// Stream-keyed caching allocator over cudaMallocAsync: blocks are binned in
+// size classes (<= 12.5% slack) and reused on the stream that freed them
+// (same-stream reuse is ordered, no events needed).  After the first solve
+// of a shape every scratch buffer comes from the cache.
+void* dev_alloc(size_t bytes, cudaStream_t s);
+void dev_free(void* p, size_t bytes, cudaStream_t s);
+// return every cached block of stream s to the pool (before destroying s)
+void dev_release_stream(cudaStream_t s);
+
 template <class T>
 struct Buf {
   T* p = nullptr;
@@ -134,10 +158,16 @@ struct Buf {
     release();
     s = st;
     n = count;
-    if (count) RAMA_CUDA(cudaMallocAsync((void**)&p, sizeof(T) * count, st));
+    if (count) {
+      auto t0 = std::chrono::steady_clock::now();
+      p = (T*)dev_alloc(sizeof(T) * count, st);
+      HostStats& hs = host_stats();
+      hs.alloc_ms += host_ms_since(t0);
+      hs.allocs++;
+    }
   }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p) dev_free(p, sizeof(T) * n, s);
     p = nullptr;
     n = 0;
   }
@@ -195,8 +225,12 @@ T read_scalar(Ctx& ctx, const T* dev) {
     fprintf(stderr, "[rama] sync\n");
     fflush(stderr);
   }
+  auto t0 = std::chrono::steady_clock::now();
   RAMA_CUDA(cudaMemcpyAsync(ctx.pinned, dev, sizeof(T), cudaMemcpyDeviceToHost, ctx.s));
   ctx.sync();
+  HostStats& hs = host_stats();
+  hs.sync_ms += host_ms_since(t0);
+  hs.syncs++;
   T v;
   memcpy(&v, ctx.pinned, sizeof(T));
   return v;

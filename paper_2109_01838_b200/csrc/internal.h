@@ -101,6 +101,12 @@ Graph reparametrized_graph(Ctx& ctx, const DualState& st);
 // edge -> slot CSR + coverage for an existing tri_edges array
 void build_slot_lists(Ctx& ctx, DualState& st);
 
+// ---- cleanup (cleanup.cu) -----------------------------------------------------
+// a20 replacement (DESIGN.md deviation D1): handshake rounds on the quotient q
+// until no mutual pair remains; writes the canonical map fc[q.n], returns the
+// number of clusters
+int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc);
+
 // ---- driver (solver.cu) -----------------------------------------------------
 struct SolveConfig {
   int mode = 1;  // 0 P, 1 PD, 2 PD+, 3 D, 4 GAEC

@@ -16,19 +16,128 @@
 #include <thrust/iterator/counting_iterator.h>
 
 #include <mutex>
+#include <map>
 #include <vector>
 
 namespace rama {
 
 static int g_num_sms = 0;
 
+HostStats& host_stats() {
+  static thread_local HostStats hs;
+  return hs;
+}
+
+// Pinned staging blocks are recycled across calls: cudaMallocHost /
+// cudaFreeHost cost milliseconds and cudaFreeHost synchronises the device.
+namespace {
+std::mutex g_pin_mu;
+std::vector<int64_t*> g_pin_free;
+}  // namespace
+
 Ctx::Ctx(cudaStream_t st) : s(st) {
   ensure_pool_configured();
-  RAMA_CUDA(cudaMallocHost((void**)&pinned, 64 * sizeof(int64_t)));
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    if (!g_pin_free.empty()) {
+      pinned = g_pin_free.back();
+      g_pin_free.pop_back();
+    }
+  }
+  if (!pinned) RAMA_CUDA(cudaMallocHost((void**)&pinned, 64 * sizeof(int64_t)));
 }
 
 Ctx::~Ctx() {
-  if (pinned) cudaFreeHost(pinned);
+  if (pinned) {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    g_pin_free.push_back(pinned);
+  }
+}
+
+// ------------------------------------------------------ caching allocator
+
+namespace {
+struct CacheKey {
+  cudaStream_t s;
+  size_t bytes;  // class size
+  bool operator<(const CacheKey& o) const { return s < o.s || (s == o.s && bytes < o.bytes); }
+};
+std::mutex g_cache_mu;
+std::map<CacheKey, std::vector<void*>> g_cache;
+size_t g_cached_bytes = 0;
+
+// classes: 256 B granules up to 64 KB, then 8 steps per power of two
+inline size_t class_bytes(size_t bytes) {
+  if (bytes <= 65536) return (bytes + 255) & ~(size_t)255;
+  int e = 63 - __builtin_clzll((unsigned long long)(bytes - 1));  // 2^e < bytes <= 2^(e+1)
+  size_t step = (size_t)1 << (e - 2);
+  return (bytes + step - 1) / step * step;
+}
+}  // namespace
+
+void* dev_alloc(size_t bytes, cudaStream_t s) {
+  size_t b = class_bytes(bytes);
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_cache.find(CacheKey{s, b});
+    if (it != g_cache.end() && !it->second.empty()) {
+      void* p = it->second.back();
+      it->second.pop_back();
+      g_cached_bytes -= b;
+      return p;
+    }
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMallocAsync(&p, b, s);
+  if (e == cudaErrorMemoryAllocation) {  // hand the cache back to the pool, retry once
+    cudaGetLastError();
+    dev_release_stream(s);
+    e = cudaMallocAsync(&p, b, s);
+  }
+  RAMA_CUDA(e);
+  return p;
+}
+
+void dev_free(void* p, size_t bytes, cudaStream_t s) {
+  size_t b = class_bytes(bytes);
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  if (g_cached_bytes + b > ((size_t)48 << 30)) {  // cap what the cache holds
+    cudaFreeAsync(p, s);
+    return;
+  }
+  g_cache[CacheKey{s, b}].push_back(p);
+  g_cached_bytes += b;
+}
+
+void dev_release_stream(cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  for (auto it = g_cache.lower_bound(CacheKey{s, 0}); it != g_cache.end() && it->first.s == s;) {
+    for (void* p : it->second) {
+      cudaFreeAsync(p, s);
+      g_cached_bytes -= it->first.bytes;
+    }
+    it = g_cache.erase(it);
+  }
+}
+
+void reserve_pool(Ctx& ctx, size_t bytes) {
+  int dev = 0;
+  RAMA_CUDA(cudaGetDevice(&dev));
+  cudaMemPool_t pool;
+  RAMA_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t have = 0;
+  RAMA_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &have));
+  if (have >= bytes) return;
+  size_t free_b = 0, total_b = 0;
+  RAMA_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  size_t want = bytes - have;
+  if (want > free_b / 2) want = free_b / 2;
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, want, ctx.s) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  RAMA_CUDA(cudaFreeAsync(p, ctx.s));
 }
 
 void ensure_pool_configured() {
