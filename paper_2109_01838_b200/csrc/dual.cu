@@ -108,11 +108,12 @@ __global__ void k_gather_i32(const int32_t* __restrict__ src, const int32_t* __r
 // edge tries the 3-cycle; the misses are compacted and try the 4-cycle; the
 // remaining misses try the 5-cycle.  (One fused kernel made nearly every
 // warp wait for its slowest 5-cycle lane.)
-__global__ void k_sep3(const int32_t* __restrict__ NQ, int64_t nq, const int32_t* __restrict__ u,
-                       const int32_t* __restrict__ v, const int32_t* __restrict__ ptr,
+__global__ void k_sep3(const int32_t* __restrict__ Q, int64_t nq, const int32_t* __restrict__ NQ,
+                       const int32_t* __restrict__ u, const int32_t* __restrict__ v, const int32_t* __restrict__ ptr,
                        const int32_t* __restrict__ adj, int L, int32_t* __restrict__ out_len,
                        int32_t* __restrict__ out_nodes, uint8_t* __restrict__ miss) {
-  GRID_STRIDE(q, nq) {
+  GRID_STRIDE(i, nq) {
+    int32_t q = Q ? Q[i] : (int32_t)i;
     int32_t e = NQ[q];
     int32_t a = u[e], b = v[e];
     int32_t pa = ptr[a], pb = ptr[b];
@@ -126,7 +127,7 @@ __global__ void k_sep3(const int32_t* __restrict__ NQ, int64_t nq, const int32_t
       out_len[q] = 0;
       for (int j = 0; j < L; j++) row[j] = 0;
     }
-    if (miss) miss[q] = (x < 0);
+    if (miss) miss[i] = (x < 0);
   }
 }
 
@@ -272,6 +273,179 @@ __global__ void k_sep5(const int32_t* __restrict__ Q, int64_t nq, const int32_t*
   }
 }
 
+// ---- source-grouped separation ------------------------------------------
+//
+// 4/5-cycles.  Repulsive edges without a triangle are grouped by their
+// source a (the smaller endpoint; the list is (u, v)-sorted, so a source's
+// edges are contiguous) and each source gets a group of kGrp lanes.  The
+// group builds a's BFS levels once -- L1 = N+(a) in shared memory and
+// L2 = {y : dist(a, y) = 2} with px(y) = min(N+(a) & N+(y)) in a shared hash
+// table, filled by scanning N+(x) for x in ascending order so the first
+// insertion is the BFS parent -- and answers all of a's edges (a, b) by
+// table lookups instead of sorted-row intersections:
+//   4-cycle  y* = argmin_(y in N(b) & L2) (px(y), y)
+//   5-cycle  z* = argmin_(z in N(b), z not in {a} u L1 u L2) (px(py), py, z)
+//            with py(z) = argmin_(y in N(z) & L2) (px(y), y).
+// Sources whose levels overflow the tables (hubs) are flagged for the
+// row-intersection kernels above.
+constexpr int kGrp = 8;                  // lanes per source
+constexpr int kGrpPerBlock = 32;         // 256 threads
+constexpr int kSrcL1 = 48;
+constexpr int kSrcHash = 128;            // per-source L2 table; used at load <= 1/2
+
+__device__ __forceinline__ int32_t src_slot(int32_t y) {
+  return (int32_t)(((uint32_t)y * 0x9E3779B1u) >> 25);  // 7 bits
+}
+
+__device__ __forceinline__ int32_t src_lookup(const int32_t* hk, const int32_t* hv, int32_t y) {
+  int32_t h = src_slot(y);
+  for (int t = 0; t < kSrcHash; t++) {
+    int32_t k = hk[h];
+    if (k == y) return hv[h];
+    if (k < 0) return -1;
+    h = (h + 1) & (kSrcHash - 1);
+  }
+  return -1;
+}
+
+__device__ __forceinline__ bool src_in_l1(const int32_t* l1, int32_t la, int32_t y) {
+  int32_t lo = 0, hi = la;
+  while (lo < hi) {
+    int32_t mid = (lo + hi) >> 1;
+    int32_t x = l1[mid];
+    if (x < y) lo = mid + 1;
+    else if (x > y) hi = mid;
+    else return true;
+  }
+  return false;
+}
+
+__device__ __forceinline__ uint64_t grp_min_u64(uint64_t x, unsigned mask) {
+#pragma unroll
+  for (int o = kGrp / 2; o > 0; o >>= 1) {
+    uint64_t y = __shfl_xor_sync(mask, x, o, kGrp);
+    x = y < x ? y : x;
+  }
+  return x;
+}
+
+__device__ __forceinline__ int32_t grp_min_i32(int32_t x, unsigned mask) {
+#pragma unroll
+  for (int o = kGrp / 2; o > 0; o >>= 1) x = min(x, __shfl_xor_sync(mask, x, o, kGrp));
+  return x;
+}
+
+// gstart[k] = first index (into Q2) of source group k; groups end at gstart[k+1] (or n2)
+__global__ void __launch_bounds__(kGrp * kGrpPerBlock) k_sep_src(
+    const int32_t* __restrict__ gstart, int64_t ng, int64_t n2, const int32_t* __restrict__ Q2,
+    const int32_t* __restrict__ NQ, const int32_t* __restrict__ u, const int32_t* __restrict__ v,
+    const int32_t* __restrict__ ptr, const int32_t* __restrict__ adj, int L, int32_t* __restrict__ out_len,
+    int32_t* __restrict__ out_nodes, uint8_t* __restrict__ fb) {
+  __shared__ int32_t s_l1[kGrpPerBlock][kSrcL1];
+  __shared__ int32_t s_hk[kGrpPerBlock][kSrcHash];
+  __shared__ int32_t s_hv[kGrpPerBlock][kSrcHash];
+  __shared__ int32_t s_cnt[kGrpPerBlock];
+  const int gi = threadIdx.x / kGrp, lane = threadIdx.x % kGrp;
+  const unsigned mask = 0xFFu << ((threadIdx.x & 31) & ~(kGrp - 1));
+  int32_t* l1 = s_l1[gi];
+  int32_t* hk = s_hk[gi];
+  int32_t* hv = s_hv[gi];
+  const int64_t ngroups = (int64_t)gridDim.x * kGrpPerBlock;
+  for (int64_t k = (int64_t)blockIdx.x * kGrpPerBlock + gi; k < ng; k += ngroups) {
+    const int32_t i0 = gstart[k], i1 = (k + 1 < ng) ? gstart[k + 1] : (int32_t)n2;
+    const int32_t a = u[NQ[Q2[i0]]];
+    const int32_t pa = ptr[a], la = ptr[a + 1] - pa;
+    bool over = la > kSrcL1;
+    if (!over) {
+      for (int32_t j = lane; j < la; j += kGrp) l1[j] = adj[pa + j];
+      for (int32_t j = lane; j < kSrcHash; j += kGrp) hk[j] = -1;
+      if (lane == 0) s_cnt[gi] = 0;
+      __syncwarp(mask);
+      for (int32_t xi = 0; xi < la && !over; xi++) {
+        const int32_t x = l1[xi];
+        const int32_t px = ptr[x], lx = ptr[x + 1] - px;
+        for (int32_t j = lane; j < lx; j += kGrp) {
+          int32_t y = adj[px + j];
+          if (y == a || src_in_l1(l1, la, y)) continue;
+          int32_t h = src_slot(y);
+          for (int t = 0; t < kSrcHash; t++) {
+            int32_t kk = atomicCAS(hk + h, -1, y);
+            if (kk == -1) {
+              hv[h] = x;
+              atomicAdd(s_cnt + gi, 1);
+              break;
+            }
+            if (kk == y) break;  // reached from a smaller x already
+            h = (h + 1) & (kSrcHash - 1);
+          }
+        }
+        __syncwarp(mask);
+        over = s_cnt[gi] > kSrcHash / 2;
+      }
+    }
+    if (over) {
+      for (int32_t i = i0 + lane; i < i1; i += kGrp) fb[i] = 1;
+      __syncwarp(mask);
+      continue;
+    }
+    for (int32_t i = i0; i < i1; i++) {
+      const int32_t q = Q2[i];
+      const int32_t b = v[NQ[q]];
+      const int32_t pb = ptr[b], lb = ptr[b + 1] - pb;
+      int32_t len = 0, r1 = 0, r2 = 0, r3 = 0;
+      uint64_t best = ~0ULL;
+      for (int32_t j = lane; j < lb; j += kGrp) {
+        int32_t y = adj[pb + j];
+        int32_t p = src_lookup(hk, hv, y);
+        if (p >= 0) {
+          uint64_t key = ((uint64_t)(uint32_t)p << 32) | (uint32_t)y;
+          best = key < best ? key : best;
+        }
+      }
+      best = grp_min_u64(best, mask);
+      if (best != ~0ULL) {
+        len = 4; r1 = (int32_t)(best >> 32); r2 = (int32_t)(uint32_t)best;
+      } else if (L >= 5) {
+        uint64_t bk = ~0ULL;
+        int32_t bz = 0x7fffffff;
+        for (int32_t j = lane; j < lb; j += kGrp) {
+          int32_t z = adj[pb + j];
+          if (z == a || src_in_l1(l1, la, z) || src_lookup(hk, hv, z) >= 0) continue;
+          const int32_t pz = ptr[z], lz = ptr[z + 1] - pz;
+          uint64_t zb = ~0ULL;
+          for (int32_t t = 0; t < lz; t++) {
+            int32_t y = adj[pz + t];
+            int32_t p = src_lookup(hk, hv, y);
+            if (p >= 0) {
+              uint64_t key = ((uint64_t)(uint32_t)p << 32) | (uint32_t)y;
+              zb = key < zb ? key : zb;
+            }
+          }
+          if (zb < bk || (zb == bk && z < bz)) { bk = zb; bz = z; }
+        }
+        uint64_t mn = grp_min_u64(bk, mask);
+        int32_t zc = grp_min_i32(bk == mn ? bz : 0x7fffffff, mask);
+        if (mn != ~0ULL) {
+          len = 5; r1 = (int32_t)(mn >> 32); r2 = (int32_t)(uint32_t)mn; r3 = zc;
+        }
+      }
+      if (lane == 0 && len) {
+        int32_t* row = out_nodes + (int64_t)q * L;
+        out_len[q] = len;
+        row[0] = a; row[1] = r1; row[2] = r2;
+        if (len == 4) row[3] = b;
+        else { row[3] = r3; row[4] = b; }
+      }
+    }
+    __syncwarp(mask);
+  }
+}
+
+__global__ void k_src_heads(const int32_t* __restrict__ Q2, int64_t n2, const int32_t* __restrict__ NQ,
+                            const int32_t* __restrict__ u, uint8_t* __restrict__ head) {
+  GRID_STRIDE(i, n2) head[i] = (i == 0) || u[NQ[Q2[i]]] != u[NQ[Q2[i - 1]]];
+}
+
 void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
   ProfScope prof(ctx.s, kFamSeparate);
   RAMA_REQUIRE(L >= 3, "max_len must be at least 3");
@@ -292,22 +466,47 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
     out.nodes.zero();
     return;
   }
+  // triangles: thread per edge, sorted-row intersection
   Buf<uint8_t> miss(nq, ctx);
-  RAMA_KERNEL(ctx, k_sep3, nq, NQ.p, nq, g.u, g.v, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p,
-              L >= 4 ? miss.p : (uint8_t*)nullptr);
+  RAMA_KERNEL(ctx, k_sep3, nq, (const int32_t*)nullptr, nq, NQ.p, g.u, g.v, csr.ptr.p, csr.adj.p, L, out.len.p,
+              out.nodes.p, L >= 4 ? miss.p : (uint8_t*)nullptr);
   if (L < 4) return;
   Buf<int32_t> Q2;
   int64_t n2 = compact_indices(ctx, miss.p, nq, Q2);
   if (n2 == 0) return;
-  RAMA_KERNEL(ctx, k_sep4, n2 * kSepLanes, Q2.p, n2, NQ.p, g.u, g.v, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p,
+  // 4/5-cycles: source-grouped BFS levels in shared memory
+  Buf<uint8_t> head(n2, ctx);
+  RAMA_KERNEL(ctx, k_src_heads, n2, Q2.p, n2, NQ.p, g.u, head.p);
+  Buf<int32_t> gstart;
+  int64_t ng = compact_indices(ctx, head.p, n2, gstart);
+  Buf<uint8_t> fb(n2, ctx);
+  fb.zero();
+  {
+    int64_t blocks = (ng + kGrpPerBlock - 1) / kGrpPerBlock;
+    int64_t cap = (int64_t)148 * 6 * 4;
+    if (blocks > cap) blocks = cap;
+    if (trace_print()) fprintf(stderr, "[rama] k_sep_src groups=%lld\n", (long long)ng);
+    k_sep_src<<<(unsigned)blocks, kGrp * kGrpPerBlock, 0, ctx.s>>>(gstart.p, ng, n2, Q2.p, NQ.p, g.u, g.v,
+                                                                   csr.ptr.p, csr.adj.p, L, out.len.p,
+                                                                   out.nodes.p, fb.p);
+    RAMA_LAUNCH_CHECK();
+    ctx.launches++;
+  }
+  // sources that did not fit the tables: sorted-row intersections
+  Buf<int32_t> I2;
+  int64_t nf = compact_indices(ctx, fb.p, n2, I2);
+  if (nf == 0) return;
+  Buf<int32_t> Q3(nf, ctx);
+  RAMA_KERNEL(ctx, k_gather_i32, nf, Q2.p, I2.p, nf, Q3.p);
+  RAMA_KERNEL(ctx, k_sep4, nf * kSepLanes, Q3.p, nf, NQ.p, g.u, g.v, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p,
               L >= 5 ? miss.p : (uint8_t*)nullptr);
   if (L < 5) return;
   Buf<int32_t> I3;
-  int64_t n3 = compact_indices(ctx, miss.p, n2, I3);
+  int64_t n3 = compact_indices(ctx, miss.p, nf, I3);
   if (n3 == 0) return;
-  Buf<int32_t> Q3(n3, ctx);
-  RAMA_KERNEL(ctx, k_gather_i32, n3, Q2.p, I3.p, n3, Q3.p);
-  RAMA_KERNEL(ctx, k_sep5, n3 * kSepLanes, Q3.p, n3, NQ.p, g.u, g.v, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p);
+  Buf<int32_t> Q4(n3, ctx);
+  RAMA_KERNEL(ctx, k_gather_i32, n3, Q3.p, I3.p, n3, Q4.p);
+  RAMA_KERNEL(ctx, k_sep5, n3 * kSepLanes, Q4.p, n3, NQ.p, g.u, g.v, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p);
 }
 
 // --------------------------------------------------------- triangulation
