@@ -151,14 +151,15 @@ def peak_hbm():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def traffic_from_profiles(family):
-    """dram bytes per launch of the dominant family from the committed ncu summary."""
+def traffic_from_profiles(kernel):
+    """dram read+write bytes of one launch of `kernel` from the committed ncu
+    --set full summary (profiles/ncu_summary.json, round-1 launch of C2)."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
         return None
     with open(p) as fh:
         d = json.load(fh)
-    return d.get("traffic_bytes_per_call", {}).get(family)
+    return d.get("traffic_bytes_per_launch", {}).get(kernel)
 
 
 # ---------------------------------------------------------------- arms
@@ -238,7 +239,6 @@ def b200_arm(args):
         flush.zero_()
     barrier()
     clocks = ClockSampler(local)
-    _lib.profile_enable(True)
     launches0 = _lib.launches
     ms = []
     for _ in range(args.steps):
@@ -251,8 +251,6 @@ def b200_arm(args):
         ms.append(e0.elapsed_time(e1))
         flush.zero_()
     barrier()
-    fam = _lib.profile_read()
-    _lib.profile_enable(False)
     launches = _lib.launches - launches0  # our kernels in the timed region (all steps)
     clk = clocks.stop()
     t_local = sum(ms)
@@ -261,6 +259,23 @@ def b200_arm(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     t_max = float(t.item())
     value = world * m * args.steps / (t_max / 1e3)
+
+    # the same steps again with per-kernel CUDA events (kept out of the timed
+    # region above): kernel and family device times for the roofline
+    _lib.profile_enable(True)
+    p_ms = 0.0
+    for _ in range(args.steps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        e1.synchronize()
+        p_ms += e0.elapsed_time(e1)
+        flush.zero_()
+    fam = _lib.profile_read()
+    kern = _lib.profile_kernels()
+    _lib.profile_enable(False)
 
     # end to end through the C ABI with host buffers
     e2e = None
@@ -294,19 +309,27 @@ def b200_arm(args):
             torch.distributed.destroy_process_group()
         return
 
-    # roofline of the dominant kernel family with defined algorithmic bytes
+    # roofline of the dominant kernel (largest device time in the profiled
+    # steps); algorithmic bytes per launch are defined in DESIGN.md section 4
     peak, peak_src = peak_hbm()
-    cands = {k: vv for k, vv in fam.items() if vv[1] > 0 and vv[0] > 0}
-    dom = max(cands, key=lambda k: cands[k][0]) if cands else None
+    ranked = sorted(kern.items(), key=lambda kv: -kv[1][0])
     roof = None
-    if dom:
-        f_ms, f_bytes, f_cnt = fam[dom]
-        achieved = f_bytes / (f_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "peak_source": peak_src,
-                "traffic": traffic_from_profiles(dom),
-                "algorithmic_bytes_per_step": f_bytes / args.steps, "ms_per_step": f_ms / args.steps,
-                "share_of_step": f_ms / t_local}
+    if ranked:
+        name, (k_ms, k_bytes, k_cnt) = ranked[0]
+        dominant = name
+        if k_bytes <= 0:  # no defined bytes: report the top kernel that has them, and say so
+            with_bytes = [kv for kv in ranked if kv[1][1] > 0]
+            if with_bytes:
+                name, (k_ms, k_bytes, k_cnt) = with_bytes[0]
+        achieved = k_bytes / (k_ms / 1e3) / 1e9 if k_ms > 0 else 0.0
+        roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "peak_source": peak_src, "traffic": traffic_from_profiles(name),
+                "algorithmic_bytes_per_launch": k_bytes / max(k_cnt, 1), "launches_per_step": k_cnt / args.steps,
+                "avg_launch_us": 1e3 * k_ms / max(k_cnt, 1), "share_of_step": k_ms / p_ms,
+                "dominant_kernel": dominant}
+    kernels = [{"kernel": k, "ms_per_step": v[0] / args.steps, "share": v[0] / p_ms, "launches_per_step": v[2] / args.steps,
+                "GB_per_s": (v[1] / (v[0] / 1e3) / 1e9) if v[1] > 0 and v[0] > 0 else None}
+               for k, v in ranked[:12]]
     families = {k: {"ms_per_step": vv[0] / args.steps, "alg_GB_per_step": vv[1] / args.steps / 1e9,
                     "scopes_per_step": vv[2] / args.steps} for k, vv in fam.items() if vv[2]}
 
@@ -334,7 +357,7 @@ def b200_arm(args):
         "solve_time_s": t_max / args.steps / 1e3,
         "objective": {"primal": primal, "lower_bound": lb, "rounds": len(trace), "gap_vs_cpu_reference": gap},
         "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": launches,
-        "kernel_families": families,
+        "top_kernels": kernels, "kernel_families": families,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

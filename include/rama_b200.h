@@ -88,6 +88,11 @@ int64_t rama_last_launch_count(void);
 #define RAMA_PROFILE_FAMILIES 10
 int rama_profile_enable(int32_t on);
 int rama_profile_read(double* ms, double* bytes, int64_t* count);
+/* Per-kernel view of the same timing: JSON text
+ * {"kernel_name": [device_ms, algorithmic_bytes, launches], ...} written to
+ * out (host, cap bytes).  Returns the size needed including the NUL; if
+ * cap is smaller nothing is written. */
+int64_t rama_profile_kernels(char* out, int64_t cap);
 
 /* ---- solver (solver.py:243-252 solve) ------------------------------------ */
 

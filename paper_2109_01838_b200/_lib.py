@@ -65,6 +65,7 @@ _SIGS = {
     "rama_last_launch_count": [],
     "rama_profile_enable": [_i32],
     "rama_profile_read": [_F64P, _F64P, _I64P],
+    "rama_profile_kernels": [ctypes.c_char_p, _i64],
     "rama_solve": [_i64, _vp, _vp, _vp, _i64, ctypes.POINTER(RamaCfg), _vp, _F64P, ctypes.POINTER(RamaRound), _i32,
                    _I32P, _vp],
     "rama_solve_host": [_i64, _vp, _vp, _vp, _i64, ctypes.POINTER(RamaCfg), _vp, _F64P, ctypes.POINTER(RamaRound),
@@ -85,7 +86,8 @@ _SIGS = {
     "rama_reparam_costs": [_i64, _vp, _i64, _vp, _vp, _vp, _vp],
     "rama_lower_bound": [_i64, _vp, _i64, _vp, _vp, _F64P, _vp],
 }
-_RESTYPES = {"rama_last_error": ctypes.c_char_p, "rama_last_launch_count": ctypes.c_int64}
+_RESTYPES = {"rama_last_error": ctypes.c_char_p, "rama_last_launch_count": ctypes.c_int64,
+             "rama_profile_kernels": ctypes.c_int64}
 
 EXPORTED = tuple(_SIGS)
 
@@ -199,3 +201,14 @@ def profile_read():
     cnt = (ctypes.c_int64 * nf)()
     call("rama_profile_read", ms, by, cnt)
     return {f: (ms[i], by[i], cnt[i]) for i, f in enumerate(FAMILIES)}
+
+
+def profile_kernels():
+    """{kernel: (ms, algorithmic_bytes, launches)} timed since profile_enable."""
+    import json
+
+    lib = load()
+    need = lib.rama_profile_kernels(None, 0)
+    buf = ctypes.create_string_buffer(int(need) + 4096)
+    lib.rama_profile_kernels(buf, len(buf))
+    return {k: tuple(v) for k, v in json.loads(buf.value.decode()).items()}

@@ -179,6 +179,8 @@ int rama_profile_read(double* ms, double* bytes, int64_t* count) {
   return guarded(nullptr, [&](Ctx&) { prof_read(ms, bytes, count); });
 }
 
+int64_t rama_profile_kernels(char* out, int64_t cap) { return prof_kernels_json(out, cap); }
+
 int rama_solve(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m, const rama_cfg* cfg,
                int32_t* labels, double* primal_lb, rama_round* trace, int32_t max_trace, int32_t* n_rounds,
                void* stream) {

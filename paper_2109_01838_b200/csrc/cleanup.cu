@@ -674,6 +674,7 @@ int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc) {
       }
       if (trace_print()) fprintf(stderr, "[rama] k_cl_tail np=%lld\n", (long long)np);
       void* kargs[] = {&A};
+      KernelScope ks(ctx.s, "k_cl_tail", 0.0);
       RAMA_CUDA(cudaLaunchCooperativeKernel((const void*)k_cl_tail, dim3(grid_blocks), dim3(kTailThreads), kargs,
                                             kTailSmem, ctx.s));
       ctx.launches++;

@@ -92,6 +92,36 @@ void prof_push(int fam, cudaEvent_t a, cudaEvent_t b, double bytes);
 void prof_read(double* ms, double* bytes, int64_t* count);
 cudaEvent_t prof_event();  // from a recycled pool (no per-scope cudaEventCreate)
 
+// per-kernel timing (same switch): an event pair around one launch, summed
+// per kernel name; `bytes` = that launch's algorithmic bytes (0 = not
+// defined for this kernel).  prof_set_bytes() tags the NEXT RAMA_KERNEL.
+void prof_kernel_push(const char* name, cudaEvent_t a, cudaEvent_t b, double bytes);
+void prof_set_bytes(double bytes);
+double prof_take_bytes();
+// JSON {"kernel": [ms, bytes, launches], ...} of the kernels timed since enable
+int64_t prof_kernels_json(char* out, int64_t cap);
+
+struct KernelScope {
+  cudaStream_t s;
+  const char* name;
+  double bytes;
+  cudaEvent_t a = nullptr, b = nullptr;
+  KernelScope(cudaStream_t st, const char* nm, double by = -1.0) : s(st), name(nm) {
+    bytes = by >= 0.0 ? by : prof_take_bytes();
+    if (prof_enabled()) {
+      a = prof_event();
+      b = prof_event();
+      cudaEventRecord(a, s);
+    }
+  }
+  ~KernelScope() {
+    if (a) {
+      cudaEventRecord(b, s);
+      prof_kernel_push(name, a, b, bytes);
+    }
+  }
+};
+
 struct ProfScope {
   cudaStream_t s;
   int fam;
@@ -202,12 +232,16 @@ bool trace_print();     // RAMA_TRACE=1 or 2: print launches and sync points
 #define RAMA_KERNEL(ctx, kernel, work, ...)                                           \
   do {                                                                                \
     int64_t _w = (int64_t)(work);                                                     \
+    if (_w <= 0) ::rama::prof_take_bytes();                                           \
     if (_w > 0) {                                                                     \
       if (::rama::trace_print()) {                                                    \
         fprintf(stderr, "[rama] %s work=%lld\n", #kernel, (long long)_w);             \
         fflush(stderr);                                                               \
       }                                                                               \
-      kernel<<<::rama::capped_grid(_w), ::rama::kBlock, 0, (ctx).s>>>(__VA_ARGS__);   \
+      {                                                                               \
+        ::rama::KernelScope _ks((ctx).s, #kernel);                                    \
+        kernel<<<::rama::capped_grid(_w), ::rama::kBlock, 0, (ctx).s>>>(__VA_ARGS__); \
+      }                                                                               \
       RAMA_LAUNCH_CHECK();                                                            \
       (ctx).launches++;                                                               \
       if (::rama::trace_enabled()) (ctx).sync();                                      \

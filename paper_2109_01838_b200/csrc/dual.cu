@@ -486,6 +486,10 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
     int64_t cap = (int64_t)148 * 6 * 4;
     if (blocks > cap) blocks = cap;
     if (trace_print()) fprintf(stderr, "[rama] k_sep_src groups=%lld\n", (long long)ng);
+    // algorithmic bytes: the positive CSR once, the miss list and its
+    // edges' endpoints, the cycle rows written
+    KernelScope ks(ctx.s, "k_sep_src",
+                   4.0 * (double)(g.n + 1) + 4.0 * (double)csr.arcs + (16.0 + 4.0 * L) * (double)n2);
     k_sep_src<<<(unsigned)blocks, kGrp * kGrpPerBlock, 0, ctx.s>>>(gstart.p, ng, n2, Q2.p, NQ.p, g.u, g.v,
                                                                    csr.ptr.p, csr.adj.p, L, out.len.p,
                                                                    out.nodes.p, fb.p);
@@ -791,7 +795,9 @@ void message_passing(Ctx& ctx, DualState& st, int iters) {
   ProfScope prof(ctx.s, kFamMP, (double)iters * (132.0 * (double)st.T + 20.0 * (double)st.m_aug));
   Buf<double> delta(st.m_aug, ctx);
   for (int it = 0; it < iters; it++) {
+    prof_set_bytes(20.0 * (double)st.m_aug + 36.0 * (double)st.T);
     RAMA_KERNEL(ctx, k_mp_edge, st.m_aug, st.m_aug, st.base.p, st.slot_ptr.p, st.slots.p, st.lam.p, delta.p);
+    prof_set_bytes(84.0 * (double)st.T);
     RAMA_KERNEL(ctx, k_mp_triplet, st.T, st.T, st.tri_edges.p, delta.p, st.lam.p, 1, 1);
   }
 }

@@ -218,6 +218,7 @@ Graph contract(Ctx& ctx, const GraphView& g, const int32_t* map, int64_t n_targe
   Buf<uint64_t> key(m, ctx);
   Buf<double> jc;
   if (joined) jc.alloc(m, ctx.s);
+  prof_set_bytes(36.0 * (double)m);
   RAMA_KERNEL(ctx, k_contract_prep, m, g.u, g.v, g.c, m, map, (int32_t)n_targets, row.p, key.p,
               joined ? jc.p : (double*)nullptr);
   if (joined) *joined = device_sum(ctx, jc.p, m);

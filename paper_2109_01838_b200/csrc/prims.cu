@@ -17,6 +17,7 @@
 
 #include <mutex>
 #include <map>
+#include <string>
 #include <vector>
 
 namespace rama {
@@ -169,6 +170,33 @@ int64_t g_prof_count[kNumFamilies] = {0};
 
 std::vector<cudaEvent_t> g_event_pool;
 std::mutex g_prof_mu;  // batch solves profile from several host threads
+struct KernRec {
+  const char* name;
+  cudaEvent_t a, b;
+  double bytes;
+};
+std::vector<KernRec> g_kern_recs;
+struct KernSum {
+  double ms = 0, bytes = 0;
+  int64_t count = 0;
+};
+std::map<std::string, KernSum> g_kern_sum;
+thread_local double g_next_bytes = 0.0;
+
+void kern_drain() {
+  for (auto& r : g_kern_recs) {
+    float ms = 0.f;
+    cudaEventSynchronize(r.b);
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    KernSum& k = g_kern_sum[r.name];
+    k.ms += ms;
+    k.bytes += r.bytes;
+    k.count += 1;
+    g_event_pool.push_back(r.a);
+    g_event_pool.push_back(r.b);
+  }
+  g_kern_recs.clear();
+}
 
 void prof_drain() {
   for (auto& r : g_prof_recs) {
@@ -201,9 +229,43 @@ cudaEvent_t prof_event() {
 
 bool prof_enabled() { return g_prof; }
 
+void prof_set_bytes(double bytes) { g_next_bytes = bytes; }
+
+double prof_take_bytes() {
+  double b = g_next_bytes;
+  g_next_bytes = 0.0;
+  return b;
+}
+
+void prof_kernel_push(const char* name, cudaEvent_t a, cudaEvent_t b, double bytes) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_kern_recs.push_back(KernRec{name, a, b, bytes});
+  if (g_kern_recs.size() > 8192) kern_drain();
+}
+
+int64_t prof_kernels_json(char* out, int64_t cap) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  kern_drain();
+  std::string js = "{";
+  char buf[512];
+  bool first = true;
+  for (auto& kv : g_kern_sum) {
+    snprintf(buf, sizeof(buf), "%s\"%s\": [%.6f, %.1f, %lld]", first ? "" : ", ", kv.first.c_str(), kv.second.ms,
+             kv.second.bytes, (long long)kv.second.count);
+    js += buf;
+    first = false;
+  }
+  js += "}";
+  int64_t need = (int64_t)js.size() + 1;
+  if (out && cap >= need) memcpy(out, js.c_str(), need);
+  return need;
+}
+
 void prof_set(bool on) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
   prof_drain();
+  kern_drain();
+  g_kern_sum.clear();
   for (int f = 0; f < kNumFamilies; f++) {
     g_prof_ms[f] = 0.0;
     g_prof_bytes[f] = 0.0;
@@ -258,9 +320,13 @@ int64_t exclusive_scan(Ctx& ctx, const int32_t* in, int32_t* out, int64_t n, boo
     size_t tb = 0;
     RAMA_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, (int)n, ctx.s));
     Buf<uint8_t> tmp(tb, ctx);
-    RAMA_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, in, out, (int)n, ctx.s));
+    {
+      KernelScope ks(ctx.s, "cub::DeviceScan", 8.0 * (double)n);
+      RAMA_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, in, out, (int)n, ctx.s));
+    }
     ctx.launches++;
   }
+  KernelScope ks_tail(ctx.s, "k_scan_tail", 0.0);
   k_scan_tail<<<1, 1, 0, ctx.s>>>(in, out, n);
   RAMA_LAUNCH_CHECK();
   ctx.launches++;
@@ -287,7 +353,10 @@ int64_t compact_indices(Ctx& ctx, const uint8_t* flags, int64_t n, Buf<int32_t>&
   size_t tb = 0;
   RAMA_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, flags, out.p, nsel.p, (int)n, ctx.s));
   Buf<uint8_t> tmp(tb, ctx);
-  RAMA_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, it, flags, out.p, nsel.p, (int)n, ctx.s));
+  {
+    KernelScope ks(ctx.s, "cub::DeviceSelect", 1.0 * (double)n);
+    RAMA_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, it, flags, out.p, nsel.p, (int)n, ctx.s));
+  }
   ctx.launches++;
   return read_scalar(ctx, nsel.p);
 }
@@ -298,6 +367,7 @@ void radix_sort_pairs(Ctx& ctx, const uint64_t* k_in, const int32_t* v_in, uint6
   size_t tb = 0;
   RAMA_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k_in, k_out, v_in, v_out, (int)N, begin_bit, end_bit, ctx.s));
   Buf<uint8_t> tmp(tb, ctx);
+  KernelScope ks(ctx.s, "cub::DeviceRadixSort", 24.0 * (double)N);
   RAMA_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, k_in, k_out, v_in, v_out, (int)N, begin_bit, end_bit, ctx.s));
   ctx.launches++;
 }
@@ -320,20 +390,32 @@ __global__ void k_partial_sum(const double* __restrict__ x, int64_t n, double* _
   if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
 }
 
+// one block, fixed tree order (deterministic)
 __global__ void k_final_sum(const double* part, int np, double* out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double s = 0.0;
-    for (int i = 0; i < np; i++) s += part[i];
-    *out = s;
+  __shared__ double sh[1024];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) acc += part[i];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
   }
+  if (threadIdx.x == 0) *out = sh[0];
 }
 
 double device_sum(Ctx& ctx, const double* x, int64_t n) {
   if (n <= 0) return 0.0;
   Buf<double> part(kSumBlocks + 1, ctx);
-  k_partial_sum<<<kSumBlocks, kBlock, 0, ctx.s>>>(x, n, part.p);
+  {
+    KernelScope ks(ctx.s, "k_partial_sum", 8.0 * (double)n);
+    k_partial_sum<<<kSumBlocks, kBlock, 0, ctx.s>>>(x, n, part.p);
+  }
   RAMA_LAUNCH_CHECK();
-  k_final_sum<<<1, 1, 0, ctx.s>>>(part.p, kSumBlocks, part.p + kSumBlocks);
+  {
+    KernelScope ks(ctx.s, "k_final_sum", 0.0);
+    k_final_sum<<<1, 1024, 0, ctx.s>>>(part.p, kSumBlocks, part.p + kSumBlocks);
+  }
   RAMA_LAUNCH_CHECK();
   ctx.launches += 2;
   return read_scalar(ctx, part.p + kSumBlocks);
@@ -510,6 +592,7 @@ void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint6
   out.row.alloc(N > 0 ? N : 1, ctx.s);
   Buf<int32_t> cnt(R > 0 ? R : 1, ctx), off(N > 0 ? N : 1, ctx);
   cnt.zero();
+  prof_set_bytes(8.0 * (double)N);
   RAMA_KERNEL(ctx, k_bucket_count, N, row, N, cnt.p, off.p);
   int64_t total = exclusive_scan(ctx, cnt.p, out.row_ptr.p, R, true);  // kept items (row >= 0)
   out.total = total;
@@ -519,6 +602,7 @@ void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint6
   }
   Buf<uint64_t> tkey(total, ctx);
   Buf<int32_t> tsrc(total, ctx);
+  prof_set_bytes(16.0 * (double)N + 16.0 * (double)total);
   RAMA_KERNEL(ctx, k_bucket_scatter, N, row, key, off.p, N, out.row_ptr.p, tkey.p, tsrc.p, out.row.p);
   off.release();
   cnt.release();
@@ -527,11 +611,13 @@ void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint6
   int32_t* huge_list = lists.p + sort_rows;
   int32_t* counters = lists.p + 2 * sort_rows;
   RAMA_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(int32_t), ctx.s));
+  prof_set_bytes(32.0 * (double)total);
   RAMA_KERNEL(ctx, k_rank_rows, total, out.row.p, out.row_ptr.p, total, sort_rows, tkey.p, tsrc.p, out.key.p,
               out.src.p, big_list, counters);
   if (!want_row) out.row.release();
   if (sort_rows == 0) return;
   unsigned gb = (unsigned)std::min<int64_t>(std::max<int64_t>(total / 256, 1), 148 * 4);
+  KernelScope ks_block(ctx.s, "k_sort_rows_block", 0.0);
   k_sort_rows_block<<<gb, 512, 0, ctx.s>>>(out.row_ptr.p, big_list, counters, tkey.p, tsrc.p, out.key.p, out.src.p,
                                            huge_list);
   RAMA_LAUNCH_CHECK();
