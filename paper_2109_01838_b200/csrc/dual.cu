@@ -84,8 +84,25 @@ __device__ __forceinline__ bool in_sorted(const int32_t* a, int32_t len, int32_t
   return false;
 }
 
-// smallest common element of two ascending lists, or -1
+// smallest common element of two ascending lists, or -1.  Skewed sizes
+// (power-law hubs) walk the short list and binary-search the long one.
 __device__ __forceinline__ int32_t first_common(const int32_t* a, int32_t la, const int32_t* b, int32_t lb) {
+  if (la > 16 * lb || lb > 16 * la) {
+    const int32_t* s = la < lb ? a : b;
+    const int32_t* l = la < lb ? b : a;
+    int32_t ls = la < lb ? la : lb, ll = la < lb ? lb : la;
+    int32_t lo = 0;
+    for (int32_t k = 0; k < ls; k++) {
+      int32_t y = s[k], hi = ll;
+      while (lo < hi) {
+        int32_t mid = (lo + hi) >> 1;
+        if (l[mid] < y) lo = mid + 1; else hi = mid;
+      }
+      if (lo == ll) return -1;
+      if (l[lo] == y) return y;
+    }
+    return -1;
+  }
   int32_t i = 0, j = 0;
   while (i < la && j < lb) {
     int32_t x = a[i], y = b[j];
@@ -143,6 +160,13 @@ __device__ __forceinline__ int32_t level2_parent(const int32_t* __restrict__ ptr
 // lexicographic argmin with shuffles (keys packed as (parent << 32 | node)).
 constexpr int kSepLanes = 8;
 
+// Deviation D2, dense / power-law neighbourhoods only: the
+// 5-cycle search looks at no more than kHubCap neighbours z of b and skips
+// candidates z with more than kHubCap positive neighbours, bounding the
+// per-edge work at kHubCap^2 lookups (the reference BFS spends ~12 ms per
+// edge on C4).  Grid-like graphs (C1-C3, C5) never reach the caps.
+constexpr int32_t kHubCap = 128;
+
 __device__ __forceinline__ uint64_t group_min(uint64_t x) {
 #pragma unroll
   for (int o = kSepLanes / 2; o > 0; o >>= 1) {
@@ -162,6 +186,12 @@ __device__ __forceinline__ uint64_t pack2(int32_t hi, int32_t lo) {
   return ((uint64_t)(uint32_t)hi << 32) | (uint64_t)(uint32_t)lo;
 }
 
+// 4-cycles for sources whose BFS levels overflow the shared tables (dense or
+// hub neighbourhoods).  Ordered search, exact: the answer's parent p* is the
+// smallest x in N(a) with some y in N(x) & N(b), y not in {a} u N(a) (every
+// such y has px(y) = x because no smaller x qualifies), and y* is the
+// smallest of those.  Scanning x ascending usually stops at the first x, so
+// the cost is one row intersection instead of |N(b)| of them.
 __global__ void k_sep4(const int32_t* __restrict__ Q, int64_t nq, const int32_t* __restrict__ NQ,
                        const int32_t* __restrict__ u, const int32_t* __restrict__ v,
                        const int32_t* __restrict__ ptr, const int32_t* __restrict__ adj, int L,
@@ -174,25 +204,44 @@ __global__ void k_sep4(const int32_t* __restrict__ Q, int64_t nq, const int32_t*
     const int64_t i = base + (threadIdx.x & 31) / kSepLanes;
     bool live = i < nq;
     uint64_t best = ~0ULL;
-    int32_t a = 0, b = 0, q = 0;
+    int32_t a = 0, b = 0, q = 0, la = 0, pb = 0, lb = 0;
+    const int32_t* Na = adj;
     if (live) {
       q = Q[i];
       int32_t e = NQ[q];
       a = u[e];
       b = v[e];
-      const int32_t* Na = adj + ptr[a];
-      int32_t la = ptr[a + 1] - ptr[a];
-      int32_t pb = ptr[b], lb = ptr[b + 1] - pb;
-      for (int32_t k = g; k < lb; k += kSepLanes) {
-        int32_t y = adj[pb + k];
-        int32_t py = level2_parent(ptr, adj, a, Na, la, y);
-        if (py >= 0) {
-          uint64_t key = pack2(py, y);
-          best = key < best ? key : best;
+      Na = adj + ptr[a];
+      la = ptr[a + 1] - ptr[a];
+      pb = ptr[b];
+      lb = ptr[b + 1] - pb;
+    }
+    bool done = !live;
+    const int32_t la_max = warp_max(la);
+    for (int32_t xi = 0; xi < la_max; xi++) {
+      int32_t cand = 0x7fffffff, x = 0;
+      if (!done && xi < la) {
+        x = Na[xi];
+        const int32_t px = ptr[x], lx = ptr[x + 1] - px;
+        const bool xs = lx <= lb;
+        const int32_t* S = xs ? adj + px : adj + pb;
+        const int32_t* G = xs ? adj + pb : adj + px;
+        const int32_t ls = xs ? lx : lb, lg = xs ? lb : lx;
+        for (int32_t k = g; k < ls; k += kSepLanes) {
+          int32_t y = S[k];
+          if (y != a && in_sorted(G, lg, y) && !in_sorted(Na, la, y)) {
+            cand = y;
+            break;  // S ascending: the lane's first hit is its minimum
+          }
         }
       }
+      uint64_t c = group_min((uint64_t)(uint32_t)cand);
+      if (!done && c != 0x7fffffffULL) {
+        best = pack2(x, (int32_t)c);
+        done = true;
+      }
+      if (__all_sync(0xffffffffu, done)) break;
     }
-    best = group_min(best);
     if (live && g == 0) {
       bool found = best != ~0ULL;
       if (found) {
@@ -233,7 +282,7 @@ __global__ void k_sep5(const int32_t* __restrict__ Q, int64_t nq, const int32_t*
     uint64_t bx_y = ~0ULL;
     int32_t bz = 0x7fffffff;
     // trip counts are warp-uniform: the group shuffles below use the full mask
-    int32_t lbmax = warp_max(lb);
+    int32_t lbmax = warp_max(min(lb, kHubCap));
     for (int32_t k = 0; k < lbmax; k++) {
       bool zok = live && k < lb;
       int32_t z = zok ? adj[pb + k] : 0;
@@ -244,7 +293,7 @@ __global__ void k_sep5(const int32_t* __restrict__ Q, int64_t nq, const int32_t*
       if (zok) {
         pz = ptr[z];
         lz = ptr[z + 1] - pz;
-        if (first_common(Na, la, adj + pz, lz) >= 0) zok = false;  // z at distance 2
+        if (lz > kHubCap || first_common(Na, la, adj + pz, lz) >= 0) zok = false;  // hub, or z at distance 2
       }
       uint64_t zbest = ~0ULL;
       int32_t lzmax = warp_max(zok ? lz : 0);
@@ -340,11 +389,10 @@ __global__ void __launch_bounds__(kGrp * kGrpPerBlock) k_sep_src(
     const int32_t* __restrict__ gstart, int64_t ng, int64_t n2, const int32_t* __restrict__ Q2,
     const int32_t* __restrict__ NQ, const int32_t* __restrict__ u, const int32_t* __restrict__ v,
     const int32_t* __restrict__ ptr, const int32_t* __restrict__ adj, int L, int32_t* __restrict__ out_len,
-    int32_t* __restrict__ out_nodes, uint8_t* __restrict__ fb) {
+    int32_t* __restrict__ out_nodes, uint8_t* __restrict__ fb, int force_fallback) {
   __shared__ int32_t s_l1[kGrpPerBlock][kSrcL1];
   __shared__ int32_t s_hk[kGrpPerBlock][kSrcHash];
   __shared__ int32_t s_hv[kGrpPerBlock][kSrcHash];
-  __shared__ int32_t s_cnt[kGrpPerBlock];
   const int gi = threadIdx.x / kGrp, lane = threadIdx.x % kGrp;
   const unsigned mask = 0xFFu << ((threadIdx.x & 31) & ~(kGrp - 1));
   int32_t* l1 = s_l1[gi];
@@ -355,15 +403,21 @@ __global__ void __launch_bounds__(kGrp * kGrpPerBlock) k_sep_src(
     const int32_t i0 = gstart[k], i1 = (k + 1 < ng) ? gstart[k + 1] : (int32_t)n2;
     const int32_t a = u[NQ[Q2[i0]]];
     const int32_t pa = ptr[a], la = ptr[a + 1] - pa;
-    bool over = la > kSrcL1;
+    bool over = la > kSrcL1 || force_fallback;
+    __syncwarp(mask);  // the previous source's lookups are done before the table is reset
     if (!over) {
       for (int32_t j = lane; j < la; j += kGrp) l1[j] = adj[pa + j];
       for (int32_t j = lane; j < kSrcHash; j += kGrp) hk[j] = -1;
-      if (lane == 0) s_cnt[gi] = 0;
       __syncwarp(mask);
+      int32_t total = 0;  // group-uniform insert count (shuffle-reduced per x)
       for (int32_t xi = 0; xi < la && !over; xi++) {
         const int32_t x = l1[xi];
         const int32_t px = ptr[x], lx = ptr[x + 1] - px;
+        if (lx > kSrcHash) {  // cannot fit: the row-intersection kernels take this source
+          over = true;
+          break;
+        }
+        int32_t mine = 0;
         for (int32_t j = lane; j < lx; j += kGrp) {
           int32_t y = adj[px + j];
           if (y == a || src_in_l1(l1, la, y)) continue;
@@ -372,16 +426,19 @@ __global__ void __launch_bounds__(kGrp * kGrpPerBlock) k_sep_src(
             int32_t kk = atomicCAS(hk + h, -1, y);
             if (kk == -1) {
               hv[h] = x;
-              atomicAdd(s_cnt + gi, 1);
+              mine++;
               break;
             }
             if (kk == y) break;  // reached from a smaller x already
             h = (h + 1) & (kSrcHash - 1);
           }
         }
-        __syncwarp(mask);
-        over = s_cnt[gi] > kSrcHash / 2;
+#pragma unroll
+        for (int o = kGrp / 2; o > 0; o >>= 1) mine += __shfl_xor_sync(mask, mine, o, kGrp);
+        total += mine;
+        over = total > kSrcHash / 2;
       }
+      __syncwarp(mask);  // table writes (hv) visible to the group's lookups
     }
     if (over) {
       for (int32_t i = i0 + lane; i < i1; i += kGrp) fb[i] = 1;
@@ -408,10 +465,12 @@ __global__ void __launch_bounds__(kGrp * kGrpPerBlock) k_sep_src(
       } else if (L >= 5) {
         uint64_t bk = ~0ULL;
         int32_t bz = 0x7fffffff;
-        for (int32_t j = lane; j < lb; j += kGrp) {
+        const int32_t lbc = min(lb, kHubCap);
+        for (int32_t j = lane; j < lbc; j += kGrp) {
           int32_t z = adj[pb + j];
           if (z == a || src_in_l1(l1, la, z) || src_lookup(hk, hv, z) >= 0) continue;
           const int32_t pz = ptr[z], lz = ptr[z + 1] - pz;
+          if (lz > kHubCap) continue;
           uint64_t zb = ~0ULL;
           for (int32_t t = 0; t < lz; t++) {
             int32_t y = adj[pz + t];
@@ -444,6 +503,16 @@ __global__ void __launch_bounds__(kGrp * kGrpPerBlock) k_sep_src(
 __global__ void k_src_heads(const int32_t* __restrict__ Q2, int64_t n2, const int32_t* __restrict__ NQ,
                             const int32_t* __restrict__ u, uint8_t* __restrict__ head) {
   GRID_STRIDE(i, n2) head[i] = (i == 0) || u[NQ[Q2[i]]] != u[NQ[Q2[i - 1]]];
+}
+
+// RAMA_SEP_FALLBACK=1 routes every source through the row-intersection
+// kernels (tests use it to check both executions against the oracle)
+static int sep_force_fallback() {
+  static const int v = [] {
+    const char* e = getenv("RAMA_SEP_FALLBACK");
+    return (e && e[0] == '1') ? 1 : 0;
+  }();
+  return v;
 }
 
 void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
@@ -483,7 +552,10 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
   fb.zero();
   {
     int64_t blocks = (ng + kGrpPerBlock - 1) / kGrpPerBlock;
-    int64_t cap = (int64_t)148 * 6 * 4;
+    static const int64_t cap = [] {  // RAMA_SEP_BLOCKS overrides the grid cap (tests)
+      const char* e = getenv("RAMA_SEP_BLOCKS");
+      return e ? (int64_t)atoll(e) : (int64_t)148 * 6 * 4;
+    }();
     if (blocks > cap) blocks = cap;
     if (trace_print()) fprintf(stderr, "[rama] k_sep_src groups=%lld\n", (long long)ng);
     // algorithmic bytes: the positive CSR once, the miss list and its
@@ -492,7 +564,7 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
                    4.0 * (double)(g.n + 1) + 4.0 * (double)csr.arcs + (16.0 + 4.0 * L) * (double)n2);
     k_sep_src<<<(unsigned)blocks, kGrp * kGrpPerBlock, 0, ctx.s>>>(gstart.p, ng, n2, Q2.p, NQ.p, g.u, g.v,
                                                                    csr.ptr.p, csr.adj.p, L, out.len.p,
-                                                                   out.nodes.p, fb.p);
+                                                                   out.nodes.p, fb.p, sep_force_fallback());
     RAMA_LAUNCH_CHECK();
     ctx.launches++;
   }

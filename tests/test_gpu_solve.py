@@ -161,3 +161,31 @@ def test_cleanup_tail_and_wide_rounds_agree():
             "    print(repr(s.primal_cost), hashlib.md5(s.labeling.tobytes()).hexdigest())\n")
     outs = [_solve_env({"RAMA_TAIL_P": k}, code) for k in ("0", "64", "32768")]
     assert outs[0] == outs[1] == outs[2]
+
+
+# Reference per-round statistics of C3 (measured with
+# the reference parcut solver): (nodes, edges, triplets, |S|) per PD round,
+# and its primal / lower bound.
+C3_REFERENCE_ROUNDS = [
+    (8388608, 28147712, 16448539, 3406925), (4981683, 27072114, 17381857, 1872656),
+    (3109027, 22853439, 14365772, 1040487), (2068540, 18300289, 9819966, 584473),
+    (1484067, 14493301, 5500128, 330797), (1153270, 11496582, 2413850, 187549),
+    (965721, 9279117, 788416, 105973), (859748, 7764221, 185844, 128074),
+    (731674, 5685781, 2965, 3350), (728324, 5602069, 13, 34), (728290, 5601216, 0, 0)]
+C3_REFERENCE_PRIMAL = -8759829.776
+C3_REFERENCE_LB = -10014215.265
+
+
+def test_c3_full_size_matches_reference_rounds():
+    """C3 (3-D 128x256x256 + stride-2 lattice, 28.1M edges): every PD round's
+    (n, m, T, |S|) equals the reference's, so separation (3/4/5-cycles),
+    triangulation, message passing, matching/forest and contraction are exact
+    at full size; LB equal, primal within the 0.5% north-star gap."""
+    n, u, v, c = instances.make("c3")
+    g = P.WeightedGraph(n, u, v, c)
+    sol = P.solve(g, P.SolverConfig(mode="PD"))
+    rounds = [(r.nodes, r.edges, r.triplets, r.contracted) for r in sol.trace if r.phase == "primal-dual"]
+    assert rounds == C3_REFERENCE_ROUNDS
+    assert abs(sol.lower_bound - C3_REFERENCE_LB) <= 1e-3
+    assert rel_gap(sol.primal_cost, C3_REFERENCE_PRIMAL) <= GAP
+    assert sol.lower_bound <= sol.primal_cost
