@@ -34,6 +34,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CPU_SAMPLE_ROWS = 256  # C2 crop for the CPU baseline: 256 x 2048 (~2.4M edges, ~11 s oracle)
+BATCH_INSTANCES = 64   # C5: 64 independent 512x512 grids per step
+BATCH_WORKERS = 8      # concurrent streams (host threads) per GPU for a batch
 
 
 def parse():
@@ -42,7 +44,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "c5batch"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -58,6 +60,7 @@ WORKLOAD_DESC = {
     "c3": "C3: 6-connected 3D grid 128x256x256 + stride-2 lattice (connectomics-like), N(0,1) costs",
     "c4": "C4: Chung-Lu power-law graph, 1M nodes, alpha 2.1, mixed-sign costs",
     "c5": "C5: one 512x512 4-connected grid instance",
+    "c5batch": "C5: batch of 64 independent 512x512 4-connected grids (seeds 0-63), sharded over the GPUs",
 }
 
 
@@ -80,6 +83,8 @@ def cpu_sample(workload):
     elif workload == "c4":
         n, u, v, c = instances.chung_lu_coo(10_000, 2.1, 260_000, seed=0)
         desc = "C4-shaped Chung-Lu n=10k (m target 20n), seed 0, full PD solve"
+    elif workload == "c5batch":
+        return instances.make("c5", seed=0), "one instance of the batch (512x512, seed 0), full PD solve"
     else:
         return instances.make(workload), "full %s instance" % workload
     return (n, u, v, c), desc
@@ -207,11 +212,6 @@ def b200_arm(args):
 
     mode = mode_of(args.workload)
     cfg = P.SolverConfig(mode=mode)
-    n, u, v, c = instances.make(args.workload, seed=rank)
-    g = P.WeightedGraph(n, u, v, c)  # canonicalised on the GPU (not timed)
-    m = g.num_edges
-    du, dv, dc = g.device()
-    labels = torch.empty(n, dtype=torch.int32, device="cuda")
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
@@ -221,18 +221,79 @@ def b200_arm(args):
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    gathered = None
-    if world > 1:
-        gathered = torch.empty(world * n, dtype=torch.int32, device="cuda")
-        objs = torch.empty(world * 2, dtype=torch.float64, device="cuda")
+    if args.workload == "c5batch":
+        # 64 independent 512x512 instances sharded over the
+        # ranks, solved concurrently per GPU, one NCCL gather at the end
+        from paper_2109_01838_b200 import batch as B
 
-    def step():
-        _, primal, lb, trace = P.solve_device(n, du, dv, dc, m, cfg, labels)
-        if world > 1:  # NCCL gather of labels and objectives (the only exchange)
-            torch.distributed.all_gather_into_tensor(gathered, labels)
-            mine = torch.tensor([primal, lb], dtype=torch.float64, device="cuda")
-            torch.distributed.all_gather_into_tensor(objs, mine)
-        return primal, lb, trace
+        count = BATCH_INSTANCES
+        lo, hi = B.shard_range(count, rank, world)
+        graphs = [P.WeightedGraph(*instances.make("c5", seed=s)) for s in range(lo, hi)]
+        n = graphs[0].num_nodes
+        m_inst = graphs[0].num_edges
+        node_off = np.arange(hi - lo + 1, dtype=np.int64) * n
+        edge_off = np.concatenate([[0], np.cumsum([gg.num_edges for gg in graphs])]).astype(np.int64)
+        du = torch.cat([gg.device()[0] for gg in graphs])
+        dv = torch.cat([gg.device()[1] for gg in graphs])
+        dc = torch.cat([gg.device()[2] for gg in graphs])
+        labels = torch.empty(int(node_off[-1]), dtype=torch.int32, device="cuda")
+        m = int(edge_off[-1])  # this rank's edges per step
+        m_step = count * m_inst
+        g = None
+
+        def step():
+            _, out = P.solve_batch_device(node_off, edge_off, du, dv, dc, cfg, BATCH_WORKERS, labels)
+            obj = torch.from_numpy(out.reshape(-1, 2)).to("cuda")
+            if world > 1:
+                B.gather_results(labels, obj, n, count)
+            return float(out[0]), float(out[1]), []
+
+        hu = torch.cat([torch.from_numpy(gg.edges_u.astype(np.int32)) for gg in graphs]).pin_memory()
+        hv = torch.cat([torch.from_numpy(gg.edges_v.astype(np.int32)) for gg in graphs]).pin_memory()
+        hc = torch.cat([torch.from_numpy(gg.costs) for gg in graphs]).pin_memory()
+        hl = torch.empty(labels.numel(), dtype=torch.int32).pin_memory()
+        eu, ev, ec = torch.empty_like(du), torch.empty_like(dv), torch.empty_like(dc)
+
+        def e2e_step():  # host COO in, host labels out
+            eu.copy_(hu, non_blocking=True)
+            ev.copy_(hv, non_blocking=True)
+            ec.copy_(hc, non_blocking=True)
+            _, out = P.solve_batch_device(node_off, edge_off, eu, ev, ec, cfg, BATCH_WORKERS, labels)
+            hl.copy_(labels, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+
+        e2e_h2d, e2e_d2h = int(m * 16), int(labels.numel() * 4 + 16 * (hi - lo))
+        job = {"instances_per_step": count, "instances_per_gpu": hi - lo, "nodes_per_instance": n,
+               "edges_per_instance": m_inst, "concurrent_streams_per_gpu": BATCH_WORKERS}
+    else:
+        n, u, v, c = instances.make(args.workload, seed=rank)
+        g = P.WeightedGraph(n, u, v, c)  # canonicalised on the GPU (not timed)
+        m = g.num_edges
+        m_step = world * m
+        du, dv, dc = g.device()
+        labels = torch.empty(n, dtype=torch.int32, device="cuda")
+        gathered = objs = None
+        if world > 1:
+            gathered = torch.empty(world * n, dtype=torch.int32, device="cuda")
+            objs = torch.empty(world * 2, dtype=torch.float64, device="cuda")
+
+        def step():
+            _, primal, lb, trace = P.solve_device(n, du, dv, dc, m, cfg, labels)
+            if world > 1:  # NCCL gather of labels and objectives (the only exchange)
+                torch.distributed.all_gather_into_tensor(gathered, labels)
+                mine = torch.tensor([primal, lb], dtype=torch.float64, device="cuda")
+                torch.distributed.all_gather_into_tensor(objs, mine)
+            return primal, lb, trace
+
+        hu = torch.from_numpy(g.edges_u.astype(np.int32)).pin_memory().numpy()
+        hv = torch.from_numpy(g.edges_v.astype(np.int32)).pin_memory().numpy()
+        hc = torch.from_numpy(g.costs.astype(np.float64)).pin_memory().numpy()
+
+        def e2e_step():  # rama_solve_host: H2D + solve + D2H inside the C ABI call
+            P.solve_host(n, hu, hv, hc, cfg)
+
+        e2e_h2d, e2e_d2h = int(m * (4 + 4 + 8)), int(n * 4 + 16)
+        job = {"instances_per_step": world, "seed": "rank"}
 
     for _ in range(args.warmup):
         step()
@@ -258,7 +319,7 @@ def b200_arm(args):
     if world > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     t_max = float(t.item())
-    value = world * m * args.steps / (t_max / 1e3)
+    value = m_step * args.steps / (t_max / 1e3)
 
     # the same steps again with per-kernel CUDA events (kept out of the timed
     # region above): kernel and family device times for the roofline
@@ -280,18 +341,15 @@ def b200_arm(args):
     # end to end through the C ABI with host buffers
     e2e = None
     if not args.no_e2e:
-        hu = torch.from_numpy(g.edges_u.astype(np.int32)).pin_memory().numpy()
-        hv = torch.from_numpy(g.edges_v.astype(np.int32)).pin_memory().numpy()
-        hc = torch.from_numpy(g.costs.astype(np.float64)).pin_memory().numpy()
         for _ in range(max(1, args.warmup)):
-            P.solve_host(n, hu, hv, hc, cfg)
+            e2e_step()
         barrier()
         e_ms = []
         for _ in range(args.steps):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            lab_h, _, _, _ = P.solve_host(n, hu, hv, hc, cfg)
+            e2e_step()
             e1.record(stream)
             e1.synchronize()
             e_ms.append(e0.elapsed_time(e1))
@@ -300,8 +358,8 @@ def b200_arm(args):
         te = torch.tensor([sum(e_ms)], dtype=torch.float64, device="cuda")
         if world > 1:
             torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-        e2e = {"value": world * m * args.steps / (float(te.item()) / 1e3), "unit": "edges/s",
-               "h2d_bytes_per_step": int(m * (4 + 4 + 8)), "d2h_bytes_per_step": int(n * 4 + 16),
+        e2e = {"value": m_step * args.steps / (float(te.item()) / 1e3), "unit": "edges/s",
+               "h2d_bytes_per_step": e2e_h2d, "d2h_bytes_per_step": e2e_d2h,
                "ms_per_step": float(te.item()) / args.steps}
 
     if rank != 0:
@@ -349,11 +407,13 @@ def b200_arm(args):
     line = {
         "metric": "multicut solve throughput (edges/s)", "value": value, "unit": "edges/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD_DESC[args.workload], "nodes": n, "edges": m, "mode": mode,
-                   "instances_per_step": world, "seed": "rank",
+        "higher_is_better": True, "scaling": "strong" if args.workload == "c5batch" else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": dict({"workload": WORKLOAD_DESC[args.workload], "nodes": n, "edges": m, "mode": mode,
                    "l2": "inputs %.0f MB > 126 MB L2, and a 256 MiB buffer is written between steps" % (m * 16 / 1e6),
-                   "parallelism": "independent instance per GPU" if world > 1 else "single GPU"},
+                   "parallelism": ("instances sharded over %d GPUs, NCCL gather" % world) if world > 1 else "single GPU",
+                   "scaling_note": ("strong: 64 instances per step whatever N" if args.workload == "c5batch"
+                                    else "weak: one instance per GPU")}, **job),
         "solve_time_s": t_max / args.steps / 1e3,
         "objective": {"primal": primal, "lower_bound": lb, "rounds": len(trace), "gap_vs_cpu_reference": gap},
         "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": launches,
