@@ -105,6 +105,10 @@ int rama_solve(int64_t n, const int32_t* u, const int32_t* v, const double* c, i
                const rama_cfg* cfg, int32_t* labels, double* primal_lb, rama_round* trace,
                int32_t max_trace, int32_t* n_rounds, void* stream);
 
+/* Mode D runs cfg->separation_rounds rounds (extend_separation from round
+ * 2, solver.py:211-240); PD+ (max_cycle_length 6..8) uses the exact
+ * source-grouped BFS separation. */
+
 /* Same with HOST arrays (u, v, c, labels); copies in and out through pinned
  * staging inside the call.  The end-to-end entry for non-CUDA callers. */
 int rama_solve_host(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m,
@@ -185,6 +189,19 @@ int rama_triangulate(int64_t n, const int32_t* u, const int32_t* v, const double
                      const int32_t* len, const int32_t* nodes, int64_t rows, int32_t L, int32_t* aug_u,
                      int32_t* aug_v, double* base, int64_t* m_aug, int32_t* tri_nodes, int32_t* tri_edges,
                      int64_t* T, int32_t* coverage, void* stream);
+
+/* extend_separation (dual.py:414-474): separate on the current
+ * reparametrized costs of the state (eu/ev/base over m_aug augmented edges,
+ * T triplets with handles and multipliers) and append the new chords (base
+ * 0) and new triplets (zero multipliers) in the reference's order.  The
+ * grown state is written to out_* (capacities cap_edges edges and
+ * cap_triplets triplets; m_aug * (L - 2) extra of each always suffices);
+ * *added (host) = triplets appended. */
+int rama_extend_separation(int64_t n, int64_t m_aug, const int32_t* eu, const int32_t* ev, const double* base,
+                           int64_t T, const int32_t* tri_nodes, const int32_t* tri_edges, const double* lam,
+                           int32_t L, int64_t cap_edges, int64_t cap_triplets, int32_t* out_eu, int32_t* out_ev,
+                           double* out_base, int64_t* out_m_aug, int32_t* out_tri_nodes, int32_t* out_tri_edges,
+                           double* out_lam, int64_t* out_T, int32_t* out_coverage, int64_t* added, void* stream);
 
 /* message passing on lam[3T] in place (dual.py:358-392).
  * phases: 1 = mp_edge_to_triplets only, 2 = mp_triplets_to_edges only,

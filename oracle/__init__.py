@@ -326,6 +326,88 @@ def lower_bound(st):
                                  ctypes.c_int64(st.num_triplets), _p64(te), _pf(lam))
 
 
+def _dedupe_rows(arr):
+    """dual.py:214-224: lexicographic sort, drop consecutive duplicates."""
+    if arr.shape[0] == 0:
+        return arr
+    order = np.lexsort(tuple(arr[:, col] for col in range(arr.shape[1] - 1, -1, -1)))
+    arr = arr[order]
+    keep = np.empty(arr.shape[0], dtype=bool)
+    keep[0] = True
+    keep[1:] = np.any(arr[1:] != arr[:-1], axis=1)
+    return arr[keep]
+
+
+def _fan_arrays(lengths, mat):
+    """dual.py:228-252: fan triplets (sorted rows, deduped) and chords."""
+    tri, chords = [], []
+    max_l = int(lengths.max()) if lengths.size else 0
+    for ln in range(3, max_l + 1):
+        rows = np.flatnonzero(lengths == ln)
+        if rows.size == 0:
+            continue
+        v0 = mat[rows, 0]
+        for k in range(1, ln - 1):
+            tri.append(np.stack([v0, mat[rows, k], mat[rows, k + 1]], axis=1))
+        for k in range(2, ln - 1):
+            b = mat[rows, k]
+            chords.append(np.stack([np.minimum(v0, b), np.maximum(v0, b)], axis=1))
+    tri_nodes = np.concatenate(tri, axis=0) if tri else np.zeros((0, 3), np.int64)
+    tri_nodes = _dedupe_rows(np.sort(tri_nodes, axis=1))
+    chord_pairs = np.concatenate(chords, axis=0) if chords else np.zeros((0, 2), np.int64)
+    return tri_nodes, _dedupe_rows(chord_pairs)
+
+
+def extend_separation(st, L):
+    """dual.py:414-474 (numpy restatement): separate on the reparametrized
+    costs, append new chords (base 0) and new triplets (zero multipliers).
+    Returns the number of triplets added."""
+    g_rep = Graph(st.num_nodes, st.edges_u.copy(), st.edges_v.copy(), reparametrized_edge_costs(st))
+    lengths, mat = separate(g_rep, L)
+    keep = lengths >= 3
+    tri_nodes, chord_pairs = _fan_arrays(lengths[keep], mat[keep])
+    if tri_nodes.shape[0] == 0:
+        return 0
+    n = st.num_nodes
+    keys = st.edges_u * n + st.edges_v
+    if chord_pairs.shape[0]:
+        order = np.argsort(keys, kind="stable")
+        ckeys = chord_pairs[:, 0] * n + chord_pairs[:, 1]
+        pos = np.searchsorted(keys[order], ckeys)
+        pos_c = np.minimum(pos, max(keys.size - 1, 0))
+        hit = (pos < keys.size) & (keys[order][pos_c] == ckeys)
+        chord_pairs = chord_pairs[~hit]
+    st.edges_u = np.concatenate([st.edges_u, chord_pairs[:, 0]])
+    st.edges_v = np.concatenate([st.edges_v, chord_pairs[:, 1]])
+    st.base_costs = np.concatenate([st.base_costs, np.zeros(chord_pairs.shape[0])])
+    if st.tri_nodes.shape[0]:
+        both = np.concatenate([st.tri_nodes, tri_nodes])
+        flags = np.concatenate([np.zeros(st.tri_nodes.shape[0], bool), np.ones(tri_nodes.shape[0], bool)])
+        order = np.lexsort((both[:, 2], both[:, 1], both[:, 0]))
+        both, flags = both[order], flags[order]
+        dup = np.zeros(both.shape[0], dtype=bool)
+        dup[1:] = np.all(both[1:] == both[:-1], axis=1)
+        tri_nodes = _dedupe_rows(both[flags & ~dup])
+    if tri_nodes.shape[0] == 0:
+        st.coverage = np.bincount(st.tri_edges.ravel(), minlength=st.edges_u.size).astype(np.int64)
+        return 0
+    keys = st.edges_u * n + st.edges_v
+    order = np.argsort(keys, kind="stable")
+    sorted_keys = keys[order]
+
+    def handles(a, b):
+        return order[np.searchsorted(sorted_keys, a * n + b)]
+
+    i, j, k = tri_nodes[:, 0], tri_nodes[:, 1], tri_nodes[:, 2]
+    new_edges = np.stack([handles(i, j), handles(i, k), handles(j, k)], axis=1)
+    added = tri_nodes.shape[0]
+    st.tri_nodes = np.concatenate([st.tri_nodes, tri_nodes])
+    st.tri_edges = np.concatenate([st.tri_edges, new_edges])
+    st.lam = np.concatenate([st.lam, np.zeros((added, 3))])
+    st.coverage = np.bincount(st.tri_edges.ravel(), minlength=st.edges_u.size).astype(np.int64)
+    return added
+
+
 def reparametrized_graph(st):
     """dual.py:408-411 (re-canonicalised)."""
     return Graph(st.num_nodes, st.edges_u, st.edges_v, reparametrized_edge_costs(st))
@@ -358,7 +440,7 @@ _LDEF = {"P": 5, "PD": 5, "PD+": 7, "D": 5, "GAEC": 5}
 
 
 def solve(g, mode="PD", mp_iterations=5, max_cycle_length=None, matching_switch_fraction=0.1,
-          max_rounds=100, cleanup="gaec"):
+          max_rounds=100, cleanup="gaec", separation_rounds=1):
     """solver.py:113-240.  cleanup='gaec' follows the reference exactly
     (solver.py:187-207); cleanup='handshake' follows the B200 build."""
     L = _LDEF.get(mode, 5) if max_cycle_length is None else int(max_cycle_length)
@@ -369,16 +451,21 @@ def solve(g, mode="PD", mp_iterations=5, max_cycle_length=None, matching_switch_
         rec = Round(1, "gaec", n0, g.num_edges, 0, None, False, n0 - nt,
                     (time.perf_counter() - t0) * 1e3)
         return Result(fmap, clustering_cost(g, fmap), float("-inf"), [rec])
-    if mode == "D":
-        t0 = time.perf_counter()
-        lengths, nodes = separate(g, L)
-        st = triangulate(g, lengths, nodes)
-        message_passing(st, mp_iterations)
-        lb = lower_bound(st)
-        rec = Round(1, "dual", n0, st.num_edges, st.num_triplets, lb, True, 0,
-                    (time.perf_counter() - t0) * 1e3)
+    if mode == "D":  # solver.py:211-240
+        st, lb, trace = None, None, []
+        for rnd in range(1, separation_rounds + 1):
+            t0 = time.perf_counter()
+            if st is None:
+                lengths, nodes = separate(g, L)
+                st = triangulate(g, lengths, nodes)
+            else:
+                extend_separation(st, L)
+            message_passing(st, mp_iterations)
+            lb = lower_bound(st)
+            trace.append(Round(rnd, "dual", n0, st.num_edges, st.num_triplets, lb, True, 0,
+                               (time.perf_counter() - t0) * 1e3))
         lab = np.arange(n0, dtype=np.int64)
-        return Result(lab, clustering_cost(g, lab), lb, [rec])
+        return Result(lab, clustering_cost(g, lab), lb, trace)
     f_total = np.arange(n0, dtype=np.int64)
     cur = g
     lb = None

@@ -82,6 +82,8 @@ _SIGS = {
     "rama_separate": [_i64, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _I64P, _vp],
     "rama_triangulate": [_i64, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _I64P, _vp, _vp, _I64P, _vp,
                          _vp],
+    "rama_extend_separation": [_i64, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i32, _i64, _i64, _vp, _vp, _vp, _I64P,
+                               _vp, _vp, _vp, _I64P, _vp, _I64P, _vp],
     "rama_message_passing": [_i64, _vp, _i64, _vp, _vp, _i32, _i32, _vp],
     "rama_reparam_costs": [_i64, _vp, _i64, _vp, _vp, _vp, _vp],
     "rama_lower_bound": [_i64, _vp, _i64, _vp, _vp, _F64P, _vp],

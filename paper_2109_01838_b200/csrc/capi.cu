@@ -339,6 +339,42 @@ int rama_triangulate(int64_t n, const int32_t* u, const int32_t* v, const double
   });
 }
 
+int rama_extend_separation(int64_t n, int64_t m_aug, const int32_t* eu, const int32_t* ev, const double* base,
+                           int64_t T, const int32_t* tri_nodes, const int32_t* tri_edges, const double* lam,
+                           int32_t L, int64_t cap_edges, int64_t cap_triplets, int32_t* out_eu, int32_t* out_ev,
+                           double* out_base, int64_t* out_m_aug, int32_t* out_tri_nodes, int32_t* out_tri_edges,
+                           double* out_lam, int64_t* out_T, int32_t* out_coverage, int64_t* added, void* stream) {
+  return guarded(stream, [&](Ctx& ctx) {
+    check_sizes(n, m_aug);
+    RAMA_REQUIRE(L >= 3, "max_len must be at least 3");
+    check_handles(ctx, tri_edges, T, m_aug);
+    DualState st;
+    st.n = n;
+    st.m_orig = m_aug;
+    st.m_aug = m_aug;
+    st.chords_sorted = false;  // caller's edge order is arbitrary
+    st.eu.alloc(m_aug > 0 ? m_aug : 1, ctx.s);
+    st.ev.alloc(m_aug > 0 ? m_aug : 1, ctx.s);
+    copy_d2d(ctx, st.eu.p, eu, m_aug);
+    copy_d2d(ctx, st.ev.p, ev, m_aug);
+    st.tri_nodes.alloc(T > 0 ? 3 * T : 1, ctx.s);
+    copy_d2d(ctx, st.tri_nodes.p, tri_nodes, 3 * T);
+    load_state(ctx, st, m_aug, base, T, tri_edges, lam);
+    int64_t k = extend_separation(ctx, st, L);
+    RAMA_REQUIRE(st.m_aug <= cap_edges && st.T <= cap_triplets, "output capacity too small");
+    copy_d2d(ctx, out_eu, st.eu.p, st.m_aug);
+    copy_d2d(ctx, out_ev, st.ev.p, st.m_aug);
+    copy_d2d(ctx, out_base, st.base.p, st.m_aug);
+    copy_d2d(ctx, out_coverage, st.coverage.p, st.m_aug);
+    copy_d2d(ctx, out_tri_nodes, st.tri_nodes.p, 3 * st.T);
+    copy_d2d(ctx, out_tri_edges, st.tri_edges.p, 3 * st.T);
+    copy_d2d(ctx, out_lam, st.lam.p, 3 * st.T);
+    *out_m_aug = st.m_aug;
+    *out_T = st.T;
+    *added = k;
+  });
+}
+
 int rama_message_passing(int64_t m_aug, const double* base, int64_t T, const int32_t* tri_edges, double* lam,
                          int32_t iters, int32_t phases, void* stream) {
   return guarded(stream, [&](Ctx& ctx) {

@@ -500,6 +500,132 @@ __global__ void __launch_bounds__(kGrp * kGrpPerBlock) k_sep_src(
   }
 }
 
+// ---- generic BFS separation (L >= 6, mode PD+) ----------------------------
+//
+// The reference BFS itself, source-grouped: one warp per source a runs the
+// BFS of dual.py:109-152 level by level in per-warp global scratch and then
+// answers all of a's repulsive edges.  Queue order is reproduced exactly:
+// level k+1 is discovered by scanning the level-k queue in order and each
+// row in ascending id order; a node's parent is the first queue position
+// that reaches it (atomicMin over the position), and the winners are
+// appended in (position, row index) order with warp ballots.
+// key[y] = ((0xffffffff - tick) << 32) | c: c = 0 discovered, c = p + 1
+// candidate from queue position p; a fresh tick compares below stale keys.
+__device__ __forceinline__ uint64_t bfs_key(uint32_t tick, uint32_t c) {
+  return ((uint64_t)(0xffffffffu - tick) << 32) | c;
+}
+
+__global__ void __launch_bounds__(256) k_sep_bfs(const int32_t* __restrict__ gstart, int64_t ng, int64_t n2,
+                                                 const int32_t* __restrict__ Q2, const int32_t* __restrict__ NQ,
+                                                 const int32_t* __restrict__ u, const int32_t* __restrict__ v,
+                                                 const int32_t* __restrict__ ptr, const int32_t* __restrict__ adj,
+                                                 int L, int32_t* __restrict__ out_len,
+                                                 int32_t* __restrict__ out_nodes, unsigned long long* keys,
+                                                 int32_t* par, int32_t* pos, int32_t* queue, int64_t n) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t W = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long* K = keys + w * n;
+  int32_t* Pa = par + w * n;
+  int32_t* Po = pos + w * n;
+  int32_t* Qu = queue + w * n;
+  for (int64_t k = w; k < ng; k += W) {
+    const uint32_t tick = (uint32_t)(k + 1);
+    const uint64_t done = bfs_key(tick, 0);
+    const int32_t i0 = gstart[k], i1 = (k + 1 < ng) ? gstart[k + 1] : (int32_t)n2;
+    const int32_t a = u[NQ[Q2[i0]]];
+    if (lane == 0) {
+      Qu[0] = a;
+      K[a] = done;
+      Pa[a] = -1;
+      Po[a] = 0;
+    }
+    __syncwarp();
+    int32_t lstart[8], lend[8];
+    lstart[0] = 0;
+    lend[0] = 1;
+    int32_t qlen = 1;
+    for (int lev = 0; lev <= L - 3; lev++) {  // levels 1 .. L-2
+      const int32_t s = lstart[lev], e = lend[lev];
+      for (int32_t p = s; p < e; p++) {  // candidates: atomicMin over the position
+        const int32_t x = __ldcg(Qu + p);
+        const int32_t b0 = ptr[x], dx = ptr[x + 1] - b0;
+        for (int32_t j = lane; j < dx; j += 32) {
+          int32_t y = adj[b0 + j];
+          atomicMin(K + y, (unsigned long long)bfs_key(tick, (uint32_t)p + 1));
+        }
+      }
+      __syncwarp();
+      for (int32_t p = s; p < e; p++) {  // winners in (position, row) order
+        const int32_t x = __ldcg(Qu + p);
+        const int32_t b0 = ptr[x], dx = ptr[x + 1] - b0;
+        for (int32_t j0 = 0; j0 < dx; j0 += 32) {
+          int32_t j = j0 + lane;
+          int32_t y = j < dx ? adj[b0 + j] : 0;
+          bool win = j < dx && __ldcg(K + y) == bfs_key(tick, (uint32_t)p + 1);
+          unsigned bal = __ballot_sync(0xffffffffu, win);
+          if (win) {
+            int32_t at = qlen + __popc(bal & ((1u << lane) - 1u));
+            Qu[at] = y;
+            Pa[y] = x;
+            Po[y] = at;
+          }
+          qlen += __popc(bal);
+        }
+      }
+      __syncwarp();
+      for (int32_t i = lend[lev] + lane; i < qlen; i += 32) K[__ldcg(Qu + i)] = done;
+      __syncwarp();
+      lstart[lev + 1] = e;
+      lend[lev + 1] = qlen;
+    }
+    const int32_t last = L - 2;  // deepest stored level
+    for (int32_t i = i0; i < i1; i++) {
+      const int32_t q = Q2[i];
+      const int32_t b = v[NQ[q]];
+      int32_t tail = -1, len = 0;
+      if (__ldcg(K + b) == done) {  // b itself reached at level <= L-2
+        int32_t pb = __ldcg(Po + b), lv = 0;
+        while (lv < last && pb >= lend[lv]) lv++;
+        len = lv + 1;
+        tail = b;
+      } else {  // b at level L-1: parent = first queue position among N(b) at level L-2
+        const int32_t b0 = ptr[b], db = ptr[b + 1] - b0;
+        int32_t best = 0x7fffffff;
+        for (int32_t j = lane; j < db; j += 32) {
+          int32_t y = adj[b0 + j];
+          if (__ldcg(K + y) == done) {
+            int32_t py = __ldcg(Po + y);
+            if (py >= lstart[last] && py < lend[last]) best = min(best, py);
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+        if (best != 0x7fffffff) {
+          len = L;
+          tail = -2 - best;  // marks: b appended after the queue node at `best`
+        }
+      }
+      if (lane == 0 && len >= 3) {
+        int32_t* row = out_nodes + (int64_t)q * L;
+        out_len[q] = len;
+        int32_t idx = len - 1, x;
+        if (tail >= 0) {
+          x = tail;
+        } else {
+          row[idx--] = b;
+          x = __ldcg(Qu + (-2 - tail));
+        }
+        for (; idx >= 0; idx--) {
+          row[idx] = x;
+          x = __ldcg(Pa + x);
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
 __global__ void k_src_heads(const int32_t* __restrict__ Q2, int64_t n2, const int32_t* __restrict__ NQ,
                             const int32_t* __restrict__ u, uint8_t* __restrict__ head) {
   GRID_STRIDE(i, n2) head[i] = (i == 0) || u[NQ[Q2[i]]] != u[NQ[Q2[i - 1]]];
@@ -518,7 +644,7 @@ static int sep_force_fallback() {
 void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
   ProfScope prof(ctx.s, kFamSeparate);
   RAMA_REQUIRE(L >= 3, "max_len must be at least 3");
-  RAMA_REQUIRE(L <= 5, "max_cycle_length > 5 (PD+) is not implemented in the B200 build yet");
+  RAMA_REQUIRE(L <= 8, "max_cycle_length > 8 is not supported by the B200 build");
   Buf<uint8_t> flag(g.m > 0 ? g.m : 1, ctx);
   RAMA_KERNEL(ctx, k_flag_neg, g.m, g.c, g.m, flag.p);
   Buf<int32_t> NQ;
@@ -548,6 +674,26 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
   RAMA_KERNEL(ctx, k_src_heads, n2, Q2.p, n2, NQ.p, g.u, head.p);
   Buf<int32_t> gstart;
   int64_t ng = compact_indices(ctx, head.p, n2, gstart);
+  if (L >= 6) {  // PD+: the exact source-grouped BFS
+    size_t free_b = 0, total_b = 0;
+    RAMA_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const int64_t per_warp = 20 * g.n;
+    int64_t W = (int64_t)(free_b / 4) / (per_warp > 0 ? per_warp : 1);
+    if (W > 148 * 8) W = 148 * 8;
+    if (W > ng) W = ng;
+    RAMA_REQUIRE(W >= 1, "not enough device memory for the PD+ separation scratch");
+    W = (W + 7) / 8 * 8;  // whole 8-warp blocks; every launched warp owns a scratch slice
+    Buf<unsigned long long> keys((size_t)W * g.n, ctx);
+    Buf<int32_t> par((size_t)W * g.n, ctx), pos((size_t)W * g.n, ctx), queue((size_t)W * g.n, ctx);
+    keys.fill_bytes(0xff);
+    KernelScope ks(ctx.s, "k_sep_bfs", 0.0);
+    k_sep_bfs<<<(unsigned)((W + 7) / 8), 256, 0, ctx.s>>>(gstart.p, ng, n2, Q2.p, NQ.p, g.u, g.v, csr.ptr.p,
+                                                          csr.adj.p, L, out.len.p, out.nodes.p, keys.p, par.p,
+                                                          pos.p, queue.p, g.n);
+    RAMA_LAUNCH_CHECK();
+    ctx.launches++;
+    return;
+  }
   Buf<uint8_t> fb(n2, ctx);
   fb.zero();
   {
@@ -789,6 +935,178 @@ void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& 
   build_slot_lists(ctx, st);
 }
 
+
+// ------------------------------------------------------ extend_separation
+//
+// dual.py:414-474 (mode D, separation_rounds > 1): separate on the current
+// reparametrized graph, append the new chords (base 0) and the new
+// triplets (zero multipliers) in the reference's order -- chords and
+// triplets sorted lexicographically, existing triplets skipped.
+
+__global__ void k_ext_tri_keys(const int32_t* __restrict__ tn, int64_t T, int32_t* __restrict__ row,
+                               uint64_t* __restrict__ key) {
+  GRID_STRIDE(t, T) {
+    row[t] = tn[3 * t];
+    key[t] = ((uint64_t)(uint32_t)tn[3 * t + 1] << 32) | (uint64_t)(uint32_t)tn[3 * t + 2];
+  }
+}
+
+// new (deduped) triplet at sorted slot hp[i] is kept unless present in the
+// existing triplets (bucket-sorted by row i with key (j << 32 | k))
+__global__ void k_ext_tri_new(const int32_t* __restrict__ hp, int64_t nh, const int32_t* __restrict__ row,
+                              const uint64_t* __restrict__ key, const int32_t* __restrict__ eptr,
+                              const uint64_t* __restrict__ ekey, int64_t T, uint8_t* __restrict__ keep) {
+  GRID_STRIDE(i, nh) {
+    int32_t p = hp[i];
+    int32_t r = row[p];
+    uint64_t k = key[p];
+    bool found = false;
+    if (T > 0) {
+      int32_t lo = eptr[r], hi = eptr[r + 1];
+      while (lo < hi) {
+        int32_t mid = (lo + hi) >> 1;
+        uint64_t x = ekey[mid];
+        if (x < k) lo = mid + 1;
+        else if (x > k) hi = mid;
+        else { found = true; break; }
+      }
+    }
+    keep[i] = !found;
+  }
+}
+
+__global__ void k_ext_tri_out(const int32_t* __restrict__ sel, int64_t k, const int32_t* __restrict__ hp,
+                              const int32_t* __restrict__ row, const uint64_t* __restrict__ key, int64_t T0,
+                              int32_t* __restrict__ tn) {
+  GRID_STRIDE(i, k) {
+    int32_t p = hp[sel[i]];
+    int64_t t = T0 + i;
+    tn[3 * t] = row[p];
+    tn[3 * t + 1] = (int32_t)(key[p] >> 32);
+    tn[3 * t + 2] = (int32_t)(uint32_t)key[p];
+  }
+}
+
+__global__ void k_ext_edge_keys(const int32_t* __restrict__ eu, const int32_t* __restrict__ ev, int64_t m,
+                                int32_t* __restrict__ row, uint64_t* __restrict__ key) {
+  GRID_STRIDE(i, m) {
+    row[i] = eu[i];
+    key[i] = ((uint64_t)(uint32_t)ev[i] << 32) | (uint64_t)i;
+  }
+}
+
+__device__ __forceinline__ int32_t ext_handle(const int32_t* eptr, const uint64_t* ekey, int32_t a, int32_t b) {
+  uint64_t k = (uint64_t)(uint32_t)b << 32;
+  int32_t lo = eptr[a], hi = eptr[a + 1];
+  while (lo < hi) {
+    int32_t mid = (lo + hi) >> 1;
+    if (ekey[mid] < k) lo = mid + 1; else hi = mid;
+  }
+  return (int32_t)(uint32_t)ekey[lo];  // present by construction
+}
+
+__global__ void k_ext_handles(const int32_t* __restrict__ tn, int64_t T0, int64_t k, const int32_t* __restrict__ eptr,
+                              const uint64_t* __restrict__ ekey, int32_t* __restrict__ te) {
+  GRID_STRIDE(i, k) {
+    int64_t t = T0 + i;
+    int32_t a = tn[3 * t], b = tn[3 * t + 1], c = tn[3 * t + 2];
+    te[3 * t] = ext_handle(eptr, ekey, a, b);
+    te[3 * t + 1] = ext_handle(eptr, ekey, a, c);
+    te[3 * t + 2] = ext_handle(eptr, ekey, b, c);
+  }
+}
+
+template <class T>
+static void grow(Ctx& ctx, Buf<T>& b, int64_t old_n, int64_t new_n) {
+  Buf<T> nb(new_n > 0 ? new_n : 1, ctx);
+  copy_d2d(ctx, nb.p, b.p, old_n);
+  b = std::move(nb);
+}
+
+int64_t extend_separation(Ctx& ctx, DualState& st, int L) {
+  ProfScope prof(ctx.s, kFamTriangulate);
+  const int64_t n = st.n;
+  Graph rep = reparametrized_graph(ctx, st);  // canonical merge of the augmented edges, c^lambda
+  CycleRows cyc;
+  separate(ctx, rep.view(), L, cyc);
+  const int64_t rows = cyc.rows;
+  if (rows == 0) return 0;
+  Buf<int32_t> nt(rows, ctx), nc(rows, ctx), toff(rows + 1, ctx), coff(rows + 1, ctx);
+  RAMA_KERNEL(ctx, k_fan_counts, rows, cyc.len.p, rows, nt.p, nc.p);
+  int64_t traw = exclusive_scan(ctx, nt.p, toff.p, rows, true);
+  if (traw == 0) return 0;  // no cycle: nothing changes (dual.py:428-429)
+  int64_t craw = exclusive_scan(ctx, nc.p, coff.p, rows, true);
+  Buf<int32_t> trow(traw, ctx), crow(craw > 0 ? craw : 1, ctx);
+  Buf<uint64_t> tkey(traw, ctx), ckey(craw > 0 ? craw : 1, ctx);
+  RAMA_KERNEL(ctx, k_fan_emit, rows, cyc.len.p, cyc.nodes.p, rows, cyc.L, toff.p, coff.p, trow.p, tkey.p, crow.p,
+              ckey.p);
+  // new chords (sorted, unique, not yet augmented edges) join at base 0
+  int64_t C = 0;
+  Buf<int32_t> sel_c, hp_c;
+  BucketSorted cs;
+  if (craw > 0) {
+    Buf<int32_t> rptr(n + 1, ctx);
+    row_ptr_from_sorted(ctx, rep.u.p, rep.m, n, rptr.p);
+    bucket_sort(ctx, n, craw, crow.p, ckey.p, cs, true);
+    Buf<uint8_t> head(craw, ctx);
+    RAMA_KERNEL(ctx, k_uniq_heads, craw, cs.row.p, cs.key.p, craw, head.p);
+    int64_t nh = compact_indices(ctx, head.p, craw, hp_c);
+    Buf<uint8_t> isnew(nh > 0 ? nh : 1, ctx);
+    RAMA_KERNEL(ctx, k_chord_new, nh, hp_c.p, nh, cs.row.p, cs.key.p, rptr.p, rep.v.p, isnew.p);
+    C = compact_indices(ctx, isnew.p, nh, sel_c);
+  }
+  const int64_t m0 = st.m_aug;
+  if (C > 0) {
+    grow(ctx, st.eu, m0, m0 + C);
+    grow(ctx, st.ev, m0, m0 + C);
+    grow(ctx, st.base, m0, m0 + C);
+    Buf<uint64_t> unused(C, ctx);
+    RAMA_KERNEL(ctx, k_chord_out, C, sel_c.p, C, hp_c.p, cs.row.p, cs.key.p, m0, st.eu.p, st.ev.p, st.base.p,
+                unused.p);
+    st.m_aug = m0 + C;
+    if (m0 > st.m_orig) st.chords_sorted = false;
+  }
+  // new triplets: fan dedupe, then drop those already present
+  BucketSorted ts;
+  bucket_sort(ctx, n, traw, trow.p, tkey.p, ts, true);
+  Buf<uint8_t> head(traw, ctx);
+  RAMA_KERNEL(ctx, k_uniq_heads, traw, ts.row.p, ts.key.p, traw, head.p);
+  Buf<int32_t> hp;
+  int64_t nh = compact_indices(ctx, head.p, traw, hp);
+  const int64_t T0 = st.T;
+  BucketSorted es;
+  Buf<int32_t> erow(T0 > 0 ? T0 : 1, ctx);
+  Buf<uint64_t> ekey(T0 > 0 ? T0 : 1, ctx);
+  if (T0 > 0) {
+    RAMA_KERNEL(ctx, k_ext_tri_keys, T0, st.tri_nodes.p, T0, erow.p, ekey.p);
+    bucket_sort(ctx, n, T0, erow.p, ekey.p, es, false);
+  }
+  Buf<uint8_t> keep(nh > 0 ? nh : 1, ctx);
+  RAMA_KERNEL(ctx, k_ext_tri_new, nh, hp.p, nh, ts.row.p, ts.key.p, T0 > 0 ? es.row_ptr.p : (const int32_t*)nullptr,
+              T0 > 0 ? es.key.p : (const uint64_t*)nullptr, T0, keep.p);
+  Buf<int32_t> sel;
+  const int64_t k = compact_indices(ctx, keep.p, nh, sel);
+  if (k > 0) {
+    grow(ctx, st.tri_nodes, 3 * T0, 3 * (T0 + k));
+    grow(ctx, st.tri_edges, 3 * T0, 3 * (T0 + k));
+    Buf<double> lam(3 * (T0 + k), ctx);
+    lam.zero();
+    copy_d2d(ctx, lam.p, st.lam.p, 3 * T0);
+    st.lam = std::move(lam);
+    RAMA_KERNEL(ctx, k_ext_tri_out, k, sel.p, k, hp.p, ts.row.p, ts.key.p, T0, st.tri_nodes.p);
+    // handles into the augmented edge list (originals, earlier chords, new chords)
+    Buf<int32_t> arow(st.m_aug, ctx);
+    Buf<uint64_t> akey(st.m_aug, ctx);
+    RAMA_KERNEL(ctx, k_ext_edge_keys, st.m_aug, st.eu.p, st.ev.p, st.m_aug, arow.p, akey.p);
+    BucketSorted as;
+    bucket_sort(ctx, n, st.m_aug, arow.p, akey.p, as, false);
+    RAMA_KERNEL(ctx, k_ext_handles, k, st.tri_nodes.p, T0, k, as.row_ptr.p, as.key.p, st.tri_edges.p);
+    st.T = T0 + k;
+  }
+  build_slot_lists(ctx, st);  // coverage over the grown edge list
+  return k;
+}
+
 // ------------------------------------------------------ message passing
 
 __device__ __forceinline__ double mn2(double a, double b) { return a < b ? a : b; }  // np.minimum
@@ -943,6 +1261,16 @@ __global__ void k_merge_scatter(int64_t m, int64_t C, const int32_t* __restrict_
   }
 }
 
+__global__ void k_sorted_edges_out(const int32_t* __restrict__ row, const uint64_t* __restrict__ key,
+                                   const double* __restrict__ cl, int64_t m, int32_t* __restrict__ ou,
+                                   int32_t* __restrict__ ov, double* __restrict__ oc) {
+  GRID_STRIDE(p, m) {
+    ou[p] = row[p];
+    ov[p] = (int32_t)(key[p] >> 32);
+    oc[p] = __dadd_rn(cl[(uint32_t)key[p]], 0.0);  // WeightedGraph ctor: x0 + pairwise([])
+  }
+}
+
 Graph reparametrized_graph(Ctx& ctx, const DualState& st) {
   ProfScope prof(ctx.s, kFamBound);
   Graph g;
@@ -955,6 +1283,15 @@ Graph reparametrized_graph(Ctx& ctx, const DualState& st) {
   if (st.m_aug == 0) return g;
   Buf<double> cl(st.m_aug, ctx);
   reparam_costs(ctx, st, cl.p);
+  if (!st.chords_sorted) {  // several chord runs (extend_separation): sort all augmented edges
+    Buf<int32_t> row(st.m_aug, ctx);
+    Buf<uint64_t> key(st.m_aug, ctx);
+    RAMA_KERNEL(ctx, k_ext_edge_keys, st.m_aug, st.eu.p, st.ev.p, st.m_aug, row.p, key.p);
+    BucketSorted bs;
+    bucket_sort(ctx, st.n, st.m_aug, row.p, key.p, bs, true);
+    RAMA_KERNEL(ctx, k_sorted_edges_out, st.m_aug, bs.row.p, bs.key.p, cl.p, st.m_aug, g.u.p, g.v.p, g.c.p);
+    return g;
+  }
   RAMA_KERNEL(ctx, k_merge_scatter, st.m_aug, st.m_orig, st.m_aug - st.m_orig, st.eu.p, st.ev.p, cl.p, g.u.p, g.v.p,
               g.c.p);
   return g;

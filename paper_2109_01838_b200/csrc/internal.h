@@ -76,6 +76,7 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out);
 
 struct DualState {
   int64_t n = 0, m_orig = 0, m_aug = 0, T = 0;
+  bool chords_sorted = true;  // [m_orig, m_aug) is one sorted run (false after extend_separation)
   Buf<int32_t> eu, ev;      // augmented edges: originals then new chords
   Buf<double> base;         // m_aug
   Buf<int32_t> tri_nodes;   // T*3 sorted (i<j<k), rows sorted lexicographically
@@ -87,6 +88,8 @@ struct DualState {
 };
 // a6/a7 _triangulate_arrays (dual.py:216-290)
 void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& st);
+// extend_separation (dual.py:414-474): returns the number of triplets added
+int64_t extend_separation(Ctx& ctx, DualState& st, int L);
 // a8 reparametrized_edge_costs (dual.py:309-316)
 void reparam_costs(Ctx& ctx, const DualState& st, double* cl);
 // a9/a10 message_passing_iteration x iters (dual.py:358-392)

@@ -75,17 +75,22 @@ void solve(Ctx& ctx, const GraphView& g, const SolveConfig& cfg, int32_t* labels
   const double nan = std::nan("");
 
   if (cfg.mode == 3) {  // D: solver.py:211-240
-    RAMA_REQUIRE(cfg.separation_rounds == 1,
-                 "separation_rounds > 1 (extend_separation) is not implemented in the B200 build yet");
-    auto t0 = clk::now();
-    CycleRows cyc;
-    separate(ctx, g, cfg.max_cycle_length, cyc);
     DualState st;
-    triangulate(ctx, g, cyc, st);
-    message_passing(ctx, st, cfg.mp_iterations);
-    double lb = lower_bound(ctx, st);
+    double lb = 0.0;
+    for (int rnd = 1; rnd <= cfg.separation_rounds; rnd++) {
+      auto t0 = clk::now();
+      if (rnd == 1) {
+        CycleRows cyc;
+        separate(ctx, g, cfg.max_cycle_length, cyc);
+        triangulate(ctx, g, cyc, st);
+      } else {
+        extend_separation(ctx, st, cfg.max_cycle_length);
+      }
+      message_passing(ctx, st, cfg.mp_iterations);
+      lb = lower_bound(ctx, st);
+      push(trace, max_trace, nr, RoundInfo{rnd, 3, n0, st.m_aug, st.T, lb, 1, 0, ms_since(t0)});
+    }
     iota(ctx, labels, n0);
-    push(trace, max_trace, nr, RoundInfo{1, 3, n0, st.m_aug, st.T, lb, 1, 0, ms_since(t0)});
     res.lb = lb;
     res.lb_finite = true;
     res.primal = clustering_cost(ctx, g, labels);

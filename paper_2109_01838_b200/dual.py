@@ -224,5 +224,33 @@ def triangle_min_marginal(state, t, e):
 
 
 def extend_separation(state, max_len):
-    """Incremental separation for mode D (dual.py:414-474): NEXT."""
-    raise NotImplementedError("extend_separation is not implemented in the B200 build yet (SURVEY.md 8(f) f2)")
+    """Separate on the current reparametrized costs and add new triplets
+    (dual.py:414-474): new chords join at base cost 0, new triplets start
+    with zero multipliers.  Returns the number of triplets added."""
+    if max_len < 3:
+        raise ValueError("max_len must be at least 3")
+    m, T, n = state.num_edges, state.num_triplets, state.num_nodes
+    if m == 0:
+        return 0
+    extra = m * max(max_len - 2, 1)
+    eu, ev, base = L.i32(state.edges_u), L.i32(state.edges_v), L.f64(state.base_costs)
+    tn = L.i32(state.tri_nodes.ravel()) if T else L.empty_i32(1)
+    te = L.i32(state.tri_edges.ravel()) if T else L.empty_i32(1)
+    lam = L.f64(np.ascontiguousarray(state.lam).ravel()) if T else L.empty_f64(1)
+    oeu, oev, obase, ocov = L.empty_i32(m + extra), L.empty_i32(m + extra), L.empty_f64(m + extra), \
+        L.empty_i32(m + extra)
+    otn, ote, olam = L.empty_i32(3 * (T + extra)), L.empty_i32(3 * (T + extra)), L.empty_f64(3 * (T + extra))
+    om, oT, added = L.ctypes.c_int64(), L.ctypes.c_int64(), L.ctypes.c_int64()
+    L.call("rama_extend_separation", n, m, L.ptr(eu), L.ptr(ev), L.ptr(base), T, L.ptr(tn), L.ptr(te), L.ptr(lam),
+           int(max_len), m + extra, T + extra, L.ptr(oeu), L.ptr(oev), L.ptr(obase), L.ctypes.byref(om),
+           L.ptr(otn), L.ptr(ote), L.ptr(olam), L.ctypes.byref(oT), L.ptr(ocov), L.ctypes.byref(added),
+           L.stream())
+    k, t = om.value, oT.value
+    state.edges_u = L.host_i64(oeu, k)
+    state.edges_v = L.host_i64(oev, k)
+    state.base_costs = L.host_f64(obase, k)
+    state.tri_nodes = L.host_i64(otn, 3 * t).reshape(t, 3)
+    state.tri_edges = L.host_i64(ote, 3 * t).reshape(t, 3)
+    state.lam = L.host_f64(olam, 3 * t).reshape(t, 3)
+    state.coverage = L.host_i64(ocov, k)
+    return int(added.value)

@@ -95,7 +95,7 @@ def _records(buf, k):
 
 
 def _max_trace(cfg, n):
-    return min(cfg.max_rounds, max(n, 1) + 1) + 2
+    return max(min(cfg.max_rounds, max(n, 1) + 1), cfg.separation_rounds) + 2
 
 
 def solve_device(n, du, dv, dc, m, cfg, labels=None):

@@ -168,10 +168,10 @@ def test_ops_oracle_parity(shape):
     assert np.array_equal(g.costs, og.costs)
     assert np.array_equal(P.select_matching(g), O.select_matching(og))
     assert np.array_equal(P.select_spanning_forest_no_conflicts(g), O.select_spanning_forest_no_conflicts(og))
-    for L in (3, 4, 5):
+    for L in (3, 4, 5, 6, 7):
         a1, b1 = P.dual._separate(g, L)
         a2, b2 = O.separate(og, L)
-        assert np.array_equal(a1, a2) and np.array_equal(b1, b2)
+        assert np.array_equal(a1, a2) and np.array_equal(b1, b2), L
     lengths, nodes = O.separate(og, 5)
     st = P.dual._triangulate_arrays(g, lengths, nodes)
     ost = O.triangulate(og, lengths, nodes)
@@ -208,3 +208,17 @@ def test_clustering_cost_matches_oracle():
     g, og = _both(n, u, v, c)
     lab = np.random.default_rng(0).integers(0, 50, n)
     assert close_sum(P.clustering_cost(g, lab), O.clustering_cost(og, lab))
+
+
+def test_pd_plus_separation_matches_reference_bfs():
+    """L = 6, 7, 8 (mode PD+): the source-grouped BFS kernel reproduces the
+    reference BFS (dual.py:109-152) row for row, on sparse random graphs
+    (long shortest cycles) and on contracted-looking dense blocks."""
+    cases = [instances.random_coo(2000, 0.0015, seed=s) for s in range(3)]
+    cases += [instances.grid_coo(60, 80, 3, seed=5), instances.grid8_coo(40, 60, strides=(2,), seed=6)]
+    for n, u, v, c in cases:
+        g, og = _both(n, u, v, c)
+        for L in (6, 7, 8):
+            a1, b1 = P.dual._separate(g, L)
+            a2, b2 = O.separate(og, L)
+            assert np.array_equal(a1, a2) and np.array_equal(b1, b2), L

@@ -189,3 +189,51 @@ def test_c3_full_size_matches_reference_rounds():
     assert abs(sol.lower_bound - C3_REFERENCE_LB) <= 1e-3
     assert rel_gap(sol.primal_cost, C3_REFERENCE_PRIMAL) <= GAP
     assert sol.lower_bound <= sol.primal_cost
+
+
+def test_pd_plus_small_matches_oracle():
+    """Mode PD+ (L = 7, solver.py:24): exact against the oracle with the D1
+    cleanup on the reference-generated small instances, and LB equal to the
+    reference's own PD+ lower bound."""
+    fx = load("solve_small.npz")
+    for i in range(fx.count("edges")):
+        g = _pg(fx, i)
+        n, u, v, c = fx.graph_arrays(i)
+        sol = P.solve(g, P.SolverConfig(mode="PD+"))
+        ref = O.solve(O.Graph(n, u, v, c, canonical=True), mode="PD+", cleanup="handshake")
+        assert np.array_equal(sol.labeling, ref.labeling), i
+        assert sol.lower_bound == pytest.approx(fx.scalar("lb_PD+", i), rel=1e-12, abs=1e-12)
+    n, u, v, c = instances.grid8_coo(96, 128, strides=(2, 3), seed=2)
+    sol = P.solve(P.WeightedGraph(n, u, v, c), P.SolverConfig(mode="PD+"))
+    ref = O.solve(O.Graph(n, u, v, c), mode="PD+", cleanup="handshake")
+    assert np.array_equal(sol.labeling, ref.labeling)
+    assert sol.lower_bound == pytest.approx(ref.lower_bound, rel=1e-12)
+
+
+def test_mode_d_separation_rounds_match_reference():
+    """Mode D with separation_rounds 2-4 (extend_separation, solver.py:211-240)
+    against the reference's own per-round (edges, triplets) and LB
+    (tests/golden/dual_rounds.npz)."""
+    d = np.load(os.path.join(DIR, "dual_rounds.npz"))
+    for i in range(int(d["count"][0])):
+        g = P.WeightedGraph._from_canonical(int(d["g%d_n" % i][0]), d["g%d_u" % i], d["g%d_v" % i], d["g%d_c" % i])
+        for r in (2, 3, 4):
+            sol = P.solve(g, P.SolverConfig(mode="D", separation_rounds=r))
+            tr = np.array([[t.edges, t.triplets] for t in sol.trace], dtype=np.int64)
+            assert np.array_equal(tr, d["g%d_r%d_trace" % (i, r)]), (i, r)
+            assert sol.lower_bound == pytest.approx(float(d["g%d_r%d_lb" % (i, r)][0]), rel=1e-12, abs=1e-12)
+            assert P.dual_bound(g, P.SolverConfig(mode="D", separation_rounds=r)) == sol.lower_bound
+
+
+def test_extend_separation_state_matches_oracle():
+    n, u, v, c = instances.grid8_coo(48, 64, strides=(2, 3), seed=8)
+    g, og = P.WeightedGraph(n, u, v, c), O.Graph(n, u, v, c)
+    lengths, nodes = O.separate(og, 5)
+    st = P.dual._triangulate_arrays(g, lengths, nodes)
+    ost = O.triangulate(og, lengths, nodes)
+    for _ in range(3):
+        P.message_passing(st, 5)
+        O.message_passing(ost, 5)
+        assert P.extend_separation(st, 5) == O.extend_separation(ost, 5)
+        for f in ("edges_u", "edges_v", "base_costs", "tri_nodes", "tri_edges", "lam", "coverage"):
+            assert np.array_equal(getattr(st, f), getattr(ost, f)), f

@@ -7,6 +7,8 @@
 3. numpy summation-order restatements vs numpy.
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -216,3 +218,16 @@ def test_handshake_cleanup_equals_contraction_rounds():
         a, na = by_contraction(g)
         b, nb = O.handshake_cleanup(g)
         assert na == nb and np.array_equal(a, b)
+
+
+def test_extend_separation_matches_reference_mode_d_rounds():
+    """Mode D with separation_rounds 2-4 (extend_separation, dual.py:414-474)
+    against the reference's own results (tests/golden/dual_rounds.npz)."""
+    d = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "dual_rounds.npz"))
+    for i in range(int(d["count"][0])):
+        g = O.Graph(int(d["g%d_n" % i][0]), d["g%d_u" % i], d["g%d_v" % i], d["g%d_c" % i], canonical=True)
+        for r in (2, 3, 4):
+            sol = O.solve(g, mode="D", separation_rounds=r)
+            tr = np.array([[t.edges, t.triplets] for t in sol.trace], dtype=np.int64)
+            assert np.array_equal(tr, d["g%d_r%d_trace" % (i, r)]), (i, r)
+            assert sol.lower_bound == pytest.approx(float(d["g%d_r%d_lb" % (i, r)][0]), rel=1e-12, abs=1e-12)
