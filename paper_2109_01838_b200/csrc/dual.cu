@@ -339,11 +339,12 @@ __global__ void k_sep5(const int32_t* __restrict__ Q, int64_t nq, const int32_t*
 // row-intersection kernels above.
 constexpr int kGrp = 8;                  // lanes per source
 constexpr int kGrpPerBlock = 32;         // 256 threads
-constexpr int kSrcL1 = 48;
-constexpr int kSrcHash = 128;            // per-source L2 table; used at load <= 1/2
+constexpr int kSrcL1 = 32;
+constexpr int kSrcHash = 64;             // per-source L2 table; used at load <= 1/2
+constexpr int kSrcHashBits = 6;
 
 __device__ __forceinline__ int32_t src_slot(int32_t y) {
-  return (int32_t)(((uint32_t)y * 0x9E3779B1u) >> 25);  // 7 bits
+  return (int32_t)(((uint32_t)y * 0x9E3779B1u) >> (32 - kSrcHashBits));
 }
 
 __device__ __forceinline__ int32_t src_lookup(const int32_t* hk, const int32_t* hv, int32_t y) {
@@ -384,61 +385,74 @@ __device__ __forceinline__ int32_t grp_min_i32(int32_t x, unsigned mask) {
   return x;
 }
 
-// gstart[k] = first index (into Q2) of source group k; groups end at gstart[k+1] (or n2)
-__global__ void __launch_bounds__(kGrp * kGrpPerBlock) k_sep_src(
-    const int32_t* __restrict__ gstart, int64_t ng, int64_t n2, const int32_t* __restrict__ Q2,
-    const int32_t* __restrict__ NQ, const int32_t* __restrict__ u, const int32_t* __restrict__ v,
-    const int32_t* __restrict__ ptr, const int32_t* __restrict__ adj, int L, int32_t* __restrict__ out_len,
-    int32_t* __restrict__ out_nodes, uint8_t* __restrict__ fb, int force_fallback) {
+// gstart[k] = first index (into Q2) of source group k (source gsrc[k]);
+// groups end at gstart[k+1] (or n2).  qb[i] = target b of the i-th miss.
+// Table values are POSITIONS in N+(a) (ascending = node order), so the
+// parent is the atomicMin over the positions that reach y and every row of
+// the level can be walked at once (no sequential x loop).
+constexpr int kSrcBuild = 256;  // max sum of |N+(x)| over x in N+(a) handled in shared memory
+
+__global__ void __launch_bounds__(kGrp * kGrpPerBlock, 8) k_sep_src(
+    const int32_t* __restrict__ gstart, const int32_t* __restrict__ gsrc, int64_t ng, int64_t n2,
+    const int32_t* __restrict__ Q2, const int32_t* __restrict__ qb, const int32_t* __restrict__ ptr,
+    const int32_t* __restrict__ adj, int L, int32_t* __restrict__ out_len, int32_t* __restrict__ out_nodes,
+    uint8_t* __restrict__ fb, int force_fallback) {
   __shared__ int32_t s_l1[kGrpPerBlock][kSrcL1];
   __shared__ int32_t s_hk[kGrpPerBlock][kSrcHash];
   __shared__ int32_t s_hv[kGrpPerBlock][kSrcHash];
   const int gi = threadIdx.x / kGrp, lane = threadIdx.x % kGrp;
-  const unsigned mask = 0xFFu << ((threadIdx.x & 31) & ~(kGrp - 1));
+  const unsigned mask = ((1u << kGrp) - 1u) << ((threadIdx.x & 31) & ~(kGrp - 1));
   int32_t* l1 = s_l1[gi];
   int32_t* hk = s_hk[gi];
   int32_t* hv = s_hv[gi];
   const int64_t ngroups = (int64_t)gridDim.x * kGrpPerBlock;
   for (int64_t k = (int64_t)blockIdx.x * kGrpPerBlock + gi; k < ng; k += ngroups) {
     const int32_t i0 = gstart[k], i1 = (k + 1 < ng) ? gstart[k + 1] : (int32_t)n2;
-    const int32_t a = u[NQ[Q2[i0]]];
+    const int32_t a = gsrc[k];
     const int32_t pa = ptr[a], la = ptr[a + 1] - pa;
     bool over = la > kSrcL1 || force_fallback;
     __syncwarp(mask);  // the previous source's lookups are done before the table is reset
     if (!over) {
       for (int32_t j = lane; j < la; j += kGrp) l1[j] = adj[pa + j];
-      for (int32_t j = lane; j < kSrcHash; j += kGrp) hk[j] = -1;
+      for (int32_t j = lane; j < kSrcHash; j += kGrp) {
+        hk[j] = -1;
+        hv[j] = 0x7fffffff;
+      }
       __syncwarp(mask);
-      int32_t total = 0;  // group-uniform insert count (shuffle-reduced per x)
-      for (int32_t xi = 0; xi < la && !over; xi++) {
+      // each lane walks whole rows N+(x) for its x positions (independent load chains)
+      int32_t work = 0;
+      for (int32_t xi = lane; xi < la; xi += kGrp) {
         const int32_t x = l1[xi];
-        const int32_t px = ptr[x], lx = ptr[x + 1] - px;
-        if (lx > kSrcHash) {  // cannot fit: the row-intersection kernels take this source
-          over = true;
-          break;
-        }
+        work += ptr[x + 1] - ptr[x];
+      }
+#pragma unroll
+      for (int o = kGrp / 2; o > 0; o >>= 1) work += __shfl_xor_sync(mask, work, o, kGrp);
+      over = work > kSrcBuild;
+      if (!over) {
         int32_t mine = 0;
-        for (int32_t j = lane; j < lx; j += kGrp) {
-          int32_t y = adj[px + j];
-          if (y == a || src_in_l1(l1, la, y)) continue;
-          int32_t h = src_slot(y);
-          for (int t = 0; t < kSrcHash; t++) {
-            int32_t kk = atomicCAS(hk + h, -1, y);
-            if (kk == -1) {
-              hv[h] = x;
-              mine++;
-              break;
+        for (int32_t xi = lane; xi < la; xi += kGrp) {
+          const int32_t x = l1[xi];
+          const int32_t px = ptr[x], lx = ptr[x + 1] - px;
+          for (int32_t j = 0; j < lx; j++) {
+            const int32_t y = adj[px + j];
+            if (y == a || src_in_l1(l1, la, y)) continue;
+            int32_t h = src_slot(y);
+            for (int t = 0; t < kSrcHash; t++) {
+              int32_t kk = atomicCAS(hk + h, -1, y);
+              if (kk == -1 || kk == y) {
+                mine += kk == -1;
+                atomicMin(hv + h, xi);  // BFS parent = smallest position reaching y
+                break;
+              }
+              h = (h + 1) & (kSrcHash - 1);
             }
-            if (kk == y) break;  // reached from a smaller x already
-            h = (h + 1) & (kSrcHash - 1);
           }
         }
 #pragma unroll
         for (int o = kGrp / 2; o > 0; o >>= 1) mine += __shfl_xor_sync(mask, mine, o, kGrp);
-        total += mine;
-        over = total > kSrcHash / 2;
+        over = mine > kSrcHash / 2;
       }
-      __syncwarp(mask);  // table writes (hv) visible to the group's lookups
+      __syncwarp(mask);  // table complete before the lookups
     }
     if (over) {
       for (int32_t i = i0 + lane; i < i1; i += kGrp) fb[i] = 1;
@@ -447,7 +461,7 @@ __global__ void __launch_bounds__(kGrp * kGrpPerBlock) k_sep_src(
     }
     for (int32_t i = i0; i < i1; i++) {
       const int32_t q = Q2[i];
-      const int32_t b = v[NQ[q]];
+      const int32_t b = qb[i];
       const int32_t pb = ptr[b], lb = ptr[b + 1] - pb;
       int32_t len = 0, r1 = 0, r2 = 0, r3 = 0;
       uint64_t best = ~0ULL;
@@ -461,7 +475,7 @@ __global__ void __launch_bounds__(kGrp * kGrpPerBlock) k_sep_src(
       }
       best = grp_min_u64(best, mask);
       if (best != ~0ULL) {
-        len = 4; r1 = (int32_t)(best >> 32); r2 = (int32_t)(uint32_t)best;
+        len = 4; r1 = l1[(int32_t)(best >> 32)]; r2 = (int32_t)(uint32_t)best;
       } else if (L >= 5) {
         uint64_t bk = ~0ULL;
         int32_t bz = 0x7fffffff;
@@ -485,7 +499,7 @@ __global__ void __launch_bounds__(kGrp * kGrpPerBlock) k_sep_src(
         uint64_t mn = grp_min_u64(bk, mask);
         int32_t zc = grp_min_i32(bk == mn ? bz : 0x7fffffff, mask);
         if (mn != ~0ULL) {
-          len = 5; r1 = (int32_t)(mn >> 32); r2 = (int32_t)(uint32_t)mn; r3 = zc;
+          len = 5; r1 = l1[(int32_t)(mn >> 32)]; r2 = (int32_t)(uint32_t)mn; r3 = zc;
         }
       }
       if (lane == 0 && len) {
@@ -497,6 +511,18 @@ __global__ void __launch_bounds__(kGrp * kGrpPerBlock) k_sep_src(
       }
     }
     __syncwarp(mask);
+  }
+}
+
+__global__ void k_src_heads(const int32_t* __restrict__ Q2, int64_t n2, const int32_t* __restrict__ NQ,
+                            const int32_t* __restrict__ u, const int32_t* __restrict__ v, uint8_t* __restrict__ head,
+                            int32_t* __restrict__ qa, int32_t* __restrict__ qb) {
+  GRID_STRIDE(i, n2) {
+    int32_t e = NQ[Q2[i]];
+    int32_t a = u[e];
+    qa[i] = a;
+    qb[i] = v[e];
+    head[i] = (i == 0) || a != u[NQ[Q2[i - 1]]];
   }
 }
 
@@ -626,11 +652,6 @@ __global__ void __launch_bounds__(256) k_sep_bfs(const int32_t* __restrict__ gst
   }
 }
 
-__global__ void k_src_heads(const int32_t* __restrict__ Q2, int64_t n2, const int32_t* __restrict__ NQ,
-                            const int32_t* __restrict__ u, uint8_t* __restrict__ head) {
-  GRID_STRIDE(i, n2) head[i] = (i == 0) || u[NQ[Q2[i]]] != u[NQ[Q2[i - 1]]];
-}
-
 // RAMA_SEP_FALLBACK=1 routes every source through the row-intersection
 // kernels (tests use it to check both executions against the oracle)
 static int sep_force_fallback() {
@@ -671,9 +692,12 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
   if (n2 == 0) return;
   // 4/5-cycles: source-grouped BFS levels in shared memory
   Buf<uint8_t> head(n2, ctx);
-  RAMA_KERNEL(ctx, k_src_heads, n2, Q2.p, n2, NQ.p, g.u, head.p);
+  Buf<int32_t> qa(n2, ctx), qb(n2, ctx);
+  RAMA_KERNEL(ctx, k_src_heads, n2, Q2.p, n2, NQ.p, g.u, g.v, head.p, qa.p, qb.p);
   Buf<int32_t> gstart;
   int64_t ng = compact_indices(ctx, head.p, n2, gstart);
+  Buf<int32_t> gsrc(ng > 0 ? ng : 1, ctx);
+  RAMA_KERNEL(ctx, k_gather_i32, ng, qa.p, gstart.p, ng, gsrc.p);
   if (L >= 6) {  // PD+: the exact source-grouped BFS
     size_t free_b = 0, total_b = 0;
     RAMA_CUDA(cudaMemGetInfo(&free_b, &total_b));
@@ -708,7 +732,7 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
     // edges' endpoints, the cycle rows written
     KernelScope ks(ctx.s, "k_sep_src",
                    4.0 * (double)(g.n + 1) + 4.0 * (double)csr.arcs + (16.0 + 4.0 * L) * (double)n2);
-    k_sep_src<<<(unsigned)blocks, kGrp * kGrpPerBlock, 0, ctx.s>>>(gstart.p, ng, n2, Q2.p, NQ.p, g.u, g.v,
+    k_sep_src<<<(unsigned)blocks, kGrp * kGrpPerBlock, 0, ctx.s>>>(gstart.p, gsrc.p, ng, n2, Q2.p, qb.p,
                                                                    csr.ptr.p, csr.adj.p, L, out.len.p,
                                                                    out.nodes.p, fb.p, sep_force_fallback());
     RAMA_LAUNCH_CHECK();
