@@ -14,6 +14,7 @@
 
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 #include <mutex>
 #include <map>
@@ -311,24 +312,24 @@ unsigned capped_grid(int64_t work, int block) {
 
 // ---------------------------------------------------------------- scans
 
-__global__ void k_scan_tail(const int32_t* in, int32_t* out, int64_t n) {
-  out[n] = n ? out[n - 1] + in[n - 1] : 0;
-}
+
+// in[i] for i < n, 0 at i == n: an exclusive scan over n + 1 items then
+// leaves the total in out[n] (no separate tail kernel)
+struct PadZero {
+  const int32_t* in;
+  int64_t n;
+  __host__ __device__ int32_t operator()(int64_t i) const { return i < n ? in[i] : 0; }
+};
 
 int64_t exclusive_scan(Ctx& ctx, const int32_t* in, int32_t* out, int64_t n, bool want_total) {
-  if (n > 0) {
-    size_t tb = 0;
-    RAMA_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, (int)n, ctx.s));
-    Buf<uint8_t> tmp(tb, ctx);
-    {
-      KernelScope ks(ctx.s, "cub::DeviceScan", 8.0 * (double)n);
-      RAMA_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, in, out, (int)n, ctx.s));
-    }
-    ctx.launches++;
+  auto it = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0), PadZero{in, n});
+  size_t tb = 0;
+  RAMA_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, it, out, (int)(n + 1), ctx.s));
+  Buf<uint8_t> tmp(tb, ctx);
+  {
+    KernelScope ks(ctx.s, "cub::DeviceScan", 8.0 * (double)n);
+    RAMA_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, it, out, (int)(n + 1), ctx.s));
   }
-  KernelScope ks_tail(ctx.s, "k_scan_tail", 0.0);
-  k_scan_tail<<<1, 1, 0, ctx.s>>>(in, out, n);
-  RAMA_LAUNCH_CHECK();
   ctx.launches++;
   if (!want_total) return -1;
   return read_scalar(ctx, out + n);
@@ -482,11 +483,12 @@ __global__ void k_bucket_scatter(const int32_t* __restrict__ row, const uint64_t
 // row_start + rank.  Neighbouring threads read the same row, so the key
 // loads are warp broadcasts.  Longer rows are listed for the block sort.
 constexpr int kSmallRow = 64;
+constexpr int kBlockRow = 4096;  // bitonic sort in shared memory: 4096 x 12 B = 48 KB
 
 __global__ void k_rank_rows(const int32_t* __restrict__ row, const int32_t* __restrict__ ptr, int64_t N,
                             int64_t sort_rows, const uint64_t* __restrict__ tkey, const int32_t* __restrict__ tsrc,
                             uint64_t* __restrict__ okey, int32_t* __restrict__ osrc, int32_t* __restrict__ big_list,
-                            int32_t* __restrict__ counters) {
+                            int32_t* __restrict__ huge_list, int32_t* __restrict__ counters) {
   GRID_STRIDE(p, N) {
     int32_t r = row[p];
     int32_t b = ptr[r], e = ptr[r + 1];
@@ -497,8 +499,11 @@ __global__ void k_rank_rows(const int32_t* __restrict__ row, const int32_t* __re
       osrc[p] = s;
       continue;
     }
-    if (e - b > kSmallRow) {
-      if (p == b) big_list[atomicAdd(counters, 1)] = r;
+    if (e - b > kSmallRow) {  // block bitonic (<= kBlockRow) or CUB segmented sort (hubs)
+      if (p == b) {
+        if (e - b > kBlockRow) huge_list[atomicAdd(counters + 1, 1)] = r;
+        else big_list[atomicAdd(counters, 1)] = r;
+      }
       continue;
     }
     int32_t rank = 0;
@@ -511,7 +516,6 @@ __global__ void k_rank_rows(const int32_t* __restrict__ row, const int32_t* __re
   }
 }
 
-constexpr int kBlockRow = 4096;  // bitonic sort in shared memory: 4096 x 12 B = 48 KB
 
 // one block per listed row: bitonic sort of (key, src) in shared memory,
 // from the scatter buffers into the output; rows longer than kBlockRow go
@@ -521,17 +525,13 @@ __global__ void __launch_bounds__(512) k_sort_rows_block(const int32_t* __restri
                                                          int32_t* __restrict__ counters,
                                                          const uint64_t* __restrict__ tkey,
                                                          const int32_t* __restrict__ tsrc, uint64_t* __restrict__ key,
-                                                         int32_t* __restrict__ src, int32_t* __restrict__ huge_list) {
+                                                         int32_t* __restrict__ src) {
   __shared__ uint64_t sk[kBlockRow];
   __shared__ int32_t ss[kBlockRow];
   int32_t nbig = counters[0];
   for (int32_t bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
     int32_t r = big_list[bi];
     int32_t b = ptr[r], len = ptr[r + 1] - b;
-    if (len > kBlockRow) {
-      if (threadIdx.x == 0) huge_list[atomicAdd(counters + 1, 1)] = r;
-      continue;
-    }
     int32_t P = 64;
     while (P < len) P <<= 1;
     for (int32_t i = threadIdx.x; i < P; i += blockDim.x) {
@@ -613,16 +613,21 @@ void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint6
   RAMA_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(int32_t), ctx.s));
   prof_set_bytes(32.0 * (double)total);
   RAMA_KERNEL(ctx, k_rank_rows, total, out.row.p, out.row_ptr.p, total, sort_rows, tkey.p, tsrc.p, out.key.p,
-              out.src.p, big_list, counters);
+              out.src.p, big_list, huge_list, counters);
   if (!want_row) out.row.release();
   if (sort_rows == 0) return;
-  unsigned gb = (unsigned)std::min<int64_t>(std::max<int64_t>(total / 256, 1), 148 * 4);
-  KernelScope ks_block(ctx.s, "k_sort_rows_block", 0.0);
-  k_sort_rows_block<<<gb, 512, 0, ctx.s>>>(out.row_ptr.p, big_list, counters, tkey.p, tsrc.p, out.key.p, out.src.p,
-                                           huge_list);
-  RAMA_LAUNCH_CHECK();
-  ctx.launches++;
-  int32_t nb = read_scalar(ctx, counters + 1);
+  // one read-back of both list sizes; the long-row sorts launch only when needed
+  RAMA_CUDA(cudaMemcpyAsync(ctx.pinned, counters, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx.s));
+  ctx.sync();
+  int32_t nbig = ((int32_t*)ctx.pinned)[0], nb = ((int32_t*)ctx.pinned)[1];
+  if (nbig > 0) {
+    unsigned gb = (unsigned)std::min<int64_t>(nbig, 148 * 4);
+    KernelScope ks_block(ctx.s, "k_sort_rows_block", 0.0);
+    k_sort_rows_block<<<gb, 512, 0, ctx.s>>>(out.row_ptr.p, big_list, counters, tkey.p, tsrc.p, out.key.p,
+                                             out.src.p);
+    RAMA_LAUNCH_CHECK();
+    ctx.launches++;
+  }
   if (nb == 0) return;
   // rare (power-law hubs): CUB segmented sort of the rows > kBlockRow
   Buf<int32_t> blen(nb, ctx), boff(nb + 1, ctx);
