@@ -203,6 +203,12 @@ int rama_extend_separation(int64_t n, int64_t m_aug, const int32_t* eu, const in
                            double* out_base, int64_t* out_m_aug, int32_t* out_tri_nodes, int32_t* out_tri_edges,
                            double* out_lam, int64_t* out_T, int32_t* out_coverage, int64_t* added, void* stream);
 
+/* check_edge_triangle_agreement (dual.py:477-531): arc consistency of the
+ * eps-optimal edge and triplet label sets; *agree (host) = 1 if every set
+ * stays non-empty. */
+int rama_check_agreement(int64_t m_aug, const double* base, int64_t T, const int32_t* tri_edges, const double* lam,
+                         double eps, int32_t* agree, void* stream);
+
 /* message passing on lam[3T] in place (dual.py:358-392).
  * phases: 1 = mp_edge_to_triplets only, 2 = mp_triplets_to_edges only,
  * 3 = message_passing_iteration; repeated `iters` times. */
@@ -216,6 +222,27 @@ int rama_reparam_costs(int64_t m_aug, const double* base, int64_t T, const int32
 /* lower_bound (dual.py:395-405); *lb host */
 int rama_lower_bound(int64_t m_aug, const double* base, int64_t T, const int32_t* tri_edges, const double* lam,
                      double* lb, void* stream);
+
+/* ---- MULTICUT text format (graph.py:160-313) -----------
+ * Host-only (no CUDA device needed).  Errors: RAMA_ERR_INVALID with the
+ * reference's ParseError message in rama_io_last_error(). */
+
+/* message of the last failed rama_parse_multicut / rama_serialize_multicut */
+const char* rama_io_last_error(void);
+
+/* parse_instance (graph.py:204-263): text[len] (host), or the file `path`
+ * (mmap'ed) when path != NULL.  Raw edges (before canonicalisation, in file
+ * order) go to host u, v, c of capacity cap; *m = edges, *n = node count
+ * (NODES, else 1 + max id).  If *m > cap nothing is copied (call again).
+ * threads: worker threads (0 = all cores). */
+int rama_parse_multicut(const char* text, int64_t len, const char* path, int64_t* n, int64_t* m, int64_t* u,
+                        int64_t* v, double* c, int64_t cap, int32_t threads);
+
+/* serialize_instance (graph.py:300-313): 'MULTICUT', 'NODES n', then
+ * '<u> <v> <repr(cost)>' per edge.  Writes to out (host, cap bytes) when it
+ * fits; *len = bytes of the text (no NUL). */
+int rama_serialize_multicut(int64_t n, const int64_t* u, const int64_t* v, const double* c, int64_t m, char* out,
+                            int64_t cap, int64_t* len, int32_t threads);
 
 #ifdef __cplusplus
 }

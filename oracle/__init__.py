@@ -408,6 +408,47 @@ def extend_separation(st, L):
     return added
 
 
+_MC = np.array([(0, 0, 0), (1, 1, 0), (1, 0, 1), (0, 1, 1), (1, 1, 1)], dtype=np.int8)  # dual.py:17-18
+
+
+def check_edge_triangle_agreement(st, eps):
+    """dual.py:477-531 (numpy restatement): arc-consistent kernel of the
+    eps-optimal edge / triplet label sets is non-empty."""
+    if eps < 0:
+        raise ValueError("eps must be non-negative")
+    cl = reparametrized_edge_costs(st)
+    best = np.minimum(cl, 0.0)
+    em = np.zeros(cl.size, dtype=np.uint8)
+    em[0.0 <= best + eps] |= 1
+    em[cl <= best + eps] |= 2
+    T = st.num_triplets
+    if T == 0:
+        return bool(np.all(em != 0))
+    lam = np.asarray(st.lam).reshape(-1, 3)
+    l0, l1, l2 = lam[:, 0], lam[:, 1], lam[:, 2]
+    pc = np.stack([np.zeros(T), -(l0 + l1), -(l0 + l2), -(l1 + l2), -((l0 + l1) + l2)], axis=1)
+    tb = pc.min(axis=1)
+    tm = np.zeros(T, dtype=np.uint8)
+    for p in range(5):
+        tm[pc[:, p] <= tb + eps] |= np.uint8(1 << p)
+    e = np.asarray(st.tri_edges).reshape(-1, 3)
+    zero_bits = [sum(1 << p for p in range(5) if _MC[p, s] == 0) for s in range(3)]
+    one_bits = [sum(1 << p for p in range(5) if _MC[p, s] == 1) for s in range(3)]
+    while True:
+        oe, ot = em.copy(), tm.copy()
+        for p in range(5):
+            ok = np.ones(T, dtype=bool)
+            for s in range(3):
+                ok &= (em[e[:, s]] & np.uint8(1 << _MC[p, s])) != 0
+            tm[~ok] &= np.uint8(~np.uint8(1 << p))
+        for s in range(3):
+            em[e[(tm & zero_bits[s]) == 0, s]] &= np.uint8(~np.uint8(1))
+            em[e[(tm & one_bits[s]) == 0, s]] &= np.uint8(~np.uint8(2))
+        if np.array_equal(em, oe) and np.array_equal(tm, ot):
+            break
+    return bool(np.all(em != 0) and np.all(tm != 0))
+
+
 def reparametrized_graph(st):
     """dual.py:408-411 (re-canonicalised)."""
     return Graph(st.num_nodes, st.edges_u, st.edges_v, reparametrized_edge_costs(st))

@@ -41,7 +41,7 @@ static void *xcalloc(size_t n, size_t s) { return calloc(n ? n : 1, s ? s : 1); 
  * PW_BLOCKSIZE 128, 8-way unrolled leaves). */
 static double pairwise(const double *a, i64 n) {
     if (n < 8) {
-        double r = 0.0;
+        double r = -0.0;  /* numpy 2.x starts the short sum at -0.0 (keeps -0.0 sums) */
         for (i64 i = 0; i < n; i++) r += a[i];
         return r;
     }

@@ -66,6 +66,9 @@ _SIGS = {
     "rama_profile_enable": [_i32],
     "rama_profile_read": [_F64P, _F64P, _I64P],
     "rama_profile_kernels": [ctypes.c_char_p, _i64],
+    "rama_io_last_error": [],
+    "rama_parse_multicut": [_vp, _i64, ctypes.c_char_p, _I64P, _I64P, _vp, _vp, _vp, _i64, _i32],
+    "rama_serialize_multicut": [_i64, _vp, _vp, _vp, _i64, _vp, _i64, _I64P, _i32],
     "rama_solve": [_i64, _vp, _vp, _vp, _i64, ctypes.POINTER(RamaCfg), _vp, _F64P, ctypes.POINTER(RamaRound), _i32,
                    _I32P, _vp],
     "rama_solve_host": [_i64, _vp, _vp, _vp, _i64, ctypes.POINTER(RamaCfg), _vp, _F64P, ctypes.POINTER(RamaRound),
@@ -84,11 +87,12 @@ _SIGS = {
                          _vp],
     "rama_extend_separation": [_i64, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i32, _i64, _i64, _vp, _vp, _vp, _I64P,
                                _vp, _vp, _vp, _I64P, _vp, _I64P, _vp],
+    "rama_check_agreement": [_i64, _vp, _i64, _vp, _vp, _f64, _I32P, _vp],
     "rama_message_passing": [_i64, _vp, _i64, _vp, _vp, _i32, _i32, _vp],
     "rama_reparam_costs": [_i64, _vp, _i64, _vp, _vp, _vp, _vp],
     "rama_lower_bound": [_i64, _vp, _i64, _vp, _vp, _F64P, _vp],
 }
-_RESTYPES = {"rama_last_error": ctypes.c_char_p, "rama_last_launch_count": ctypes.c_int64,
+_RESTYPES = {"rama_last_error": ctypes.c_char_p, "rama_io_last_error": ctypes.c_char_p, "rama_last_launch_count": ctypes.c_int64,
              "rama_profile_kernels": ctypes.c_int64}
 
 EXPORTED = tuple(_SIGS)
@@ -127,6 +131,18 @@ def call(name, *args):
         raise ValueError(msg)
     if rc == RAMA_ERR_NOMEM:
         raise MemoryError(msg)
+    raise RuntimeError("%s failed (%d): %s" % (name, rc, msg))
+
+
+def call_host(name, *args):
+    """Host-only entry points (MULTICUT I/O): no CUDA device required."""
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc == RAMA_OK:
+        return
+    msg = lib.rama_io_last_error().decode(errors="replace")
+    if rc == RAMA_ERR_INVALID:
+        raise ValueError(msg)
     raise RuntimeError("%s failed (%d): %s" % (name, rc, msg))
 
 

@@ -375,6 +375,17 @@ int rama_extend_separation(int64_t n, int64_t m_aug, const int32_t* eu, const in
   });
 }
 
+int rama_check_agreement(int64_t m_aug, const double* base, int64_t T, const int32_t* tri_edges, const double* lam,
+                         double eps, int32_t* agree, void* stream) {
+  return guarded(stream, [&](Ctx& ctx) {
+    check_sizes(0, m_aug);
+    check_handles(ctx, tri_edges, T, m_aug);
+    DualState st;
+    load_state(ctx, st, m_aug, base, T, tri_edges, lam);
+    *agree = check_edge_triangle_agreement(ctx, st, eps) ? 1 : 0;
+  });
+}
+
 int rama_message_passing(int64_t m_aug, const double* base, int64_t T, const int32_t* tri_edges, double* lam,
                          int32_t iters, int32_t phases, void* stream) {
   return guarded(stream, [&](Ctx& ctx) {

@@ -322,7 +322,7 @@ void row_ptr_from_sorted(Ctx& ctx, const int32_t* u, int64_t m, int64_t n, int32
 // numpy summation orders on device (see oracle/rama_oracle.c)
 __device__ __forceinline__ double pw_leaf(const double* a, int64_t n) {
   if (n < 8) {
-    double r = 0.0;
+    double r = -0.0;  // numpy 2.x starts the short sum at -0.0 (keeps -0.0 sums)
     for (int64_t i = 0; i < n; i++) r = __dadd_rn(r, a[i]);
     return r;
   }
@@ -378,7 +378,7 @@ __device__ __forceinline__ double pw_sum(const double* a, int64_t n) {
 // one np.add.reduceat segment: x[0] + pairwise(x[1:])
 __device__ __forceinline__ double seg_sum(const double* a, int64_t n) {
   if (n <= 0) return 0.0;
-  if (n == 1) return __dadd_rn(a[0], 0.0);
+  if (n == 1) return a[0];  // x0 + pairwise([]) = x0 + (-0.0) = x0
   return __dadd_rn(a[0], pw_sum(a + 1, n - 1));
 }
 

@@ -1261,6 +1261,110 @@ double lower_bound(Ctx& ctx, const DualState& st) {
   return total;
 }
 
+
+// ------------------------------------------- check_edge_triangle_agreement
+//
+// dual.py:477-531: arc consistency between the near-optimal label sets of
+// edges (bit 0 uncut, bit 1 cut) and triplets (bit p = pattern p of
+// MC_TRIANGLE = 000, 110, 101, 011, 111).  Jacobi sweeps exactly like the
+// reference: triplet pass against the current edge sets, then edge pass
+// against the new triplet sets (bits only ever clear), until no change.
+__constant__ uint8_t kMcPat[5][3] = {{0, 0, 0}, {1, 1, 0}, {1, 0, 1}, {0, 1, 1}, {1, 1, 1}};
+
+__global__ void k_agree_init_edges(const double* __restrict__ cl, int64_t m, double eps, uint32_t* __restrict__ em) {
+  GRID_STRIDE(e, m) {
+    double x = cl[e];
+    double best = mn2(x, 0.0);
+    uint32_t b = 0;
+    if (0.0 <= __dadd_rn(best, eps)) b |= 1u;
+    if (x <= __dadd_rn(best, eps)) b |= 2u;
+    em[e] = b;
+  }
+}
+
+__global__ void k_agree_init_tri(const double* __restrict__ lam, int64_t T, double eps, uint8_t* __restrict__ tm) {
+  GRID_STRIDE(t, T) {
+    double l0 = lam[3 * t], l1 = lam[3 * t + 1], l2 = lam[3 * t + 2];
+    double pc[5];
+    pc[0] = 0.0;
+    pc[1] = -__dadd_rn(l0, l1);
+    pc[2] = -__dadd_rn(l0, l2);
+    pc[3] = -__dadd_rn(l1, l2);
+    pc[4] = -__dadd_rn(__dadd_rn(l0, l1), l2);
+    double best = pc[0];
+    for (int p = 1; p < 5; p++) best = mn2(best, pc[p]);
+    uint8_t b = 0;
+    for (int p = 0; p < 5; p++)
+      if (pc[p] <= __dadd_rn(best, eps)) b |= (uint8_t)(1u << p);
+    tm[t] = b;
+  }
+}
+
+__global__ void k_agree_tri(const int32_t* __restrict__ te, int64_t T, const uint32_t* __restrict__ em,
+                            uint8_t* __restrict__ tm, int32_t* __restrict__ changed) {
+  GRID_STRIDE(t, T) {
+    uint8_t b = tm[t], nb = b;
+    uint32_t e0 = em[te[3 * t]], e1 = em[te[3 * t + 1]], e2 = em[te[3 * t + 2]];
+    for (int p = 0; p < 5; p++) {
+      bool ok = (e0 & (1u << kMcPat[p][0])) && (e1 & (1u << kMcPat[p][1])) && (e2 & (1u << kMcPat[p][2]));
+      if (!ok) nb &= (uint8_t)~(1u << p);
+    }
+    if (nb != b) {
+      tm[t] = nb;
+      *changed = 1;
+    }
+  }
+}
+
+__global__ void k_agree_edges(const int32_t* __restrict__ te, int64_t T, const uint8_t* __restrict__ tm,
+                              uint32_t* __restrict__ em, int32_t* __restrict__ changed) {
+  GRID_STRIDE(t, T) {
+    uint8_t b = tm[t];
+    for (int s = 0; s < 3; s++) {
+      bool has0 = false, has1 = false;
+      for (int p = 0; p < 5; p++)
+        if (b & (1u << p)) {
+          if (kMcPat[p][s]) has1 = true; else has0 = true;
+        }
+      uint32_t clear = (has0 ? 0u : 1u) | (has1 ? 0u : 2u);
+      if (clear) {
+        uint32_t old = atomicAnd(em + te[3 * t + s], ~clear);
+        if (old & clear) *changed = 1;
+      }
+    }
+  }
+}
+
+__global__ void k_agree_empty_e(const uint32_t* __restrict__ em, int64_t m, int32_t* __restrict__ bad) {
+  GRID_STRIDE(e, m) if (em[e] == 0) *bad = 1;
+}
+
+__global__ void k_agree_empty_t(const uint8_t* __restrict__ tm, int64_t T, int32_t* __restrict__ bad) {
+  GRID_STRIDE(t, T) if (tm[t] == 0) *bad = 1;
+}
+
+bool check_edge_triangle_agreement(Ctx& ctx, const DualState& st, double eps) {
+  RAMA_REQUIRE(eps >= 0.0, "eps must be non-negative");
+  const int64_t m = st.m_aug, T = st.T;
+  Buf<double> cl(m > 0 ? m : 1, ctx);
+  reparam_costs(ctx, st, cl.p);
+  Buf<uint32_t> em(m > 0 ? m : 1, ctx);
+  Buf<uint8_t> tm(T > 0 ? T : 1, ctx);
+  Buf<int32_t> flag(2, ctx);
+  RAMA_KERNEL(ctx, k_agree_init_edges, m, cl.p, m, eps, em.p);
+  RAMA_KERNEL(ctx, k_agree_init_tri, T, st.lam.p, T, eps, tm.p);
+  while (T > 0) {
+    flag.zero();
+    RAMA_KERNEL(ctx, k_agree_tri, T, st.tri_edges.p, T, em.p, tm.p, flag.p);
+    RAMA_KERNEL(ctx, k_agree_edges, T, st.tri_edges.p, T, tm.p, em.p, flag.p);
+    if (read_scalar(ctx, flag.p) == 0) break;
+  }
+  flag.zero();
+  RAMA_KERNEL(ctx, k_agree_empty_e, m, em.p, m, flag.p);
+  RAMA_KERNEL(ctx, k_agree_empty_t, T, tm.p, T, flag.p);
+  return read_scalar(ctx, flag.p) == 0;
+}
+
 // --------------------------------------------------- reparametrized graph
 
 // merge position of originals [0, m) and chords [m, m_aug) (both sorted)
@@ -1281,7 +1385,7 @@ __global__ void k_merge_scatter(int64_t m, int64_t C, const int32_t* __restrict_
     int64_t pos = self + (lo - l0);
     ou[pos] = a;
     ov[pos] = b;
-    oc[pos] = __dadd_rn(cl[i], 0.0);  // WeightedGraph ctor: x0 + pairwise([]) per unique pair
+    oc[pos] = cl[i];  // WeightedGraph ctor: x0 + pairwise([]) = x0 per unique pair
   }
 }
 
@@ -1291,7 +1395,7 @@ __global__ void k_sorted_edges_out(const int32_t* __restrict__ row, const uint64
   GRID_STRIDE(p, m) {
     ou[p] = row[p];
     ov[p] = (int32_t)(key[p] >> 32);
-    oc[p] = __dadd_rn(cl[(uint32_t)key[p]], 0.0);  // WeightedGraph ctor: x0 + pairwise([])
+    oc[p] = cl[(uint32_t)key[p]];  // WeightedGraph ctor: x0 + pairwise([]) = x0
   }
 }
 

@@ -96,6 +96,8 @@ void reparam_costs(Ctx& ctx, const DualState& st, double* cl);
 void message_passing(Ctx& ctx, DualState& st, int iters);
 // mp_edge_to_triplets / mp_triplets_to_edges individually (dual.py:358, 374)
 void mp_phases(Ctx& ctx, DualState& st, bool edge_phase, bool triplet_phase);
+// check_edge_triangle_agreement (dual.py:477-531)
+bool check_edge_triangle_agreement(Ctx& ctx, const DualState& st, double eps);
 // a11 lower_bound (dual.py:395-405)
 double lower_bound(Ctx& ctx, const DualState& st);
 // a12 reparametrized_graph (dual.py:408-411): canonical merge of originals

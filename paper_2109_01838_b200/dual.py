@@ -254,3 +254,20 @@ def extend_separation(state, max_len):
     state.lam = L.host_f64(olam, 3 * t).reshape(t, 3)
     state.coverage = L.host_i64(ocov, k)
     return int(added.value)
+
+
+def check_edge_triangle_agreement(state, eps):
+    """Arc consistency of the eps-optimal edge and triplet label sets
+    (dual.py:477-531): True iff every set stays non-empty.  On the device
+    (rama_check_agreement: Jacobi sweeps until no bit changes)."""
+    if eps < 0:
+        raise ValueError("eps must be non-negative")
+    if state.num_edges == 0:
+        return True
+    base, te, lam = state._dev()
+    if state.num_triplets == 0:
+        te, lam = L.empty_i32(1), L.empty_f64(1)
+    out = L.ctypes.c_int32()
+    L.call("rama_check_agreement", state.num_edges, L.ptr(base), state.num_triplets, L.ptr(te), L.ptr(lam),
+           float(eps), L.ctypes.byref(out), L.stream())
+    return bool(out.value)

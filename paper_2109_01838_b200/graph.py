@@ -183,73 +183,61 @@ def canonical_labels(labels):
 # Host file plumbing (NEXT); same grammar and errors
 # as graph.py:160-313.
 
-def parse_instance(text):
-    """Parse MULTICUT instance text into a WeightedGraph."""
-    if isinstance(text, bytes):
-        text = text.decode("utf-8")
-    lines = text.splitlines()
-    i = 0
-    while i < len(lines) and (not lines[i].strip() or lines[i].strip().startswith("#")):
-        i += 1
-    if i == len(lines):
-        raise ParseError("missing MULTICUT header")
-    if lines[i] != "MULTICUT":
-        raise ParseError("line %d: expected MULTICUT header, got %r" % (i + 1, lines[i]))
-    i += 1
-    declared = None
-    j = i
-    while j < len(lines) and (not lines[j].strip() or lines[j].strip().startswith("#")):
-        j += 1
-    if j < len(lines):
-        tok = lines[j].split()
-        if tok[0] == "NODES":
-            if len(tok) != 2:
-                raise ParseError("line %d: expected 'NODES <n>'" % (j + 1))
-            try:
-                declared = int(tok[1])
-            except ValueError:
-                raise ParseError("line %d: NODES count must be an integer" % (j + 1)) from None
-            if declared < 0:
-                raise ParseError("line %d: NODES count must be non-negative" % (j + 1))
-            i = j + 1
-    us, vs, cs = [], [], []
-    for k in range(i, len(lines)):
-        s = lines[k].strip()
-        if not s or s.startswith("#"):
-            continue
-        tok = s.split()
-        if len(tok) != 3:
-            raise ParseError("line %d: expected '<u> <v> <cost>', got %r" % (k + 1, lines[k]))
-        try:
-            a, b = int(tok[0]), int(tok[1])
-        except ValueError:
-            raise ParseError("line %d: node ids must be decimal integers" % (k + 1)) from None
-        try:
-            w = float(tok[2])
-        except ValueError:
-            raise ParseError("line %d: malformed cost %r" % (k + 1, tok[2])) from None
-        if not np.isfinite(w):
-            raise ParseError("line %d: cost must be finite" % (k + 1))
-        if a < 0 or b < 0:
-            raise ParseError("line %d: negative node id" % (k + 1))
-        if a == b:
-            raise ParseError("line %d: self-loop edge (%d, %d)" % (k + 1, a, b))
-        if declared is not None and (a >= declared or b >= declared):
-            raise ParseError("line %d: node id exceeds declared NODES %d" % (k + 1, declared))
-        us.append(a)
-        vs.append(b)
-        cs.append(w)
-    if declared is not None:
-        n = declared
-    elif us:
-        n = max(max(us), max(vs)) + 1
+def _parse_native(text=None, path=None, threads=0):
+    if path is not None:
+        import os
+
+        size = os.path.getsize(path)
+        data, length, cpath = None, 0, os.fsencode(path)
     else:
-        n = 0
-    return WeightedGraph(n, us, vs, cs)
+        if isinstance(text, str):
+            text = text.encode("utf-8")
+        data, length, cpath = text, len(text), None
+        size = length
+    cap = size // 5 + 2  # an edge line takes at least 6 bytes
+    while True:
+        u = np.empty(cap, np.int64)
+        v = np.empty(cap, np.int64)
+        c = np.empty(cap, np.float64)
+        n, m = L.ctypes.c_int64(), L.ctypes.c_int64()
+        try:
+            L.call_host("rama_parse_multicut", data, length, cpath, L.ctypes.byref(n), L.ctypes.byref(m),
+                        u.ctypes.data, v.ctypes.data, c.ctypes.data, cap, int(threads))
+        except ValueError as exc:
+            raise ParseError(str(exc)) from None
+        if m.value <= cap:
+            return n.value, u[: m.value], v[: m.value], c[: m.value]
+        cap = m.value
 
 
-def serialize_instance(g):
-    """MULTICUT text with a NODES line; costs via repr (bit-exact round trip)."""
-    out = ["MULTICUT", "NODES %d" % g.num_nodes]
-    out.extend("%d %d %r" % e for e in g.edges)
-    return "\n".join(out) + "\n"
+def parse_instance(text, threads=0):
+    """Parse MULTICUT instance text into a WeightedGraph (graph.py:204-263).
+
+    Native C++ parser (rama_parse_multicut: line-aligned chunks parsed by a
+    thread pool with std::from_chars) with the reference's acceptance rules
+    and ParseError messages; the COO is then canonicalised on the GPU.
+    """
+    n, u, v, c = _parse_native(text=text, threads=threads)
+    return WeightedGraph(n, u, v, c)
+
+
+def read_instance(path, threads=0):
+    """parse_instance on a file, memory-mapped by the native parser."""
+    n, u, v, c = _parse_native(path=path, threads=threads)
+    return WeightedGraph(n, u, v, c)
+
+
+def serialize_instance(g, threads=0):
+    """MULTICUT text with a NODES line; costs as Python repr, so parsing the
+    output reproduces them bit-exactly (graph.py:300-313).  Native
+    (rama_serialize_multicut, Python float repr rules)."""
+    u = np.ascontiguousarray(g.edges_u, dtype=np.int64)
+    v = np.ascontiguousarray(g.edges_v, dtype=np.int64)
+    c = np.ascontiguousarray(g.costs, dtype=np.float64)
+    length = L.ctypes.c_int64()
+    L.call_host("rama_serialize_multicut", int(g.num_nodes), u.ctypes.data, v.ctypes.data, c.ctypes.data, u.size,
+                None, 0, L.ctypes.byref(length), int(threads))
+    buf = L.ctypes.create_string_buffer(length.value + 1)
+    L.call_host("rama_serialize_multicut", int(g.num_nodes), u.ctypes.data, v.ctypes.data, c.ctypes.data, u.size,
+                buf, length.value + 1, L.ctypes.byref(length), int(threads))
+    return buf.raw[: length.value].decode("ascii")

@@ -222,3 +222,33 @@ def test_pd_plus_separation_matches_reference_bfs():
             a1, b1 = P.dual._separate(g, L)
             a2, b2 = O.separate(og, L)
             assert np.array_equal(a1, a2) and np.array_equal(b1, b2), L
+
+
+def test_agreement_matches_reference_and_oracle():
+    """check_edge_triangle_agreement on the device (dual.py:477-531) against
+    the reference's verdicts (golden/agreement.json) and the oracle on
+    larger states."""
+    import json
+    import os
+
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "agreement.json")) as fh:
+        cases = json.load(fh)
+    for case in cases:
+        n, u, v = case["n"], np.array(case["u"]), np.array(case["v"])
+        c = np.array([float(x) for x in case["c"]])
+        g = P.WeightedGraph._from_canonical(n, u, v, c)
+        lengths, nodes = O.separate(O.Graph(n, u, v, c, canonical=True), 5)
+        st = P.dual._triangulate_arrays(g, lengths, nodes)
+        if case["iters"]:
+            P.message_passing(st, case["iters"])
+        assert P.check_edge_triangle_agreement(st, case["eps"]) == case["agree"]
+    n, u, v, c = instances.grid8_coo(40, 50, strides=(2, 3), seed=4)
+    g, og = _both(n, u, v, c)
+    lengths, nodes = O.separate(og, 5)
+    st, ost = P.dual._triangulate_arrays(g, lengths, nodes), O.triangulate(og, lengths, nodes)
+    for iters in (0, 10, 100):
+        if iters:
+            P.message_passing(st, iters - (0 if iters == 10 else 10))
+            O.message_passing(ost, iters - (0 if iters == 10 else 10))
+        for eps in (1e-6, 1e-3, 0.5):
+            assert P.check_edge_triangle_agreement(st, eps) == O.check_edge_triangle_agreement(ost, eps)

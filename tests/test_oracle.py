@@ -7,6 +7,7 @@
 3. numpy summation-order restatements vs numpy.
 """
 
+import json
 import os
 
 import numpy as np
@@ -33,6 +34,10 @@ def test_seg_sum_matches_reduceat():
     for _ in range(300):
         x = rng.standard_normal(int(rng.integers(1, 700)))
         assert O.seg_sum(x) == float(np.add.reduceat(x, [0])[0])
+    # signed zeros: numpy keeps -0.0 (short sums start at -0.0)
+    for x in ([-0.0], [-0.0, -0.0], [-0.0, 0.0], [0.0, -0.0], [-0.0] * 9, [1.0, -1.0], [-1.0, 1.0, -0.0]):
+        x = np.array(x)
+        assert np.signbit(O.seg_sum(x)) == np.signbit(np.add.reduceat(x, [0])[0]), x
 
 
 # -------------------------------------------------- known-answer vectors
@@ -231,3 +236,19 @@ def test_extend_separation_matches_reference_mode_d_rounds():
             tr = np.array([[t.edges, t.triplets] for t in sol.trace], dtype=np.int64)
             assert np.array_equal(tr, d["g%d_r%d_trace" % (i, r)]), (i, r)
             assert sol.lower_bound == pytest.approx(float(d["g%d_r%d_lb" % (i, r)][0]), rel=1e-12, abs=1e-12)
+
+
+def _agreement_cases():
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "agreement.json")) as fh:
+        return json.load(fh)
+
+
+def test_agreement_matches_reference():
+    """check_edge_triangle_agreement (dual.py:477-531) on states after 0-200
+    MP iterations, against the reference's verdicts (golden/agreement.json)."""
+    for case in _agreement_cases():
+        g = O.Graph(case["n"], case["u"], case["v"], [float(x) for x in case["c"]], canonical=True)
+        lengths, nodes = O.separate(g, 5)
+        st = O.triangulate(g, lengths, nodes)
+        O.message_passing(st, case["iters"])
+        assert O.check_edge_triangle_agreement(st, case["eps"]) == case["agree"], case["iters"]
