@@ -387,7 +387,7 @@ def b200_arm(args):
                 "dominant_kernel": dominant}
     kernels = [{"kernel": k, "ms_per_step": v[0] / args.steps, "share": v[0] / p_ms, "launches_per_step": v[2] / args.steps,
                 "GB_per_s": (v[1] / (v[0] / 1e3) / 1e9) if v[1] > 0 and v[0] > 0 else None}
-               for k, v in ranked[:12]]
+               for k, v in ranked[:40]]
     families = {k: {"ms_per_step": vv[0] / args.steps, "alg_GB_per_step": vv[1] / args.steps / 1e9,
                     "scopes_per_step": vv[2] / args.steps} for k, vv in fam.items() if vv[2]}
 

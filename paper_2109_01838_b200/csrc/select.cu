@@ -25,6 +25,7 @@
 //     smallest undecided candidate.
 #include "internal.h"
 
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 namespace rama {
@@ -283,20 +284,6 @@ __global__ void k_rank_init(const int32_t* __restrict__ succ, int64_t na, int32_
   GRID_STRIDE(a, na) d[a] = succ[a] < 0 ? 0 : 1;
 }
 
-__global__ void k_rank_step(int64_t na, const int32_t* __restrict__ d, const int32_t* __restrict__ nx,
-                            int32_t* __restrict__ d2, int32_t* __restrict__ nx2) {
-  GRID_STRIDE(a, na) {
-    int32_t s = nx[a];
-    if (s >= 0) {
-      d2[a] = d[a] + d[s];
-      nx2[a] = nx[s];
-    } else {
-      d2[a] = d[a];
-      nx2[a] = -1;
-    }
-  }
-}
-
 __global__ void k_root_init(int64_t n, int32_t* __restrict__ par, int32_t* __restrict__ pedge,
                             int32_t* __restrict__ enter, int32_t* __restrict__ exit_) {
   GRID_STRIDE(x, n) {
@@ -331,25 +318,82 @@ __device__ __forceinline__ bool is_anc(const int32_t* enter, const int32_t* exit
   return exit_[x] < ew && ew < enter[x];
 }
 
-__global__ void k_lift0(int64_t n, const int32_t* __restrict__ par, const int32_t* __restrict__ pedge,
-                        const int32_t* __restrict__ edge_val, int32_t* __restrict__ up0, int32_t* __restrict__ mn0) {
+// ---- cooperative (one launch, grid.sync() between levels) -----------------
+// Binary-lifting tables and list ranking are level-synchronous pointer
+// jumping: one persistent launch replaces LOG (or log2 |arcs|) launches and
+// their gaps.  Reads of the previous level bypass L1 (written by other SMs).
+
+// level 0 from the parent links, then levels 1..LOG-1; up (if build_up) and
+// up to two min tables over edge values va / vb (nullptr = skip)
+__global__ void k_lift_coop(int64_t n, int LOG, const int32_t* __restrict__ par, const int32_t* __restrict__ pedge,
+                            int build_up, int32_t* up, const int32_t* __restrict__ va, int32_t* mna,
+                            const int32_t* __restrict__ vb, int32_t* mnb) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
   GRID_STRIDE(x, n) {
-    if (up0) up0[x] = par[x];
+    if (build_up) up[x] = par[x];
     int32_t f = pedge[x];
-    mn0[x] = f < 0 ? 0x7fffffff : edge_val[f];
+    if (mna) mna[x] = f < 0 ? 0x7fffffff : va[f];
+    if (mnb) mnb[x] = f < 0 ? 0x7fffffff : vb[f];
+  }
+  grid.sync();
+  for (int j = 1; j < LOG; j++) {
+    const int32_t* uj = up + (int64_t)(j - 1) * n;
+    GRID_STRIDE(x, n) {
+      int32_t y = __ldcg(uj + x);
+      if (build_up) up[(int64_t)j * n + x] = __ldcg(uj + y);
+      if (mna) {
+        const int32_t* mj = mna + (int64_t)(j - 1) * n;
+        mna[(int64_t)j * n + x] = min(__ldcg(mj + x), __ldcg(mj + y));
+      }
+      if (mnb) {
+        const int32_t* mj = mnb + (int64_t)(j - 1) * n;
+        mnb[(int64_t)j * n + x] = min(__ldcg(mj + x), __ldcg(mj + y));
+      }
+    }
+    grid.sync();
   }
 }
 
-__global__ void k_lift_up(int64_t n, const int32_t* __restrict__ upj, int32_t* __restrict__ upn) {
-  GRID_STRIDE(x, n) upn[x] = upj[upj[x]];
+// Wyllie list ranking: d = distance to the list end, in `steps` jumps
+__global__ void k_rank_coop(int64_t na, int steps, int32_t* d1, int32_t* n1, int32_t* d2, int32_t* n2) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  for (int s = 0; s < steps; s++) {
+    const int32_t* d = (s & 1) ? d2 : d1;
+    const int32_t* nx = (s & 1) ? n2 : n1;
+    int32_t* dd = (s & 1) ? d1 : d2;
+    int32_t* nn = (s & 1) ? n1 : n2;
+    GRID_STRIDE(a, na) {
+      int32_t t = __ldcg(nx + a);
+      if (t >= 0) {
+        dd[a] = __ldcg(d + a) + __ldcg(d + t);
+        nn[a] = __ldcg(nx + t);
+      } else {
+        dd[a] = __ldcg(d + a);
+        nn[a] = -1;
+      }
+    }
+    grid.sync();
+  }
 }
 
-__global__ void k_lift_min(int64_t n, const int32_t* __restrict__ upj, const int32_t* __restrict__ mnj,
-                           int32_t* __restrict__ mnn) {
-  GRID_STRIDE(x, n) {
-    int32_t a = mnj[x], b = mnj[upj[x]];
-    mnn[x] = a < b ? a : b;
+static unsigned coop_blocks(const void* fn) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    RAMA_CUDA(cudaGetDevice(&dev));
+    RAMA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
+  int per_sm = 0;
+  RAMA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBlock, 0));
+  return (unsigned)(sms * (per_sm < 4 ? per_sm : 4));
+}
+
+static void launch_coop(Ctx& ctx, const void* fn, const char* name, void** args) {
+  KernelScope ks(ctx.s, name, 0.0);
+  RAMA_CUDA(cudaLaunchCooperativeKernel(fn, dim3(coop_blocks(fn)), dim3(kBlock), args, 0, ctx.s));
+  ctx.launches++;
 }
 
 struct Lift {
@@ -462,14 +506,6 @@ __global__ void k_gather_pairs(const int32_t* __restrict__ idx, int64_t k, const
   }
 }
 
-static void build_min_table(Ctx& ctx, int64_t n, int LOG, const int32_t* up, const int32_t* par,
-                            const int32_t* pedge, const int32_t* edge_val, Buf<int32_t>& mn) {
-  mn.alloc((size_t)LOG * n, ctx.s);
-  RAMA_KERNEL(ctx, k_lift0, n, n, par, pedge, edge_val, (int32_t*)nullptr, mn.p);
-  for (int j = 1; j < LOG; j++)
-    RAMA_KERNEL(ctx, k_lift_min, n, n, up + (int64_t)(j - 1) * n, mn.p + (int64_t)(j - 1) * n, mn.p + (int64_t)j * n);
-}
-
 int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_t>& sv) {
   ProfScope prof(ctx.s, kFamForest);
   int64_t n = g.n, m = g.m;
@@ -540,10 +576,16 @@ int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_
     copy_d2d(ctx, n1.p, succ.p, na);
     int steps = 0;
     while ((1LL << steps) < na) steps++;
-    for (int s = 0; s <= steps; s++) {
-      RAMA_KERNEL(ctx, k_rank_step, na, na, d1.p, n1.p, d2.p, n2.p);
-      std::swap(d1, d2);
-      std::swap(n1, n2);
+    steps += 1;
+    {
+      int64_t na_ = na;
+      int32_t *pd1 = d1.p, *pn1 = n1.p, *pd2 = d2.p, *pn2 = n2.p;
+      void* args[] = {&na_, &steps, &pd1, &pn1, &pd2, &pn2};
+      launch_coop(ctx, (const void*)k_rank_coop, "k_rank_coop", args);
+      if (steps & 1) {  // result lives in the second buffer pair
+        std::swap(d1, d2);
+        std::swap(n1, n2);
+      }
     }
     Buf<int32_t> par(n, ctx), pedge(n, ctx), enter(n, ctx), exit_(n, ctx);
     RAMA_KERNEL(ctx, k_root_init, n, n, par.p, pedge.p, enter.p, exit_.p);
@@ -553,10 +595,15 @@ int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_
     int LOG = 1;
     while ((1LL << LOG) <= kf) LOG++;
     Buf<int32_t> up((size_t)LOG * n, ctx);
-    copy_d2d(ctx, up.p, par.p, n);
-    for (int j = 1; j < LOG; j++) RAMA_KERNEL(ctx, k_lift_up, n, n, up.p + (int64_t)(j - 1) * n, up.p + (int64_t)j * n);
-    Buf<int32_t> mn;
-    build_min_table(ctx, n, LOG, up.p, par.p, pedge.p, fkey.p, mn);
+    Buf<int32_t> mn((size_t)LOG * n, ctx);
+    {
+      int64_t n_ = n;
+      int build = 1;
+      int32_t *pup = up.p, *pmn = mn.p, *pnull = nullptr;
+      const int32_t *ppar = par.p, *ppe = pedge.p, *pva = fkey.p, *pvnull = nullptr;
+      void* args[] = {&n_, &LOG, &ppar, &ppe, &build, &pup, &pva, &pmn, &pvnull, &pnull};
+      launch_coop(ctx, (const void*)k_lift_coop, "k_lift_coop", args);
+    }
 
     Buf<int32_t> qa(nq, ctx), qb(nq, ctx), ql(nq, ctx), qe(nq, ctx);
     RAMA_KERNEL(ctx, k_cand_paths, nq, Q.p, nq, g.u, g.v, up.p, mn.p, LOG, n, enter.p, exit_.p, fsorted.p, qa.p,
@@ -570,8 +617,16 @@ int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_
       RAMA_KERNEL(ctx, k_fill_i32, kf, rf.p, kf, 0x7fffffff);
       RAMA_KERNEL(ctx, k_fill_i32, kf, ru.p, kf, 0x7fffffff);
       RAMA_KERNEL(ctx, k_earliest, nq, qe.p, state.p, nq, rf.p, ru.p);
-      build_min_table(ctx, n, LOG, up.p, par.p, pedge.p, rf.p, mf);
-      build_min_table(ctx, n, LOG, up.p, par.p, pedge.p, ru.p, mu);
+      mf.alloc((size_t)LOG * n, ctx.s);
+      mu.alloc((size_t)LOG * n, ctx.s);
+      {
+        int64_t n_ = n;
+        int build = 0;
+        int32_t *pup = up.p, *pmf = mf.p, *pmu = mu.p;
+        const int32_t *ppar = par.p, *ppe = pedge.p, *prf = rf.p, *pru = ru.p;
+        void* args[] = {&n_, &LOG, &ppar, &ppe, &build, &pup, &prf, &pmf, &pru, &pmu};
+        launch_coop(ctx, (const void*)k_lift_coop, "k_lift_coop", args);
+      }
       left.zero();
       RAMA_KERNEL(ctx, k_resolve, nq, nq, qa.p, qb.p, ql.p, up.p, mf.p, mu.p, LOG, n, enter.p, exit_.p, state.p,
                   left.p);
