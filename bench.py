@@ -35,7 +35,7 @@ sys.path.insert(0, ROOT)
 
 CPU_SAMPLE_ROWS = 256  # C2 crop for the CPU baseline: 256 x 2048 (~2.4M edges, ~11 s oracle)
 BATCH_INSTANCES = 64   # C5: 64 independent 512x512 grids per step
-BATCH_WORKERS = 8      # concurrent streams (host threads) per GPU for a batch
+BATCH_WORKERS = int(os.environ.get("RAMA_BATCH_WORKERS", "8"))  # concurrent streams (host threads) per GPU for a batch
 
 
 def parse():

@@ -675,7 +675,11 @@ int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc) {
       if (trace_print()) fprintf(stderr, "[rama] k_cl_tail np=%lld\n", (long long)np);
       void* kargs[] = {&A};
       KernelScope ks(ctx.s, "k_cl_tail", 0.0);
-      RAMA_CUDA(cudaLaunchCooperativeKernel((const void*)k_cl_tail, dim3(grid_blocks), dim3(kTailThreads), kargs,
+      // small quotients (batch instances) get a smaller grid: fewer CTAs in
+      // every grid.sync and SMs left to concurrent solves
+      int64_t want = np / 128 + 32;
+      unsigned tail_blocks = (unsigned)(want < grid_blocks ? want : grid_blocks);
+      RAMA_CUDA(cudaLaunchCooperativeKernel((const void*)k_cl_tail, dim3(tail_blocks), dim3(kTailThreads), kargs,
                                             kTailSmem, ctx.s));
       ctx.launches++;
       int32_t st[SC_COUNT];

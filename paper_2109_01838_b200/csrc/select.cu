@@ -390,9 +390,12 @@ static unsigned coop_blocks(const void* fn) {
   return (unsigned)(sms * (per_sm < 4 ? per_sm : 4));
 }
 
-static void launch_coop(Ctx& ctx, const void* fn, const char* name, void** args) {
+static void launch_coop(Ctx& ctx, const void* fn, const char* name, void** args, int64_t work) {
   KernelScope ks(ctx.s, name, 0.0);
-  RAMA_CUDA(cudaLaunchCooperativeKernel(fn, dim3(coop_blocks(fn)), dim3(kBlock), args, 0, ctx.s));
+  int64_t want = (work + 4 * kBlock - 1) / (4 * kBlock);  // ~4 items per thread per level
+  unsigned cap = coop_blocks(fn);
+  unsigned blocks = (unsigned)(want < 1 ? 1 : (want < cap ? want : cap));
+  RAMA_CUDA(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kBlock), args, 0, ctx.s));
   ctx.launches++;
 }
 
@@ -581,7 +584,7 @@ int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_
       int64_t na_ = na;
       int32_t *pd1 = d1.p, *pn1 = n1.p, *pd2 = d2.p, *pn2 = n2.p;
       void* args[] = {&na_, &steps, &pd1, &pn1, &pd2, &pn2};
-      launch_coop(ctx, (const void*)k_rank_coop, "k_rank_coop", args);
+      launch_coop(ctx, (const void*)k_rank_coop, "k_rank_coop", args, na);
       if (steps & 1) {  // result lives in the second buffer pair
         std::swap(d1, d2);
         std::swap(n1, n2);
@@ -602,7 +605,7 @@ int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_
       int32_t *pup = up.p, *pmn = mn.p, *pnull = nullptr;
       const int32_t *ppar = par.p, *ppe = pedge.p, *pva = fkey.p, *pvnull = nullptr;
       void* args[] = {&n_, &LOG, &ppar, &ppe, &build, &pup, &pva, &pmn, &pvnull, &pnull};
-      launch_coop(ctx, (const void*)k_lift_coop, "k_lift_coop", args);
+      launch_coop(ctx, (const void*)k_lift_coop, "k_lift_coop", args, n);
     }
 
     Buf<int32_t> qa(nq, ctx), qb(nq, ctx), ql(nq, ctx), qe(nq, ctx);
@@ -625,7 +628,7 @@ int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_
         int32_t *pup = up.p, *pmf = mf.p, *pmu = mu.p;
         const int32_t *ppar = par.p, *ppe = pedge.p, *prf = rf.p, *pru = ru.p;
         void* args[] = {&n_, &LOG, &ppar, &ppe, &build, &pup, &prf, &pmf, &pru, &pmu};
-        launch_coop(ctx, (const void*)k_lift_coop, "k_lift_coop", args);
+        launch_coop(ctx, (const void*)k_lift_coop, "k_lift_coop", args, n);
       }
       left.zero();
       RAMA_KERNEL(ctx, k_resolve, nq, nq, qa.p, qb.p, ql.p, up.p, mf.p, mu.p, LOG, n, enter.p, exit_.p, state.p,
