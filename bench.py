@@ -41,7 +41,7 @@ BATCH_WORKERS = int(os.environ.get("RAMA_BATCH_WORKERS", "8"))  # concurrent str
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "c5batch"])
@@ -118,7 +118,7 @@ class ClockSampler:
                 ["nvidia-smi", "-i", str(index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
@@ -139,13 +139,12 @@ class ClockSampler:
             except ValueError:
                 continue
             smax = mx
-            if util > 0:
-                sm.append(clk)
+            sm.append(clk)  # every sample falls inside the timed region
             for nm, val in zip(names, f[3:7]):
                 if val.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples_under_load": len(sm)}
+                "samples": len(sm), "interval_ms": 20}
 
 
 def peak_hbm():
