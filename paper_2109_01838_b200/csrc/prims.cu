@@ -464,16 +464,26 @@ __global__ void k_bucket_count(const int32_t* __restrict__ row, int64_t N, int32
   }
 }
 
+// scattered item: one 16-byte store per item instead of three partial-sector
+// stores into separate arrays (the scatter's DRAM traffic was 4x its bytes)
+struct __align__(16) BItem {
+  uint64_t key;
+  int32_t src;
+  int32_t row;
+};
+
 __global__ void k_bucket_scatter(const int32_t* __restrict__ row, const uint64_t* __restrict__ key,
                                  const int32_t* __restrict__ off, int64_t N, const int32_t* __restrict__ ptr,
-                                 uint64_t* __restrict__ tkey, int32_t* __restrict__ tsrc, int32_t* __restrict__ orow) {
+                                 BItem* __restrict__ items) {
   GRID_STRIDE(i, N) {
     int32_t r = row[i];
     if (r < 0) continue;
     int32_t p = ptr[r] + off[i];
-    tkey[p] = key[i];
-    tsrc[p] = (int32_t)i;
-    orow[p] = r;
+    BItem it;
+    it.key = key[i];
+    it.src = (int32_t)i;
+    it.row = r;
+    items[p] = it;
   }
 }
 
@@ -485,18 +495,18 @@ __global__ void k_bucket_scatter(const int32_t* __restrict__ row, const uint64_t
 constexpr int kSmallRow = 64;
 constexpr int kBlockRow = 4096;  // bitonic sort in shared memory: 4096 x 12 B = 48 KB
 
-__global__ void k_rank_rows(const int32_t* __restrict__ row, const int32_t* __restrict__ ptr, int64_t N,
-                            int64_t sort_rows, const uint64_t* __restrict__ tkey, const int32_t* __restrict__ tsrc,
-                            uint64_t* __restrict__ okey, int32_t* __restrict__ osrc, int32_t* __restrict__ big_list,
-                            int32_t* __restrict__ huge_list, int32_t* __restrict__ counters) {
+__global__ void k_rank_rows(const BItem* __restrict__ items, const int32_t* __restrict__ ptr, int64_t N,
+                            int64_t sort_rows, uint64_t* __restrict__ okey, int32_t* __restrict__ osrc,
+                            int32_t* __restrict__ orow, int32_t* __restrict__ big_list, int32_t* __restrict__ huge_list,
+                            int32_t* __restrict__ counters) {
   GRID_STRIDE(p, N) {
-    int32_t r = row[p];
+    const BItem it = items[p];
+    const int32_t r = it.row;
+    if (orow) orow[p] = r;  // rows keep their ranges
     int32_t b = ptr[r], e = ptr[r + 1];
-    uint64_t k = tkey[p];
-    int32_t s = tsrc[p];
     if (e - b == 1 || r >= sort_rows) {
-      okey[p] = k;
-      osrc[p] = s;
+      okey[p] = it.key;
+      osrc[p] = it.src;
       continue;
     }
     if (e - b > kSmallRow) {  // block bitonic (<= kBlockRow) or CUB segmented sort (hubs)
@@ -508,14 +518,13 @@ __global__ void k_rank_rows(const int32_t* __restrict__ row, const int32_t* __re
     }
     int32_t rank = 0;
     for (int32_t q = b; q < e; q++) {
-      uint64_t x = tkey[q];
-      rank += (x < k) || (x == k && q < (int32_t)p);
+      uint64_t x = items[q].key;
+      rank += (x < it.key) || (x == it.key && q < (int32_t)p);
     }
-    okey[b + rank] = k;
-    osrc[b + rank] = s;
+    okey[b + rank] = it.key;
+    osrc[b + rank] = it.src;
   }
 }
-
 
 // one block per listed row: bitonic sort of (key, src) in shared memory,
 // from the scatter buffers into the output; rows longer than kBlockRow go
@@ -523,9 +532,8 @@ __global__ void k_rank_rows(const int32_t* __restrict__ row, const int32_t* __re
 __global__ void __launch_bounds__(512) k_sort_rows_block(const int32_t* __restrict__ ptr,
                                                          const int32_t* __restrict__ big_list,
                                                          int32_t* __restrict__ counters,
-                                                         const uint64_t* __restrict__ tkey,
-                                                         const int32_t* __restrict__ tsrc, uint64_t* __restrict__ key,
-                                                         int32_t* __restrict__ src) {
+                                                         const BItem* __restrict__ items,
+                                                         uint64_t* __restrict__ key, int32_t* __restrict__ src) {
   __shared__ uint64_t sk[kBlockRow];
   __shared__ int32_t ss[kBlockRow];
   int32_t nbig = counters[0];
@@ -535,7 +543,7 @@ __global__ void __launch_bounds__(512) k_sort_rows_block(const int32_t* __restri
     int32_t P = 64;
     while (P < len) P <<= 1;
     for (int32_t i = threadIdx.x; i < P; i += blockDim.x) {
-      if (i < len) { sk[i] = tkey[b + i]; ss[i] = tsrc[b + i]; }
+      if (i < len) { sk[i] = items[b + i].key; ss[i] = items[b + i].src; }
       else { sk[i] = ~0ULL; ss[i] = 0x7fffffff; }
     }
     __syncthreads();
@@ -569,16 +577,29 @@ __global__ void k_big_lens(const int32_t* __restrict__ rows, int64_t nb, const i
 }
 
 // move huge rows between the row layout and a contiguous staging area
-__global__ void k_big_move(const int32_t* __restrict__ rows, int64_t nb, const int32_t* __restrict__ ptr,
-                           const int32_t* __restrict__ off, const uint64_t* __restrict__ key_in,
-                           const int32_t* __restrict__ src_in, uint64_t* __restrict__ key_out,
-                           int32_t* __restrict__ src_out, bool to_stage) {
+__global__ void k_big_stage(const int32_t* __restrict__ rows, int64_t nb, const int32_t* __restrict__ ptr,
+                            const int32_t* __restrict__ off, const BItem* __restrict__ items,
+                            uint64_t* __restrict__ key_out, int32_t* __restrict__ src_out) {
   for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
     int32_t r = rows[b];
     int32_t base = ptr[r], len = ptr[r + 1] - base, o = off[b];
     for (int32_t j = threadIdx.x; j < len; j += blockDim.x) {
-      if (to_stage) { key_out[o + j] = key_in[base + j]; src_out[o + j] = src_in[base + j]; }
-      else { key_out[base + j] = key_in[o + j]; src_out[base + j] = src_in[o + j]; }
+      key_out[o + j] = items[base + j].key;
+      src_out[o + j] = items[base + j].src;
+    }
+  }
+}
+
+__global__ void k_big_unstage(const int32_t* __restrict__ rows, int64_t nb, const int32_t* __restrict__ ptr,
+                              const int32_t* __restrict__ off, const uint64_t* __restrict__ key_in,
+                              const int32_t* __restrict__ src_in, uint64_t* __restrict__ key_out,
+                              int32_t* __restrict__ src_out) {
+  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    int32_t r = rows[b];
+    int32_t base = ptr[r], len = ptr[r + 1] - base, o = off[b];
+    for (int32_t j = threadIdx.x; j < len; j += blockDim.x) {
+      key_out[base + j] = key_in[o + j];
+      src_out[base + j] = src_in[o + j];
     }
   }
 }
@@ -589,7 +610,7 @@ void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint6
   out.row_ptr.alloc(R + 1, ctx.s);
   out.key.alloc(N > 0 ? N : 1, ctx.s);
   out.src.alloc(N > 0 ? N : 1, ctx.s);
-  out.row.alloc(N > 0 ? N : 1, ctx.s);
+  if (want_row) out.row.alloc(N > 0 ? N : 1, ctx.s);
   Buf<int32_t> cnt(R > 0 ? R : 1, ctx), off(N > 0 ? N : 1, ctx);
   cnt.zero();
   prof_set_bytes(8.0 * (double)N);
@@ -600,10 +621,9 @@ void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint6
     if (!want_row) out.row.release();
     return;
   }
-  Buf<uint64_t> tkey(total, ctx);
-  Buf<int32_t> tsrc(total, ctx);
+  Buf<BItem> items(total, ctx);
   prof_set_bytes(16.0 * (double)N + 16.0 * (double)total);
-  RAMA_KERNEL(ctx, k_bucket_scatter, N, row, key, off.p, N, out.row_ptr.p, tkey.p, tsrc.p, out.row.p);
+  RAMA_KERNEL(ctx, k_bucket_scatter, N, row, key, off.p, N, out.row_ptr.p, items.p);
   off.release();
   cnt.release();
   Buf<int32_t> lists(2 * sort_rows + 2, ctx);  // big list | huge list | counters
@@ -611,9 +631,9 @@ void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint6
   int32_t* huge_list = lists.p + sort_rows;
   int32_t* counters = lists.p + 2 * sort_rows;
   RAMA_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(int32_t), ctx.s));
-  prof_set_bytes(32.0 * (double)total);
-  RAMA_KERNEL(ctx, k_rank_rows, total, out.row.p, out.row_ptr.p, total, sort_rows, tkey.p, tsrc.p, out.key.p,
-              out.src.p, big_list, huge_list, counters);
+  prof_set_bytes(16.0 * (double)total + 12.0 * (double)total + (want_row ? 4.0 * (double)total : 0.0));
+  RAMA_KERNEL(ctx, k_rank_rows, total, items.p, out.row_ptr.p, total, sort_rows, out.key.p, out.src.p,
+              want_row ? out.row.p : (int32_t*)nullptr, big_list, huge_list, counters);
   if (!want_row) out.row.release();
   if (sort_rows == 0) return;
   // one read-back of both list sizes; the long-row sorts launch only when needed
@@ -623,8 +643,7 @@ void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint6
   if (nbig > 0) {
     unsigned gb = (unsigned)std::min<int64_t>(nbig, 148 * 4);
     KernelScope ks_block(ctx.s, "k_sort_rows_block", 0.0);
-    k_sort_rows_block<<<gb, 512, 0, ctx.s>>>(out.row_ptr.p, big_list, counters, tkey.p, tsrc.p, out.key.p,
-                                             out.src.p);
+    k_sort_rows_block<<<gb, 512, 0, ctx.s>>>(out.row_ptr.p, big_list, counters, items.p, out.key.p, out.src.p);
     RAMA_LAUNCH_CHECK();
     ctx.launches++;
   }
@@ -636,7 +655,7 @@ void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint6
   Buf<uint64_t> k1(tot, ctx), k2(tot, ctx);
   Buf<int32_t> s1(tot, ctx), s2(tot, ctx);
   unsigned g = (unsigned)std::min<int64_t>(nb, 4096);
-  k_big_move<<<g, kBlock, 0, ctx.s>>>(huge_list, nb, out.row_ptr.p, boff.p, tkey.p, tsrc.p, k1.p, s1.p, true);
+  k_big_stage<<<g, kBlock, 0, ctx.s>>>(huge_list, nb, out.row_ptr.p, boff.p, items.p, k1.p, s1.p);
   RAMA_LAUNCH_CHECK();
   size_t tb = 0;
   RAMA_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, tb, k1.p, k2.p, s1.p, s2.p, (int)tot, (int)nb, boff.p,
@@ -644,7 +663,7 @@ void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint6
   Buf<uint8_t> tmp(tb, ctx);
   RAMA_CUDA(cub::DeviceSegmentedSort::SortPairs(tmp.p, tb, k1.p, k2.p, s1.p, s2.p, (int)tot, (int)nb, boff.p,
                                                 boff.p + 1, ctx.s));
-  k_big_move<<<g, kBlock, 0, ctx.s>>>(huge_list, nb, out.row_ptr.p, boff.p, k2.p, s2.p, out.key.p, out.src.p, false);
+  k_big_unstage<<<g, kBlock, 0, ctx.s>>>(huge_list, nb, out.row_ptr.p, boff.p, k2.p, s2.p, out.key.p, out.src.p);
   RAMA_LAUNCH_CHECK();
   ctx.launches += 3;
 }
