@@ -849,27 +849,21 @@ __global__ void k_tri_out(const int32_t* __restrict__ heads, int64_t T, const in
   }
 }
 
-__device__ __forceinline__ int32_t edge_handle(const int32_t* rptr, const int32_t* gv, const uint64_t* ckeys,
-                                               int64_t C, int64_t m, int32_t a, int32_t b) {
+__device__ __forceinline__ int32_t edge_handle(const int32_t* rptr, const int32_t* gv, const int32_t* crptr,
+                                               const int32_t* cv, int64_t m, int32_t a, int32_t b) {
   int32_t e = find_in_row(rptr, gv, a, b);
   if (e >= 0) return e;
-  uint64_t k = ((uint64_t)(uint32_t)a << 32) | (uint64_t)(uint32_t)b;
-  int64_t lo = 0, hi = C;
-  while (lo < hi) {
-    int64_t mid = (lo + hi) >> 1;
-    if (ckeys[mid] < k) lo = mid + 1; else hi = mid;
-  }
-  return (int32_t)(m + lo);  // present by construction
+  return (int32_t)(m + find_in_row(crptr, cv, a, b));  // a chord: present by construction
 }
 
 __global__ void k_tri_handles(const int32_t* __restrict__ tn, int64_t T, const int32_t* __restrict__ rptr,
-                              const int32_t* __restrict__ gv, const uint64_t* __restrict__ ckeys, int64_t C,
-                              int64_t m, int32_t* __restrict__ te) {
+                              const int32_t* __restrict__ gv, const int32_t* __restrict__ crptr,
+                              const int32_t* __restrict__ cv, int64_t m, int32_t* __restrict__ te) {
   GRID_STRIDE(t, T) {
     int32_t i = tn[3 * t], j = tn[3 * t + 1], k = tn[3 * t + 2];
-    te[3 * t] = edge_handle(rptr, gv, ckeys, C, m, i, j);
-    te[3 * t + 1] = edge_handle(rptr, gv, ckeys, C, m, i, k);
-    te[3 * t + 2] = edge_handle(rptr, gv, ckeys, C, m, j, k);
+    te[3 * t] = edge_handle(rptr, gv, crptr, cv, m, i, j);
+    te[3 * t + 1] = edge_handle(rptr, gv, crptr, cv, m, i, k);
+    te[3 * t + 2] = edge_handle(rptr, gv, crptr, cv, m, j, k);
   }
 }
 
@@ -910,8 +904,9 @@ void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& 
               ckey.p);
 
   // chords: dedupe, drop existing edges
-  Buf<int32_t> rptr(n + 1, ctx);
-  row_ptr_from_sorted(ctx, g.u, m, n, rptr.p);
+  st.orig_ptr.alloc(n + 1, ctx.s);
+  int32_t* rptr_p = st.orig_ptr.p;
+  row_ptr_from_sorted(ctx, g.u, m, n, rptr_p);
   int64_t C = 0;
   Buf<uint64_t> ckeys(1, ctx);
   st.eu.alloc(m + craw > 0 ? m + craw : 1, ctx.s);
@@ -928,13 +923,16 @@ void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& 
     Buf<int32_t> hp;
     int64_t nh = compact_indices(ctx, head.p, craw, hp);
     Buf<uint8_t> isnew(nh > 0 ? nh : 1, ctx);
-    RAMA_KERNEL(ctx, k_chord_new, nh, hp.p, nh, cs.row.p, cs.key.p, rptr.p, g.v, isnew.p);
+    RAMA_KERNEL(ctx, k_chord_new, nh, hp.p, nh, cs.row.p, cs.key.p, rptr_p, g.v, isnew.p);
     Buf<int32_t> sel;
     C = compact_indices(ctx, isnew.p, nh, sel);
     ckeys.alloc(C > 0 ? C : 1, ctx.s);
     RAMA_KERNEL(ctx, k_chord_out, C, sel.p, C, hp.p, cs.row.p, cs.key.p, m, st.eu.p, st.ev.p, st.base.p, ckeys.p);
   }
   st.m_aug = m + C;
+  st.chords_sorted = true;
+  st.chord_ptr.alloc(n + 1, ctx.s);
+  row_ptr_from_sorted(ctx, st.eu.p + m, C, n, st.chord_ptr.p);
 
   // triplets: dedupe (lexicographic), handles
   int64_t T = 0;
@@ -948,7 +946,8 @@ void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& 
     st.tri_nodes.alloc(3 * T, ctx.s);
     st.tri_edges.alloc(3 * T, ctx.s);
     RAMA_KERNEL(ctx, k_tri_out, T, hp.p, T, ts.row.p, ts.key.p, st.tri_nodes.p);
-    RAMA_KERNEL(ctx, k_tri_handles, T, st.tri_nodes.p, T, rptr.p, g.v, ckeys.p, C, m, st.tri_edges.p);
+    RAMA_KERNEL(ctx, k_tri_handles, T, st.tri_nodes.p, T, rptr_p, g.v, st.chord_ptr.p, st.ev.p + m, m,
+                st.tri_edges.p);
   } else {
     st.tri_nodes.alloc(1, ctx.s);
     st.tri_edges.alloc(1, ctx.s);
@@ -1088,7 +1087,11 @@ int64_t extend_separation(Ctx& ctx, DualState& st, int L) {
     RAMA_KERNEL(ctx, k_chord_out, C, sel_c.p, C, hp_c.p, cs.row.p, cs.key.p, m0, st.eu.p, st.ev.p, st.base.p,
                 unused.p);
     st.m_aug = m0 + C;
-    if (m0 > st.m_orig) st.chords_sorted = false;
+    if (m0 > st.m_orig) {
+      st.chords_sorted = false;
+    } else if (st.chords_sorted && st.chord_ptr.p) {  // the new chords are the only run: refresh its rows
+      row_ptr_from_sorted(ctx, st.eu.p + st.m_orig, st.m_aug - st.m_orig, n, st.chord_ptr.p);
+    }
   }
   // new triplets: fan dedupe, then drop those already present
   BucketSorted ts;
@@ -1244,13 +1247,13 @@ __global__ void k_tri_min(int64_t T, const double* __restrict__ lam, double* __r
   }
 }
 
-double lower_bound(Ctx& ctx, const DualState& st) {
+double lower_bound(Ctx& ctx, const DualState& st, double* cl_out) {
   ProfScope prof(ctx.s, kFamBound);
   double total = 0.0;
   if (st.m_aug > 0) {
     Buf<double> neg(st.m_aug, ctx);
     RAMA_KERNEL(ctx, k_reparam, st.m_aug, st.m_aug, st.base.p, st.T ? st.slot_ptr.p : (const int32_t*)nullptr,
-                st.slots.p, st.lam.p, (double*)nullptr, neg.p);
+                st.slots.p, st.lam.p, cl_out, neg.p);
     total = device_sum(ctx, neg.p, st.m_aug);
   }
   if (st.T > 0) {
@@ -1367,22 +1370,25 @@ bool check_edge_triangle_agreement(Ctx& ctx, const DualState& st, double eps) {
 
 // --------------------------------------------------- reparametrized graph
 
-// merge position of originals [0, m) and chords [m, m_aug) (both sorted)
+// merge position of originals [0, m) and chords [m, m_aug) (both sorted):
+// the count of the other list's keys below (a, b) is that list's row start
+// plus a search inside its (short) row a
+__device__ __forceinline__ int32_t row_lower(const int32_t* ptr, const int32_t* col, int32_t a, int32_t b) {
+  int32_t lo = ptr[a], hi = ptr[a + 1];
+  while (lo < hi) {
+    int32_t mid = (lo + hi) >> 1;
+    if (col[mid] < b) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
 __global__ void k_merge_scatter(int64_t m, int64_t C, const int32_t* __restrict__ eu, const int32_t* __restrict__ ev,
-                                const double* __restrict__ cl, int32_t* __restrict__ ou, int32_t* __restrict__ ov,
+                                const double* __restrict__ cl, const int32_t* __restrict__ optr,
+                                const int32_t* __restrict__ cptr, int32_t* __restrict__ ou, int32_t* __restrict__ ov,
                                 double* __restrict__ oc) {
   GRID_STRIDE(i, m + C) {
     int32_t a = eu[i], b = ev[i];
-    int64_t lo, hi, self;
-    if (i < m) { lo = m; hi = m + C; self = i; }
-    else { lo = 0; hi = m; self = i - m; }
-    int64_t l0 = lo;
-    while (lo < hi) {  // count of other-list keys < (a, b)
-      int64_t mid = (lo + hi) >> 1;
-      int32_t x = eu[mid], y = ev[mid];
-      if (x < a || (x == a && y < b)) lo = mid + 1; else hi = mid;
-    }
-    int64_t pos = self + (lo - l0);
+    int64_t pos = i < m ? i + row_lower(cptr, ev + m, a, b) : (i - m) + row_lower(optr, ev, a, b);
     ou[pos] = a;
     ov[pos] = b;
     oc[pos] = cl[i];  // WeightedGraph ctor: x0 + pairwise([]) = x0 per unique pair
@@ -1399,7 +1405,7 @@ __global__ void k_sorted_edges_out(const int32_t* __restrict__ row, const uint64
   }
 }
 
-Graph reparametrized_graph(Ctx& ctx, const DualState& st) {
+Graph reparametrized_graph(Ctx& ctx, const DualState& st, const double* cl_in) {
   ProfScope prof(ctx.s, kFamBound);
   Graph g;
   g.n = st.n;
@@ -1409,19 +1415,24 @@ Graph reparametrized_graph(Ctx& ctx, const DualState& st) {
   g.v.alloc(ma, ctx.s);
   g.c.alloc(ma, ctx.s);
   if (st.m_aug == 0) return g;
-  Buf<double> cl(st.m_aug, ctx);
-  reparam_costs(ctx, st, cl.p);
-  if (!st.chords_sorted) {  // several chord runs (extend_separation): sort all augmented edges
+  Buf<double> cl_own;
+  const double* cl = cl_in;
+  if (!cl) {
+    cl_own.alloc(st.m_aug, ctx.s);
+    reparam_costs(ctx, st, cl_own.p);
+    cl = cl_own.p;
+  }
+  if (!st.chords_sorted || !st.orig_ptr.p || !st.chord_ptr.p) {  // general edge order: sort all augmented edges
     Buf<int32_t> row(st.m_aug, ctx);
     Buf<uint64_t> key(st.m_aug, ctx);
     RAMA_KERNEL(ctx, k_ext_edge_keys, st.m_aug, st.eu.p, st.ev.p, st.m_aug, row.p, key.p);
     BucketSorted bs;
     bucket_sort(ctx, st.n, st.m_aug, row.p, key.p, bs, true);
-    RAMA_KERNEL(ctx, k_sorted_edges_out, st.m_aug, bs.row.p, bs.key.p, cl.p, st.m_aug, g.u.p, g.v.p, g.c.p);
+    RAMA_KERNEL(ctx, k_sorted_edges_out, st.m_aug, bs.row.p, bs.key.p, cl, st.m_aug, g.u.p, g.v.p, g.c.p);
     return g;
   }
-  RAMA_KERNEL(ctx, k_merge_scatter, st.m_aug, st.m_orig, st.m_aug - st.m_orig, st.eu.p, st.ev.p, cl.p, g.u.p, g.v.p,
-              g.c.p);
+  RAMA_KERNEL(ctx, k_merge_scatter, st.m_aug, st.m_orig, st.m_aug - st.m_orig, st.eu.p, st.ev.p, cl, st.orig_ptr.p,
+              st.chord_ptr.p, g.u.p, g.v.p, g.c.p);
   return g;
 }
 

@@ -82,6 +82,8 @@ struct DualState {
   Buf<int32_t> tri_nodes;   // T*3 sorted (i<j<k), rows sorted lexicographically
   Buf<int32_t> tri_edges;   // T*3 handles (ij, ik, jk)
   Buf<int32_t> coverage;    // m_aug
+  Buf<int32_t> orig_ptr;    // n + 1: rows of the originals [0, m_orig) (sorted by (u, v))
+  Buf<int32_t> chord_ptr;   // n + 1: rows of the chords [m_orig, m_aug) (valid while chords_sorted)
   Buf<int32_t> slot_ptr;    // m_aug + 1 : edge -> ascending slot list
   Buf<int32_t> slots;       // 3T
   Buf<double> lam;          // 3T
@@ -99,10 +101,12 @@ void mp_phases(Ctx& ctx, DualState& st, bool edge_phase, bool triplet_phase);
 // check_edge_triangle_agreement (dual.py:477-531)
 bool check_edge_triangle_agreement(Ctx& ctx, const DualState& st, double eps);
 // a11 lower_bound (dual.py:395-405)
-double lower_bound(Ctx& ctx, const DualState& st);
+// (cl_out: optional m_aug buffer receiving c^lambda for a following
+// reparametrized_graph call)
+double lower_bound(Ctx& ctx, const DualState& st, double* cl_out = nullptr);
 // a12 reparametrized_graph (dual.py:408-411): canonical merge of originals
 // and chords carrying c^lambda
-Graph reparametrized_graph(Ctx& ctx, const DualState& st);
+Graph reparametrized_graph(Ctx& ctx, const DualState& st, const double* cl = nullptr);
 // edge -> slot CSR + coverage for an existing tri_edges array
 void build_slot_lists(Ctx& ctx, DualState& st);
 

@@ -130,10 +130,11 @@ void solve(Ctx& ctx, const GraphView& g, const SolveConfig& cfg, int32_t* labels
       DualState st;
       triangulate(ctx, cur.view(), cyc, st);
       message_passing(ctx, st, cfg.mp_iterations);
-      lb_r = lower_bound(ctx, st);
+      Buf<double> cl(st.m_aug > 0 ? st.m_aug : 1, ctx);
+      lb_r = lower_bound(ctx, st, cl.p);  // c^lambda computed once for the bound and the graph
       T = st.T;
       if (rnd == 1) lb = lb_r;
-      Graph rep = reparametrized_graph(ctx, st);
+      Graph rep = reparametrized_graph(ctx, st, cl.p);
       contraction_step(ctx, rep.view(), 3, cfg.switch_fraction, step);
     } else {
       contraction_step(ctx, cur.view(), 3, cfg.switch_fraction, step);
