@@ -424,7 +424,18 @@ double device_sum(Ctx& ctx, const double* x, int64_t n) {
 
 // ----------------------------------------------------------- row ptrs
 
-__global__ void k_row_ptr(const int32_t* __restrict__ u, int64_t m, int64_t n, int32_t* __restrict__ ptr) {
+// dense lists (m >= n): one pass over the sorted u, edge i opens the rows
+// (u[i-1], u[i]] -- the gaps are short; sparse lists: one binary search per
+// row (a long gap would serialise a thread)
+__global__ void k_row_ptr_fill(const int32_t* __restrict__ u, int64_t m, int64_t n, int32_t* __restrict__ ptr) {
+  GRID_STRIDE(i, m + 1) {
+    int64_t prev = i > 0 ? (int64_t)u[i - 1] : -1;
+    int64_t cur = i < m ? (int64_t)u[i] : n;
+    for (int64_t x = prev + 1; x <= cur; x++) ptr[x] = (int32_t)i;
+  }
+}
+
+__global__ void k_row_ptr_search(const int32_t* __restrict__ u, int64_t m, int64_t n, int32_t* __restrict__ ptr) {
   GRID_STRIDE(x, n + 1) {
     int64_t lo = 0, hi = m;
     while (lo < hi) {
@@ -436,7 +447,8 @@ __global__ void k_row_ptr(const int32_t* __restrict__ u, int64_t m, int64_t n, i
 }
 
 void row_ptr_from_sorted(Ctx& ctx, const int32_t* u, int64_t m, int64_t n, int32_t* ptr) {
-  RAMA_KERNEL(ctx, k_row_ptr, n + 1, u, m, n, ptr);
+  if (m >= 4 * n) RAMA_KERNEL(ctx, k_row_ptr_fill, m + 1, u, m, n, ptr);
+  else RAMA_KERNEL(ctx, k_row_ptr_search, n + 1, u, m, n, ptr);
 }
 
 // ---------------------------------------------------------- bucket sort
