@@ -237,3 +237,32 @@ def test_extend_separation_state_matches_oracle():
         assert P.extend_separation(st, 5) == O.extend_separation(ost, 5)
         for f in ("edges_u", "edges_v", "base_costs", "tri_nodes", "tri_edges", "lam", "coverage"):
             assert np.array_equal(getattr(st, f), getattr(ost, f)), f
+
+
+def test_edge_cases_all_modes():
+    """Degenerate inputs through every mode: no nodes, isolated nodes, one
+    edge of either sign, all-negative, all-positive, duplicated and
+    reversed edges (summed by the constructor), disconnected pieces."""
+    cases = [
+        (0, [], [], []),
+        (1, [], [], []),
+        (4, [], [], []),
+        (2, [0], [1], [1.5]),
+        (2, [0], [1], [-1.5]),
+        (3, [0, 1, 0], [1, 2, 2], [-1.0, -2.0, -3.0]),
+        (3, [0, 1, 0], [1, 2, 2], [1.0, 2.0, 3.0]),
+        (3, [1, 0, 2, 0], [0, 1, 1, 2], [1.0, 0.5, -4.0, 2.0]),
+        (6, [0, 1, 3, 4], [1, 2, 4, 5], [1.0, -1.0, 2.0, 2.0]),
+    ]
+    for n, u, v, c in cases:
+        g = P.WeightedGraph(n, u, v, c)
+        og = O.Graph(n, u, v, c)
+        for mode in ("P", "PD", "PD+", "D", "GAEC"):
+            sol = P.solve(g, P.SolverConfig(mode=mode))
+            ref = O.solve(og, mode=mode, cleanup="handshake")
+            assert np.array_equal(sol.labeling, ref.labeling), (n, u, mode)
+            assert sol.primal_cost == pytest.approx(ref.primal_cost, abs=1e-12)
+            if mode in ("P", "GAEC"):
+                assert sol.lower_bound == float("-inf")
+            else:
+                assert sol.lower_bound == pytest.approx(ref.lower_bound, abs=1e-12)
