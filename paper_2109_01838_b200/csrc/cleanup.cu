@@ -616,7 +616,7 @@ int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc) {
   int32_t* d_npos = sc.p + SC_NPOS;
   int64_t total = 0;
   int skip = 0, backoff = 1;  // wide rounds before retrying the tail after a bail
-  int wide_rounds = 0, tail_rounds = 0, tail_calls = 0;
+  int wide_rounds = 0, tail_rounds = 0, tail_calls = 0, wide_big = 0;
   auto t_start = std::chrono::steady_clock::now();
   int bits = 1;
   while ((1LL << bits) < n) bits++;
@@ -628,6 +628,7 @@ int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc) {
     RAMA_KERNEL(ctx, k_cl_vote1, m, u.p, v.p, c.p, alive.p, m, bc.p, d_npos);
     int32_t npos = read_scalar(ctx, d_npos);
     if (npos == 0) break;
+    if (npos > tail_entry_limit()) wide_big++;
     if (npos <= tail_entry_limit() && skip == 0) {
       // ---- persistent tail: P list and incidence rows, one CTA ------------
       bc.zero();
@@ -718,8 +719,9 @@ int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc) {
     RAMA_KERNEL(ctx, k_cl_fold, k, k, key2.p, slot.p, c.p, alive.p);
   }
   if (getenv("RAMA_CLEANUP_STATS"))
-    fprintf(stderr, "[rama] cleanup n %lld m %lld: %d wide rounds, %d tail calls, %d tail rounds, %lld pairs, %.2f ms\n",
-            (long long)n, (long long)m, wide_rounds, tail_calls, tail_rounds, (long long)total,
+    fprintf(stderr, "[rama] cleanup n %lld m %lld: %d wide rounds (%d above the tail limit), %d tail calls, %d tail "
+            "rounds, %lld pairs, %.2f ms\n",
+            (long long)n, (long long)m, wide_rounds, wide_big, tail_calls, tail_rounds, (long long)total,
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
   return components(ctx, n, pr.p, pa.p, total, fc);
 }
