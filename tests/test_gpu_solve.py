@@ -149,17 +149,17 @@ def _solve_env(env, code):
     return r.stdout
 
 
-def test_cleanup_tail_and_wide_rounds_agree():
-    """The cleanup's persistent single-CTA tail and the wide grid rounds run
-    the same D1 round; forcing the wide path everywhere (RAMA_TAIL_P=0) or
-    entering the tail early must give bit-identical solves."""
+def test_cleanup_pool_rebuilds_agree():
+    """The cleanup kernel hands back to the host when its row pool runs out
+    (the host rebuilds P and the rows and relaunches); a tiny pool forces
+    many rebuilds and must give bit-identical solves."""
     code = ("import sys, hashlib; sys.path.insert(0, '..')\n"
             "import paper_2109_01838_b200 as P\nfrom paper_2109_01838_b200 import instances\n"
             "for args in [(160, 200, (2, 3), 1), (96, 96, (2,), 5)]:\n"
             "    g = P.WeightedGraph(*instances.grid8_coo(args[0], args[1], strides=args[2], seed=args[3]))\n"
             "    s = P.solve(g, P.SolverConfig(mode='PD'))\n"
             "    print(repr(s.primal_cost), hashlib.md5(s.labeling.tobytes()).hexdigest())\n")
-    outs = [_solve_env({"RAMA_TAIL_P": k}, code) for k in ("0", "64", "32768")]
+    outs = [_solve_env({"RAMA_CLEANUP_POOL": k}, code) for k in ("64", "5000", "-1")]
     assert outs[0] == outs[1] == outs[2]
 
 
