@@ -496,7 +496,7 @@ __global__ void k_cl_posflag(const double* __restrict__ c, const uint8_t* __rest
 }
 
 // RAMA_CLEANUP_POOL=<k>: pool slack in entries (tests shrink it to force the
-// rebuild path); default max(2 * arcs, 1M)
+// rebuild path); default max(8 * arcs, 4M)
 static int64_t pool_slack_override() {
   static const int64_t v = [] {
     const char* e = getenv("RAMA_CLEANUP_POOL");
@@ -566,7 +566,7 @@ int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc) {
     cur.zero();
     RAMA_KERNEL(ctx, k_cl_degree, m, u.p, v.p, alive.p, m, deg.p);
     int64_t arcs = exclusive_scan(ctx, deg.p, off.p, n, true);
-    int64_t slack = pool_slack_override() >= 0 ? pool_slack_override() : std::max<int64_t>(2 * arcs, 1 << 20);
+    int64_t slack = pool_slack_override() >= 0 ? pool_slack_override() : std::max<int64_t>(8 * arcs, 1 << 22);
     int64_t cap = 2 * arcs + slack;
     if (cap > 0x7fffffffLL) cap = 0x7fffffffLL;
     Buf<int32_t> pool(cap, ctx);
