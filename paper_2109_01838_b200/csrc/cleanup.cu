@@ -33,6 +33,7 @@
 #include <cooperative_groups.h>
 
 #include <chrono>
+#include <vector>
 
 namespace rama {
 
@@ -55,6 +56,7 @@ __device__ __forceinline__ uint32_t key_hash(uint64_t k) {
 
 constexpr int kThreads = 512;
 constexpr uint64_t kEmpty = ~0ULL;
+constexpr int32_t kBigRow = 2048;  // rows longer than this are copied by a whole CTA
 
 enum CleanupStatus : int32_t { kRunning = 0, kDone = 1, kPoolFull = 2 };
 
@@ -71,7 +73,8 @@ enum {
   SC_RSUM = 8,    // this round: sum of absorbed row lengths
   SC_RREP = 9,    // this round: sum of representative row lengths
   SC_RNP2 = 10,   // this round: next |P|
-  SC_MEM = 11,    // this round: member-list top
+  SC_PBASE = 11,  // first pair of the previous round (its rp entries are reset next round)
+  SC_EFILL = 12,  // edge hash entries (upper bound)
   SC_COUNT = 16
 };
 
@@ -80,36 +83,38 @@ struct Args {
   int32_t* v;
   double* c;
   uint8_t* alive;
-  int32_t* tmark;          // per slot, clean (0) between rounds
-  unsigned long long* bc;  // per node, clean (0) between rounds; also the row fill cursor
+  int32_t* tmark;          // per slot, clean (0) between rounds; R: 1 | 2/4 (endpoint kept); ext: 8
+  unsigned long long* bc;  // per node, clean (0) between rounds: vote maximum, then new row entries
   int32_t* bn;             // per node, "none" (>= n) between rounds
-  int32_t* rp;             // per node, -1 unless in a pair this round
+  int32_t* rp;             // per node, -1 unless in a pair of this (or, until reset, the last) round
   int32_t* minid;          // per node: canonical id of the cluster
   int32_t* size;           // per node: member count
   int32_t* P0;             // positive alive slots (double buffered, capacity m)
   int32_t* P1;
   int32_t* row_off;        // per node: incidence row (slot ids, may hold dead slots) in pool
   int32_t* row_len;
+  int32_t* row_cap;
   int32_t* pool;
   int64_t pool_cap;
   int32_t* pr;             // global pair list (representative, absorbed)
   int32_t* pa;
-  int32_t* ooff;           // per pair of the round: representative's old row
-  int32_t* olen;
   int32_t* apref;          // prefix of absorbed row lengths (npairs + 1)
-  int32_t* rpref;          // prefix of representative row lengths
+  int32_t* part;           // per CTA partial sums of absorbed row lengths
   int32_t* R;              // rewritten slots of the round
-  uint64_t* Rk;            // their new keys (kEmpty: became internal)
-  int32_t* Rg;             // their group (hash position)
-  uint64_t* hkey;          // group hash table (capacity hcap, power of two)
+  int32_t* Rg;             // their group (hash position), -1: became internal
+  int32_t* Rnext;          // group member list (R indices, linked)
+  uint64_t* hkey;          // group hash table (capacity hcap, power of two), clean between rounds
   int32_t* hcnt;           // R members per group
   int32_t* hhead;          // smallest R slot per group
   int32_t* hext;           // the slot outside R with the same key, or -1
-  int32_t* hoff;           // member list offset (groups with >= 2 R members)
-  int32_t* hfill;
-  int32_t* mem;            // member lists
+  int32_t* hlist;          // first member (R index) of the group's list, or -1
   uint32_t hmask;
+  uint64_t* ekey;          // edge hash: every alive slot under its current key (stale entries
+  int32_t* eslot;          //   of dead or re-keyed slots stay and are skipped)
+  uint32_t emask;
   int32_t* sc;             // device scalars, SC_*
+  long long* trace;        // RAMA_CLEANUP_STATS=2: per round {np, npairs, nt, asum, rrep, t_ns}
+  int32_t trace_cap;
 };
 
 // arrays written or updated with atomics earlier in the same launch by
@@ -131,12 +136,30 @@ __device__ __forceinline__ int32_t owner_of(const int32_t* pref, int32_t n, int3
   return lo;
 }
 
-// CTA-wide exclusive scan of f(k), k < n, into pref[0..n]
+// CTA-wide sum of x (all threads get it)
+__device__ __forceinline__ int32_t block_sum(int32_t x) {
+  __shared__ int32_t part[kThreads / 32];
+  __shared__ int32_t total;
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t acc = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); i++) acc += part[i];
+    total = acc;
+  }
+  __syncthreads();
+  int32_t t = total;
+  __syncthreads();
+  return t;
+}
+
+// CTA-wide exclusive scan of f(k), k < n, into pref[0..n), starting at carry0
 template <class F>
-__device__ void block_prefix(int32_t* pref, int32_t n, F f) {
+__device__ void block_prefix(int32_t* pref, int32_t n, int32_t carry0, F f) {
   __shared__ int32_t part[kThreads / 32 + 1];
   __shared__ int32_t carry;
-  if (threadIdx.x == 0) carry = 0;
+  if (threadIdx.x == 0) carry = carry0;
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int32_t b0 = 0; b0 < n; b0 += blockDim.x) {
@@ -160,7 +183,6 @@ __device__ void block_prefix(int32_t* pref, int32_t n, F f) {
     if (threadIdx.x == 0) carry += part[nw];
     __syncthreads();
   }
-  if (threadIdx.x == 0) pref[n] = carry;
 }
 
 // group position of key k, inserting it
@@ -174,30 +196,65 @@ __device__ __forceinline__ int32_t h_insert(const Args& A, uint64_t k) {
   }
 }
 
-// group position of an existing key, or -1
-__device__ __forceinline__ int32_t h_find(const Args& A, uint64_t k) {
-  uint32_t h = key_hash(k) & A.hmask;
+// edge hash: a new entry (duplicates of a key are allowed; readers validate)
+__device__ __forceinline__ void e_insert(const Args& A, uint64_t k, int32_t s) {
+  uint32_t h = key_hash(k) & A.emask;
   while (true) {
-    uint64_t x = LD(A.hkey + h);
-    if (x == k) return (int32_t)h;
-    if (x == kEmpty) return -1;
-    h = (h + 1) & A.hmask;
+    unsigned long long old = atomicCAS((unsigned long long*)(A.ekey + h), (unsigned long long)kEmpty,
+                                       (unsigned long long)k);
+    if (old == kEmpty) {
+      A.eslot[h] = s;
+      return;
+    }
+    h = (h + 1) & A.emask;
   }
+}
+
+// the alive slot outside R whose current key is k, or -1 (at most one: alive
+// keys are unique between rounds)
+__device__ __forceinline__ int32_t e_find(const Args& A, uint64_t k) {
+  uint32_t h = key_hash(k) & A.emask;
+  while (true) {
+    uint64_t x = LD(A.ekey + h);
+    if (x == kEmpty) return -1;
+    if (x == k) {
+      int32_t s = LD(A.eslot + h);
+      if (LD(A.alive + s) && !(LD(A.tmark + s) & 1) && pair_key(LD(A.u + s), LD(A.v + s)) == k) return s;
+    }
+    h = (h + 1) & A.emask;
+  }
+}
+
+// a surviving R slot enters its representatives' rows where it is new
+__device__ __forceinline__ void count_new(const Args& A, int32_t s) {
+  int32_t mk = LD(A.tmark + s);
+  int32_t a = LD(A.u + s), b = LD(A.v + s);
+  if (LD(A.rp + a) == a && !(mk & 2)) atomicAdd(A.bc + a, 1ULL);
+  if (LD(A.rp + b) == b && !(mk & 4)) atomicAdd(A.bc + b, 1ULL);
 }
 
 __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
+  __shared__ int32_t s_small[kThreads], s_big[kThreads];
+  __shared__ int32_t s_nsmall, s_nbig, s_cnt, s_off;
   int32_t* sc = A.sc;
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t GT = (int64_t)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   while (true) {
     const int32_t np = LD(sc + SC_NP);
     const int32_t which = LD(sc + SC_WHICH);
     const int32_t base = LD(sc + SC_NPAIRS);
+    const int32_t pbase = LD(sc + SC_PBASE);
     const int32_t* P = which ? A.P1 : A.P0;
     int32_t* P2 = which ? A.P0 : A.P1;
-    // ---- handshake votes over the positive slots (contraction.py:207 rule)
+    // ---- handshake votes over the positive slots (contraction.py:207 rule);
+    // the previous round's pairs leave rp
+    for (int64_t k = pbase + gtid; k < base; k += GT) {
+      A.rp[LD(A.pr + k)] = -1;
+      A.rp[LD(A.pa + k)] = -1;
+    }
     for (int64_t i = gtid; i < np; i += GT) {
       int32_t s = LD(P + i);
       unsigned long long bits = dbits(LD(A.c + s));
@@ -232,18 +289,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
       int32_t s = LD(P + i);
       int32_t a = LD(A.u + s), b = LD(A.v + s);
       A.bc[a] = 0ULL;
-      A.bc[b] = 0ULL;
       A.bn[a] = 0x7fffffff;
+      A.bc[b] = 0ULL;
       A.bn[b] = 0x7fffffff;
     }
     const int32_t npairs = LD(sc + SC_RPAIRS);
+    const int32_t rsum = LD(sc + SC_RSUM), rrep = LD(sc + SC_RREP);
     int32_t stop = 0;
     if (npairs == 0) stop = kDone;
-    else if ((int64_t)LD(sc + SC_POOL) + LD(sc + SC_RREP) + LD(sc + SC_RSUM) > A.pool_cap) stop = kPoolFull;
+    else if ((int64_t)LD(sc + SC_POOL) + 2 * ((int64_t)rrep + rsum) + 16LL * npairs > A.pool_cap ||
+             (int64_t)LD(sc + SC_EFILL) + rsum > (int64_t)(A.emask >> 1))
+      stop = kPoolFull;
     if (stop) {  // nothing was modified: the host rebuilds the rows and the round is redone
       grid.sync();
       if (gtid == 0) {
         sc[SC_STATUS] = stop;
+        sc[SC_PBASE] = base;
         sc[SC_RPAIRS] = 0; sc[SC_RSUM] = 0; sc[SC_RREP] = 0;
       }
       break;
@@ -254,15 +315,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
       int32_t r = LD(pr + k), t = LD(pa + k);
       A.rp[r] = r;
       A.rp[t] = r;
-      A.ooff[k] = LD(A.row_off + r);
-      A.olen[k] = LD(A.row_len + r);
     }
-    if (blockIdx.x == 0) {
-      block_prefix(A.apref, npairs, [&](int32_t k) { return LD(A.row_len + LD(pa + k)); });
-      block_prefix(A.rpref, npairs, [&](int32_t k) { return LD(A.row_len + LD(pr + k)); });
+    // absorbed row lengths: CTA b sums its chunk of the pairs
+    const int32_t chunk = (npairs + gridDim.x - 1) / gridDim.x;
+    const int32_t c_lo = min(npairs, (int32_t)blockIdx.x * chunk), c_hi = min(npairs, c_lo + chunk);
+    {
+      int32_t x = 0;
+      for (int32_t k = c_lo + threadIdx.x; k < c_hi; k += blockDim.x) x += LD(A.row_len + LD(pa + k));
+      x = block_sum(x);
+      if (threadIdx.x == 0) A.part[blockIdx.x] = x;
     }
     grid.sync();
-    const int32_t asum = LD(A.apref + npairs), rsum = LD(A.rpref + npairs);
+    {
+      int32_t before = 0, all = 0;
+      for (int32_t j = threadIdx.x; j < (int32_t)gridDim.x; j += blockDim.x) {
+        int32_t x = LD(A.part + j);
+        all += x;
+        if (j < (int32_t)blockIdx.x) before += x;
+      }
+      before = block_sum(before);
+      all = block_sum(all);
+      block_prefix(A.apref + c_lo, c_hi - c_lo, before, [&](int32_t k) { return LD(A.row_len + LD(pa + c_lo + k)); });
+      if (gtid == 0) A.apref[npairs] = all;
+    }
+    grid.sync();
+    const int32_t asum = LD(A.apref + npairs);
     // ---- R = alive slots of the absorbed clusters (deduplicated), flattened
     for (int64_t i = gtid; i < asum; i += GT) {
       int32_t k = owner_of(A.apref, npairs, (int32_t)i);
@@ -272,16 +349,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
     }
     grid.sync();
     const int32_t nt = LD(sc + SC_RNT);
-    // ---- rewrite R to the representatives (internal slots die) and group
-    // equal keys.  tmark = 1 | mask of the new endpoints the slot was already
-    // incident to (2: low, 4: high): the row update appends only where new.
+    // ---- rewrite R to the representatives (internal slots die), group equal
+    // keys, and find each group's slot outside R (it joins a representative
+    // with a cluster that is not absorbed and keeps its key) in the edge hash.
+    // tmark = 1 | mask of the new endpoints the slot was already incident to
+    // (2: low, 4: high): the row update appends only where new.
     for (int64_t i = gtid; i < nt; i += GT) {
       int32_t s = LD(A.R + i);
       int32_t x = LD(A.u + s), y = LD(A.v + s);
       int32_t a = rep_of(A.rp, x), b = rep_of(A.rp, y);
       if (a == b) {
         A.alive[s] = 0;
-        A.Rk[i] = kEmpty;
         A.Rg[i] = -1;
       } else {
         int32_t lo = min(a, b), hi = max(a, b);
@@ -289,176 +367,188 @@ __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
         A.v[s] = hi;
         A.tmark[s] = 1 | ((lo == x || lo == y) ? 2 : 0) | ((hi == x || hi == y) ? 4 : 0);
         uint64_t key = pair_key(lo, hi);
-        A.Rk[i] = key;
         int32_t g = h_insert(A, key);
         A.Rg[i] = g;
         atomicAdd(A.hcnt + g, 1);
         atomicMin(A.hhead + g, s);
+        A.Rnext[i] = atomicExch(A.hlist + g, (int32_t)i);
+        int32_t e = e_find(A, key);
+        if (e >= 0 && atomicCAS(A.hext + g, -1, e) == -1) A.tmark[e] = 8;
       }
-    }
-    grid.sync();
-    // ---- the slot outside R with a group's key: it joins a representative
-    // with a cluster that is not absorbed, keeps its key, and sits in that
-    // representative's row (at most one per key).  Groups with >= 2 R
-    // members reserve their member list.
-    for (int64_t i = gtid; i < rsum; i += GT) {
-      int32_t k = owner_of(A.rpref, npairs, (int32_t)i);
-      int32_t s = LD(A.pool + LD(A.ooff + k) + ((int32_t)i - LD(A.rpref + k)));
-      if (!LD(A.alive + s) || LD(A.tmark + s)) continue;
-      int32_t g = h_find(A, pair_key(LD(A.u + s), LD(A.v + s)));
-      if (g >= 0 && atomicCAS(A.hext + g, -1, s) == -1) A.tmark[s] = 8;
-    }
-    for (int64_t i = gtid; i < nt; i += GT) {
-      int32_t g = LD(A.Rg + i);
-      if (g < 0 || LD(A.hhead + g) != LD(A.R + i)) continue;
-      int32_t cnt = LD(A.hcnt + g);
-      if (cnt >= 2) A.hoff[g] = atomicAdd(sc + SC_MEM, cnt);
-    }
-    grid.sync();
-    for (int64_t i = gtid; i < nt; i += GT) {
-      int32_t g = LD(A.Rg + i);
-      if (g < 0 || LD(A.hcnt + g) < 2) continue;
-      A.mem[LD(A.hoff + g) + atomicAdd(A.hfill + g, 1)] = LD(A.R + i);
     }
     grid.sync();
     // ---- fold each group (R members + the outside slot) into its smallest
     // slot, sequential sum in slot order; survivors enter the next P when
-    // positive, untouched positive slots stay
+    // positive, untouched positive slots stay.  A group has at most 3 R
+    // members and one outside slot (a matching merges each cluster once).
     for (int64_t i = gtid; i < nt; i += GT) {
       const int32_t g = LD(A.Rg + i);
       const int32_t s0 = LD(A.R + i);
       if (g < 0 || LD(A.hhead + g) != s0) continue;
       const int32_t cnt = LD(A.hcnt + g), ext = LD(A.hext + g);
+      const uint64_t key = pair_key(LD(A.u + s0), LD(A.v + s0));
+      int32_t surv = s0;
       if (cnt == 1 && ext < 0) {
         if (LD(A.c + s0) > 0.0) P2[atomicAdd(sc + SC_RNP2, 1)] = s0;
-        continue;
-      }
-      const int32_t* list = cnt >= 2 ? A.mem + LD(A.hoff + g) : nullptr;
-      const int32_t total = cnt + (ext >= 0 ? 1 : 0);
-      int32_t surv = s0;
-      if (total <= 16) {  // small groups: insertion sort in registers / local memory
-        int32_t buf[16];
-        int32_t k = 0;
-        if (list) {
-          for (int32_t j = 0; j < cnt; j++) buf[k++] = LD(list + j);
-        } else {
-          buf[k++] = s0;
-        }
-        if (ext >= 0) buf[k++] = ext;
-        for (int32_t a = 1; a < k; a++) {
-          int32_t x = buf[a], b = a - 1;
-          while (b >= 0 && buf[b] > x) { buf[b + 1] = buf[b]; b--; }
-          buf[b + 1] = x;
-        }
-        surv = buf[0];
-        double acc = LD(A.c + buf[0]);
-        for (int32_t j = 1; j < k; j++) {
-          acc = __dadd_rn(acc, LD(A.c + buf[j]));
-          A.alive[buf[j]] = 0;
-        }
-        A.c[surv] = acc;
-      } else {  // large group (rare): repeated minimum extraction over the list
-        int32_t prev = -1;
-        double acc = 0.0;
-        for (int32_t j = 0; j < total; j++) {
-          int32_t nxt = 0x7fffffff;
-          for (int32_t t = 0; t < cnt; t++) {
-            int32_t x = LD(list + t);
-            if (x > prev && x < nxt) nxt = x;
+      } else {
+        const int32_t total = cnt + (ext >= 0 ? 1 : 0);
+        if (total <= 16) {  // insertion sort in registers / local memory
+          int32_t buf[16];
+          int32_t k = 0;
+          for (int32_t j = LD(A.hlist + g); j >= 0; j = LD(A.Rnext + j)) buf[k++] = LD(A.R + j);
+          if (ext >= 0) buf[k++] = ext;
+          for (int32_t a = 1; a < k; a++) {
+            int32_t x = buf[a], b = a - 1;
+            while (b >= 0 && buf[b] > x) { buf[b + 1] = buf[b]; b--; }
+            buf[b + 1] = x;
           }
-          if (ext > prev && ext < nxt) nxt = ext;
-          if (j == 0) {
-            surv = nxt;
-            acc = LD(A.c + nxt);
-          } else {
-            acc = __dadd_rn(acc, LD(A.c + nxt));
-            A.alive[nxt] = 0;
+          surv = buf[0];
+          double acc = LD(A.c + buf[0]);
+          for (int32_t j = 1; j < k; j++) {
+            acc = __dadd_rn(acc, LD(A.c + buf[j]));
+            A.alive[buf[j]] = 0;
           }
-          prev = nxt;
+          A.c[surv] = acc;
+        } else {  // not reachable under a matching; kept exact: repeated minimum extraction
+          int32_t prev = -1;
+          double acc = 0.0;
+          for (int32_t j = 0; j < total; j++) {
+            int32_t nxt = 0x7fffffff;
+            for (int32_t t = LD(A.hlist + g); t >= 0; t = LD(A.Rnext + t)) {
+              int32_t x = LD(A.R + t);
+              if (x > prev && x < nxt) nxt = x;
+            }
+            if (ext > prev && ext < nxt) nxt = ext;
+            if (j == 0) {
+              surv = nxt;
+              acc = LD(A.c + nxt);
+            } else {
+              acc = __dadd_rn(acc, LD(A.c + nxt));
+              A.alive[nxt] = 0;
+            }
+            prev = nxt;
+          }
+          A.c[surv] = acc;
         }
-        A.c[surv] = acc;
+        if (LD(A.c + surv) > 0.0) P2[atomicAdd(sc + SC_RNP2, 1)] = surv;
       }
-      if (LD(A.c + surv) > 0.0) P2[atomicAdd(sc + SC_RNP2, 1)] = surv;
+      if (surv != ext) {  // an R slot under its new key: edge hash entry, new row entries
+        e_insert(A, key, surv);
+        count_new(A, surv);
+      }
     }
     for (int64_t i = gtid; i < np; i += GT) {
       int32_t s = LD(P + i);
       if (!LD(A.tmark + s)) P2[atomicAdd(sc + SC_RNP2, 1)] = s;
     }
     grid.sync();
-    // ---- rows: a representative keeps its alive slots and gains the R
-    // survivors new to it (bc counts, then serves as the fill cursor)
-    for (int64_t i = gtid; i < rsum; i += GT) {
-      int32_t k = owner_of(A.rpref, npairs, (int32_t)i);
-      int32_t s = LD(A.pool + LD(A.ooff + k) + ((int32_t)i - LD(A.rpref + k)));
-      if (LD(A.alive + s)) atomicAdd(A.bc + LD(pr + k), 1ULL);
-    }
-    for (int64_t i = gtid; i < nt; i += GT) {
-      int32_t s = LD(A.R + i);
-      if (LD(A.Rk + i) == kEmpty || !LD(A.alive + s)) continue;
-      int32_t mk = LD(A.tmark + s);
-      int32_t a = LD(A.u + s), b = LD(A.v + s);
-      if (LD(A.rp + a) == a && !(mk & 2)) atomicAdd(A.bc + a, 1ULL);
-      if (LD(A.rp + b) == b && !(mk & 4)) atomicAdd(A.bc + b, 1ULL);
+    // ---- representatives whose row would overflow get a new one (twice the
+    // need, dead slots dropped): small rows one warp each, long rows one CTA
+    for (int64_t k0 = (int64_t)blockIdx.x * blockDim.x; k0 < npairs; k0 += GT) {
+      if (threadIdx.x == 0) { s_nsmall = 0; s_nbig = 0; }
+      __syncthreads();
+      const int64_t k = k0 + threadIdx.x;
+      if (k < npairs) {
+        int32_t r = LD(pr + k);
+        int32_t len = LD(A.row_len + r);
+        int32_t need = len + (int32_t)LD(A.bc + r);
+        A.bc[r] = 0ULL;
+        if (need > LD(A.row_cap + r)) {
+          A.row_cap[r] = need;  // replaced below
+          if (len > kBigRow) s_big[atomicAdd(&s_nbig, 1)] = r;
+          else s_small[atomicAdd(&s_nsmall, 1)] = r;
+        }
+      }
+      __syncthreads();
+      for (int32_t j = warp; j < s_nsmall; j += nwarps) {
+        const int32_t r = s_small[j];
+        const int32_t cap = max(2 * LD(A.row_cap + r), 16);
+        int32_t off = 0;
+        if (lane == 0) off = atomicAdd(sc + SC_POOL, cap);
+        off = __shfl_sync(0xffffffffu, off, 0);
+        const int32_t old = LD(A.row_off + r), len = LD(A.row_len + r);
+        int32_t cnt = 0;
+        for (int32_t e0 = 0; e0 < len; e0 += 32) {
+          int32_t s = e0 + lane < len ? LD(A.pool + old + e0 + lane) : -1;
+          bool keep = s >= 0 && LD(A.alive + s);
+          unsigned bal = __ballot_sync(0xffffffffu, keep);
+          if (keep) A.pool[off + cnt + __popc(bal & ((1u << lane) - 1))] = s;
+          cnt += __popc(bal);
+        }
+        if (lane == 0) {
+          A.row_off[r] = off;
+          A.row_len[r] = cnt;
+          A.row_cap[r] = cap;
+        }
+      }
+      for (int32_t j = 0; j < s_nbig; j++) {
+        const int32_t r = s_big[j];
+        if (threadIdx.x == 0) {
+          int32_t cap = 2 * LD(A.row_cap + r);
+          s_off = atomicAdd(sc + SC_POOL, cap);
+          s_cnt = 0;
+          A.row_cap[r] = cap;
+        }
+        __syncthreads();
+        const int32_t old = LD(A.row_off + r), len = LD(A.row_len + r);
+        for (int32_t e = threadIdx.x; e < len; e += blockDim.x) {
+          int32_t s = LD(A.pool + old + e);
+          if (LD(A.alive + s)) A.pool[s_off + atomicAdd(&s_cnt, 1)] = s;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          A.row_off[r] = s_off;
+          A.row_len[r] = s_cnt;
+        }
+        __syncthreads();
+      }
+      __syncthreads();
     }
     grid.sync();
-    for (int64_t k = gtid; k < npairs; k += GT) {  // new rows past the pool top
-      int32_t x = LD(pr + k);
-      int32_t cnt = (int32_t)LD(A.bc + x);
-      A.row_off[x] = atomicAdd(sc + SC_POOL, cnt);
-      A.row_len[x] = cnt;
-      A.bc[x] = 0ULL;
-    }
-    grid.sync();
-    for (int64_t i = gtid; i < rsum; i += GT) {
-      int32_t k = owner_of(A.rpref, npairs, (int32_t)i);
-      int32_t s = LD(A.pool + LD(A.ooff + k) + ((int32_t)i - LD(A.rpref + k)));
-      int32_t x = LD(pr + k);
-      if (LD(A.alive + s)) A.pool[LD(A.row_off + x) + (int32_t)atomicAdd(A.bc + x, 1ULL)] = s;
-    }
+    // ---- rows gain the new slots; round state back to clean (the group's
+    // head resets the group); cluster bookkeeping
     for (int64_t i = gtid; i < nt; i += GT) {
-      int32_t s = LD(A.R + i);
-      if (LD(A.Rk + i) == kEmpty || !LD(A.alive + s)) continue;
-      int32_t mk = LD(A.tmark + s);
-      int32_t a = LD(A.u + s), b = LD(A.v + s);
-      if (LD(A.rp + a) == a && !(mk & 2)) A.pool[LD(A.row_off + a) + (int32_t)atomicAdd(A.bc + a, 1ULL)] = s;
-      if (LD(A.rp + b) == b && !(mk & 4)) A.pool[LD(A.row_off + b) + (int32_t)atomicAdd(A.bc + b, 1ULL)] = s;
-    }
-    grid.sync();
-    // ---- back to clean; cluster bookkeeping
-    for (int64_t i = gtid; i < nt; i += GT) {
-      A.tmark[LD(A.R + i)] = 0;
-      int32_t g = LD(A.Rg + i);
+      const int32_t s = LD(A.R + i);
+      const int32_t g = LD(A.Rg + i);
+      const int32_t mk = LD(A.tmark + s);
+      A.tmark[s] = 0;
       if (g < 0) continue;
-      int32_t e = LD(A.hext + g);
-      if (e >= 0) A.tmark[e] = 0;
+      if (LD(A.alive + s)) {
+        int32_t a = LD(A.u + s), b = LD(A.v + s);
+        if (LD(A.rp + a) == a && !(mk & 2)) A.pool[LD(A.row_off + a) + atomicAdd(A.row_len + a, 1)] = s;
+        if (LD(A.rp + b) == b && !(mk & 4)) A.pool[LD(A.row_off + b) + atomicAdd(A.row_len + b, 1)] = s;
+      }
+      if (LD(A.hhead + g) == s) {
+        int32_t e = LD(A.hext + g);
+        if (e >= 0) A.tmark[e] = 0;
+        A.hkey[g] = kEmpty;
+        A.hcnt[g] = 0;
+        A.hhead[g] = 0x7fffffff;
+        A.hext[g] = -1;
+        A.hlist[g] = -1;
+      }
     }
     for (int64_t k = gtid; k < npairs; k += GT) {
       int32_t x = LD(pr + k), t = LD(pa + k);
-      A.bc[x] = 0ULL;
       A.row_len[t] = 0;
       A.size[x] = LD(A.size + x) + LD(A.size + t);
       A.minid[x] = min(LD(A.minid + x), LD(A.minid + t));
     }
-    grid.sync();
-    for (int64_t i = gtid; i < nt; i += GT) {  // hash groups back to empty (after the ext reads)
-      int32_t g = LD(A.Rg + i);
-      if (g < 0) continue;
-      A.hkey[g] = kEmpty;
-      A.hcnt[g] = 0;
-      A.hhead[g] = 0x7fffffff;
-      A.hext[g] = -1;
-      A.hfill[g] = 0;
-    }
-    for (int64_t k = gtid; k < npairs; k += GT) {
-      A.rp[LD(pr + k)] = -1;
-      A.rp[LD(pa + k)] = -1;
-    }
     if (gtid == 0) {
+      const int32_t r = LD(sc + SC_ROUNDS);
+      if (A.trace && r < A.trace_cap) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        long long* e = A.trace + 6 * (int64_t)r;
+        e[0] = np; e[1] = npairs; e[2] = nt; e[3] = asum; e[4] = rrep; e[5] = (long long)t;
+      }
+      sc[SC_PBASE] = base;
       sc[SC_NPAIRS] = base + npairs;
       sc[SC_NP] = LD(sc + SC_RNP2);
       sc[SC_WHICH] = which ^ 1;
-      sc[SC_ROUNDS] += 1;
-      sc[SC_RPAIRS] = 0; sc[SC_RNT] = 0; sc[SC_RSUM] = 0; sc[SC_RNP2] = 0; sc[SC_RREP] = 0; sc[SC_MEM] = 0;
+      sc[SC_ROUNDS] = r + 1;
+      sc[SC_EFILL] = LD(sc + SC_EFILL) + nt;
+      sc[SC_RPAIRS] = 0; sc[SC_RNT] = 0; sc[SC_RSUM] = 0; sc[SC_RNP2] = 0; sc[SC_RREP] = 0;
     }
     grid.sync();
   }
@@ -479,6 +569,11 @@ __global__ void k_cl_degree(const int32_t* __restrict__ u, const int32_t* __rest
   }
 }
 
+// initial row capacity: room for the first merges without a copy
+__global__ void k_cl_rowcap(const int32_t* __restrict__ deg, int64_t n, int32_t* __restrict__ cap) {
+  GRID_STRIDE(i, n) cap[i] = 2 * deg[i] + 4;
+}
+
 __global__ void k_cl_fill_rows(const int32_t* __restrict__ u, const int32_t* __restrict__ v,
                                const uint8_t* __restrict__ alive, int64_t m, const int32_t* __restrict__ off,
                                int32_t* __restrict__ cursor, int32_t* __restrict__ pool) {
@@ -493,6 +588,13 @@ __global__ void k_cl_fill_rows(const int32_t* __restrict__ u, const int32_t* __r
 __global__ void k_cl_posflag(const double* __restrict__ c, const uint8_t* __restrict__ alive, int64_t m,
                              uint8_t* __restrict__ f) {
   GRID_STRIDE(i, m) f[i] = alive[i] && c[i] > 0.0;
+}
+
+__global__ void k_cl_ehash_build(const int32_t* __restrict__ u, const int32_t* __restrict__ v,
+                                 const uint8_t* __restrict__ alive, int64_t m, Args A) {
+  GRID_STRIDE(i, m) {
+    if (alive[i]) e_insert(A, pair_key(u[i], v[i]), (int32_t)i);
+  }
 }
 
 // RAMA_CLEANUP_POOL=<k>: pool slack in entries (tests shrink it to force the
@@ -529,18 +631,22 @@ int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc) {
   tmark.zero();
   iota(ctx, minid.p, n);
   RAMA_KERNEL(ctx, k_cl_fill_i32, n, size.p, n, 1);
-  Buf<int32_t> P0(m, ctx), P1(m, ctx), ooff(n, ctx), olen(n, ctx), apref(n + 1, ctx), rpref(n + 1, ctx);
-  Buf<int32_t> R(m, ctx), Rg(m, ctx), mem(m, ctx);
-  Buf<uint64_t> Rk(m, ctx);
+  Buf<int32_t> P0(m, ctx), P1(m, ctx), apref(n + 1, ctx);
+  Buf<int32_t> R(m, ctx), Rg(m, ctx), Rnext(m, ctx);
   uint32_t hcap = 1024;
   while ((int64_t)hcap < 2 * m) hcap <<= 1;
   Buf<uint64_t> hkey(hcap, ctx);
-  Buf<int32_t> hcnt(hcap, ctx), hhead(hcap, ctx), hext(hcap, ctx), hoff(hcap, ctx), hfill(hcap, ctx);
+  Buf<int32_t> hcnt(hcap, ctx), hhead(hcap, ctx), hext(hcap, ctx), hlist(hcap, ctx);
   hkey.fill_bytes(0xff);
   hcnt.zero();
-  hfill.zero();
   hext.fill_bytes(0xff);
+  hlist.fill_bytes(0xff);
   RAMA_KERNEL(ctx, k_cl_fill_i32, hcap, hhead.p, hcap, 0x7fffffff);
+  uint32_t ecap = 4096;
+  while ((int64_t)ecap < 4 * m && ecap < (1u << 30)) ecap <<= 1;
+  Buf<uint64_t> ekey;
+  Buf<int32_t> eslot;
+  int64_t grow = 1;  // doubles when a launch could not run a single round
   Buf<int32_t> sc(SC_COUNT, ctx);
   static int grid_blocks = 0;
   if (!grid_blocks) {
@@ -551,38 +657,58 @@ int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc) {
     RAMA_REQUIRE(per_sm >= 1, "cleanup kernel cannot be resident");
     grid_blocks = sms;  // one CTA per SM
   }
+  Buf<int32_t> part(grid_blocks + 1, ctx);
   int64_t total = 0;
   int launches = 0, rounds = 0;
+  const char* stats_env = getenv("RAMA_CLEANUP_STATS");
+  const bool round_trace = stats_env && atoi(stats_env) >= 2;
+  constexpr int32_t kTraceCap = 4096;
+  Buf<long long> trace(round_trace ? 6 * kTraceCap : 1, ctx);
+  Args A;
+  A.u = u.p; A.v = v.p; A.c = c.p; A.alive = alive.p; A.tmark = tmark.p; A.bc = bc.p; A.bn = bn.p;
+  A.rp = rp.p; A.minid = minid.p; A.size = size.p; A.P0 = P0.p; A.P1 = P1.p;
+  A.pr = pr.p; A.pa = pa.p; A.apref = apref.p; A.part = part.p;
+  A.R = R.p; A.Rg = Rg.p; A.Rnext = Rnext.p;
+  A.hkey = hkey.p; A.hcnt = hcnt.p; A.hhead = hhead.p; A.hext = hext.p; A.hlist = hlist.p; A.hmask = hcap - 1;
+  A.sc = sc.p;
+  A.trace = round_trace ? trace.p : nullptr;
+  A.trace_cap = kTraceCap;
   while (true) {
-    // P and the rows, from the current slots
+    // P, the rows and the edge hash, from the current slots
     Buf<uint8_t> pf(m, ctx);
     RAMA_KERNEL(ctx, k_cl_posflag, m, c.p, alive.p, m, pf.p);
     Buf<int32_t> Pl;
     int64_t np = compact_indices(ctx, pf.p, m, Pl);
     if (np == 0) break;
     copy_d2d(ctx, P0.p, Pl.p, np);
-    Buf<int32_t> deg(n, ctx), off(n + 1, ctx), cur(n, ctx);
+    Buf<int32_t> deg(n, ctx), rcap(n, ctx), off(n + 1, ctx), cur(n, ctx);
     deg.zero();
     cur.zero();
     RAMA_KERNEL(ctx, k_cl_degree, m, u.p, v.p, alive.p, m, deg.p);
-    int64_t arcs = exclusive_scan(ctx, deg.p, off.p, n, true);
+    RAMA_KERNEL(ctx, k_cl_rowcap, n, deg.p, n, rcap.p);
+    int64_t used = exclusive_scan(ctx, rcap.p, off.p, n, true);
+    int64_t arcs = (used - 4 * n) / 2;
     int64_t slack = pool_slack_override() >= 0 ? pool_slack_override() : std::max<int64_t>(8 * arcs, 1 << 22);
-    int64_t cap = 2 * arcs + slack;
+    int64_t cap = used + slack * grow;
     if (cap > 0x7fffffffLL) cap = 0x7fffffffLL;
+    RAMA_REQUIRE(used <= cap, "cleanup rows exceed the pool");
     Buf<int32_t> pool(cap, ctx);
     RAMA_KERNEL(ctx, k_cl_fill_rows, m, u.p, v.p, alive.p, m, off.p, cur.p, pool.p);
+    if (ekey.n != ecap) {
+      ekey.alloc(ecap, ctx.s);
+      eslot.alloc(ecap, ctx.s);
+    }
+    ekey.fill_bytes(0xff);
+    A.ekey = ekey.p; A.eslot = eslot.p; A.emask = ecap - 1;
+    A.row_off = off.p; A.row_len = deg.p; A.row_cap = rcap.p; A.pool = pool.p; A.pool_cap = cap;
+    RAMA_KERNEL(ctx, k_cl_ehash_build, m, u.p, v.p, alive.p, m, A);
     int32_t init[SC_COUNT] = {0};
     init[SC_NPAIRS] = (int32_t)total;
+    init[SC_PBASE] = (int32_t)total;
     init[SC_NP] = (int32_t)np;
-    init[SC_POOL] = (int32_t)arcs;
+    init[SC_POOL] = (int32_t)used;
+    init[SC_EFILL] = (int32_t)m;
     RAMA_CUDA(cudaMemcpyAsync(sc.p, init, sizeof(init), cudaMemcpyHostToDevice, ctx.s));
-    Args A;
-    A.u = u.p; A.v = v.p; A.c = c.p; A.alive = alive.p; A.tmark = tmark.p; A.bc = bc.p; A.bn = bn.p;
-    A.rp = rp.p; A.minid = minid.p; A.size = size.p; A.P0 = P0.p; A.P1 = P1.p;
-    A.row_off = off.p; A.row_len = deg.p; A.pool = pool.p; A.pool_cap = cap;
-    A.pr = pr.p; A.pa = pa.p; A.ooff = ooff.p; A.olen = olen.p; A.apref = apref.p; A.rpref = rpref.p;
-    A.R = R.p; A.Rk = Rk.p; A.Rg = Rg.p; A.hkey = hkey.p; A.hcnt = hcnt.p; A.hhead = hhead.p; A.hext = hext.p;
-    A.hoff = hoff.p; A.hfill = hfill.p; A.mem = mem.p; A.hmask = hcap - 1; A.sc = sc.p;
     if (trace_print()) fprintf(stderr, "[rama] k_cl_rounds np=%lld\n", (long long)np);
     {
       KernelScope ks(ctx.s, "k_cl_rounds", 0.0);
@@ -597,11 +723,27 @@ int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc) {
     ctx.sync();
     memcpy(st, ctx.pinned, sizeof(st));
     total = st[SC_NPAIRS];
+    if (round_trace) {
+      const int32_t k = std::min(st[SC_ROUNDS], kTraceCap);
+      std::vector<long long> h(6 * (size_t)k);
+      if (k) RAMA_CUDA(cudaMemcpy(h.data(), trace.p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+      for (int32_t r = 0; r < k; r++) {
+        const long long* e = &h[6 * (size_t)r];
+        long long prev = r ? h[6 * (size_t)(r - 1) + 5] : e[5];
+        fprintf(stderr, "[rama] cl launch %d round %d np %lld pairs %lld nt %lld asum %lld rrep %lld dt_us %.1f\n",
+                launches, rounds + r, e[0], e[1], e[2], e[3], e[4], (e[5] - prev) / 1e3);
+      }
+    }
     rounds += st[SC_ROUNDS];
     if (st[SC_STATUS] == kDone) break;
     RAMA_REQUIRE(st[SC_STATUS] == kPoolFull, "cleanup kernel ended in an unknown state");
+    if (st[SC_ROUNDS] == 0) {  // one round does not fit: larger pool and edge hash
+      RAMA_REQUIRE(grow < (1 << 20), "cleanup cannot make progress");
+      grow *= 2;
+      if (ecap < (1u << 30)) ecap <<= 1;
+    }
   }
-  if (getenv("RAMA_CLEANUP_STATS"))
+  if (stats_env)
     fprintf(stderr, "[rama] cleanup n %lld m %lld: %d rounds in %d launches, %lld pairs, %.2f ms\n", (long long)n,
             (long long)m, rounds, launches, (long long)total,
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
