@@ -21,13 +21,18 @@
 //     neighbour per round for hundreds of rounds, as on 3-D grids);
 //   * P, the alive positive slots (the only ones that vote);
 //   * per-cluster incidence rows in a bump-allocated pool (lazy: dead slots
-//     are skipped, representatives get a compacted row when they merge).
-// A round: votes over P, mutual pairs, R = alive slots of the absorbed
-// clusters, rewrite R to the representatives, group equal (u', v') in a
-// global hash table (the one slot outside R with the same key, if any, is
-// found in the representative's row), fold each group in slot order,
-// rebuild the representatives' rows.  The host only rebuilds P and the rows
-// when the pool runs out.
+//     stay until the row is reallocated; rows grow by doubling);
+//   * an edge hash holding every alive slot under its current key.
+// A round is five phases: (1) votes over P, one 128-bit atomic max of
+// (cost, neighbour id) per endpoint; (2) mutual pairs, each getting its
+// index and the offset of its absorbed row from one warp-aggregated packed
+// atomic; (3) R = alive slots of the absorbed clusters, and representatives
+// whose row could overflow get a larger one; (4) rewrite R to the
+// representatives, group equal keys in a hash table, find each group's slot
+// outside R in the edge hash; (5) fold each group in slot order, append
+// survivors to the representatives' rows.  The round's marks are cleared in
+// the next round's phase 1.  The host only rebuilds P, the rows and the
+// edge hash when the pool or the hash runs out.
 #include "internal.h"
 
 #include <cooperative_groups.h>
@@ -60,21 +65,19 @@ constexpr int32_t kBigRow = 2048;  // rows longer than this are copied by a whol
 
 enum CleanupStatus : int32_t { kRunning = 0, kDone = 1, kPoolFull = 2 };
 
-// device scalars (int32)
+// device scalars (int32).  Per-round counters live in two banks (round
+// parity): a bank is zeroed one round after its last use, so no extra grid
+// barrier is needed for the reset.
 enum {
   SC_NPAIRS = 0,  // committed pairs (pair list length)
-  SC_NP = 1,      // |P| of the current buffer
-  SC_WHICH = 2,   // current P buffer
-  SC_POOL = 3,    // pool top
-  SC_STATUS = 4,
-  SC_ROUNDS = 5,
-  SC_RPAIRS = 6,  // this round: pairs found
-  SC_RNT = 7,     // this round: |R|
-  SC_RSUM = 8,    // this round: sum of absorbed row lengths
-  SC_RREP = 9,    // this round: sum of representative row lengths
-  SC_RNP2 = 10,   // this round: next |P|
-  SC_PBASE = 11,  // first pair of the previous round (its rp entries are reset next round)
-  SC_EFILL = 12,  // edge hash entries (upper bound)
+  SC_NP = 1,      // |P| at launch
+  SC_POOL = 2,    // pool top
+  SC_STATUS = 3,
+  SC_ROUNDS = 4,  // rounds run by the launch
+  SC_EFILL = 5,   // edge hash entries (upper bound)
+  SC_RREP = 6,    // + bank: sum of representative row lengths
+  SC_RNT = 8,     // + bank: |R|
+  SC_RNP2 = 10,   // + bank: next |P|
   SC_COUNT = 16
 };
 
@@ -84,9 +87,8 @@ struct Args {
   double* c;
   uint8_t* alive;
   int32_t* tmark;          // per slot, clean (0) between rounds; R: 1 | 2/4 (endpoint kept); ext: 8
-  unsigned long long* bc;  // per node, clean (0) between rounds: vote maximum, then new row entries
-  int32_t* bn;             // per node, "none" (>= n) between rounds
-  int32_t* rp;             // per node, -1 unless in a pair of this (or, until reset, the last) round
+  ulonglong2* vote;        // per node, 0 between rounds: max of (cost bits, ~canonical id of the neighbour)
+  int32_t* rp;             // per node, -1 unless in a pair of this round
   int32_t* minid;          // per node: canonical id of the cluster
   int32_t* size;           // per node: member count
   int32_t* P0;             // positive alive slots (double buffered, capacity m)
@@ -98,8 +100,8 @@ struct Args {
   int64_t pool_cap;
   int32_t* pr;             // global pair list (representative, absorbed)
   int32_t* pa;
-  int32_t* apref;          // prefix of absorbed row lengths (npairs + 1)
-  int32_t* part;           // per CTA partial sums of absorbed row lengths
+  int32_t* apref;          // per pair of the round: offset of its absorbed row in the flattened R scan
+  unsigned long long* pk;  // per bank: (pairs << 32) | sum of absorbed row lengths
   int32_t* R;              // rewritten slots of the round
   int32_t* Rg;             // their group (hash position), -1: became internal
   int32_t* Rnext;          // group member list (R indices, linked)
@@ -134,55 +136,6 @@ __device__ __forceinline__ int32_t owner_of(const int32_t* pref, int32_t n, int3
     if (LD(pref + mid) <= i) lo = mid; else hi = mid;
   }
   return lo;
-}
-
-// CTA-wide sum of x (all threads get it)
-__device__ __forceinline__ int32_t block_sum(int32_t x) {
-  __shared__ int32_t part[kThreads / 32];
-  __shared__ int32_t total;
-  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = x;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int32_t acc = 0;
-    for (int i = 0; i < (int)(blockDim.x >> 5); i++) acc += part[i];
-    total = acc;
-  }
-  __syncthreads();
-  int32_t t = total;
-  __syncthreads();
-  return t;
-}
-
-// CTA-wide exclusive scan of f(k), k < n, into pref[0..n), starting at carry0
-template <class F>
-__device__ void block_prefix(int32_t* pref, int32_t n, int32_t carry0, F f) {
-  __shared__ int32_t part[kThreads / 32 + 1];
-  __shared__ int32_t carry;
-  if (threadIdx.x == 0) carry = carry0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int32_t b0 = 0; b0 < n; b0 += blockDim.x) {
-    int32_t k = b0 + threadIdx.x;
-    int32_t x = k < n ? f(k) : 0;
-    int32_t incl = x;
-    for (int o = 1; o < 32; o <<= 1) {
-      int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane == 31) part[w] = incl;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int32_t acc = 0;
-      for (int i = 0; i < nw; i++) { int32_t t = part[i]; part[i] = acc; acc += t; }
-      part[nw] = acc;
-    }
-    __syncthreads();
-    if (k < n) pref[k] = carry + part[w] + incl - x;
-    __syncthreads();
-    if (threadIdx.x == 0) carry += part[nw];
-    __syncthreads();
-  }
 }
 
 // group position of key k, inserting it
@@ -225,12 +178,39 @@ __device__ __forceinline__ int32_t e_find(const Args& A, uint64_t k) {
   }
 }
 
-// a surviving R slot enters its representatives' rows where it is new
-__device__ __forceinline__ void count_new(const Args& A, int32_t s) {
-  int32_t mk = LD(A.tmark + s);
-  int32_t a = LD(A.u + s), b = LD(A.v + s);
-  if (LD(A.rp + a) == a && !(mk & 2)) atomicAdd(A.bc + a, 1ULL);
-  if (LD(A.rp + b) == b && !(mk & 4)) atomicAdd(A.bc + b, 1ULL);
+__device__ __forceinline__ unsigned lanes_below() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// warp-aggregated slot in a global list: every lane with `take` gets a
+// distinct index (all 32 lanes must call)
+__device__ __forceinline__ int32_t warp_claim(int32_t* counter, bool take) {
+  const unsigned bal = __ballot_sync(0xffffffffu, take);
+  if (!bal) return -1;
+  const int leader = __ffs(bal) - 1;
+  int32_t b = 0;
+  if ((int)(threadIdx.x & 31) == leader) b = atomicAdd(counter, __popc(bal));
+  b = __shfl_sync(0xffffffffu, b, leader);
+  return take ? b + __popc(bal & lanes_below()) : -1;
+}
+
+// vote[x] = max(vote[x], key) over (hi, lo) as one unsigned 128-bit value
+__device__ __forceinline__ void vote_max(ulonglong2* p, unsigned long long hi, unsigned long long lo) {
+  unsigned __int128 key = ((unsigned __int128)hi << 64) | lo;
+  unsigned __int128 cur = 0;
+  while (key > cur) {
+    unsigned __int128 old = atomicCAS((unsigned __int128*)p, cur, key);
+    if (old == cur) return;
+    cur = old;
+  }
+}
+
+// the vote a node casts for neighbour y over a slot of cost bits `bits`:
+// larger cost first, then smaller canonical id (contraction.py:207)
+__device__ __forceinline__ unsigned long long vote_lo(int32_t minid_y) {
+  return (unsigned long long)(0xffffffffu - (uint32_t)minid_y);
 }
 
 __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
@@ -242,208 +222,137 @@ __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t GT = (int64_t)gridDim.x * blockDim.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  // loop state, identical in every thread
+  int32_t base = LD(sc + SC_NPAIRS), np = LD(sc + SC_NP), efill = LD(sc + SC_EFILL);
+  const int32_t round0 = LD(sc + SC_ROUNDS);
+  int32_t prev_base = base, prev_nt = 0, which = 0, rounds = 0;
   while (true) {
-    const int32_t np = LD(sc + SC_NP);
-    const int32_t which = LD(sc + SC_WHICH);
-    const int32_t base = LD(sc + SC_NPAIRS);
-    const int32_t pbase = LD(sc + SC_PBASE);
+    const int q = rounds & 1;
     const int32_t* P = which ? A.P1 : A.P0;
     int32_t* P2 = which ? A.P0 : A.P1;
-    // ---- handshake votes over the positive slots (contraction.py:207 rule);
-    // the previous round's pairs leave rp
-    for (int64_t k = pbase + gtid; k < base; k += GT) {
+    // ---- 1. the last round's marks back to clean (the group's head resets
+    // the group); handshake votes over the positive slots
+    for (int64_t k = prev_base + gtid; k < base; k += GT) {
       A.rp[LD(A.pr + k)] = -1;
       A.rp[LD(A.pa + k)] = -1;
     }
-    for (int64_t i = gtid; i < np; i += GT) {
-      int32_t s = LD(P + i);
-      unsigned long long bits = dbits(LD(A.c + s));
-      atomicMax(A.bc + LD(A.u + s), bits);
-      atomicMax(A.bc + LD(A.v + s), bits);
+    for (int64_t i = gtid; i < prev_nt; i += GT) {
+      const int32_t s = LD(A.R + i), g = LD(A.Rg + i);
+      A.tmark[s] = 0;
+      if (g >= 0 && LD(A.hhead + g) == s) {
+        int32_t e = LD(A.hext + g);
+        if (e >= 0) A.tmark[e] = 0;
+        A.hkey[g] = kEmpty;
+        A.hcnt[g] = 0;
+        A.hhead[g] = 0x7fffffff;
+        A.hext[g] = -1;
+        A.hlist[g] = -1;
+      }
     }
-    grid.sync();
     for (int64_t i = gtid; i < np; i += GT) {
       int32_t s = LD(P + i);
       unsigned long long bits = dbits(LD(A.c + s));
       int32_t a = LD(A.u + s), b = LD(A.v + s);
-      if (bits == LD(A.bc + a)) atomicMin(A.bn + a, LD(A.minid + b));
-      if (bits == LD(A.bc + b)) atomicMin(A.bn + b, LD(A.minid + a));
+      vote_max(A.vote + a, bits, vote_lo(LD(A.minid + b)));
+      vote_max(A.vote + b, bits, vote_lo(LD(A.minid + a)));
     }
     grid.sync();
-    for (int64_t i = gtid; i < np; i += GT) {  // mutual pairs: their slot is both ends' best
-      int32_t s = LD(P + i);
-      int32_t a = LD(A.u + s), b = LD(A.v + s);
-      int32_t ma = LD(A.minid + a), mb = LD(A.minid + b);
-      if (LD(A.bn + a) == mb && LD(A.bn + b) == ma) {
-        int32_t r = rep_first(LD(A.size + a), ma, LD(A.size + b), mb) ? a : b;
-        int32_t t = r == a ? b : a;
-        int32_t k = atomicAdd(sc + SC_RPAIRS, 1);
+    // ---- 2. mutual pairs: the slot is both ends' vote.  One packed atomic
+    // per warp gives each pair its index and the offset of its absorbed row.
+    if (gtid == 0) {
+      A.pk[q ^ 1] = 0ULL;
+      sc[SC_RREP + (q ^ 1)] = 0;
+      sc[SC_RNT + (q ^ 1)] = 0;
+      sc[SC_RNP2 + (q ^ 1)] = 0;
+    }
+    for (int64_t i0 = gtid - lane; i0 < np; i0 += GT) {
+      const int64_t i = i0 + lane;
+      bool found = false;
+      int32_t r = 0, t = 0, len = 0, rlen = 0;
+      if (i < np) {
+        int32_t s = LD(P + i);
+        unsigned long long bits = dbits(LD(A.c + s));
+        int32_t a = LD(A.u + s), b = LD(A.v + s);
+        int32_t ma = LD(A.minid + a), mb = LD(A.minid + b);
+        ulonglong2 va = __ldcg(A.vote + a), vb = __ldcg(A.vote + b);
+        if (va.y == bits && va.x == vote_lo(mb) && vb.y == bits && vb.x == vote_lo(ma)) {
+          found = true;
+          r = rep_first(LD(A.size + a), ma, LD(A.size + b), mb) ? a : b;
+          t = r == a ? b : a;
+          len = LD(A.row_len + t);
+          rlen = LD(A.row_len + r);
+          A.rp[r] = r;
+          A.rp[t] = r;
+        }
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, found);
+      if (!bal) continue;
+      int32_t incl = len, rsum = rlen;
+      for (int o = 1; o < 32; o <<= 1) {
+        int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      for (int o = 16; o > 0; o >>= 1) rsum += __shfl_xor_sync(0xffffffffu, rsum, o);
+      const int32_t wsum = __shfl_sync(0xffffffffu, incl, 31);
+      const int leader = __ffs(bal) - 1;
+      unsigned long long old = 0;
+      if (lane == leader) {
+        old = atomicAdd(A.pk + q, ((unsigned long long)__popc(bal) << 32) | (unsigned long long)(uint32_t)wsum);
+        atomicAdd(sc + SC_RREP + q, rsum);
+      }
+      old = __shfl_sync(0xffffffffu, old, leader);
+      if (found) {
+        const int32_t k = (int32_t)(old >> 32) + __popc(bal & lanes_below());
         A.pr[base + k] = r;
         A.pa[base + k] = t;
-        atomicAdd(sc + SC_RSUM, LD(A.row_len + t));
-        atomicAdd(sc + SC_RREP, LD(A.row_len + r));
+        A.apref[k] = (int32_t)(uint32_t)old + incl - len;
       }
     }
     grid.sync();
-    for (int64_t i = gtid; i < np; i += GT) {  // votes back to clean
-      int32_t s = LD(P + i);
-      int32_t a = LD(A.u + s), b = LD(A.v + s);
-      A.bc[a] = 0ULL;
-      A.bn[a] = 0x7fffffff;
-      A.bc[b] = 0ULL;
-      A.bn[b] = 0x7fffffff;
-    }
-    const int32_t npairs = LD(sc + SC_RPAIRS);
-    const int32_t rsum = LD(sc + SC_RSUM), rrep = LD(sc + SC_RREP);
+    const unsigned long long pk = LD(A.pk + q);
+    const int32_t npairs = (int32_t)(pk >> 32), asum = (int32_t)(uint32_t)pk;
+    const int32_t rrep = LD(sc + SC_RREP + q);
     int32_t stop = 0;
     if (npairs == 0) stop = kDone;
-    else if ((int64_t)LD(sc + SC_POOL) + 2 * ((int64_t)rrep + rsum) + 16LL * npairs > A.pool_cap ||
-             (int64_t)LD(sc + SC_EFILL) + rsum > (int64_t)(A.emask >> 1))
+    else if ((int64_t)LD(sc + SC_POOL) + 2 * ((int64_t)rrep + asum) + 16LL * npairs > A.pool_cap ||
+             (int64_t)efill + asum > (int64_t)(A.emask >> 1))
       stop = kPoolFull;
-    if (stop) {  // nothing was modified: the host rebuilds the rows and the round is redone
-      grid.sync();
+    const int32_t* pr = A.pr + base;
+    const int32_t* pa = A.pa + base;
+    for (int64_t i = gtid; i < np; i += GT) {  // votes back to clean
+      int32_t s = LD(P + i);
+      A.vote[LD(A.u + s)] = make_ulonglong2(0ULL, 0ULL);
+      A.vote[LD(A.v + s)] = make_ulonglong2(0ULL, 0ULL);
+    }
+    if (stop) {  // nothing was modified: the host rebuilds P and the rows, and the round is redone
+      for (int64_t k = gtid; k < npairs; k += GT) {
+        A.rp[LD(pr + k)] = -1;
+        A.rp[LD(pa + k)] = -1;
+      }
       if (gtid == 0) {
         sc[SC_STATUS] = stop;
-        sc[SC_PBASE] = base;
-        sc[SC_RPAIRS] = 0; sc[SC_RSUM] = 0; sc[SC_RREP] = 0;
+        sc[SC_NPAIRS] = base;
+        sc[SC_ROUNDS] = round0 + rounds;
       }
       break;
     }
-    const int32_t* pr = A.pr + base;
-    const int32_t* pa = A.pa + base;
-    for (int64_t k = gtid; k < npairs; k += GT) {
-      int32_t r = LD(pr + k), t = LD(pa + k);
-      A.rp[r] = r;
-      A.rp[t] = r;
-    }
-    // absorbed row lengths: CTA b sums its chunk of the pairs
-    const int32_t chunk = (npairs + gridDim.x - 1) / gridDim.x;
-    const int32_t c_lo = min(npairs, (int32_t)blockIdx.x * chunk), c_hi = min(npairs, c_lo + chunk);
-    {
-      int32_t x = 0;
-      for (int32_t k = c_lo + threadIdx.x; k < c_hi; k += blockDim.x) x += LD(A.row_len + LD(pa + k));
-      x = block_sum(x);
-      if (threadIdx.x == 0) A.part[blockIdx.x] = x;
-    }
-    grid.sync();
-    {
-      int32_t before = 0, all = 0;
-      for (int32_t j = threadIdx.x; j < (int32_t)gridDim.x; j += blockDim.x) {
-        int32_t x = LD(A.part + j);
-        all += x;
-        if (j < (int32_t)blockIdx.x) before += x;
+    // ---- 3. R = alive slots of the absorbed clusters (deduplicated)
+    for (int64_t i0 = gtid - lane; i0 < asum; i0 += GT) {
+      const int64_t i = i0 + lane;
+      int32_t s = -1;
+      bool take = false;
+      if (i < asum) {
+        int32_t k = owner_of(A.apref, npairs, (int32_t)i);
+        int32_t y = LD(pa + k);
+        s = LD(A.pool + LD(A.row_off + y) + ((int32_t)i - LD(A.apref + k)));
+        take = LD(A.alive + s) && atomicExch(A.tmark + s, 1) == 0;
       }
-      before = block_sum(before);
-      all = block_sum(all);
-      block_prefix(A.apref + c_lo, c_hi - c_lo, before, [&](int32_t k) { return LD(A.row_len + LD(pa + c_lo + k)); });
-      if (gtid == 0) A.apref[npairs] = all;
+      int32_t at = warp_claim(sc + SC_RNT + q, take);
+      if (take) A.R[at] = s;
     }
-    grid.sync();
-    const int32_t asum = LD(A.apref + npairs);
-    // ---- R = alive slots of the absorbed clusters (deduplicated), flattened
-    for (int64_t i = gtid; i < asum; i += GT) {
-      int32_t k = owner_of(A.apref, npairs, (int32_t)i);
-      int32_t y = LD(pa + k);
-      int32_t s = LD(A.pool + LD(A.row_off + y) + ((int32_t)i - LD(A.apref + k)));
-      if (LD(A.alive + s) && atomicExch(A.tmark + s, 1) == 0) A.R[atomicAdd(sc + SC_RNT, 1)] = s;
-    }
-    grid.sync();
-    const int32_t nt = LD(sc + SC_RNT);
-    // ---- rewrite R to the representatives (internal slots die), group equal
-    // keys, and find each group's slot outside R (it joins a representative
-    // with a cluster that is not absorbed and keeps its key) in the edge hash.
-    // tmark = 1 | mask of the new endpoints the slot was already incident to
-    // (2: low, 4: high): the row update appends only where new.
-    for (int64_t i = gtid; i < nt; i += GT) {
-      int32_t s = LD(A.R + i);
-      int32_t x = LD(A.u + s), y = LD(A.v + s);
-      int32_t a = rep_of(A.rp, x), b = rep_of(A.rp, y);
-      if (a == b) {
-        A.alive[s] = 0;
-        A.Rg[i] = -1;
-      } else {
-        int32_t lo = min(a, b), hi = max(a, b);
-        A.u[s] = lo;
-        A.v[s] = hi;
-        A.tmark[s] = 1 | ((lo == x || lo == y) ? 2 : 0) | ((hi == x || hi == y) ? 4 : 0);
-        uint64_t key = pair_key(lo, hi);
-        int32_t g = h_insert(A, key);
-        A.Rg[i] = g;
-        atomicAdd(A.hcnt + g, 1);
-        atomicMin(A.hhead + g, s);
-        A.Rnext[i] = atomicExch(A.hlist + g, (int32_t)i);
-        int32_t e = e_find(A, key);
-        if (e >= 0 && atomicCAS(A.hext + g, -1, e) == -1) A.tmark[e] = 8;
-      }
-    }
-    grid.sync();
-    // ---- fold each group (R members + the outside slot) into its smallest
-    // slot, sequential sum in slot order; survivors enter the next P when
-    // positive, untouched positive slots stay.  A group has at most 3 R
-    // members and one outside slot (a matching merges each cluster once).
-    for (int64_t i = gtid; i < nt; i += GT) {
-      const int32_t g = LD(A.Rg + i);
-      const int32_t s0 = LD(A.R + i);
-      if (g < 0 || LD(A.hhead + g) != s0) continue;
-      const int32_t cnt = LD(A.hcnt + g), ext = LD(A.hext + g);
-      const uint64_t key = pair_key(LD(A.u + s0), LD(A.v + s0));
-      int32_t surv = s0;
-      if (cnt == 1 && ext < 0) {
-        if (LD(A.c + s0) > 0.0) P2[atomicAdd(sc + SC_RNP2, 1)] = s0;
-      } else {
-        const int32_t total = cnt + (ext >= 0 ? 1 : 0);
-        if (total <= 16) {  // insertion sort in registers / local memory
-          int32_t buf[16];
-          int32_t k = 0;
-          for (int32_t j = LD(A.hlist + g); j >= 0; j = LD(A.Rnext + j)) buf[k++] = LD(A.R + j);
-          if (ext >= 0) buf[k++] = ext;
-          for (int32_t a = 1; a < k; a++) {
-            int32_t x = buf[a], b = a - 1;
-            while (b >= 0 && buf[b] > x) { buf[b + 1] = buf[b]; b--; }
-            buf[b + 1] = x;
-          }
-          surv = buf[0];
-          double acc = LD(A.c + buf[0]);
-          for (int32_t j = 1; j < k; j++) {
-            acc = __dadd_rn(acc, LD(A.c + buf[j]));
-            A.alive[buf[j]] = 0;
-          }
-          A.c[surv] = acc;
-        } else {  // not reachable under a matching; kept exact: repeated minimum extraction
-          int32_t prev = -1;
-          double acc = 0.0;
-          for (int32_t j = 0; j < total; j++) {
-            int32_t nxt = 0x7fffffff;
-            for (int32_t t = LD(A.hlist + g); t >= 0; t = LD(A.Rnext + t)) {
-              int32_t x = LD(A.R + t);
-              if (x > prev && x < nxt) nxt = x;
-            }
-            if (ext > prev && ext < nxt) nxt = ext;
-            if (j == 0) {
-              surv = nxt;
-              acc = LD(A.c + nxt);
-            } else {
-              acc = __dadd_rn(acc, LD(A.c + nxt));
-              A.alive[nxt] = 0;
-            }
-            prev = nxt;
-          }
-          A.c[surv] = acc;
-        }
-        if (LD(A.c + surv) > 0.0) P2[atomicAdd(sc + SC_RNP2, 1)] = surv;
-      }
-      if (surv != ext) {  // an R slot under its new key: edge hash entry, new row entries
-        e_insert(A, key, surv);
-        count_new(A, surv);
-      }
-    }
-    for (int64_t i = gtid; i < np; i += GT) {
-      int32_t s = LD(P + i);
-      if (!LD(A.tmark + s)) P2[atomicAdd(sc + SC_RNP2, 1)] = s;
-    }
-    grid.sync();
-    // ---- representatives whose row would overflow get a new one (twice the
-    // need, dead slots dropped): small rows one warp each, long rows one CTA
+    // representatives whose row could overflow (it gains at most the absorbed
+    // row) get a new one, twice the bound, dead slots dropped: short rows one
+    // warp each, long rows one CTA
     for (int64_t k0 = (int64_t)blockIdx.x * blockDim.x; k0 < npairs; k0 += GT) {
       if (threadIdx.x == 0) { s_nsmall = 0; s_nbig = 0; }
       __syncthreads();
@@ -451,17 +360,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
       if (k < npairs) {
         int32_t r = LD(pr + k);
         int32_t len = LD(A.row_len + r);
-        int32_t need = len + (int32_t)LD(A.bc + r);
-        A.bc[r] = 0ULL;
+        int32_t need = len + LD(A.row_len + LD(pa + k));
         if (need > LD(A.row_cap + r)) {
           A.row_cap[r] = need;  // replaced below
-          if (len > kBigRow) s_big[atomicAdd(&s_nbig, 1)] = r;
-          else s_small[atomicAdd(&s_nsmall, 1)] = r;
+          if (len > kBigRow) s_big[atomicAdd(&s_nbig, 1)] = (int32_t)k;
+          else s_small[atomicAdd(&s_nsmall, 1)] = (int32_t)k;
         }
       }
       __syncthreads();
       for (int32_t j = warp; j < s_nsmall; j += nwarps) {
-        const int32_t r = s_small[j];
+        const int32_t r = LD(pr + s_small[j]);
         const int32_t cap = max(2 * LD(A.row_cap + r), 16);
         int32_t off = 0;
         if (lane == 0) off = atomicAdd(sc + SC_POOL, cap);
@@ -472,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
           int32_t s = e0 + lane < len ? LD(A.pool + old + e0 + lane) : -1;
           bool keep = s >= 0 && LD(A.alive + s);
           unsigned bal = __ballot_sync(0xffffffffu, keep);
-          if (keep) A.pool[off + cnt + __popc(bal & ((1u << lane) - 1))] = s;
+          if (keep) A.pool[off + cnt + __popc(bal & lanes_below())] = s;
           cnt += __popc(bal);
         }
         if (lane == 0) {
@@ -482,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
         }
       }
       for (int32_t j = 0; j < s_nbig; j++) {
-        const int32_t r = s_big[j];
+        const int32_t r = LD(pr + s_big[j]);
         if (threadIdx.x == 0) {
           int32_t cap = 2 * LD(A.row_cap + r);
           s_off = atomicAdd(sc + SC_POOL, cap);
@@ -505,52 +413,132 @@ __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
       __syncthreads();
     }
     grid.sync();
-    // ---- rows gain the new slots; round state back to clean (the group's
-    // head resets the group); cluster bookkeeping
+    const int32_t nt = LD(sc + SC_RNT + q);
+    if (gtid == 0 && A.trace && round0 + rounds < A.trace_cap) {
+      unsigned long long tns;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tns));
+      long long* e = A.trace + 6 * (int64_t)(round0 + rounds);
+      e[0] = np; e[1] = npairs; e[2] = nt; e[3] = asum; e[4] = rrep; e[5] = (long long)tns;
+    }
+    // ---- 4. rewrite R to the representatives (internal slots die), group
+    // equal keys, and find each group's slot outside R (it joins a
+    // representative with a cluster that is not absorbed and keeps its key)
+    // in the edge hash.  tmark = 1 | mask of the new endpoints the slot was
+    // already incident to (2: low, 4: high): rows gain it only where new.
     for (int64_t i = gtid; i < nt; i += GT) {
-      const int32_t s = LD(A.R + i);
-      const int32_t g = LD(A.Rg + i);
-      const int32_t mk = LD(A.tmark + s);
-      A.tmark[s] = 0;
-      if (g < 0) continue;
-      if (LD(A.alive + s)) {
-        int32_t a = LD(A.u + s), b = LD(A.v + s);
-        if (LD(A.rp + a) == a && !(mk & 2)) A.pool[LD(A.row_off + a) + atomicAdd(A.row_len + a, 1)] = s;
-        if (LD(A.rp + b) == b && !(mk & 4)) A.pool[LD(A.row_off + b) + atomicAdd(A.row_len + b, 1)] = s;
-      }
-      if (LD(A.hhead + g) == s) {
-        int32_t e = LD(A.hext + g);
-        if (e >= 0) A.tmark[e] = 0;
-        A.hkey[g] = kEmpty;
-        A.hcnt[g] = 0;
-        A.hhead[g] = 0x7fffffff;
-        A.hext[g] = -1;
-        A.hlist[g] = -1;
+      int32_t s = LD(A.R + i);
+      int32_t x = LD(A.u + s), y = LD(A.v + s);
+      int32_t a = rep_of(A.rp, x), b = rep_of(A.rp, y);
+      if (a == b) {
+        A.alive[s] = 0;
+        A.Rg[i] = -1;
+      } else {
+        int32_t lo = min(a, b), hi = max(a, b);
+        A.u[s] = lo;
+        A.v[s] = hi;
+        A.tmark[s] = 1 | ((lo == x || lo == y) ? 2 : 0) | ((hi == x || hi == y) ? 4 : 0);
+        uint64_t key = pair_key(lo, hi);
+        int32_t g = h_insert(A, key);
+        A.Rg[i] = g;
+        atomicAdd(A.hcnt + g, 1);
+        atomicMin(A.hhead + g, s);
+        A.Rnext[i] = atomicExch(A.hlist + g, (int32_t)i);
+        int32_t e = e_find(A, key);
+        if (e >= 0 && atomicCAS(A.hext + g, -1, e) == -1) A.tmark[e] = 8;
       }
     }
-    for (int64_t k = gtid; k < npairs; k += GT) {
+    for (int64_t k = gtid; k < npairs; k += GT) {  // cluster bookkeeping
       int32_t x = LD(pr + k), t = LD(pa + k);
       A.row_len[t] = 0;
       A.size[x] = LD(A.size + x) + LD(A.size + t);
       A.minid[x] = min(LD(A.minid + x), LD(A.minid + t));
     }
-    if (gtid == 0) {
-      const int32_t r = LD(sc + SC_ROUNDS);
-      if (A.trace && r < A.trace_cap) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        long long* e = A.trace + 6 * (int64_t)r;
-        e[0] = np; e[1] = npairs; e[2] = nt; e[3] = asum; e[4] = rrep; e[5] = (long long)t;
+    grid.sync();
+    // ---- 5. fold each group (R members + the outside slot) into its smallest
+    // slot, sequential sum in slot order; survivors enter the next P when
+    // positive and their new representatives' rows; untouched positive slots
+    // stay.  A group has at most 3 R members and one outside slot (a matching
+    // merges each cluster once).
+    for (int64_t i0 = gtid - lane; i0 < nt; i0 += GT) {
+      const int64_t i = i0 + lane;
+      int32_t surv = -1;
+      bool pos = false;
+      if (i < nt) {
+        const int32_t g = LD(A.Rg + i);
+        const int32_t s0 = LD(A.R + i);
+        if (g >= 0 && LD(A.hhead + g) == s0) {
+          const int32_t cnt = LD(A.hcnt + g), ext = LD(A.hext + g);
+          const uint64_t key = pair_key(LD(A.u + s0), LD(A.v + s0));
+          surv = s0;
+          if (cnt > 1 || ext >= 0) {
+            const int32_t total = cnt + (ext >= 0 ? 1 : 0);
+            if (total <= 16) {  // insertion sort in registers / local memory
+              int32_t buf[16];
+              int32_t k = 0;
+              for (int32_t j = LD(A.hlist + g); j >= 0; j = LD(A.Rnext + j)) buf[k++] = LD(A.R + j);
+              if (ext >= 0) buf[k++] = ext;
+              for (int32_t a = 1; a < k; a++) {
+                int32_t x = buf[a], b = a - 1;
+                while (b >= 0 && buf[b] > x) { buf[b + 1] = buf[b]; b--; }
+                buf[b + 1] = x;
+              }
+              surv = buf[0];
+              double acc = LD(A.c + buf[0]);
+              for (int32_t j = 1; j < k; j++) {
+                acc = __dadd_rn(acc, LD(A.c + buf[j]));
+                A.alive[buf[j]] = 0;
+              }
+              A.c[surv] = acc;
+            } else {  // not reachable under a matching; kept exact: repeated minimum extraction
+              int32_t prev = -1;
+              double acc = 0.0;
+              for (int32_t j = 0; j < total; j++) {
+                int32_t nxt = 0x7fffffff;
+                for (int32_t t = LD(A.hlist + g); t >= 0; t = LD(A.Rnext + t)) {
+                  int32_t x = LD(A.R + t);
+                  if (x > prev && x < nxt) nxt = x;
+                }
+                if (ext > prev && ext < nxt) nxt = ext;
+                if (j == 0) {
+                  surv = nxt;
+                  acc = LD(A.c + nxt);
+                } else {
+                  acc = __dadd_rn(acc, LD(A.c + nxt));
+                  A.alive[nxt] = 0;
+                }
+                prev = nxt;
+              }
+              A.c[surv] = acc;
+            }
+          }
+          pos = LD(A.c + surv) > 0.0;
+          if (surv != ext) {  // an R slot under its new key
+            e_insert(A, key, surv);
+            const int32_t mk = LD(A.tmark + surv);
+            const int32_t a = LD(A.u + surv), b = LD(A.v + surv);
+            if (LD(A.rp + a) == a && !(mk & 2)) A.pool[LD(A.row_off + a) + atomicAdd(A.row_len + a, 1)] = surv;
+            if (LD(A.rp + b) == b && !(mk & 4)) A.pool[LD(A.row_off + b) + atomicAdd(A.row_len + b, 1)] = surv;
+          }
+        }
       }
-      sc[SC_PBASE] = base;
-      sc[SC_NPAIRS] = base + npairs;
-      sc[SC_NP] = LD(sc + SC_RNP2);
-      sc[SC_WHICH] = which ^ 1;
-      sc[SC_ROUNDS] = r + 1;
-      sc[SC_EFILL] = LD(sc + SC_EFILL) + nt;
-      sc[SC_RPAIRS] = 0; sc[SC_RNT] = 0; sc[SC_RSUM] = 0; sc[SC_RNP2] = 0; sc[SC_RREP] = 0;
+      const int32_t at = warp_claim(sc + SC_RNP2 + q, pos);
+      if (pos) P2[at] = surv;
+    }
+    for (int64_t i0 = gtid - lane; i0 < np; i0 += GT) {
+      const int64_t i = i0 + lane;
+      int32_t s = i < np ? LD(P + i) : 0;
+      const bool keep = i < np && !LD(A.tmark + s);
+      const int32_t at = warp_claim(sc + SC_RNP2 + q, keep);
+      if (keep) P2[at] = s;
     }
     grid.sync();
+    np = LD(sc + SC_RNP2 + q);
+    prev_base = base;
+    base += npairs;
+    prev_nt = nt;
+    efill += nt;
+    which ^= 1;
+    rounds++;
   }
 }
 #undef LD
@@ -623,15 +611,15 @@ int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc) {
   copy_d2d(ctx, c.p, q.c, m);
   Buf<uint8_t> alive(m, ctx);
   alive.fill_bytes(1);
-  Buf<unsigned long long> bc(n, ctx);
-  bc.zero();
-  Buf<int32_t> bn(n, ctx), pr(n, ctx), pa(n, ctx), rp(n, ctx), minid(n, ctx), size(n, ctx), tmark(m, ctx);
-  bn.fill_bytes(0x7f);
+  Buf<ulonglong2> vote(n, ctx);
+  vote.zero();
+  Buf<unsigned long long> pk(2, ctx);
+  Buf<int32_t> pr(n, ctx), pa(n, ctx), rp(n, ctx), minid(n, ctx), size(n, ctx), tmark(m, ctx);
   rp.fill_bytes(0xff);
   tmark.zero();
   iota(ctx, minid.p, n);
   RAMA_KERNEL(ctx, k_cl_fill_i32, n, size.p, n, 1);
-  Buf<int32_t> P0(m, ctx), P1(m, ctx), apref(n + 1, ctx);
+  Buf<int32_t> P0(m, ctx), P1(m, ctx), apref(n, ctx);
   Buf<int32_t> R(m, ctx), Rg(m, ctx), Rnext(m, ctx);
   uint32_t hcap = 1024;
   while ((int64_t)hcap < 2 * m) hcap <<= 1;
@@ -657,7 +645,6 @@ int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc) {
     RAMA_REQUIRE(per_sm >= 1, "cleanup kernel cannot be resident");
     grid_blocks = sms;  // one CTA per SM
   }
-  Buf<int32_t> part(grid_blocks + 1, ctx);
   int64_t total = 0;
   int launches = 0, rounds = 0;
   const char* stats_env = getenv("RAMA_CLEANUP_STATS");
@@ -665,9 +652,9 @@ int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc) {
   constexpr int32_t kTraceCap = 4096;
   Buf<long long> trace(round_trace ? 6 * kTraceCap : 1, ctx);
   Args A;
-  A.u = u.p; A.v = v.p; A.c = c.p; A.alive = alive.p; A.tmark = tmark.p; A.bc = bc.p; A.bn = bn.p;
+  A.u = u.p; A.v = v.p; A.c = c.p; A.alive = alive.p; A.tmark = tmark.p; A.vote = vote.p;
   A.rp = rp.p; A.minid = minid.p; A.size = size.p; A.P0 = P0.p; A.P1 = P1.p;
-  A.pr = pr.p; A.pa = pa.p; A.apref = apref.p; A.part = part.p;
+  A.pr = pr.p; A.pa = pa.p; A.apref = apref.p; A.pk = pk.p;
   A.R = R.p; A.Rg = Rg.p; A.Rnext = Rnext.p;
   A.hkey = hkey.p; A.hcnt = hcnt.p; A.hhead = hhead.p; A.hext = hext.p; A.hlist = hlist.p; A.hmask = hcap - 1;
   A.sc = sc.p;
@@ -704,11 +691,12 @@ int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc) {
     RAMA_KERNEL(ctx, k_cl_ehash_build, m, u.p, v.p, alive.p, m, A);
     int32_t init[SC_COUNT] = {0};
     init[SC_NPAIRS] = (int32_t)total;
-    init[SC_PBASE] = (int32_t)total;
+    init[SC_ROUNDS] = rounds;
     init[SC_NP] = (int32_t)np;
     init[SC_POOL] = (int32_t)used;
     init[SC_EFILL] = (int32_t)m;
     RAMA_CUDA(cudaMemcpyAsync(sc.p, init, sizeof(init), cudaMemcpyHostToDevice, ctx.s));
+    pk.zero();
     if (trace_print()) fprintf(stderr, "[rama] k_cl_rounds np=%lld\n", (long long)np);
     {
       KernelScope ks(ctx.s, "k_cl_rounds", 0.0);
@@ -724,20 +712,21 @@ int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc) {
     memcpy(st, ctx.pinned, sizeof(st));
     total = st[SC_NPAIRS];
     if (round_trace) {
-      const int32_t k = std::min(st[SC_ROUNDS], kTraceCap);
-      std::vector<long long> h(6 * (size_t)k);
-      if (k) RAMA_CUDA(cudaMemcpy(h.data(), trace.p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
-      for (int32_t r = 0; r < k; r++) {
+      const int32_t k0 = std::min(rounds, kTraceCap), k1 = std::min(st[SC_ROUNDS], kTraceCap);
+      std::vector<long long> h(6 * (size_t)k1);
+      if (k1) RAMA_CUDA(cudaMemcpy(h.data(), trace.p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+      for (int32_t r = k0; r < k1; r++) {
         const long long* e = &h[6 * (size_t)r];
-        long long prev = r ? h[6 * (size_t)(r - 1) + 5] : e[5];
+        long long prev = r > k0 ? h[6 * (size_t)(r - 1) + 5] : e[5];
         fprintf(stderr, "[rama] cl launch %d round %d np %lld pairs %lld nt %lld asum %lld rrep %lld dt_us %.1f\n",
-                launches, rounds + r, e[0], e[1], e[2], e[3], e[4], (e[5] - prev) / 1e3);
+                launches, r, e[0], e[1], e[2], e[3], e[4], (e[5] - prev) / 1e3);
       }
     }
-    rounds += st[SC_ROUNDS];
+    const bool progress = st[SC_ROUNDS] > rounds;
+    rounds = st[SC_ROUNDS];
     if (st[SC_STATUS] == kDone) break;
     RAMA_REQUIRE(st[SC_STATUS] == kPoolFull, "cleanup kernel ended in an unknown state");
-    if (st[SC_ROUNDS] == 0) {  // one round does not fit: larger pool and edge hash
+    if (!progress) {  // one round does not fit: larger pool and edge hash
       RAMA_REQUIRE(grow < (1 << 20), "cleanup cannot make progress");
       grow *= 2;
       if (ecap < (1u << 30)) ecap <<= 1;
