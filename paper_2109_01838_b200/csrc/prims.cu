@@ -504,7 +504,7 @@ __global__ void k_bucket_scatter(const int32_t* __restrict__ row, const uint64_t
 // result is a permutation even for duplicate keys) and writes its item to
 // row_start + rank.  Neighbouring threads read the same row, so the key
 // loads are warp broadcasts.  Longer rows are listed for the block sort.
-constexpr int kSmallRow = 64;
+constexpr int kSmallRow = 256;
 constexpr int kBlockRow = 4096;  // bitonic sort in shared memory: 4096 x 12 B = 48 KB
 
 __global__ void k_rank_rows(const BItem* __restrict__ items, const int32_t* __restrict__ ptr, int64_t N,
@@ -652,6 +652,9 @@ void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint6
   RAMA_CUDA(cudaMemcpyAsync(ctx.pinned, counters, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx.s));
   ctx.sync();
   int32_t nbig = ((int32_t*)ctx.pinned)[0], nb = ((int32_t*)ctx.pinned)[1];
+  if (getenv("RAMA_SORT_STATS") && (nbig || nb))
+    fprintf(stderr, "[rama] bucket_sort R %lld N %lld kept %lld: %d rows > %d, %d rows > %d\n", (long long)R,
+            (long long)N, (long long)total, nbig, kSmallRow, nb, kBlockRow);
   if (nbig > 0) {
     unsigned gb = (unsigned)std::min<int64_t>(nbig, 148 * 4);
     KernelScope ks_block(ctx.s, "k_sort_rows_block", 0.0);
