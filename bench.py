@@ -417,6 +417,10 @@ def b200_arm(args):
         "objective": {"primal": primal, "lower_bound": lb, "rounds": len(trace), "gap_vs_cpu_reference": gap},
         "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": launches,
         "top_kernels": kernels, "kernel_families": families,
+        "device_busy": {"kernel_ms_per_step": sum(v[0] for v in kern.values()) / args.steps,
+                        "profiled_step_ms": p_ms / args.steps,
+                        "note": "sum of our kernels' event-timed durations vs the profiled step (per-kernel events "
+                                "add small gaps); the rest is launch latency and host round trips"},
     }
     print(json.dumps(line), flush=True)
     if world > 1:
