@@ -134,7 +134,8 @@ __global__ void k_sep3(const int32_t* __restrict__ Q, int64_t nq, const int32_t*
     int32_t e = NQ[q];
     int32_t a = u[e], b = v[e];
     int32_t pa = ptr[a], pb = ptr[b];
-    int32_t x = first_common(adj + pa, ptr[a + 1] - pa, adj + pb, ptr[b + 1] - pb);
+    int32_t la = ptr[a + 1] - pa, lb = ptr[b + 1] - pb;
+    int32_t x = first_common(adj + pa, la, adj + pb, lb);
     int32_t* row = out_nodes + q * (int64_t)L;
     if (x >= 0) {
       out_len[q] = 3;
@@ -144,7 +145,7 @@ __global__ void k_sep3(const int32_t* __restrict__ Q, int64_t nq, const int32_t*
       out_len[q] = 0;
       for (int j = 0; j < L; j++) row[j] = 0;
     }
-    if (miss) miss[i] = (x < 0);
+    if (miss) miss[i] = x < 0 && la > 0 && lb > 0;  // a longer cycle needs both ends on E+
   }
 }
 
@@ -662,6 +663,18 @@ static int sep_force_fallback() {
   return v;
 }
 
+// RAMA_SEP_STATS=1: per call, miss edges by outcome and neighbourhood sizes
+__global__ void k_sep_stats(const int32_t* __restrict__ Q2, const int32_t* __restrict__ qa,
+                            const int32_t* __restrict__ qb, int64_t n2, const int32_t* __restrict__ ptr,
+                            const int32_t* __restrict__ len, unsigned long long* st) {
+  GRID_STRIDE(i, n2) {
+    int32_t l = len[Q2[i]];
+    atomicAdd(st + (l == 4 ? 1 : l == 5 ? 2 : 0), 1ULL);
+    atomicAdd(st + 3, (unsigned long long)(ptr[qa[i] + 1] - ptr[qa[i]]));
+    atomicAdd(st + 4, (unsigned long long)(ptr[qb[i] + 1] - ptr[qb[i]]));
+  }
+}
+
 void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
   ProfScope prof(ctx.s, kFamSeparate);
   RAMA_REQUIRE(L >= 3, "max_len must be at least 3");
@@ -741,6 +754,16 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
   // sources that did not fit the tables: sorted-row intersections
   Buf<int32_t> I2;
   int64_t nf = compact_indices(ctx, fb.p, n2, I2);
+  if (getenv("RAMA_SEP_STATS")) {
+    Buf<unsigned long long> st(5, ctx);
+    st.zero();
+    RAMA_KERNEL(ctx, k_sep_stats, n2, Q2.p, qa.p, qb.p, n2, csr.ptr.p, out.len.p, st.p);
+    unsigned long long h[5];
+    RAMA_CUDA(cudaMemcpy(h, st.p, sizeof(h), cudaMemcpyDeviceToHost));
+    fprintf(stderr, "[rama] sep n=%lld m=%lld arcs+=%lld nq=%lld n2=%lld sources=%lld fallback=%lld | none %llu c4 %llu c5 %llu | avg deg+ a %.2f b %.2f\n",
+            (long long)g.n, (long long)g.m, (long long)csr.arcs, (long long)nq, (long long)n2, (long long)ng,
+            (long long)nf, h[0], h[1], h[2], (double)h[3] / n2, (double)h[4] / n2);
+  }
   if (nf == 0) return;
   Buf<int32_t> Q3(nf, ctx);
   RAMA_KERNEL(ctx, k_gather_i32, nf, Q2.p, I2.p, nf, Q3.p);
