@@ -336,25 +336,36 @@ __global__ void k_sep5(const int32_t* __restrict__ Q, int64_t nq, const int32_t*
 //   4-cycle  y* = argmin_(y in N(b) & L2) (px(y), y)
 //   5-cycle  z* = argmin_(z in N(b), z not in {a} u L1 u L2) (px(py), py, z)
 //            with py(z) = argmin_(y in N(z) & L2) (px(y), y).
-// Sources whose levels overflow the tables (hubs) are flagged for the
-// row-intersection kernels above.
-constexpr int kGrp = 8;                  // lanes per source
-constexpr int kGrpPerBlock = 32;         // 256 threads
-constexpr int kSrcL1 = 32;
-constexpr int kSrcHash = 64;             // per-source L2 table; used at load <= 1/2
-constexpr int kSrcHashBits = 6;
+// Two table sizes: tier 1 (8 lanes per source, 32 sources per block) fits
+// grid-like neighbourhoods; the sources it cannot hold go to tier 2 (a warp
+// per source, 4x the L1, 16x the L2 table); what overflows tier 2 (hubs)
+// is flagged for the row-intersection kernels above.
+template <int G, int NL1, int HBITS, int BUILD>
+struct SrcTier {
+  static constexpr int kGrp = G;              // lanes per source
+  static constexpr int kL1 = NL1;             // |N+(a)| capacity
+  static constexpr int kHashBits = HBITS;
+  static constexpr int kHash = 1 << HBITS;    // per-source L2 table; used at load <= 1/2
+  static constexpr int kBuild = BUILD;        // max sum of |N+(x)| over x in N+(a)
+};
+using SrcTier1 = SrcTier<8, 32, 6, 256>;
+using SrcTier2 = SrcTier<32, 128, 10, 4096>;
+constexpr int kSrcThreads1 = 256, kSrcThreads2 = 128;
 
+template <int HBITS>
 __device__ __forceinline__ int32_t src_slot(int32_t y) {
-  return (int32_t)(((uint32_t)y * 0x9E3779B1u) >> (32 - kSrcHashBits));
+  return (int32_t)(((uint32_t)y * 0x9E3779B1u) >> (32 - HBITS));
 }
 
+template <int HBITS>
 __device__ __forceinline__ int32_t src_lookup(const int32_t* hk, const int32_t* hv, int32_t y) {
-  int32_t h = src_slot(y);
-  for (int t = 0; t < kSrcHash; t++) {
+  constexpr int H = 1 << HBITS;
+  int32_t h = src_slot<HBITS>(y);
+  for (int t = 0; t < H; t++) {
     int32_t k = hk[h];
     if (k == y) return hv[h];
     if (k < 0) return -1;
-    h = (h + 1) & (kSrcHash - 1);
+    h = (h + 1) & (H - 1);
   }
   return -1;
 }
@@ -371,53 +382,65 @@ __device__ __forceinline__ bool src_in_l1(const int32_t* l1, int32_t la, int32_t
   return false;
 }
 
+template <int G>
 __device__ __forceinline__ uint64_t grp_min_u64(uint64_t x, unsigned mask) {
 #pragma unroll
-  for (int o = kGrp / 2; o > 0; o >>= 1) {
-    uint64_t y = __shfl_xor_sync(mask, x, o, kGrp);
+  for (int o = G / 2; o > 0; o >>= 1) {
+    uint64_t y = __shfl_xor_sync(mask, x, o, G);
     x = y < x ? y : x;
   }
   return x;
 }
 
+template <int G>
 __device__ __forceinline__ int32_t grp_min_i32(int32_t x, unsigned mask) {
 #pragma unroll
-  for (int o = kGrp / 2; o > 0; o >>= 1) x = min(x, __shfl_xor_sync(mask, x, o, kGrp));
+  for (int o = G / 2; o > 0; o >>= 1) x = min(x, __shfl_xor_sync(mask, x, o, G));
+  return x;
+}
+
+template <int G>
+__device__ __forceinline__ int32_t grp_sum_i32(int32_t x, unsigned mask) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) x += __shfl_xor_sync(mask, x, o, G);
   return x;
 }
 
 // gstart[k] = first index (into Q2) of source group k (source gsrc[k]);
 // groups end at gstart[k+1] (or n2).  qb[i] = target b of the i-th miss.
+// glist (tier 2): the groups to run, else all ng.  A group that overflows
+// the tables sets gover[k] (tier 1, when given) or fb of its edges.
 // Table values are POSITIONS in N+(a) (ascending = node order), so the
 // parent is the atomicMin over the positions that reach y and every row of
 // the level can be walked at once (no sequential x loop).
-constexpr int kSrcBuild = 256;  // max sum of |N+(x)| over x in N+(a) handled in shared memory
-
-__global__ void __launch_bounds__(kGrp * kGrpPerBlock, 8) k_sep_src(
-    const int32_t* __restrict__ gstart, const int32_t* __restrict__ gsrc, int64_t ng, int64_t n2,
-    const int32_t* __restrict__ Q2, const int32_t* __restrict__ qb, const int32_t* __restrict__ ptr,
-    const int32_t* __restrict__ adj, int L, int32_t* __restrict__ out_len, int32_t* __restrict__ out_nodes,
-    uint8_t* __restrict__ fb, int force_fallback) {
-  __shared__ int32_t s_l1[kGrpPerBlock][kSrcL1];
-  __shared__ int32_t s_hk[kGrpPerBlock][kSrcHash];
-  __shared__ int32_t s_hv[kGrpPerBlock][kSrcHash];
+template <class T, int THREADS, int MINB, bool kListed>
+__global__ void __launch_bounds__(THREADS, MINB) k_sep_src(
+    const int32_t* __restrict__ gstart, const int32_t* __restrict__ gsrc, const int32_t* __restrict__ glist,
+    int64_t nlist, int64_t ng, int64_t n2, const int32_t* __restrict__ Q2, const int32_t* __restrict__ qb,
+    const int32_t* __restrict__ ptr, const int32_t* __restrict__ adj, int L, int32_t* __restrict__ out_len,
+    int32_t* __restrict__ out_nodes, uint8_t* __restrict__ gover, uint8_t* __restrict__ fb, int force_fallback) {
+  constexpr int kGrp = T::kGrp, kPer = THREADS / T::kGrp, kH = T::kHash;
+  __shared__ int32_t s_l1[kPer][T::kL1];
+  __shared__ int32_t s_hk[kPer][kH];
+  __shared__ int32_t s_hv[kPer][kH];
   const int gi = threadIdx.x / kGrp, lane = threadIdx.x % kGrp;
-  const unsigned mask = ((1u << kGrp) - 1u) << ((threadIdx.x & 31) & ~(kGrp - 1));
+  const unsigned mask = kGrp == 32 ? 0xffffffffu : ((1u << kGrp) - 1u) << ((threadIdx.x & 31) & ~(kGrp - 1));
   int32_t* l1 = s_l1[gi];
   int32_t* hk = s_hk[gi];
   int32_t* hv = s_hv[gi];
-  const int64_t ngroups = (int64_t)gridDim.x * kGrpPerBlock;
-  for (int64_t k = (int64_t)blockIdx.x * kGrpPerBlock + gi; k < ng; k += ngroups) {
-    const int32_t i0 = gstart[k], i1 = (k + 1 < ng) ? gstart[k + 1] : (int32_t)n2;
+  const int64_t ngroups = (int64_t)gridDim.x * kPer;
+  for (int64_t j = (int64_t)blockIdx.x * kPer + gi; j < nlist; j += ngroups) {
+    const int64_t k = kListed ? glist[j] : j;
+    const int32_t e0 = gstart[k], e1 = k + 1 < ng ? gstart[k + 1] : (int32_t)n2;
     const int32_t a = gsrc[k];
     const int32_t pa = ptr[a], la = ptr[a + 1] - pa;
-    bool over = la > kSrcL1 || force_fallback;
+    bool over = la > T::kL1 || force_fallback;
     __syncwarp(mask);  // the previous source's lookups are done before the table is reset
     if (!over) {
-      for (int32_t j = lane; j < la; j += kGrp) l1[j] = adj[pa + j];
-      for (int32_t j = lane; j < kSrcHash; j += kGrp) {
-        hk[j] = -1;
-        hv[j] = 0x7fffffff;
+      for (int32_t t = lane; t < la; t += kGrp) l1[t] = adj[pa + t];
+      for (int32_t t = lane; t < kH; t += kGrp) {
+        hk[t] = -1;
+        hv[t] = 0x7fffffff;
       }
       __syncwarp(mask);
       // each lane walks whole rows N+(x) for its x positions (independent load chains)
@@ -426,70 +449,72 @@ __global__ void __launch_bounds__(kGrp * kGrpPerBlock, 8) k_sep_src(
         const int32_t x = l1[xi];
         work += ptr[x + 1] - ptr[x];
       }
-#pragma unroll
-      for (int o = kGrp / 2; o > 0; o >>= 1) work += __shfl_xor_sync(mask, work, o, kGrp);
-      over = work > kSrcBuild;
+      work = grp_sum_i32<kGrp>(work, mask);
+      over = work > T::kBuild;
       if (!over) {
         int32_t mine = 0;
         for (int32_t xi = lane; xi < la; xi += kGrp) {
           const int32_t x = l1[xi];
           const int32_t px = ptr[x], lx = ptr[x + 1] - px;
-          for (int32_t j = 0; j < lx; j++) {
-            const int32_t y = adj[px + j];
+          for (int32_t t = 0; t < lx; t++) {
+            const int32_t y = adj[px + t];
             if (y == a || src_in_l1(l1, la, y)) continue;
-            int32_t h = src_slot(y);
-            for (int t = 0; t < kSrcHash; t++) {
+            int32_t h = src_slot<T::kHashBits>(y);
+            for (int r = 0; r < kH; r++) {
               int32_t kk = atomicCAS(hk + h, -1, y);
               if (kk == -1 || kk == y) {
                 mine += kk == -1;
                 atomicMin(hv + h, xi);  // BFS parent = smallest position reaching y
                 break;
               }
-              h = (h + 1) & (kSrcHash - 1);
+              h = (h + 1) & (kH - 1);
             }
           }
         }
-#pragma unroll
-        for (int o = kGrp / 2; o > 0; o >>= 1) mine += __shfl_xor_sync(mask, mine, o, kGrp);
-        over = mine > kSrcHash / 2;
+        mine = grp_sum_i32<kGrp>(mine, mask);
+        over = mine > kH / 2;
       }
       __syncwarp(mask);  // table complete before the lookups
     }
     if (over) {
-      for (int32_t i = i0 + lane; i < i1; i += kGrp) fb[i] = 1;
+      if (!kListed) {
+        if (lane == 0) gover[k] = 1;
+      } else {
+        for (int32_t i = e0 + lane; i < e1; i += kGrp) fb[i] = 1;
+      }
       __syncwarp(mask);
       continue;
     }
-    for (int32_t i = i0; i < i1; i++) {
+    for (int32_t i = e0; i < e1; i++) {
       const int32_t q = Q2[i];
       const int32_t b = qb[i];
       const int32_t pb = ptr[b], lb = ptr[b + 1] - pb;
       int32_t len = 0, r1 = 0, r2 = 0, r3 = 0;
       uint64_t best = ~0ULL;
-      for (int32_t j = lane; j < lb; j += kGrp) {
-        int32_t y = adj[pb + j];
-        int32_t p = src_lookup(hk, hv, y);
+      for (int32_t t = lane; t < lb; t += kGrp) {
+        int32_t y = adj[pb + t];
+        int32_t p = src_lookup<T::kHashBits>(hk, hv, y);
         if (p >= 0) {
           uint64_t key = ((uint64_t)(uint32_t)p << 32) | (uint32_t)y;
           best = key < best ? key : best;
         }
       }
-      best = grp_min_u64(best, mask);
+      best = grp_min_u64<kGrp>(best, mask);
       if (best != ~0ULL) {
         len = 4; r1 = l1[(int32_t)(best >> 32)]; r2 = (int32_t)(uint32_t)best;
       } else if (L >= 5) {
         uint64_t bk = ~0ULL;
         int32_t bz = 0x7fffffff;
         const int32_t lbc = min(lb, kHubCap);
-        for (int32_t j = lane; j < lbc; j += kGrp) {
-          int32_t z = adj[pb + j];
-          if (z == a || src_in_l1(l1, la, z) || src_lookup(hk, hv, z) >= 0) continue;
+        for (int32_t t = lane; t < lbc; t += kGrp) {
+          int32_t z = adj[pb + t];
+          if (z == a || src_in_l1(l1, la, z) || src_lookup<T::kHashBits>(hk, hv, z) >= 0) continue;
           const int32_t pz = ptr[z], lz = ptr[z + 1] - pz;
           if (lz > kHubCap) continue;
           uint64_t zb = ~0ULL;
-          for (int32_t t = 0; t < lz; t++) {
-            int32_t y = adj[pz + t];
-            int32_t p = src_lookup(hk, hv, y);
+          for (int32_t w = 0; w < lz; w++) {
+            int32_t y = adj[pz + w];
+            int32_t p = src_lookup<T::kHashBits>(hk, hv, y);
             if (p >= 0) {
               uint64_t key = ((uint64_t)(uint32_t)p << 32) | (uint32_t)y;
               zb = key < zb ? key : zb;
@@ -497,8 +522,8 @@ __global__ void __launch_bounds__(kGrp * kGrpPerBlock, 8) k_sep_src(
           }
           if (zb < bk || (zb == bk && z < bz)) { bk = zb; bz = z; }
         }
-        uint64_t mn = grp_min_u64(bk, mask);
-        int32_t zc = grp_min_i32(bk == mn ? bz : 0x7fffffff, mask);
+        uint64_t mn = grp_min_u64<kGrp>(bk, mask);
+        int32_t zc = grp_min_i32<kGrp>(bk == mn ? bz : 0x7fffffff, mask);
         if (mn != ~0ULL) {
           len = 5; r1 = l1[(int32_t)(mn >> 32)]; r2 = (int32_t)(uint32_t)mn; r3 = zc;
         }
@@ -654,11 +679,12 @@ __global__ void __launch_bounds__(256) k_sep_bfs(const int32_t* __restrict__ gst
 }
 
 // RAMA_SEP_FALLBACK=1 routes every source through the row-intersection
-// kernels (tests use it to check both executions against the oracle)
+// kernels, =2 every source through the tier-2 tables (tests use them to
+// check all executions against the oracle)
 static int sep_force_fallback() {
   static const int v = [] {
     const char* e = getenv("RAMA_SEP_FALLBACK");
-    return (e && e[0] == '1') ? 1 : 0;
+    return (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
   }();
   return v;
 }
@@ -731,25 +757,41 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
     ctx.launches++;
     return;
   }
-  Buf<uint8_t> fb(n2, ctx);
+  Buf<uint8_t> fb(n2, ctx), gover(ng, ctx);
   fb.zero();
+  gover.zero();
+  static const int64_t cap = [] {  // RAMA_SEP_BLOCKS overrides the grid cap (tests)
+    const char* e = getenv("RAMA_SEP_BLOCKS");
+    return e ? (int64_t)atoll(e) : (int64_t)148 * 6 * 4;
+  }();
+  const int force = sep_force_fallback();
   {
-    int64_t blocks = (ng + kGrpPerBlock - 1) / kGrpPerBlock;
-    static const int64_t cap = [] {  // RAMA_SEP_BLOCKS overrides the grid cap (tests)
-      const char* e = getenv("RAMA_SEP_BLOCKS");
-      return e ? (int64_t)atoll(e) : (int64_t)148 * 6 * 4;
-    }();
-    if (blocks > cap) blocks = cap;
+    constexpr int kPer = kSrcThreads1 / SrcTier1::kGrp;
+    int64_t blocks = std::min<int64_t>((ng + kPer - 1) / kPer, cap);
     if (trace_print()) fprintf(stderr, "[rama] k_sep_src groups=%lld\n", (long long)ng);
     // algorithmic bytes: the positive CSR once, the miss list and its
     // edges' endpoints, the cycle rows written
     KernelScope ks(ctx.s, "k_sep_src",
                    4.0 * (double)(g.n + 1) + 4.0 * (double)csr.arcs + (16.0 + 4.0 * L) * (double)n2);
-    k_sep_src<<<(unsigned)blocks, kGrp * kGrpPerBlock, 0, ctx.s>>>(gstart.p, gsrc.p, ng, n2, Q2.p, qb.p,
-                                                                   csr.ptr.p, csr.adj.p, L, out.len.p,
-                                                                   out.nodes.p, fb.p, sep_force_fallback());
+    k_sep_src<SrcTier1, kSrcThreads1, 8, false><<<(unsigned)blocks, kSrcThreads1, 0, ctx.s>>>(
+        gstart.p, gsrc.p, (const int32_t*)nullptr, ng, ng, n2, Q2.p, qb.p, csr.ptr.p, csr.adj.p, L, out.len.p,
+        out.nodes.p, gover.p, fb.p, force ? 1 : 0);
     RAMA_LAUNCH_CHECK();
     ctx.launches++;
+  }
+  {  // sources too large for tier 1: a warp each, larger tables
+    Buf<int32_t> G2;
+    int64_t ng2 = compact_indices(ctx, gover.p, ng, G2);
+    if (ng2 > 0) {
+      constexpr int kPer = kSrcThreads2 / SrcTier2::kGrp;
+      int64_t blocks = std::min<int64_t>((ng2 + kPer - 1) / kPer, cap);
+      KernelScope ks(ctx.s, "k_sep_src_wide", 0.0);
+      k_sep_src<SrcTier2, kSrcThreads2, 6, true><<<(unsigned)blocks, kSrcThreads2, 0, ctx.s>>>(
+          gstart.p, gsrc.p, G2.p, ng2, ng, n2, Q2.p, qb.p, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p,
+          (uint8_t*)nullptr, fb.p, force == 1 ? 1 : 0);
+      RAMA_LAUNCH_CHECK();
+      ctx.launches++;
+    }
   }
   // sources that did not fit the tables: sorted-row intersections
   Buf<int32_t> I2;

@@ -163,6 +163,22 @@ def test_cleanup_pool_rebuilds_agree():
     assert outs[0] == outs[1] == outs[2]
 
 
+def test_separation_tiers_agree():
+    """The 4/5-cycle search runs in tier-1 tables, tier-2 tables or the
+    row-intersection kernels depending on neighbourhood size; forcing every
+    source through tier 2 (RAMA_SEP_FALLBACK=2) or the row intersections (=1)
+    must give bit-identical solves and traces."""
+    code = ("import sys, hashlib; sys.path.insert(0, '..')\n"
+            "import paper_2109_01838_b200 as P\nfrom paper_2109_01838_b200 import instances\n"
+            "for coo in [instances.grid3d_coo(24, 40, 40, stride=2, seed=3), instances.random_coo(400, 0.2, seed=1),\n"
+            "            instances.chung_lu_coo(20000, 2.1, 200000, seed=2)]:\n"
+            "    s = P.solve(P.WeightedGraph(*coo), P.SolverConfig(mode='PD'))\n"
+            "    t = [(r.nodes, r.edges, r.triplets, r.contracted, r.lb) for r in s.trace]\n"
+            "    print(repr(s.primal_cost), repr(s.lower_bound), hashlib.md5(s.labeling.tobytes()).hexdigest(), t)\n")
+    outs = [_solve_env({"RAMA_SEP_FALLBACK": k}, code) for k in ("0", "1", "2")]
+    assert outs[0] == outs[1] == outs[2]
+
+
 # Reference per-round statistics of C3 (SURVEY.md Appendix A, measured with
 # the reference parcut solver): (nodes, edges, triplets, |S|) per PD round,
 # and its primal / lower bound (BASELINE.md section 2).
