@@ -334,7 +334,7 @@ def b200_arm(args):
         p_ms += e0.elapsed_time(e1)
         flush.zero_()
     fam = _lib.profile_read()
-    kern = _lib.profile_kernels()
+    kern, fam_kern = _lib.profile_kernels(by_family=True)
     _lib.profile_enable(False)
 
     # end to end through the C ABI with host buffers
@@ -387,7 +387,8 @@ def b200_arm(args):
     kernels = [{"kernel": k, "ms_per_step": v[0] / args.steps, "share": v[0] / p_ms, "launches_per_step": v[2] / args.steps,
                 "GB_per_s": (v[1] / (v[0] / 1e3) / 1e9) if v[1] > 0 and v[0] > 0 else None}
                for k, v in ranked[:40]]
-    families = {k: {"ms_per_step": vv[0] / args.steps, "alg_GB_per_step": vv[1] / args.steps / 1e9,
+    families = {k: {"ms_per_step": vv[0] / args.steps, "kernel_ms_per_step": fam_kern.get(k, (0.0,))[0] / args.steps,
+                    "alg_GB_per_step": vv[1] / args.steps / 1e9,
                     "scopes_per_step": vv[2] / args.steps} for k, vv in fam.items() if vv[2]}
 
     gap = None

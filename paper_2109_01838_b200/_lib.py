@@ -221,12 +221,19 @@ def profile_read():
     return {f: (ms[i], by[i], cnt[i]) for i, f in enumerate(FAMILIES)}
 
 
-def profile_kernels():
-    """{kernel: (ms, algorithmic_bytes, launches)} timed since profile_enable."""
+def profile_kernels(by_family=False):
+    """{kernel: (ms, algorithmic_bytes, launches)} timed since profile_enable;
+    by_family: also {family: (kernel ms, bytes, launches)} of the kernels
+    launched inside each family scope."""
     import json
 
     lib = load()
     need = lib.rama_profile_kernels(None, 0)
     buf = ctypes.create_string_buffer(int(need) + 4096)
     lib.rama_profile_kernels(buf, len(buf))
-    return {k: tuple(v) for k, v in json.loads(buf.value.decode()).items()}
+    raw = json.loads(buf.value.decode())
+    kern = {k: tuple(v) for k, v in raw.items() if not k.startswith("@")}
+    if not by_family:
+        return kern
+    fam = {FAMILIES[int(k[1:])]: tuple(v) for k, v in raw.items() if k.startswith("@")}
+    return kern, fam

@@ -81,6 +81,22 @@ enum {
   SC_COUNT = 16
 };
 
+struct alignas(32) Group {  // one sector per group
+  unsigned long long key;
+  int32_t cnt;   // R members
+  int32_t head;  // smallest R slot
+  int32_t ext;   // the slot outside R with the same key, or -1
+  int32_t list;  // first member (R index) of the group's list, or -1
+  int32_t pad[2];
+  __host__ __device__ static Group empty() { return Group{~0ULL, 0, 0x7fffffff, -1, -1, {0, 0}}; }
+};
+
+struct alignas(16) EdgeEnt {
+  unsigned long long key;
+  int32_t slot;
+  int32_t pad;
+};
+
 struct Args {
   int32_t* u;
   int32_t* v;
@@ -105,14 +121,10 @@ struct Args {
   int32_t* R;              // rewritten slots of the round
   int32_t* Rg;             // their group (hash position), -1: became internal
   int32_t* Rnext;          // group member list (R indices, linked)
-  uint64_t* hkey;          // group hash table (capacity hcap, power of two), clean between rounds
-  int32_t* hcnt;           // R members per group
-  int32_t* hhead;          // smallest R slot per group
-  int32_t* hext;           // the slot outside R with the same key, or -1
-  int32_t* hlist;          // first member (R index) of the group's list, or -1
+  Group* grp;              // group hash table (capacity hmask + 1), clean between rounds
   uint32_t hmask;
-  uint64_t* ekey;          // edge hash: every alive slot under its current key (stale entries
-  int32_t* eslot;          //   of dead or re-keyed slots stay and are skipped)
+  EdgeEnt* eh;             // edge hash: every alive slot under its current key (stale entries
+                           //   of dead or re-keyed slots stay and are skipped)
   uint32_t emask;
   int32_t* sc;             // device scalars, SC_*
   long long* trace;        // RAMA_CLEANUP_STATS=2: per round {np, npairs, nt, asum, rrep, t_ns}
@@ -142,7 +154,7 @@ __device__ __forceinline__ int32_t owner_of(const int32_t* pref, int32_t n, int3
 __device__ __forceinline__ int32_t h_insert(const Args& A, uint64_t k) {
   uint32_t h = key_hash(k) & A.hmask;
   while (true) {
-    unsigned long long old = atomicCAS((unsigned long long*)(A.hkey + h), (unsigned long long)kEmpty,
+    unsigned long long old = atomicCAS((unsigned long long*)&A.grp[h].key, (unsigned long long)kEmpty,
                                        (unsigned long long)k);
     if (old == kEmpty || old == k) return (int32_t)h;
     h = (h + 1) & A.hmask;
@@ -153,10 +165,10 @@ __device__ __forceinline__ int32_t h_insert(const Args& A, uint64_t k) {
 __device__ __forceinline__ void e_insert(const Args& A, uint64_t k, int32_t s) {
   uint32_t h = key_hash(k) & A.emask;
   while (true) {
-    unsigned long long old = atomicCAS((unsigned long long*)(A.ekey + h), (unsigned long long)kEmpty,
+    unsigned long long old = atomicCAS((unsigned long long*)&A.eh[h].key, (unsigned long long)kEmpty,
                                        (unsigned long long)k);
     if (old == kEmpty) {
-      A.eslot[h] = s;
+      A.eh[h].slot = s;
       return;
     }
     h = (h + 1) & A.emask;
@@ -168,10 +180,10 @@ __device__ __forceinline__ void e_insert(const Args& A, uint64_t k, int32_t s) {
 __device__ __forceinline__ int32_t e_find(const Args& A, uint64_t k) {
   uint32_t h = key_hash(k) & A.emask;
   while (true) {
-    uint64_t x = LD(A.ekey + h);
+    uint64_t x = LD(&A.eh[h].key);
     if (x == kEmpty) return -1;
     if (x == k) {
-      int32_t s = LD(A.eslot + h);
+      int32_t s = LD(&A.eh[h].slot);
       if (LD(A.alive + s) && !(LD(A.tmark + s) & 1) && pair_key(LD(A.u + s), LD(A.v + s)) == k) return s;
     }
     h = (h + 1) & A.emask;
@@ -239,14 +251,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
     for (int64_t i = gtid; i < prev_nt; i += GT) {
       const int32_t s = LD(A.R + i), g = LD(A.Rg + i);
       A.tmark[s] = 0;
-      if (g >= 0 && LD(A.hhead + g) == s) {
-        int32_t e = LD(A.hext + g);
+      if (g >= 0 && LD(&A.grp[g].head) == s) {
+        int32_t e = LD(&A.grp[g].ext);
         if (e >= 0) A.tmark[e] = 0;
-        A.hkey[g] = kEmpty;
-        A.hcnt[g] = 0;
-        A.hhead[g] = 0x7fffffff;
-        A.hext[g] = -1;
-        A.hlist[g] = -1;
+        A.grp[g] = Group::empty();
       }
     }
     for (int64_t i = gtid; i < np; i += GT) {
@@ -315,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
     int32_t stop = 0;
     if (npairs == 0) stop = kDone;
     else if ((int64_t)LD(sc + SC_POOL) + 2 * ((int64_t)rrep + asum) + 16LL * npairs > A.pool_cap ||
-             (int64_t)efill + asum > (int64_t)(A.emask >> 1))
+             (int64_t)efill + asum > (int64_t)(A.emask >> 1) || asum > (int32_t)(A.hmask >> 1))
       stop = kPoolFull;
     const int32_t* pr = A.pr + base;
     const int32_t* pa = A.pa + base;
@@ -440,11 +448,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
         uint64_t key = pair_key(lo, hi);
         int32_t g = h_insert(A, key);
         A.Rg[i] = g;
-        atomicAdd(A.hcnt + g, 1);
-        atomicMin(A.hhead + g, s);
-        A.Rnext[i] = atomicExch(A.hlist + g, (int32_t)i);
+        atomicAdd(&A.grp[g].cnt, 1);
+        atomicMin(&A.grp[g].head, s);
+        A.Rnext[i] = atomicExch(&A.grp[g].list, (int32_t)i);
         int32_t e = e_find(A, key);
-        if (e >= 0 && atomicCAS(A.hext + g, -1, e) == -1) A.tmark[e] = 8;
+        if (e >= 0 && atomicCAS(&A.grp[g].ext, -1, e) == -1) A.tmark[e] = 8;
       }
     }
     for (int64_t k = gtid; k < npairs; k += GT) {  // cluster bookkeeping
@@ -466,8 +474,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
       if (i < nt) {
         const int32_t g = LD(A.Rg + i);
         const int32_t s0 = LD(A.R + i);
-        if (g >= 0 && LD(A.hhead + g) == s0) {
-          const int32_t cnt = LD(A.hcnt + g), ext = LD(A.hext + g);
+        if (g >= 0 && LD(&A.grp[g].head) == s0) {
+          const int32_t cnt = LD(&A.grp[g].cnt), ext = LD(&A.grp[g].ext);
           const uint64_t key = pair_key(LD(A.u + s0), LD(A.v + s0));
           surv = s0;
           if (cnt > 1 || ext >= 0) {
@@ -475,7 +483,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
             if (total <= 16) {  // insertion sort in registers / local memory
               int32_t buf[16];
               int32_t k = 0;
-              for (int32_t j = LD(A.hlist + g); j >= 0; j = LD(A.Rnext + j)) buf[k++] = LD(A.R + j);
+              for (int32_t j = LD(&A.grp[g].list); j >= 0; j = LD(A.Rnext + j)) buf[k++] = LD(A.R + j);
               if (ext >= 0) buf[k++] = ext;
               for (int32_t a = 1; a < k; a++) {
                 int32_t x = buf[a], b = a - 1;
@@ -494,7 +502,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
               double acc = 0.0;
               for (int32_t j = 0; j < total; j++) {
                 int32_t nxt = 0x7fffffff;
-                for (int32_t t = LD(A.hlist + g); t >= 0; t = LD(A.Rnext + t)) {
+                for (int32_t t = LD(&A.grp[g].list); t >= 0; t = LD(A.Rnext + t)) {
                   int32_t x = LD(A.R + t);
                   if (x > prev && x < nxt) nxt = x;
                 }
@@ -542,6 +550,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
   }
 }
 #undef LD
+
+__global__ void k_cl_group_init(Group* g, int64_t n) {
+  GRID_STRIDE(i, n) g[i] = Group::empty();
+}
 
 __global__ void k_cl_fill_i32(int32_t* x, int64_t n, int32_t val) {
   GRID_STRIDE(i, n) x[i] = val;
@@ -621,19 +633,14 @@ int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc) {
   RAMA_KERNEL(ctx, k_cl_fill_i32, n, size.p, n, 1);
   Buf<int32_t> P0(m, ctx), P1(m, ctx), apref(n, ctx);
   Buf<int32_t> R(m, ctx), Rg(m, ctx), Rnext(m, ctx);
-  uint32_t hcap = 1024;
-  while ((int64_t)hcap < 2 * m) hcap <<= 1;
-  Buf<uint64_t> hkey(hcap, ctx);
-  Buf<int32_t> hcnt(hcap, ctx), hhead(hcap, ctx), hext(hcap, ctx), hlist(hcap, ctx);
-  hkey.fill_bytes(0xff);
-  hcnt.zero();
-  hext.fill_bytes(0xff);
-  hlist.fill_bytes(0xff);
-  RAMA_KERNEL(ctx, k_cl_fill_i32, hcap, hhead.p, hcap, 0x7fffffff);
+  // group table: at most asum groups per round (checked each round); sized
+  // to stay in L2 on typical rounds, grown by the host when a round needs more
+  uint32_t hcap = 4096;
+  while ((int64_t)hcap < m && hcap < (1u << 30)) hcap <<= 1;
+  Buf<Group> grp;
   uint32_t ecap = 4096;
   while ((int64_t)ecap < 4 * m && ecap < (1u << 30)) ecap <<= 1;
-  Buf<uint64_t> ekey;
-  Buf<int32_t> eslot;
+  Buf<EdgeEnt> eh;
   int64_t grow = 1;  // doubles when a launch could not run a single round
   Buf<int32_t> sc(SC_COUNT, ctx);
   static int grid_blocks = 0;
@@ -656,7 +663,6 @@ int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc) {
   A.rp = rp.p; A.minid = minid.p; A.size = size.p; A.P0 = P0.p; A.P1 = P1.p;
   A.pr = pr.p; A.pa = pa.p; A.apref = apref.p; A.pk = pk.p;
   A.R = R.p; A.Rg = Rg.p; A.Rnext = Rnext.p;
-  A.hkey = hkey.p; A.hcnt = hcnt.p; A.hhead = hhead.p; A.hext = hext.p; A.hlist = hlist.p; A.hmask = hcap - 1;
   A.sc = sc.p;
   A.trace = round_trace ? trace.p : nullptr;
   A.trace_cap = kTraceCap;
@@ -681,12 +687,14 @@ int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc) {
     RAMA_REQUIRE(used <= cap, "cleanup rows exceed the pool");
     Buf<int32_t> pool(cap, ctx);
     RAMA_KERNEL(ctx, k_cl_fill_rows, m, u.p, v.p, alive.p, m, off.p, cur.p, pool.p);
-    if (ekey.n != ecap) {
-      ekey.alloc(ecap, ctx.s);
-      eslot.alloc(ecap, ctx.s);
+    if (eh.n != ecap) eh.alloc(ecap, ctx.s);
+    eh.fill_bytes(0xff);
+    A.eh = eh.p; A.emask = ecap - 1;
+    if (grp.n != hcap) {
+      grp.alloc(hcap, ctx.s);
+      RAMA_KERNEL(ctx, k_cl_group_init, hcap, grp.p, hcap);
     }
-    ekey.fill_bytes(0xff);
-    A.ekey = ekey.p; A.eslot = eslot.p; A.emask = ecap - 1;
+    A.grp = grp.p; A.hmask = hcap - 1;
     A.row_off = off.p; A.row_len = deg.p; A.row_cap = rcap.p; A.pool = pool.p; A.pool_cap = cap;
     RAMA_KERNEL(ctx, k_cl_ehash_build, m, u.p, v.p, alive.p, m, A);
     int32_t init[SC_COUNT] = {0};
@@ -730,6 +738,7 @@ int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc) {
       RAMA_REQUIRE(grow < (1 << 20), "cleanup cannot make progress");
       grow *= 2;
       if (ecap < (1u << 30)) ecap <<= 1;
+      if (hcap < (1u << 30)) hcap <<= 1;
     }
   }
   if (stats_env)

@@ -96,6 +96,9 @@ cudaEvent_t prof_event();  // from a recycled pool (no per-scope cudaEventCreate
 // per kernel name; `bytes` = that launch's algorithmic bytes (0 = not
 // defined for this kernel).  prof_set_bytes() tags the NEXT RAMA_KERNEL.
 void prof_kernel_push(const char* name, cudaEvent_t a, cudaEvent_t b, double bytes);
+// the innermost open family scope on this thread (-1: none); kernel time is
+// also summed per family ("@<family index>" entries of the kernel JSON)
+int prof_family_swap(int fam);
 void prof_set_bytes(double bytes);
 double prof_take_bytes();
 // JSON {"kernel": [ms, bytes, launches], ...} of the kernels timed since enable
@@ -127,7 +130,9 @@ struct ProfScope {
   int fam;
   double bytes;
   cudaEvent_t a = nullptr, b = nullptr;
+  int outer;
   ProfScope(cudaStream_t st, int f, double by = 0.0) : s(st), fam(f), bytes(by) {
+    outer = prof_family_swap(f);
     if (prof_enabled()) {
       a = prof_event();
       b = prof_event();
@@ -136,6 +141,7 @@ struct ProfScope {
   }
   void add_bytes(double by) { bytes += by; }
   ~ProfScope() {
+    prof_family_swap(outer);
     if (a) {
       cudaEventRecord(b, s);
       prof_push(fam, a, b, bytes);

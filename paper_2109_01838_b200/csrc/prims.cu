@@ -175,7 +175,10 @@ struct KernRec {
   const char* name;
   cudaEvent_t a, b;
   double bytes;
+  int fam;
 };
+thread_local int g_cur_fam = -1;
+const char* const kFamKeys[kNumFamilies] = {"@0", "@1", "@2", "@3", "@4", "@5", "@6", "@7", "@8", "@9"};
 std::vector<KernRec> g_kern_recs;
 struct KernSum {
   double ms = 0, bytes = 0;
@@ -193,6 +196,12 @@ void kern_drain() {
     k.ms += ms;
     k.bytes += r.bytes;
     k.count += 1;
+    if (r.fam >= 0 && r.fam < kNumFamilies) {
+      KernSum& f = g_kern_sum[kFamKeys[r.fam]];
+      f.ms += ms;
+      f.bytes += r.bytes;
+      f.count += 1;
+    }
     g_event_pool.push_back(r.a);
     g_event_pool.push_back(r.b);
   }
@@ -230,6 +239,12 @@ cudaEvent_t prof_event() {
 
 bool prof_enabled() { return g_prof; }
 
+int prof_family_swap(int fam) {
+  int old = g_cur_fam;
+  g_cur_fam = fam;
+  return old;
+}
+
 void prof_set_bytes(double bytes) { g_next_bytes = bytes; }
 
 double prof_take_bytes() {
@@ -240,7 +255,7 @@ double prof_take_bytes() {
 
 void prof_kernel_push(const char* name, cudaEvent_t a, cudaEvent_t b, double bytes) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
-  g_kern_recs.push_back(KernRec{name, a, b, bytes});
+  g_kern_recs.push_back(KernRec{name, a, b, bytes, g_cur_fam});
   if (g_kern_recs.size() > 8192) kern_drain();
 }
 

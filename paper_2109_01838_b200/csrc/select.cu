@@ -59,39 +59,39 @@ __global__ void k_flag_positive(const double* __restrict__ c, int64_t m, uint8_t
 
 // ----------------------------------------------------------------- matching
 
-__global__ void k_match_vote1(const int32_t* __restrict__ P, int64_t np, const int32_t* __restrict__ u,
-                              const int32_t* __restrict__ v, const double* __restrict__ c,
-                              const uint8_t* __restrict__ matched, unsigned long long* __restrict__ bc) {
+// one pass of votes: every unmatched endpoint keeps the max of
+// (cost bits, ~neighbour id) as one 128-bit value -- the best positive edge,
+// ties toward the smaller neighbour (contraction.py:207)
+__device__ __forceinline__ void vote_max128(ulonglong2* p, unsigned long long hi, unsigned long long lo) {
+  unsigned __int128 key = ((unsigned __int128)hi << 64) | lo;
+  unsigned __int128 cur = 0;
+  while (key > cur) {
+    unsigned __int128 old = atomicCAS((unsigned __int128*)p, cur, key);
+    if (old == cur) return;
+    cur = old;
+  }
+}
+
+__global__ void k_match_vote(const int32_t* __restrict__ P, int64_t np, const int32_t* __restrict__ u,
+                             const int32_t* __restrict__ v, const double* __restrict__ c,
+                             const uint8_t* __restrict__ matched, ulonglong2* __restrict__ vote) {
   GRID_STRIDE(i, np) {
     int32_t e = P[i];
     int32_t a = u[e], b = v[e];
     if (matched[a] | matched[b]) continue;
     unsigned long long bits = dbits(c[e]);
-    atomicMax(bc + a, bits);
-    atomicMax(bc + b, bits);
+    vote_max128(vote + a, bits, 0xffffffffULL - (uint32_t)b);
+    vote_max128(vote + b, bits, 0xffffffffULL - (uint32_t)a);
   }
 }
 
-__global__ void k_match_vote2(const int32_t* __restrict__ P, int64_t np, const int32_t* __restrict__ u,
-                              const int32_t* __restrict__ v, const double* __restrict__ c,
-                              const uint8_t* __restrict__ matched, const unsigned long long* __restrict__ bc,
-                              int32_t* __restrict__ bn) {
-  GRID_STRIDE(i, np) {
-    int32_t e = P[i];
-    int32_t a = u[e], b = v[e];
-    if (matched[a] | matched[b]) continue;
-    unsigned long long bits = dbits(c[e]);
-    if (bits == bc[a]) atomicMin(bn + a, b);
-    if (bits == bc[b]) atomicMin(bn + b, a);
-  }
-}
-
-__global__ void k_match_pair(int64_t n, const unsigned long long* __restrict__ bc, const int32_t* __restrict__ bn,
-                             uint8_t* __restrict__ matched, int32_t* __restrict__ partner) {
+__global__ void k_match_pair(int64_t n, const ulonglong2* __restrict__ vote, uint8_t* __restrict__ matched,
+                             int32_t* __restrict__ partner) {
   GRID_STRIDE(x, n) {
-    if (bc[x] == 0ULL) continue;
-    int32_t t = bn[x];
-    if ((int32_t)x < t && bn[t] == (int32_t)x) {
+    ulonglong2 vx = vote[x];
+    if (vx.y == 0ULL) continue;
+    int32_t t = (int32_t)(0xffffffffULL - vx.x);
+    if ((int32_t)x < t && vote[t].x == 0xffffffffULL - (uint32_t)x) {
       partner[x] = t;
       matched[x] = 1;
       matched[t] = 1;
@@ -125,15 +125,13 @@ int64_t select_matching(Ctx& ctx, const GraphView& g, int rounds, Buf<int32_t>& 
   if (np == 0) return 0;
   Buf<uint8_t> matched(n, ctx);
   matched.zero();
-  Buf<unsigned long long> bc(n, ctx);
-  Buf<int32_t> bn(n, ctx), partner(n, ctx);
+  Buf<ulonglong2> vote(n, ctx);
+  Buf<int32_t> partner(n, ctx);
   partner.fill_bytes(0xff);
   for (int r = 0; r < rounds; r++) {
-    bc.zero();
-    bn.fill_bytes(0x7f);
-    RAMA_KERNEL(ctx, k_match_vote1, np, P.p, np, g.u, g.v, g.c, matched.p, bc.p);
-    RAMA_KERNEL(ctx, k_match_vote2, np, P.p, np, g.u, g.v, g.c, matched.p, bc.p, bn.p);
-    RAMA_KERNEL(ctx, k_match_pair, n, n, bc.p, bn.p, matched.p, partner.p);
+    vote.zero();
+    RAMA_KERNEL(ctx, k_match_vote, np, P.p, np, g.u, g.v, g.c, matched.p, vote.p);
+    RAMA_KERNEL(ctx, k_match_pair, n, n, vote.p, matched.p, partner.p);
   }
   Buf<uint8_t> lf(n, ctx);
   RAMA_KERNEL(ctx, k_flag_lower, n, partner.p, n, lf.p);
