@@ -54,7 +54,9 @@ def main():
         for d in launches(rep):
             d["capture"] = label or rep
             summary["launches"].append(d)
-    summary["traffic_bytes_per_launch"] = {d["kernel"]: d["traffic_bytes"] for d in summary["launches"]}
+    # keyed by the capture label (the library's kernel scope name, e.g.
+    # "k_sep_src" for the templated tier-1 instantiation)
+    summary["traffic_bytes_per_launch"] = {d["capture"]: d["traffic_bytes"] for d in summary["launches"]}
     with open(out_path, "w") as fh:
         json.dump(summary, fh, indent=1)
     print(json.dumps(summary, indent=1))
