@@ -276,6 +276,20 @@ T read_scalar(Ctx& ctx, const T* dev) {
   return v;
 }
 
+// two int32 device scalars in one round trip
+inline void read_pair(Ctx& ctx, const int32_t* a, const int32_t* b, int64_t& x, int64_t& y) {
+  auto t0 = std::chrono::steady_clock::now();
+  int32_t* hp = (int32_t*)ctx.pinned;
+  RAMA_CUDA(cudaMemcpyAsync(hp, a, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx.s));
+  RAMA_CUDA(cudaMemcpyAsync(hp + 1, b, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx.s));
+  ctx.sync();
+  HostStats& hs = host_stats();
+  hs.sync_ms += host_ms_since(t0);
+  hs.syncs++;
+  x = hp[0];
+  y = hp[1];
+}
+
 template <class T>
 void copy_d2d(Ctx& ctx, T* dst, const T* src, int64_t count) {
   if (count > 0) RAMA_CUDA(cudaMemcpyAsync(dst, src, sizeof(T) * count, cudaMemcpyDeviceToDevice, ctx.s));

@@ -961,8 +961,10 @@ void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& 
   Buf<int32_t> nt(rows > 0 ? rows : 1, ctx), nc(rows > 0 ? rows : 1, ctx);
   Buf<int32_t> toff(rows + 1, ctx), coff(rows + 1, ctx);
   RAMA_KERNEL(ctx, k_fan_counts, rows, cyc.len.p, rows, nt.p, nc.p);
-  int64_t traw = exclusive_scan(ctx, nt.p, toff.p, rows, true);
-  int64_t craw = exclusive_scan(ctx, nc.p, coff.p, rows, true);
+  exclusive_scan(ctx, nt.p, toff.p, rows, false);
+  exclusive_scan(ctx, nc.p, coff.p, rows, false);
+  int64_t traw = 0, craw = 0;
+  read_pair(ctx, toff.p + rows, coff.p + rows, traw, craw);
   Buf<int32_t> trow(traw > 0 ? traw : 1, ctx), crow(craw > 0 ? craw : 1, ctx);
   Buf<uint64_t> tkey(traw > 0 ? traw : 1, ctx), ckey(craw > 0 ? craw : 1, ctx);
   RAMA_KERNEL(ctx, k_fan_emit, rows, cyc.len.p, cyc.nodes.p, rows, cyc.L, toff.p, coff.p, trow.p, tkey.p, crow.p,

@@ -522,10 +522,11 @@ __global__ void k_bucket_scatter(const int32_t* __restrict__ row, const uint64_t
 constexpr int kSmallRow = 256;
 constexpr int kBlockRow = 4096;  // bitonic sort in shared memory: 4096 x 12 B = 48 KB
 
-__global__ void k_rank_rows(const BItem* __restrict__ items, const int32_t* __restrict__ ptr, int64_t N,
-                            int64_t sort_rows, uint64_t* __restrict__ okey, int32_t* __restrict__ osrc,
-                            int32_t* __restrict__ orow, int32_t* __restrict__ big_list, int32_t* __restrict__ huge_list,
-                            int32_t* __restrict__ counters) {
+__global__ void k_rank_rows(const BItem* __restrict__ items, const int32_t* __restrict__ ptr,
+                            const int32_t* __restrict__ kept, int64_t sort_rows, uint64_t* __restrict__ okey,
+                            int32_t* __restrict__ osrc, int32_t* __restrict__ orow, int32_t* __restrict__ big_list,
+                            int32_t* __restrict__ huge_list, int32_t* __restrict__ counters) {
+  const int64_t N = *kept;  // kept items (row >= 0), on the device: no host read-back before this kernel
   GRID_STRIDE(p, N) {
     const BItem it = items[p];
     const int32_t r = it.row;
@@ -642,14 +643,16 @@ void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint6
   cnt.zero();
   prof_set_bytes(8.0 * (double)N);
   RAMA_KERNEL(ctx, k_bucket_count, N, row, N, cnt.p, off.p);
-  int64_t total = exclusive_scan(ctx, cnt.p, out.row_ptr.p, R, true);  // kept items (row >= 0)
-  out.total = total;
-  if (total == 0 || R == 0) {
+  exclusive_scan(ctx, cnt.p, out.row_ptr.p, R, false);  // row_ptr[R] = kept items (row >= 0)
+  if (R == 0 || N == 0) {
+    out.total = 0;
     if (!want_row) out.row.release();
     return;
   }
-  Buf<BItem> items(total, ctx);
-  prof_set_bytes(16.0 * (double)N + 16.0 * (double)total);
+  // sized for all N items; the kept count stays on the device until the one
+  // read-back at the end
+  Buf<BItem> items(N, ctx);
+  prof_set_bytes(16.0 * (double)N + 16.0 * (double)N);
   RAMA_KERNEL(ctx, k_bucket_scatter, N, row, key, off.p, N, out.row_ptr.p, items.p);
   off.release();
   cnt.release();
@@ -658,25 +661,28 @@ void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint6
   int32_t* huge_list = lists.p + sort_rows;
   int32_t* counters = lists.p + 2 * sort_rows;
   RAMA_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(int32_t), ctx.s));
-  prof_set_bytes(16.0 * (double)total + 12.0 * (double)total + (want_row ? 4.0 * (double)total : 0.0));
-  RAMA_KERNEL(ctx, k_rank_rows, total, items.p, out.row_ptr.p, total, sort_rows, out.key.p, out.src.p,
+  prof_set_bytes(16.0 * (double)N + 12.0 * (double)N + (want_row ? 4.0 * (double)N : 0.0));
+  RAMA_KERNEL(ctx, k_rank_rows, N, items.p, out.row_ptr.p, out.row_ptr.p + R, sort_rows, out.key.p, out.src.p,
               want_row ? out.row.p : (int32_t*)nullptr, big_list, huge_list, counters);
   if (!want_row) out.row.release();
-  if (sort_rows == 0) return;
-  // one read-back of both list sizes; the long-row sorts launch only when needed
-  RAMA_CUDA(cudaMemcpyAsync(ctx.pinned, counters, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx.s));
-  ctx.sync();
-  int32_t nbig = ((int32_t*)ctx.pinned)[0], nb = ((int32_t*)ctx.pinned)[1];
-  if (getenv("RAMA_SORT_STATS") && (nbig || nb))
-    fprintf(stderr, "[rama] bucket_sort R %lld N %lld kept %lld: %d rows > %d, %d rows > %d\n", (long long)R,
-            (long long)N, (long long)total, nbig, kSmallRow, nb, kBlockRow);
-  if (nbig > 0) {
-    unsigned gb = (unsigned)std::min<int64_t>(nbig, 148 * 4);
+  if (sort_rows > 0 && N > kSmallRow) {  // rows of kSmallRow+1..kBlockRow items: the list size is read on the device
+    unsigned gb = (unsigned)std::min<int64_t>(std::max<int64_t>(N / (kSmallRow + 1), 1), 148 * 4);
     KernelScope ks_block(ctx.s, "k_sort_rows_block", 0.0);
     k_sort_rows_block<<<gb, 512, 0, ctx.s>>>(out.row_ptr.p, big_list, counters, items.p, out.key.p, out.src.p);
     RAMA_LAUNCH_CHECK();
     ctx.launches++;
   }
+  // one read-back: the kept count and the number of hub rows
+  int32_t* hp = (int32_t*)ctx.pinned;
+  RAMA_CUDA(cudaMemcpyAsync(hp, out.row_ptr.p + R, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx.s));
+  RAMA_CUDA(cudaMemcpyAsync(hp + 1, counters, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx.s));
+  ctx.sync();
+  const int64_t total = hp[0];
+  const int32_t nbig = hp[1], nb = hp[2];
+  out.total = total;
+  if (getenv("RAMA_SORT_STATS") && (nbig || nb))
+    fprintf(stderr, "[rama] bucket_sort R %lld N %lld kept %lld: %d rows > %d, %d rows > %d\n", (long long)R,
+            (long long)N, (long long)total, nbig, kSmallRow, nb, kBlockRow);
   if (nb == 0) return;
   // rare (power-law hubs): CUB segmented sort of the rows > kBlockRow
   Buf<int32_t> blen(nb, ctx), boff(nb + 1, ctx);
