@@ -370,6 +370,29 @@ __device__ __forceinline__ int32_t src_lookup(const int32_t* hk, const int32_t* 
   return -1;
 }
 
+// 128-bit membership filters held in registers (no false negatives): a
+// miss skips the shared-memory binary search / hash probe
+struct Bloom128 {
+  uint64_t lo = 0, hi = 0;
+  __device__ __forceinline__ static uint32_t bit(int32_t y) { return ((uint32_t)y * 0x2545F491u) >> 25; }
+  __device__ __forceinline__ void add(int32_t y) {
+    uint32_t b = bit(y);
+    if (b < 64) lo |= 1ULL << b; else hi |= 1ULL << (b - 64);
+  }
+  __device__ __forceinline__ bool maybe(int32_t y) const {
+    uint32_t b = bit(y);
+    return ((b < 64 ? lo : hi) >> (b & 63)) & 1ULL;
+  }
+  template <int G>
+  __device__ __forceinline__ void group_or(unsigned mask) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+      lo |= __shfl_xor_sync(mask, lo, o, G);
+      hi |= __shfl_xor_sync(mask, hi, o, G);
+    }
+  }
+};
+
 __device__ __forceinline__ bool src_in_l1(const int32_t* l1, int32_t la, int32_t y) {
   int32_t lo = 0, hi = la;
   while (lo < hi) {
@@ -435,9 +458,15 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sep_src(
     const int32_t a = gsrc[k];
     const int32_t pa = ptr[a], la = ptr[a + 1] - pa;
     bool over = la > T::kL1 || force_fallback;
+    Bloom128 f1, f2;  // L1 and L2 members
     __syncwarp(mask);  // the previous source's lookups are done before the table is reset
     if (!over) {
-      for (int32_t t = lane; t < la; t += kGrp) l1[t] = adj[pa + t];
+      for (int32_t t = lane; t < la; t += kGrp) {
+        const int32_t x = adj[pa + t];
+        l1[t] = x;
+        f1.add(x);
+      }
+      f1.group_or<kGrp>(mask);
       for (int32_t t = lane; t < kH; t += kGrp) {
         hk[t] = -1;
         hv[t] = 0x7fffffff;
@@ -458,12 +487,13 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sep_src(
           const int32_t px = ptr[x], lx = ptr[x + 1] - px;
           for (int32_t t = 0; t < lx; t++) {
             const int32_t y = adj[px + t];
-            if (y == a || src_in_l1(l1, la, y)) continue;
+            if (y == a || (f1.maybe(y) && src_in_l1(l1, la, y))) continue;
             int32_t h = src_slot<T::kHashBits>(y);
             for (int r = 0; r < kH; r++) {
               int32_t kk = atomicCAS(hk + h, -1, y);
               if (kk == -1 || kk == y) {
                 mine += kk == -1;
+                f2.add(y);
                 atomicMin(hv + h, xi);  // BFS parent = smallest position reaching y
                 break;
               }
@@ -473,6 +503,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sep_src(
         }
         mine = grp_sum_i32<kGrp>(mine, mask);
         over = mine > kH / 2;
+        f2.group_or<kGrp>(mask);
       }
       __syncwarp(mask);  // table complete before the lookups
     }
@@ -493,7 +524,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sep_src(
       uint64_t best = ~0ULL;
       for (int32_t t = lane; t < lb; t += kGrp) {
         int32_t y = adj[pb + t];
-        int32_t p = src_lookup<T::kHashBits>(hk, hv, y);
+        int32_t p = f2.maybe(y) ? src_lookup<T::kHashBits>(hk, hv, y) : -1;
         if (p >= 0) {
           uint64_t key = ((uint64_t)(uint32_t)p << 32) | (uint32_t)y;
           best = key < best ? key : best;
@@ -508,13 +539,15 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sep_src(
         const int32_t lbc = min(lb, kHubCap);
         for (int32_t t = lane; t < lbc; t += kGrp) {
           int32_t z = adj[pb + t];
-          if (z == a || src_in_l1(l1, la, z) || src_lookup<T::kHashBits>(hk, hv, z) >= 0) continue;
+          if (z == a || (f1.maybe(z) && src_in_l1(l1, la, z)) ||
+              (f2.maybe(z) && src_lookup<T::kHashBits>(hk, hv, z) >= 0))
+            continue;
           const int32_t pz = ptr[z], lz = ptr[z + 1] - pz;
           if (lz > kHubCap) continue;
           uint64_t zb = ~0ULL;
           for (int32_t w = 0; w < lz; w++) {
             int32_t y = adj[pz + w];
-            int32_t p = src_lookup<T::kHashBits>(hk, hv, y);
+            int32_t p = f2.maybe(y) ? src_lookup<T::kHashBits>(hk, hv, y) : -1;
             if (p >= 0) {
               uint64_t key = ((uint64_t)(uint32_t)p << 32) | (uint32_t)y;
               zb = key < zb ? key : zb;
@@ -773,7 +806,7 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
     // edges' endpoints, the cycle rows written
     KernelScope ks(ctx.s, "k_sep_src",
                    4.0 * (double)(g.n + 1) + 4.0 * (double)csr.arcs + (16.0 + 4.0 * L) * (double)n2);
-    k_sep_src<SrcTier1, kSrcThreads1, 8, false><<<(unsigned)blocks, kSrcThreads1, 0, ctx.s>>>(
+    k_sep_src<SrcTier1, kSrcThreads1, 6, false><<<(unsigned)blocks, kSrcThreads1, 0, ctx.s>>>(
         gstart.p, gsrc.p, (const int32_t*)nullptr, ng, ng, n2, Q2.p, qb.p, csr.ptr.p, csr.adj.p, L, out.len.p,
         out.nodes.p, gover.p, fb.p, force ? 1 : 0);
     RAMA_LAUNCH_CHECK();
