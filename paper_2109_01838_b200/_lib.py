@@ -11,7 +11,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "librama_b200.so")
+# RAMA_LIB (A/B experiments): another build of the same library
+LIB_PATH = os.environ.get("RAMA_LIB") or os.path.join(_HERE, "_lib", "librama_b200.so")
 
 _i32p = ctypes.c_void_p  # device pointers travel as void*
 _i64 = ctypes.c_int64

@@ -339,8 +339,23 @@ double device_sum(Ctx& ctx, const double* x, int64_t n);
 // row pointers of a (u, v)-sorted edge list: ptr[x] = first edge with u >= x
 void row_ptr_from_sorted(Ctx& ctx, const int32_t* u, int64_t m, int64_t n, int32_t* ptr);
 
-// numpy summation orders on device (see oracle/rama_oracle.c)
-__device__ __forceinline__ double pw_leaf(const double* a, int64_t n) {
+// numpy summation orders on device (see oracle/rama_oracle.c).  The
+// summands come through an accessor: a contiguous array, or values gathered
+// by index (so segment sums read c[src[p]] without a gathered copy).
+struct DirectF64 {
+  const double* p;
+  __device__ __forceinline__ double operator[](int64_t i) const { return p[i]; }
+  __device__ __forceinline__ DirectF64 operator+(int64_t k) const { return DirectF64{p + k}; }
+};
+struct GatherF64 {
+  const double* c;
+  const int32_t* idx;
+  __device__ __forceinline__ double operator[](int64_t i) const { return c[idx[i]]; }
+  __device__ __forceinline__ GatherF64 operator+(int64_t k) const { return GatherF64{c, idx + k}; }
+};
+
+template <class A>
+__device__ __forceinline__ double pw_leaf(A a, int64_t n) {
   if (n < 8) {
     double r = -0.0;  // numpy 2.x starts the short sum at -0.0 (keeps -0.0 sums)
     for (int64_t i = 0; i < n; i++) r = __dadd_rn(r, a[i]);
@@ -362,7 +377,8 @@ __device__ __forceinline__ double pw_leaf(const double* a, int64_t n) {
 
 // numpy pairwise sum; iterative post-order walk of numpy's fixed recursion
 // tree (split at n/2 rounded down to a multiple of 8, leaves <= 128).
-__device__ __forceinline__ double pw_sum(const double* a, int64_t n) {
+template <class A>
+__device__ __forceinline__ double pw_sum(A a, int64_t n) {
   if (n <= 128) return pw_leaf(a, n);
   int64_t fo[40], fl[40];
   double fleft[40];
@@ -395,12 +411,17 @@ __device__ __forceinline__ double pw_sum(const double* a, int64_t n) {
   }
 }
 
+__device__ __forceinline__ double pw_leaf(const double* a, int64_t n) { return pw_leaf(DirectF64{a}, n); }
+__device__ __forceinline__ double pw_sum(const double* a, int64_t n) { return pw_sum(DirectF64{a}, n); }
+
 // one np.add.reduceat segment: x[0] + pairwise(x[1:])
-__device__ __forceinline__ double seg_sum(const double* a, int64_t n) {
+template <class A>
+__device__ __forceinline__ double seg_sum(A a, int64_t n) {
   if (n <= 0) return 0.0;
   if (n == 1) return a[0];  // x0 + pairwise([]) = x0 + (-0.0) = x0
   return __dadd_rn(a[0], pw_sum(a + 1, n - 1));
 }
+__device__ __forceinline__ double seg_sum(const double* a, int64_t n) { return seg_sum(DirectF64{a}, n); }
 
 __device__ __forceinline__ uint64_t dbits(double x) { return (uint64_t)__double_as_longlong(x); }
 

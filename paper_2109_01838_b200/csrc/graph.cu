@@ -28,22 +28,17 @@ __global__ void k_seg_heads(const int32_t* __restrict__ row, const uint64_t* __r
   }
 }
 
-__global__ void k_gather_f64(const double* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
-                             double* __restrict__ dst) {
-  GRID_STRIDE(i, n) dst[i] = src[idx[i]];
-}
-
 // out edge j = segment [heads[j], heads[j+1]) of the sorted slots
 __global__ void k_seg_reduce(const int32_t* __restrict__ heads, int64_t k, int64_t limit,
                              const int32_t* __restrict__ row, const uint64_t* __restrict__ key,
-                             const double* __restrict__ cs, int32_t* __restrict__ ou, int32_t* __restrict__ ov,
-                             double* __restrict__ oc) {
+                             const double* __restrict__ c, const int32_t* __restrict__ src,
+                             int32_t* __restrict__ ou, int32_t* __restrict__ ov, double* __restrict__ oc) {
   GRID_STRIDE(j, k) {
     int64_t b = heads[j];
     int64_t e = (j + 1 < k) ? heads[j + 1] : limit;
     ou[j] = row[b];
     ov[j] = (int32_t)(key[b] >> 32);
-    oc[j] = seg_sum(cs + b, e - b);
+    oc[j] = seg_sum(GatherF64{c, src + b}, e - b);  // c in sorted order, gathered in place
   }
 }
 
@@ -53,15 +48,13 @@ static Graph reduce_sorted(Ctx& ctx, int64_t n_out, int64_t limit, BucketSorted&
   out.n = n_out;
   Buf<uint8_t> head(limit > 0 ? limit : 1, ctx);
   RAMA_KERNEL(ctx, k_seg_heads, limit, bs.row.p, bs.key.p, limit, head.p);
-  Buf<double> cs(limit > 0 ? limit : 1, ctx);
-  RAMA_KERNEL(ctx, k_gather_f64, limit, c, bs.src.p, limit, cs.p);
   Buf<int32_t> hp;
   int64_t k = compact_indices(ctx, head.p, limit, hp);
   out.m = k;
   out.u.alloc(k > 0 ? k : 1, ctx.s);
   out.v.alloc(k > 0 ? k : 1, ctx.s);
   out.c.alloc(k > 0 ? k : 1, ctx.s);
-  RAMA_KERNEL(ctx, k_seg_reduce, k, hp.p, k, limit, bs.row.p, bs.key.p, cs.p, out.u.p, out.v.p, out.c.p);
+  RAMA_KERNEL(ctx, k_seg_reduce, k, hp.p, k, limit, bs.row.p, bs.key.p, c, bs.src.p, out.u.p, out.v.p, out.c.p);
   return out;
 }
 

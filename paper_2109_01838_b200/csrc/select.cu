@@ -230,14 +230,37 @@ __global__ void k_flag_conflicts(const int32_t* __restrict__ u, const int32_t* _
   GRID_STRIDE(i, m) f[i] = (c[i] < 0.0) && comp[u[i]] == comp[v[i]];
 }
 
+// the forest's nodes get local ids 0..nf-1 (ascending node order), so the
+// Euler tour, the lifting tables and the path queries scale with the forest,
+// not the graph (late rounds: a few thousand forest nodes in a graph of 10^5-10^6)
+__global__ void k_mark_fnodes(const int32_t* __restrict__ Fi, int64_t kf, const int32_t* __restrict__ P,
+                              const int32_t* __restrict__ u, const int32_t* __restrict__ v,
+                              uint8_t* __restrict__ isf) {
+  GRID_STRIDE(i, kf) {
+    int32_t e = P[Fi[i]];
+    isf[u[e]] = 1;
+    isf[v[e]] = 1;
+  }
+}
+
+__global__ void k_scatter_loc(const int32_t* __restrict__ FN, int64_t nf, int32_t* __restrict__ loc) {
+  GRID_STRIDE(i, nf) loc[FN[i]] = (int32_t)i;
+}
+
+__global__ void k_comp_local(const int32_t* __restrict__ FN, int64_t nf, const int32_t* __restrict__ comp,
+                             const int32_t* __restrict__ loc, int32_t* __restrict__ comp_loc) {
+  GRID_STRIDE(i, nf) comp_loc[i] = loc[comp[FN[i]]];  // a tree's root (its smallest node) is a forest node
+}
+
 __global__ void k_forest_edges(const int32_t* __restrict__ Fi, int64_t kf, const int32_t* __restrict__ P,
                                const int32_t* __restrict__ u, const int32_t* __restrict__ v,
-                               const double* __restrict__ c, int32_t* __restrict__ fu, int32_t* __restrict__ fv,
+                               const int32_t* __restrict__ loc, const double* __restrict__ c,
+                               int32_t* __restrict__ fu, int32_t* __restrict__ fv,
                                uint64_t* __restrict__ fkey_bits, int32_t* __restrict__ fval) {
   GRID_STRIDE(i, kf) {
     int32_t e = P[Fi[i]];
-    fu[i] = u[e];
-    fv[i] = v[e];
+    fu[i] = loc[u[e]];
+    fv[i] = loc[v[e]];
     fkey_bits[i] = dbits(c[e]);  // ascending cost, ties keep (u, v) order
     fval[i] = (int32_t)i;
   }
@@ -430,14 +453,15 @@ __device__ __forceinline__ int32_t lca(const int32_t* up, int LOG, int64_t n, co
 }
 
 __global__ void k_cand_paths(const int32_t* __restrict__ Q, int64_t nq, const int32_t* __restrict__ u,
-                             const int32_t* __restrict__ v, const int32_t* __restrict__ up,
+                             const int32_t* __restrict__ v, const int32_t* __restrict__ loc,
+                             const int32_t* __restrict__ up,
                              const int32_t* __restrict__ mn, int LOG, int64_t n, const int32_t* __restrict__ enter,
                              const int32_t* __restrict__ exit_, const int32_t* __restrict__ key_inv,
                              int32_t* __restrict__ qa, int32_t* __restrict__ qb, int32_t* __restrict__ ql,
                              int32_t* __restrict__ qe) {
   GRID_STRIDE(q, nq) {
     int32_t e = Q[q];
-    int32_t a = u[e], b = v[e];
+    int32_t a = loc[u[e]], b = loc[v[e]];  // both ends lie in one tree: forest nodes
     int32_t l = lca(up, LOG, n, enter, exit_, a, b);
     int32_t m1 = climb_min(up, mn, LOG, n, enter, exit_, a, l);
     int32_t m2 = climb_min(up, mn, LOG, n, enter, exit_, b, l);
@@ -513,6 +537,17 @@ int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_
   su.alloc(1, ctx.s);
   sv.alloc(1, ctx.s);
   if (n == 0 || m == 0) return 0;
+  static const bool phase_prof = getenv("RAMA_ROUND_PROF") != nullptr;
+  double ph[8] = {0};
+  int bv_iters = 0, rs_iters = 0;
+  auto tp = std::chrono::steady_clock::now();
+  auto mark = [&](int i) {
+    if (!phase_prof) return;
+    ctx.sync();
+    auto t = std::chrono::steady_clock::now();
+    ph[i] += std::chrono::duration<double, std::milli>(t - tp).count();
+    tp = t;
+  };
   Buf<uint8_t> flag(m, ctx);
   RAMA_KERNEL(ctx, k_flag_positive, m, g.c, m, flag.p);
   Buf<int32_t> P;
@@ -525,6 +560,7 @@ int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_
   RAMA_KERNEL(ctx, k_neg_bits, np, P.p, np, g.c, k1.p, v1.p);
   radix_sort_pairs(ctx, k1.p, v1.p, k2.p, order.p, np);
   RAMA_KERNEL(ctx, k_scatter_rank, np, order.p, np, rank.p);
+  mark(0);
 
   // Boruvka
   Buf<int32_t> comp(n, ctx), any(1, ctx);
@@ -536,6 +572,7 @@ int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_
     best.fill_bytes(0xff);
     any.zero();
     RAMA_KERNEL(ctx, k_bv_vote, np, P.p, np, g.u, g.v, rank.p, comp.p, best.p, any.p);
+    bv_iters++;
     if (read_scalar(ctx, any.p) == 0) break;
     RAMA_KERNEL(ctx, k_bv_hook, n, n, best.p, order.p, P.p, g.u, g.v, comp.p, in_forest.p);
     RAMA_KERNEL(ctx, k_flatten, n, comp.p, n);
@@ -552,13 +589,22 @@ int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_
   RAMA_KERNEL(ctx, k_flag_conflicts, m, g.u, g.v, g.c, m, comp.p, cflag.p);
   Buf<int32_t> Q;
   int64_t nq = compact_indices(ctx, cflag.p, m, Q);
+  mark(1);
 
   Buf<uint8_t> removed(kf > 0 ? kf : 1, ctx);
   removed.zero();
   if (nq > 0 && kf > 0) {
+    Buf<uint8_t> isf(n, ctx);
+    isf.zero();
+    RAMA_KERNEL(ctx, k_mark_fnodes, kf, Fi.p, kf, P.p, g.u, g.v, isf.p);
+    Buf<int32_t> FN;
+    const int64_t nf = compact_indices(ctx, isf.p, n, FN);
+    Buf<int32_t> loc(n, ctx), comp_loc(nf, ctx);
+    RAMA_KERNEL(ctx, k_scatter_loc, nf, FN.p, nf, loc.p);
+    RAMA_KERNEL(ctx, k_comp_local, nf, FN.p, nf, comp.p, loc.p, comp_loc.p);
     Buf<int32_t> fu(kf, ctx), fv(kf, ctx), fval(kf, ctx), fsorted(kf, ctx), fkey(kf, ctx);
     Buf<uint64_t> fbits(kf, ctx), fbits2(kf, ctx);
-    RAMA_KERNEL(ctx, k_forest_edges, kf, Fi.p, kf, P.p, g.u, g.v, g.c, fu.p, fv.p, fbits.p, fval.p);
+    RAMA_KERNEL(ctx, k_forest_edges, kf, Fi.p, kf, P.p, g.u, g.v, loc.p, g.c, fu.p, fv.p, fbits.p, fval.p);
     radix_sort_pairs(ctx, fbits.p, fval.p, fbits2.p, fsorted.p, kf);  // key_inv: rank -> forest edge
     RAMA_KERNEL(ctx, k_scatter_rank, kf, fsorted.p, kf, fkey.p);  // fkey: forest edge -> rank
 
@@ -568,10 +614,10 @@ int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_
     Buf<uint64_t> akey(na, ctx);
     RAMA_KERNEL(ctx, k_arcs, na, fu.p, fv.p, kf, arow.p, akey.p);
     BucketSorted bs;
-    bucket_sort(ctx, n, na, arow.p, akey.p, bs, true);
+    bucket_sort(ctx, nf, na, arow.p, akey.p, bs, true);
     Buf<int32_t> pos(na, ctx), succ(na, ctx);
     RAMA_KERNEL(ctx, k_arc_pos, na, bs.src.p, na, pos.p);
-    RAMA_KERNEL(ctx, k_euler_succ, na, na, bs.src.p, pos.p, bs.row.p, bs.row_ptr.p, comp.p, succ.p);
+    RAMA_KERNEL(ctx, k_euler_succ, na, na, bs.src.p, pos.p, bs.row.p, bs.row_ptr.p, comp_loc.p, succ.p);
     Buf<int32_t> d1(na, ctx), d2(na, ctx), n1(na, ctx), n2(na, ctx);
     RAMA_KERNEL(ctx, k_rank_init, na, succ.p, na, d1.p);
     copy_d2d(ctx, n1.p, succ.p, na);
@@ -588,28 +634,30 @@ int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_
         std::swap(n1, n2);
       }
     }
-    Buf<int32_t> par(n, ctx), pedge(n, ctx), enter(n, ctx), exit_(n, ctx);
-    RAMA_KERNEL(ctx, k_root_init, n, n, par.p, pedge.p, enter.p, exit_.p);
+    Buf<int32_t> par(nf, ctx), pedge(nf, ctx), enter(nf, ctx), exit_(nf, ctx);
+    RAMA_KERNEL(ctx, k_root_init, nf, nf, par.p, pedge.p, enter.p, exit_.p);
     RAMA_KERNEL(ctx, k_orient, na, na, d1.p, fu.p, fv.p, par.p, pedge.p, enter.p, exit_.p);
+    mark(2);
 
     // binary lifting tables (depth <= kf)
     int LOG = 1;
     while ((1LL << LOG) <= kf) LOG++;
-    Buf<int32_t> up((size_t)LOG * n, ctx);
-    Buf<int32_t> mn((size_t)LOG * n, ctx);
+    Buf<int32_t> up((size_t)LOG * nf, ctx);
+    Buf<int32_t> mn((size_t)LOG * nf, ctx);
     {
-      int64_t n_ = n;
+      int64_t n_ = nf;
       int build = 1;
       int32_t *pup = up.p, *pmn = mn.p, *pnull = nullptr;
       const int32_t *ppar = par.p, *ppe = pedge.p, *pva = fkey.p, *pvnull = nullptr;
       void* args[] = {&n_, &LOG, &ppar, &ppe, &build, &pup, &pva, &pmn, &pvnull, &pnull};
-      launch_coop(ctx, (const void*)k_lift_coop, "k_lift_coop", args, n);
+      launch_coop(ctx, (const void*)k_lift_coop, "k_lift_coop", args, nf);
     }
 
     Buf<int32_t> qa(nq, ctx), qb(nq, ctx), ql(nq, ctx), qe(nq, ctx);
-    RAMA_KERNEL(ctx, k_cand_paths, nq, Q.p, nq, g.u, g.v, up.p, mn.p, LOG, n, enter.p, exit_.p, fsorted.p, qa.p,
-                qb.p, ql.p, qe.p);
+    RAMA_KERNEL(ctx, k_cand_paths, nq, Q.p, nq, g.u, g.v, loc.p, up.p, mn.p, LOG, nf, enter.p, exit_.p, fsorted.p,
+                qa.p, qb.p, ql.p, qe.p);
     mn.release();
+    mark(3);
 
     Buf<uint8_t> state(nq, ctx);
     state.zero();
@@ -618,22 +666,28 @@ int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_
       RAMA_KERNEL(ctx, k_fill_i32, kf, rf.p, kf, 0x7fffffff);
       RAMA_KERNEL(ctx, k_fill_i32, kf, ru.p, kf, 0x7fffffff);
       RAMA_KERNEL(ctx, k_earliest, nq, qe.p, state.p, nq, rf.p, ru.p);
-      mf.alloc((size_t)LOG * n, ctx.s);
-      mu.alloc((size_t)LOG * n, ctx.s);
+      mf.alloc((size_t)LOG * nf, ctx.s);
+      mu.alloc((size_t)LOG * nf, ctx.s);
       {
-        int64_t n_ = n;
+        int64_t n_ = nf;
         int build = 0;
         int32_t *pup = up.p, *pmf = mf.p, *pmu = mu.p;
         const int32_t *ppar = par.p, *ppe = pedge.p, *prf = rf.p, *pru = ru.p;
         void* args[] = {&n_, &LOG, &ppar, &ppe, &build, &pup, &prf, &pmf, &pru, &pmu};
-        launch_coop(ctx, (const void*)k_lift_coop, "k_lift_coop", args, n);
+        launch_coop(ctx, (const void*)k_lift_coop, "k_lift_coop", args, nf);
       }
       left.zero();
-      RAMA_KERNEL(ctx, k_resolve, nq, nq, qa.p, qb.p, ql.p, up.p, mf.p, mu.p, LOG, n, enter.p, exit_.p, state.p,
+      RAMA_KERNEL(ctx, k_resolve, nq, nq, qa.p, qb.p, ql.p, up.p, mf.p, mu.p, LOG, nf, enter.p, exit_.p, state.p,
                   left.p);
+      rs_iters++;
       if (read_scalar(ctx, left.p) == 0) break;
     }
     RAMA_KERNEL(ctx, k_mark_removed, nq, qe.p, state.p, nq, removed.p);
+    mark(4);
+    if (phase_prof)
+      fprintf(stderr, "[rama]   forest n %lld m+ %lld kf %lld conflicts %lld LOG %d: rank sort %.2f boruvka %.2f (%d) "
+              "euler %.2f lift+paths %.2f resolve %.2f (%d) ms\n", (long long)n, (long long)np, (long long)kf,
+              (long long)nq, LOG, ph[0], ph[1], bv_iters, ph[2], ph[3], ph[4], rs_iters);
   }
   RAMA_KERNEL(ctx, k_forest_keep, kf, Fi.p, kf, removed.p, keep.p);
   Buf<int32_t> idx;

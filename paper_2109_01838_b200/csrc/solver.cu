@@ -125,17 +125,36 @@ void solve(Ctx& ctx, const GraphView& g, const SolveConfig& cfg, int32_t* labels
     double lb_r = nan;
     StepResult step;
     if (dual) {
+      // RAMA_ROUND_PROF=1: per-phase wall time of every round (synchronizes between phases)
+      static const bool phase_prof = getenv("RAMA_ROUND_PROF") != nullptr;
+      double ph[6] = {0};
+      auto tp = clk::now();
+      auto mark = [&](int i) {
+        if (!phase_prof) return;
+        ctx.sync();
+        ph[i] = ms_since(tp);
+        tp = clk::now();
+      };
       CycleRows cyc;
       separate(ctx, cur.view(), cfg.max_cycle_length, cyc);
+      mark(0);
       DualState st;
       triangulate(ctx, cur.view(), cyc, st);
+      mark(1);
       message_passing(ctx, st, cfg.mp_iterations);
       Buf<double> cl(st.m_aug > 0 ? st.m_aug : 1, ctx);
       lb_r = lower_bound(ctx, st, cl.p);  // c^lambda computed once for the bound and the graph
       T = st.T;
       if (rnd == 1) lb = lb_r;
+      mark(2);
       Graph rep = reparametrized_graph(ctx, st, cl.p);
+      mark(3);
       contraction_step(ctx, rep.view(), 3, cfg.switch_fraction, step);
+      mark(4);
+      if (phase_prof)
+        fprintf(stderr, "[rama] round %d n %lld m %lld T %lld: separate %.2f triangulate %.2f mp+lb %.2f "
+                "reparam %.2f contraction %.2f ms%s\n", rnd, (long long)cur.n, (long long)cur.m, (long long)st.T,
+                ph[0], ph[1], ph[2], ph[3], ph[4], step.used_forest ? " (forest)" : "");
     } else {
       contraction_step(ctx, cur.view(), 3, cfg.switch_fraction, step);
     }
