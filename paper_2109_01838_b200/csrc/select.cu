@@ -252,6 +252,13 @@ __global__ void k_comp_local(const int32_t* __restrict__ FN, int64_t nf, const i
   GRID_STRIDE(i, nf) comp_loc[i] = loc[comp[FN[i]]];  // a tree's root (its smallest node) is a forest node
 }
 
+// largest tree (node count): bounds the depth, so the lifting tables need
+// log2(largest tree) levels instead of log2(forest size)
+__global__ void k_tree_sizes(const int32_t* __restrict__ comp_loc, int64_t nf, int32_t* __restrict__ sz,
+                             int32_t* __restrict__ maxsz) {
+  GRID_STRIDE(i, nf) atomicMax(maxsz, atomicAdd(sz + comp_loc[i], 1) + 1);
+}
+
 __global__ void k_forest_edges(const int32_t* __restrict__ Fi, int64_t kf, const int32_t* __restrict__ P,
                                const int32_t* __restrict__ u, const int32_t* __restrict__ v,
                                const int32_t* __restrict__ loc, const double* __restrict__ c,
@@ -639,9 +646,16 @@ int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_
     RAMA_KERNEL(ctx, k_orient, na, na, d1.p, fu.p, fv.p, par.p, pedge.p, enter.p, exit_.p);
     mark(2);
 
-    // binary lifting tables (depth <= kf)
+    // binary lifting tables (depth < largest tree)
+    int64_t maxdepth = kf;
+    {
+      Buf<int32_t> sz(nf + 1, ctx);
+      sz.zero();
+      RAMA_KERNEL(ctx, k_tree_sizes, nf, comp_loc.p, nf, sz.p, sz.p + nf);
+      maxdepth = (int64_t)read_scalar(ctx, sz.p + nf) - 1;
+    }
     int LOG = 1;
-    while ((1LL << LOG) <= kf) LOG++;
+    while ((1LL << LOG) <= maxdepth) LOG++;
     Buf<int32_t> up((size_t)LOG * nf, ctx);
     Buf<int32_t> mn((size_t)LOG * nf, ctx);
     {
