@@ -609,6 +609,14 @@ int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_
     Buf<int32_t> loc(n, ctx), comp_loc(nf, ctx);
     RAMA_KERNEL(ctx, k_scatter_loc, nf, FN.p, nf, loc.p);
     RAMA_KERNEL(ctx, k_comp_local, nf, FN.p, nf, comp.p, loc.p, comp_loc.p);
+    int64_t maxsz = nf;  // largest tree: bounds tour lengths and depths
+    {
+      Buf<int32_t> sz(nf + 1, ctx);
+      sz.zero();
+      RAMA_KERNEL(ctx, k_tree_sizes, nf, comp_loc.p, nf, sz.p, sz.p + nf);
+      maxsz = (int64_t)read_scalar(ctx, sz.p + nf);
+    }
+    const int64_t maxdepth = maxsz - 1;
     Buf<int32_t> fu(kf, ctx), fv(kf, ctx), fval(kf, ctx), fsorted(kf, ctx), fkey(kf, ctx);
     Buf<uint64_t> fbits(kf, ctx), fbits2(kf, ctx);
     RAMA_KERNEL(ctx, k_forest_edges, kf, Fi.p, kf, P.p, g.u, g.v, loc.p, g.c, fu.p, fv.p, fbits.p, fval.p);
@@ -628,8 +636,8 @@ int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_
     Buf<int32_t> d1(na, ctx), d2(na, ctx), n1(na, ctx), n2(na, ctx);
     RAMA_KERNEL(ctx, k_rank_init, na, succ.p, na, d1.p);
     copy_d2d(ctx, n1.p, succ.p, na);
-    int steps = 0;
-    while ((1LL << steps) < na) steps++;
+    int steps = 0;  // pointer jumping over the longest tour (2 (|T| - 1) arcs)
+    while ((1LL << steps) < 2 * maxsz) steps++;
     steps += 1;
     {
       int64_t na_ = na;
@@ -647,13 +655,6 @@ int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_
     mark(2);
 
     // binary lifting tables (depth < largest tree)
-    int64_t maxdepth = kf;
-    {
-      Buf<int32_t> sz(nf + 1, ctx);
-      sz.zero();
-      RAMA_KERNEL(ctx, k_tree_sizes, nf, comp_loc.p, nf, sz.p, sz.p + nf);
-      maxdepth = (int64_t)read_scalar(ctx, sz.p + nf) - 1;
-    }
     int LOG = 1;
     while ((1LL << LOG) <= maxdepth) LOG++;
     Buf<int32_t> up((size_t)LOG * nf, ctx);
