@@ -91,12 +91,6 @@ struct alignas(32) Group {  // one sector per group
   __host__ __device__ static Group empty() { return Group{~0ULL, 0, 0x7fffffff, -1, -1, {0, 0}}; }
 };
 
-struct alignas(16) EdgeEnt {
-  unsigned long long key;
-  int32_t slot;
-  int32_t pad;
-};
-
 struct Args {
   int32_t* u;
   int32_t* v;
@@ -121,13 +115,14 @@ struct Args {
   int32_t* R;              // rewritten slots of the round
   int32_t* Rg;             // their group (hash position), -1: became internal
   int32_t* Rnext;          // group member list (R indices, linked)
-  Group* grp;              // group hash table (capacity hmask + 1), clean between rounds
-  uint32_t hmask;
-  EdgeEnt* eh;             // edge hash: every alive slot under its current key (stale entries
+  Group* grp;              // group hash table (capacity hmask + 1), clean between rounds; a round
+  uint32_t hmask;          //   uses only its first 2 |R| entries or so, which stay in L2
+  int32_t* eh;             // edge hash of slot ids: every alive slot under its current key (stale entries
                            //   of dead or re-keyed slots stay and are skipped)
   uint32_t emask;
   int32_t* sc;             // device scalars, SC_*
   long long* trace;        // RAMA_CLEANUP_STATS=2: per round {np, npairs, nt, asum, rrep, t_ns}
+  long long* ptrace;       // RAMA_CLEANUP_STATS=3: per round, the end time of each of the 5 phases
   int32_t trace_cap;
 };
 
@@ -150,29 +145,28 @@ __device__ __forceinline__ int32_t owner_of(const int32_t* pref, int32_t n, int3
   return lo;
 }
 
+// the group table positions a round uses: 2 |R| rounded up (|R| <= asum)
+__device__ __forceinline__ uint32_t round_mask(int32_t asum, uint32_t hmask) {
+  uint32_t m = 4095;
+  while ((int64_t)m + 1 < 2 * (int64_t)asum && m < hmask) m = 2 * m + 1;
+  return m < hmask ? m : hmask;
+}
+
 // group position of key k, inserting it
-__device__ __forceinline__ int32_t h_insert(const Args& A, uint64_t k) {
-  uint32_t h = key_hash(k) & A.hmask;
+__device__ __forceinline__ int32_t h_insert(const Args& A, uint64_t k, uint32_t mask) {
+  uint32_t h = key_hash(k) & mask;
   while (true) {
     unsigned long long old = atomicCAS((unsigned long long*)&A.grp[h].key, (unsigned long long)kEmpty,
                                        (unsigned long long)k);
     if (old == kEmpty || old == k) return (int32_t)h;
-    h = (h + 1) & A.hmask;
+    h = (h + 1) & mask;
   }
 }
 
-// edge hash: a new entry (duplicates of a key are allowed; readers validate)
+// edge hash: a new entry (entries of dead or re-keyed slots stay; readers validate)
 __device__ __forceinline__ void e_insert(const Args& A, uint64_t k, int32_t s) {
   uint32_t h = key_hash(k) & A.emask;
-  while (true) {
-    unsigned long long old = atomicCAS((unsigned long long*)&A.eh[h].key, (unsigned long long)kEmpty,
-                                       (unsigned long long)k);
-    if (old == kEmpty) {
-      A.eh[h].slot = s;
-      return;
-    }
-    h = (h + 1) & A.emask;
-  }
+  while (atomicCAS(A.eh + h, -1, s) != -1) h = (h + 1) & A.emask;
 }
 
 // the alive slot outside R whose current key is k, or -1 (at most one: alive
@@ -180,12 +174,9 @@ __device__ __forceinline__ void e_insert(const Args& A, uint64_t k, int32_t s) {
 __device__ __forceinline__ int32_t e_find(const Args& A, uint64_t k) {
   uint32_t h = key_hash(k) & A.emask;
   while (true) {
-    uint64_t x = LD(&A.eh[h].key);
-    if (x == kEmpty) return -1;
-    if (x == k) {
-      int32_t s = LD(&A.eh[h].slot);
-      if (LD(A.alive + s) && !(LD(A.tmark + s) & 1) && pair_key(LD(A.u + s), LD(A.v + s)) == k) return s;
-    }
+    int32_t s = LD(A.eh + h);
+    if (s < 0) return -1;
+    if (pair_key(LD(A.u + s), LD(A.v + s)) == k && LD(A.alive + s) && !(LD(A.tmark + s) & 1)) return s;
     h = (h + 1) & A.emask;
   }
 }
@@ -224,6 +215,16 @@ __device__ __forceinline__ void vote_max(ulonglong2* p, unsigned long long hi, u
 __device__ __forceinline__ unsigned long long vote_lo(int32_t minid_y) {
   return (unsigned long long)(0xffffffffu - (uint32_t)minid_y);
 }
+
+// RAMA_CLEANUP_STATS=3: the time each phase of each round ends
+#define PHASE_MARK(k)                                                                        \
+  do {                                                                                       \
+    if (A.ptrace && gtid == 0 && round0 + rounds < A.trace_cap) {                            \
+      unsigned long long tns_;                                                               \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tns_));                             \
+      A.ptrace[5 * (int64_t)(round0 + rounds) + (k)] = (long long)tns_;                      \
+    }                                                                                        \
+  } while (0)
 
 __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
   namespace cg = cooperative_groups;
@@ -265,6 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
       vote_max(A.vote + b, bits, vote_lo(LD(A.minid + a)));
     }
     grid.sync();
+    PHASE_MARK(0);
     // ---- 2. mutual pairs: the slot is both ends' vote.  One packed atomic
     // per warp gives each pair its index and the offset of its absorbed row.
     if (gtid == 0) {
@@ -285,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
         ulonglong2 va = __ldcg(A.vote + a), vb = __ldcg(A.vote + b);
         if (va.y == bits && va.x == vote_lo(mb) && vb.y == bits && vb.x == vote_lo(ma)) {
           found = true;
-          r = rep_first(LD(A.size + a), ma, LD(A.size + b), mb) ? a : b;
+          r = rep_first(LD(A.row_len + a), ma, LD(A.row_len + b), mb) ? a : b;  // the longer row stays
           t = r == a ? b : a;
           len = LD(A.row_len + t);
           rlen = LD(A.row_len + r);
@@ -317,6 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
       }
     }
     grid.sync();
+    PHASE_MARK(1);
     const unsigned long long pk = LD(A.pk + q);
     const int32_t npairs = (int32_t)(pk >> 32), asum = (int32_t)(uint32_t)pk;
     const int32_t rrep = LD(sc + SC_RREP + q);
@@ -384,12 +387,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
         off = __shfl_sync(0xffffffffu, off, 0);
         const int32_t old = LD(A.row_off + r), len = LD(A.row_len + r);
         int32_t cnt = 0;
-        for (int32_t e0 = 0; e0 < len; e0 += 32) {
-          int32_t s = e0 + lane < len ? LD(A.pool + old + e0 + lane) : -1;
-          bool keep = s >= 0 && LD(A.alive + s);
-          unsigned bal = __ballot_sync(0xffffffffu, keep);
-          if (keep) A.pool[off + cnt + __popc(bal & lanes_below())] = s;
-          cnt += __popc(bal);
+        for (int32_t e0 = 0; e0 < len; e0 += 128) {  // four independent loads per lane in flight
+          int32_t sl[4];
+          bool keep[4];
+#pragma unroll
+          for (int j = 0; j < 4; j++) {
+            int32_t e = e0 + 32 * j + lane;
+            sl[j] = e < len ? LD(A.pool + old + e) : -1;
+          }
+#pragma unroll
+          for (int j = 0; j < 4; j++) keep[j] = sl[j] >= 0 && LD(A.alive + sl[j]);
+#pragma unroll
+          for (int j = 0; j < 4; j++) {
+            unsigned bal = __ballot_sync(0xffffffffu, keep[j]);
+            if (keep[j]) A.pool[off + cnt + __popc(bal & lanes_below())] = sl[j];
+            cnt += __popc(bal);
+          }
         }
         if (lane == 0) {
           A.row_off[r] = off;
@@ -421,7 +434,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
       __syncthreads();
     }
     grid.sync();
+    PHASE_MARK(2);
     const int32_t nt = LD(sc + SC_RNT + q);
+    const uint32_t gmask = round_mask(asum, A.hmask);
     if (gtid == 0 && A.trace && round0 + rounds < A.trace_cap) {
       unsigned long long tns;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tns));
@@ -446,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
         A.v[s] = hi;
         A.tmark[s] = 1 | ((lo == x || lo == y) ? 2 : 0) | ((hi == x || hi == y) ? 4 : 0);
         uint64_t key = pair_key(lo, hi);
-        int32_t g = h_insert(A, key);
+        int32_t g = h_insert(A, key, gmask);
         A.Rg[i] = g;
         atomicAdd(&A.grp[g].cnt, 1);
         atomicMin(&A.grp[g].head, s);
@@ -462,6 +477,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
       A.minid[x] = min(LD(A.minid + x), LD(A.minid + t));
     }
     grid.sync();
+    PHASE_MARK(3);
     // ---- 5. fold each group (R members + the outside slot) into its smallest
     // slot, sequential sum in slot order; survivors enter the next P when
     // positive and their new representatives' rows; untouched positive slots
@@ -540,6 +556,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
       if (keep) P2[at] = s;
     }
     grid.sync();
+    PHASE_MARK(4);
     np = LD(sc + SC_RNP2 + q);
     prev_base = base;
     base += npairs;
@@ -640,7 +657,7 @@ int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc) {
   Buf<Group> grp;
   uint32_t ecap = 4096;
   while ((int64_t)ecap < 4 * m && ecap < (1u << 30)) ecap <<= 1;
-  Buf<EdgeEnt> eh;
+  Buf<int32_t> eh;
   int64_t grow = 1;  // doubles when a launch could not run a single round
   Buf<int32_t> sc(SC_COUNT, ctx);
   static int grid_blocks = 0;
@@ -658,6 +675,8 @@ int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc) {
   const bool round_trace = stats_env && atoi(stats_env) >= 2;
   constexpr int32_t kTraceCap = 4096;
   Buf<long long> trace(round_trace ? 6 * kTraceCap : 1, ctx);
+  const bool phase_trace = stats_env && atoi(stats_env) >= 3;
+  Buf<long long> ptrace(phase_trace ? 5 * kTraceCap : 1, ctx);
   Args A;
   A.u = u.p; A.v = v.p; A.c = c.p; A.alive = alive.p; A.tmark = tmark.p; A.vote = vote.p;
   A.rp = rp.p; A.minid = minid.p; A.size = size.p; A.P0 = P0.p; A.P1 = P1.p;
@@ -665,6 +684,7 @@ int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc) {
   A.R = R.p; A.Rg = Rg.p; A.Rnext = Rnext.p;
   A.sc = sc.p;
   A.trace = round_trace ? trace.p : nullptr;
+  A.ptrace = phase_trace ? ptrace.p : nullptr;
   A.trace_cap = kTraceCap;
   while (true) {
     // P, the rows and the edge hash, from the current slots
@@ -728,6 +748,16 @@ int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc) {
         long long prev = r > k0 ? h[6 * (size_t)(r - 1) + 5] : e[5];
         fprintf(stderr, "[rama] cl launch %d round %d np %lld pairs %lld nt %lld asum %lld rrep %lld dt_us %.1f\n",
                 launches, r, e[0], e[1], e[2], e[3], e[4], (e[5] - prev) / 1e3);
+      }
+      if (phase_trace && k1 > k0) {
+        std::vector<long long> q(5 * (size_t)k1);
+        RAMA_CUDA(cudaMemcpy(q.data(), ptrace.p, q.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+        for (int32_t r = k0 + 1; r < k1; r++) {
+          const long long* e = &q[5 * (size_t)r];
+          fprintf(stderr, "[rama] cl phases round %d np %lld: %.1f %.1f %.1f %.1f %.1f us\n", r, h[6 * (size_t)r],
+                  (e[0] - q[5 * (size_t)(r - 1) + 4]) / 1e3, (e[1] - e[0]) / 1e3, (e[2] - e[1]) / 1e3,
+                  (e[3] - e[2]) / 1e3, (e[4] - e[3]) / 1e3);
+        }
       }
     }
     const bool progress = st[SC_ROUNDS] > rounds;
