@@ -15,10 +15,11 @@
 // Execution: ONE cooperative persistent kernel (one CTA per SM, grid.sync()
 // between phases) runs round after round with no host round trip.  State:
 //   * edge slots (u, v, c, alive) over INTERNAL cluster ids.  A pair's
-//     internal representative is the larger cluster (member count, ties by
-//     canonical id), so only the smaller side's edges are rewritten
-//     (union-by-size: O(m log n) rewrites even when one cluster absorbs a
-//     neighbour per round for hundreds of rounds, as on 3-D grids);
+//     internal representative is the cluster with the longer incidence row
+//     (ties by canonical id), so only the shorter row is rewritten -- cheap
+//     even when one cluster absorbs a neighbour per round for hundreds of
+//     rounds, as on 3-D grids.  Internal ids never reach the results: every
+//     tie-break compares canonical ids;
 //   * P, the alive positive slots (the only ones that vote);
 //   * per-cluster incidence rows in a bump-allocated pool (lazy: dead slots
 //     stay until the row is reallocated; rows grow by doubling);
