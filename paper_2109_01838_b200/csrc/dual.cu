@@ -340,16 +340,21 @@ __global__ void k_sep5(const int32_t* __restrict__ Q, int64_t nq, const int32_t*
 // grid-like neighbourhoods; the sources it cannot hold go to tier 2 (a warp
 // per source, 4x the L1, 16x the L2 table); what overflows tier 2 (hubs)
 // is flagged for the row-intersection kernels above.
-template <int G, int NL1, int HBITS, int BUILD>
+// A group answers its source's edges one after another, so sources with
+// very many repulsive edges (power-law hubs' neighbours) would serialize a
+// whole launch behind one group: tier 2 passes those to the per-edge kernels.
+template <int G, int NL1, int HBITS, int BUILD, int EDGES, bool ABORT>
 struct SrcTier {
+  static constexpr bool kAbort = ABORT;       // shared L2 counter: stop building on overflow
   static constexpr int kGrp = G;              // lanes per source
   static constexpr int kL1 = NL1;             // |N+(a)| capacity
   static constexpr int kHashBits = HBITS;
   static constexpr int kHash = 1 << HBITS;    // per-source L2 table; used at load <= 1/2
   static constexpr int kBuild = BUILD;        // max sum of |N+(x)| over x in N+(a)
+  static constexpr int kEdges = EDGES;        // max repulsive edges of the source
 };
-using SrcTier1 = SrcTier<8, 32, 6, 256>;
-using SrcTier2 = SrcTier<32, 128, 10, 4096>;
+using SrcTier1 = SrcTier<8, 32, 6, 256, 1 << 30, false>;
+using SrcTier2 = SrcTier<32, 128, 10, 1024, 64, true>;
 constexpr int kSrcThreads1 = 256, kSrcThreads2 = 128;
 
 template <int HBITS>
@@ -446,6 +451,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sep_src(
   __shared__ int32_t s_l1[kPer][T::kL1];
   __shared__ int32_t s_hk[kPer][kH];
   __shared__ int32_t s_hv[kPer][kH];
+  __shared__ int32_t s_fill[kPer];
   const int gi = threadIdx.x / kGrp, lane = threadIdx.x % kGrp;
   const unsigned mask = kGrp == 32 ? 0xffffffffu : ((1u << kGrp) - 1u) << ((threadIdx.x & 31) & ~(kGrp - 1));
   int32_t* l1 = s_l1[gi];
@@ -457,7 +463,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sep_src(
     const int32_t e0 = gstart[k], e1 = k + 1 < ng ? gstart[k + 1] : (int32_t)n2;
     const int32_t a = gsrc[k];
     const int32_t pa = ptr[a], la = ptr[a + 1] - pa;
-    bool over = la > T::kL1 || force_fallback;
+    bool over = la > T::kL1 || e1 - e0 > T::kEdges || force_fallback;
     Bloom128 f1, f2;  // L1 and L2 members
     __syncwarp(mask);  // the previous source's lookups are done before the table is reset
     if (!over) {
@@ -471,6 +477,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sep_src(
         hk[t] = -1;
         hv[t] = 0x7fffffff;
       }
+      if (T::kAbort && lane == 0) s_fill[gi] = 0;
       __syncwarp(mask);
       // each lane walks whole rows N+(x) for its x positions (independent load chains)
       int32_t work = 0;
@@ -481,28 +488,57 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sep_src(
       work = grp_sum_i32<kGrp>(work, mask);
       over = work > T::kBuild;
       if (!over) {
-        int32_t mine = 0;
-        for (int32_t xi = lane; xi < la; xi += kGrp) {
-          const int32_t x = l1[xi];
-          const int32_t px = ptr[x], lx = ptr[x + 1] - px;
-          for (int32_t t = 0; t < lx; t++) {
-            const int32_t y = adj[px + t];
-            if (y == a || (f1.maybe(y) && src_in_l1(l1, la, y))) continue;
-            int32_t h = src_slot<T::kHashBits>(y);
-            for (int r = 0; r < kH; r++) {
-              int32_t kk = atomicCAS(hk + h, -1, y);
-              if (kk == -1 || kk == y) {
-                mine += kk == -1;
-                f2.add(y);
-                atomicMin(hv + h, xi);  // BFS parent = smallest position reaching y
-                break;
+        if (T::kAbort) {
+          // tier 2: the group's L2 count is shared, so a source whose L2
+          // outgrows the table stops building at once instead of finishing
+          // its rows (power-law neighbourhoods)
+          volatile int32_t* fill = s_fill + gi;
+          for (int32_t xi = lane; xi < la && *fill <= kH / 2; xi += kGrp) {
+            const int32_t x = l1[xi];
+            const int32_t px = ptr[x], lx = ptr[x + 1] - px;
+            for (int32_t t = 0; t < lx; t++) {
+              const int32_t y = adj[px + t];
+              if (y == a || (f1.maybe(y) && src_in_l1(l1, la, y))) continue;
+              int32_t h = src_slot<T::kHashBits>(y);
+              for (int r = 0; r < kH; r++) {
+                int32_t kk = atomicCAS(hk + h, -1, y);
+                if (kk == -1 || kk == y) {
+                  if (kk == -1) atomicAdd(s_fill + gi, 1);
+                  f2.add(y);
+                  atomicMin(hv + h, xi);  // BFS parent = smallest position reaching y
+                  break;
+                }
+                h = (h + 1) & (kH - 1);
               }
-              h = (h + 1) & (kH - 1);
+              if (*fill > kH / 2) break;
             }
           }
+          __syncwarp(mask);
+          over = *fill > kH / 2;
+        } else {
+          int32_t mine = 0;
+          for (int32_t xi = lane; xi < la; xi += kGrp) {
+            const int32_t x = l1[xi];
+            const int32_t px = ptr[x], lx = ptr[x + 1] - px;
+            for (int32_t t = 0; t < lx; t++) {
+              const int32_t y = adj[px + t];
+              if (y == a || (f1.maybe(y) && src_in_l1(l1, la, y))) continue;
+              int32_t h = src_slot<T::kHashBits>(y);
+              for (int r = 0; r < kH; r++) {
+                int32_t kk = atomicCAS(hk + h, -1, y);
+                if (kk == -1 || kk == y) {
+                  mine += kk == -1;
+                  f2.add(y);
+                  atomicMin(hv + h, xi);  // BFS parent = smallest position reaching y
+                  break;
+                }
+                h = (h + 1) & (kH - 1);
+              }
+            }
+          }
+          mine = grp_sum_i32<kGrp>(mine, mask);
+          over = mine > kH / 2;
         }
-        mine = grp_sum_i32<kGrp>(mine, mask);
-        over = mine > kH / 2;
         f2.group_or<kGrp>(mask);
       }
       __syncwarp(mask);  // table complete before the lookups

@@ -13,6 +13,10 @@ g = P.WeightedGraph(*instances.grid8_coo(20, 24, strides=(2, 3), seed=3))
 print("8conn", P.solve(g, P.SolverConfig(mode="PD")).primal_cost)
 g = P.WeightedGraph(*instances.chung_lu_coo(600, 2.1, 9000, seed=1))
 print("chunglu", P.solve(g, P.SolverConfig(mode="PD")).primal_cost)
+g = P.WeightedGraph(*instances.random_coo(160, 0.35, seed=4))  # dense: tier-2 separation tables
+print("dense", P.solve(g, P.SolverConfig(mode="PD")).primal_cost)
+g = P.WeightedGraph(*instances.grid3d_coo(8, 12, 12, stride=2, seed=2))
+print("3d", P.solve(g, P.SolverConfig(mode="PD")).primal_cost)
 gs = [P.WeightedGraph(*instances.grid_coo(16, 16, 0, seed=s)) for s in range(4)]
 print("batch", [s.primal_cost for s in P.solve_batch(gs, P.SolverConfig(mode="PD"), workers=2)])
 n, u, v, c = instances.random_coo(40, 0.3, seed=5)
