@@ -218,7 +218,30 @@ __global__ void k_sep4(const int32_t* __restrict__ Q, int64_t nq, const int32_t*
       lb = ptr[b + 1] - pb;
     }
     bool done = !live;
-    const int32_t la_max = warp_max(la);
+    // hub sources (|N(a)| >> |N(b)|): the same answer from b's side,
+    // argmin over y in N(b) of (px(y), y), one level-2 test per y
+    const bool bside = live && la > 4 * lb;
+    const int32_t lb_max = warp_max(bside ? lb : 0);
+    if (lb_max > 0) {
+      uint64_t bb = ~0ULL;
+      for (int32_t k0 = 0; k0 < lb_max; k0 += kSepLanes) {
+        const int32_t k = k0 + g;
+        if (bside && k < lb) {
+          const int32_t y = adj[pb + k];
+          const int32_t p = level2_parent(ptr, adj, a, Na, la, y);
+          if (p >= 0) {
+            const uint64_t key = pack2(p, y);
+            bb = key < bb ? key : bb;
+          }
+        }
+      }
+      bb = group_min(bb);
+      if (bside) {
+        best = bb;
+        done = true;
+      }
+    }
+    const int32_t la_max = warp_max(done ? 0 : la);
     for (int32_t xi = 0; xi < la_max; xi++) {
       int32_t cand = 0x7fffffff, x = 0;
       if (!done && xi < la) {
