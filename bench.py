@@ -287,9 +287,10 @@ def b200_arm(args):
         hu = torch.from_numpy(g.edges_u.astype(np.int32)).pin_memory().numpy()
         hv = torch.from_numpy(g.edges_v.astype(np.int32)).pin_memory().numpy()
         hc = torch.from_numpy(g.costs.astype(np.float64)).pin_memory().numpy()
+        hlab = torch.empty(max(n, 1), dtype=torch.int32).pin_memory().numpy()
 
         def e2e_step():  # rama_solve_host: H2D + solve + D2H inside the C ABI call
-            P.solve_host(n, hu, hv, hc, cfg)
+            P.solve_host(n, hu, hv, hc, cfg, labels=hlab)
 
         e2e_h2d, e2e_d2h = int(m * (4 + 4 + 8)), int(n * 4 + 16)
         job = {"instances_per_step": world, "seed": "rank"}

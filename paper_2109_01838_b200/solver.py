@@ -133,13 +133,17 @@ def solve(g, cfg):
     return Solution(L.host_i64(labels, n), primal, lb, trace)
 
 
-def solve_host(n, u, v, c, cfg):
-    """Host-buffer entry (``rama_solve_host``): numpy canonical COO in, numpy labels out."""
+def solve_host(n, u, v, c, cfg, labels=None):
+    """Host-buffer entry (``rama_solve_host``): numpy canonical COO in, numpy labels out.
+    ``labels``: optional int32 output array of >= max(n, 1) entries (e.g. pinned memory)."""
     cfg.validate()
     u = np.ascontiguousarray(u, dtype=np.int32)
     v = np.ascontiguousarray(v, dtype=np.int32)
     c = np.ascontiguousarray(c, dtype=np.float64)
-    labels = np.empty(max(n, 1), dtype=np.int32)
+    if labels is None:
+        labels = np.empty(max(n, 1), dtype=np.int32)
+    elif labels.dtype != np.int32 or labels.size < max(n, 1) or not labels.flags.c_contiguous:
+        raise ValueError("labels must be a contiguous int32 array of at least max(n, 1) entries")
     k = _max_trace(cfg, n)
     trace = (L.RamaRound * k)()
     out = (L.ctypes.c_double * 2)()
