@@ -661,15 +661,17 @@ int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc) {
   Buf<int32_t> eh;
   int64_t grow = 1;  // doubles when a launch could not run a single round
   Buf<int32_t> sc(SC_COUNT, ctx);
-  static int grid_blocks = 0;
-  if (!grid_blocks) {
+  static const int max_blocks = [] {  // at most one CTA per SM (thread-safe init: batch workers)
     int dev = 0, sms = 0, per_sm = 0;
     RAMA_CUDA(cudaGetDevice(&dev));
     RAMA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     RAMA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cl_rounds, kThreads, 0));
     RAMA_REQUIRE(per_sm >= 1, "cleanup kernel cannot be resident");
-    grid_blocks = sms;  // one CTA per SM
-  }
+    return sms;
+  }();
+  // sized by the quotient: a small cleanup (batch instances) leaves the
+  // other SMs to concurrent solves instead of claiming the whole GPU
+  const int grid_blocks = (int)std::min<int64_t>(max_blocks, std::max<int64_t>(8, (m + 8191) / 8192));
   int64_t total = 0;
   int launches = 0, rounds = 0;
   const char* stats_env = getenv("RAMA_CLEANUP_STATS");
