@@ -35,6 +35,7 @@
 // the next round's phase 1.  The host only rebuilds P, the rows and the
 // edge hash when the pool or the hash runs out.
 #include "internal.h"
+#include "compact.cuh"
 
 #include <cooperative_groups.h>
 
@@ -603,11 +604,6 @@ __global__ void k_cl_fill_rows(const int32_t* __restrict__ u, const int32_t* __r
   }
 }
 
-__global__ void k_cl_posflag(const double* __restrict__ c, const uint8_t* __restrict__ alive, int64_t m,
-                             uint8_t* __restrict__ f) {
-  GRID_STRIDE(i, m) f[i] = alive[i] && c[i] > 0.0;
-}
-
 __global__ void k_cl_ehash_build(const int32_t* __restrict__ u, const int32_t* __restrict__ v,
                                  const uint8_t* __restrict__ alive, int64_t m, Args A) {
   GRID_STRIDE(i, m) {
@@ -691,10 +687,8 @@ int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc) {
   A.trace_cap = kTraceCap;
   while (true) {
     // P, the rows and the edge hash, from the current slots
-    Buf<uint8_t> pf(m, ctx);
-    RAMA_KERNEL(ctx, k_cl_posflag, m, c.p, alive.p, m, pf.p);
     Buf<int32_t> Pl;
-    int64_t np = compact_indices(ctx, pf.p, m, Pl);
+    int64_t np = compact_if(ctx, m, PosAlive{c.p, alive.p}, Pl);
     if (np == 0) break;
     copy_d2d(ctx, P0.p, Pl.p, np);
     Buf<int32_t> deg(n, ctx), rcap(n, ctx), off(n + 1, ctx), cur(n, ctx);

@@ -22,14 +22,11 @@
 // All arithmetic is explicitly rounded (__dadd_rn/__dmul_rn/__ddiv_rn), so
 // nvcc cannot contract into FMAs and lam is bit-identical to numpy's.
 #include "internal.h"
+#include "compact.cuh"
 
 namespace rama {
 
 // ---------------------------------------------------------------- CSR
-
-__global__ void k_pos_flag(const double* __restrict__ c, int64_t m, uint8_t* __restrict__ f) {
-  GRID_STRIDE(i, m) f[i] = c[i] > 0.0;
-}
 
 __global__ void k_pos_arcs(const int32_t* __restrict__ P, int64_t np, const int32_t* __restrict__ u,
                            const int32_t* __restrict__ v, int32_t* __restrict__ row, uint64_t* __restrict__ key) {
@@ -54,10 +51,8 @@ struct PosCSR {
 
 // _positive_csr (dual.py:155-166): symmetric CSR of E+ sorted by (head, tail)
 static void positive_csr(Ctx& ctx, const GraphView& g, PosCSR& out) {
-  Buf<uint8_t> flag(g.m > 0 ? g.m : 1, ctx);
-  RAMA_KERNEL(ctx, k_pos_flag, g.m, g.c, g.m, flag.p);
   Buf<int32_t> P;
-  int64_t np = compact_indices(ctx, flag.p, g.m, P);
+  int64_t np = compact_if(ctx, g.m, PosCost{g.c}, P);
   int64_t na = 2 * np;
   Buf<int32_t> row(na > 0 ? na : 1, ctx);
   Buf<uint64_t> key(na > 0 ? na : 1, ctx);
@@ -110,10 +105,6 @@ __device__ __forceinline__ int32_t first_common(const int32_t* a, int32_t la, co
     if (x < y) i++; else j++;
   }
   return -1;
-}
-
-__global__ void k_flag_neg(const double* __restrict__ c, int64_t m, uint8_t* __restrict__ f) {
-  GRID_STRIDE(i, m) f[i] = c[i] < 0.0;
 }
 
 __global__ void k_gather_i32(const int32_t* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
@@ -797,10 +788,8 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
   ProfScope prof(ctx.s, kFamSeparate);
   RAMA_REQUIRE(L >= 3, "max_len must be at least 3");
   RAMA_REQUIRE(L <= 8, "max_cycle_length > 8 is not supported by the B200 build");
-  Buf<uint8_t> flag(g.m > 0 ? g.m : 1, ctx);
-  RAMA_KERNEL(ctx, k_flag_neg, g.m, g.c, g.m, flag.p);
   Buf<int32_t> NQ;
-  int64_t nq = compact_indices(ctx, flag.p, g.m, NQ);
+  int64_t nq = compact_if(ctx, g.m, NegCost{g.c}, NQ);
   out.rows = nq;
   out.L = L;
   out.len.alloc(nq > 0 ? nq : 1, ctx.s);
@@ -954,11 +943,6 @@ __global__ void k_fan_emit(const int32_t* __restrict__ len, const int32_t* __res
   }
 }
 
-__global__ void k_uniq_heads(const int32_t* __restrict__ row, const uint64_t* __restrict__ key, int64_t n,
-                             uint8_t* __restrict__ head) {
-  GRID_STRIDE(p, n) head[p] = (p == 0) || row[p] != row[p - 1] || key[p] != key[p - 1];
-}
-
 __device__ __forceinline__ int32_t find_in_row(const int32_t* __restrict__ rptr, const int32_t* __restrict__ ev,
                                                int32_t a, int32_t b) {
   int32_t lo = rptr[a], hi = rptr[a + 1];
@@ -1077,10 +1061,8 @@ void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& 
   if (craw > 0) {
     BucketSorted cs;
     bucket_sort(ctx, n, craw, crow.p, ckey.p, cs, true);
-    Buf<uint8_t> head(craw, ctx);
-    RAMA_KERNEL(ctx, k_uniq_heads, craw, cs.row.p, cs.key.p, craw, head.p);
     Buf<int32_t> hp;
-    int64_t nh = compact_indices(ctx, head.p, craw, hp);
+    int64_t nh = compact_if(ctx, craw, SortedHead{cs.row.p, cs.key.p}, hp);
     Buf<uint8_t> isnew(nh > 0 ? nh : 1, ctx);
     RAMA_KERNEL(ctx, k_chord_new, nh, hp.p, nh, cs.row.p, cs.key.p, rptr_p, g.v, isnew.p);
     Buf<int32_t> sel;
@@ -1098,10 +1080,8 @@ void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& 
   if (traw > 0) {
     BucketSorted ts;
     bucket_sort(ctx, n, traw, trow.p, tkey.p, ts, true);
-    Buf<uint8_t> head(traw, ctx);
-    RAMA_KERNEL(ctx, k_uniq_heads, traw, ts.row.p, ts.key.p, traw, head.p);
     Buf<int32_t> hp;
-    T = compact_indices(ctx, head.p, traw, hp);
+    T = compact_if(ctx, traw, SortedHead{ts.row.p, ts.key.p}, hp);
     st.tri_nodes.alloc(3 * T, ctx.s);
     st.tri_edges.alloc(3 * T, ctx.s);
     RAMA_KERNEL(ctx, k_tri_out, T, hp.p, T, ts.row.p, ts.key.p, st.tri_nodes.p);
@@ -1230,9 +1210,7 @@ int64_t extend_separation(Ctx& ctx, DualState& st, int L) {
     Buf<int32_t> rptr(n + 1, ctx);
     row_ptr_from_sorted(ctx, rep.u.p, rep.m, n, rptr.p);
     bucket_sort(ctx, n, craw, crow.p, ckey.p, cs, true);
-    Buf<uint8_t> head(craw, ctx);
-    RAMA_KERNEL(ctx, k_uniq_heads, craw, cs.row.p, cs.key.p, craw, head.p);
-    int64_t nh = compact_indices(ctx, head.p, craw, hp_c);
+    int64_t nh = compact_if(ctx, craw, SortedHead{cs.row.p, cs.key.p}, hp_c);
     Buf<uint8_t> isnew(nh > 0 ? nh : 1, ctx);
     RAMA_KERNEL(ctx, k_chord_new, nh, hp_c.p, nh, cs.row.p, cs.key.p, rptr.p, rep.v.p, isnew.p);
     C = compact_indices(ctx, isnew.p, nh, sel_c);
@@ -1255,10 +1233,8 @@ int64_t extend_separation(Ctx& ctx, DualState& st, int L) {
   // new triplets: fan dedupe, then drop those already present
   BucketSorted ts;
   bucket_sort(ctx, n, traw, trow.p, tkey.p, ts, true);
-  Buf<uint8_t> head(traw, ctx);
-  RAMA_KERNEL(ctx, k_uniq_heads, traw, ts.row.p, ts.key.p, traw, head.p);
   Buf<int32_t> hp;
-  int64_t nh = compact_indices(ctx, head.p, traw, hp);
+  int64_t nh = compact_if(ctx, traw, SortedHead{ts.row.p, ts.key.p}, hp);
   const int64_t T0 = st.T;
   BucketSorted es;
   Buf<int32_t> erow(T0 > 0 ? T0 : 1, ctx);

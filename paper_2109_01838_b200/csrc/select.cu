@@ -24,6 +24,7 @@
 //     undecided candidate per edge"); each pass decides at least the
 //     smallest undecided candidate.
 #include "internal.h"
+#include "compact.cuh"
 
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
@@ -51,10 +52,6 @@ __device__ __forceinline__ void sf_union(int32_t* p, int32_t a, int32_t b) {
     a = lo;
     b = old;
   }
-}
-
-__global__ void k_flag_positive(const double* __restrict__ c, int64_t m, uint8_t* __restrict__ f) {
-  GRID_STRIDE(i, m) f[i] = c[i] > 0.0;
 }
 
 // ----------------------------------------------------------------- matching
@@ -118,10 +115,8 @@ int64_t select_matching(Ctx& ctx, const GraphView& g, int rounds, Buf<int32_t>& 
   su.alloc(1, ctx.s);
   sv.alloc(1, ctx.s);
   if (n == 0 || m == 0) return 0;
-  Buf<uint8_t> flag(m, ctx);
-  RAMA_KERNEL(ctx, k_flag_positive, m, g.c, m, flag.p);
   Buf<int32_t> P;
-  int64_t np = compact_indices(ctx, flag.p, m, P);
+  int64_t np = compact_if(ctx, m, PosCost{g.c}, P);
   if (np == 0) return 0;
   Buf<uint8_t> matched(n, ctx);
   matched.zero();
@@ -555,10 +550,8 @@ int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_
     ph[i] += std::chrono::duration<double, std::milli>(t - tp).count();
     tp = t;
   };
-  Buf<uint8_t> flag(m, ctx);
-  RAMA_KERNEL(ctx, k_flag_positive, m, g.c, m, flag.p);
   Buf<int32_t> P;
-  int64_t np = compact_indices(ctx, flag.p, m, P);
+  int64_t np = compact_if(ctx, m, PosCost{g.c}, P);
   if (np == 0) return 0;
 
   // strict rank: cost desc, (u, v) asc == stable sort of the canonical order
