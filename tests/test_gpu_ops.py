@@ -190,6 +190,22 @@ def test_ops_oracle_parity(shape):
     assert np.array_equal(g2.edges_u, og2.edges_u) and np.array_equal(g2.costs, og2.costs)
 
 
+def test_separation_dense_and_hub_sources_match_oracle():
+    """Sources too large for the 8-lane tables (dense neighbourhoods: tier-2
+    tables) and power-law hubs (row-intersection kernels, including the
+    4-cycle search from the target's side when |N(a)| > 4 |N(b)|) give the
+    reference's cycles.  Power-law graphs are compared up to L = 4: the
+    5-cycle search caps hub neighbourhoods (DESIGN.md deviation D2)."""
+    cases = [(instances.random_coo(300, 0.15, seed=s), (3, 4, 5)) for s in range(2)]
+    cases += [(instances.chung_lu_coo(3000, 2.1, 40000, seed=s), (3, 4)) for s in range(2)]
+    for (n, u, v, c), lengths in cases:
+        g, og = _both(n, u, v, c)
+        for L in lengths:
+            a1, b1 = P.dual._separate(g, L)
+            a2, b2 = O.separate(og, L)
+            assert np.array_equal(a1, a2) and np.array_equal(b1, b2), (n, L)
+
+
 def test_forest_conflict_resolution_exact():
     # dense positive trees with many in-tree repulsive edges: the sequential
     # conflict pass (contraction.py:231-284) must be reproduced exactly
