@@ -422,7 +422,8 @@ def b200_arm(args):
         "device_busy": {"kernel_ms_per_step": sum(v[0] for v in kern.values()) / args.steps,
                         "profiled_step_ms": p_ms / args.steps,
                         "note": "sum of our kernels' event-timed durations vs the profiled step (per-kernel events "
-                                "add small gaps); the rest is launch latency and host round trips"},
+                                "add small gaps); the rest is launch latency and host round trips.  With concurrent "
+                                "streams (c5batch) kernels overlap and the sum exceeds the step"},
     }
     print(json.dumps(line), flush=True)
     if world > 1:
