@@ -395,8 +395,10 @@ struct Bloom128 {
   uint64_t lo = 0, hi = 0;
   __device__ __forceinline__ static uint32_t bit(int32_t y) { return ((uint32_t)y * 0x2545F491u) >> 25; }
   __device__ __forceinline__ void add(int32_t y) {
-    uint32_t b = bit(y);
-    if (b < 64) lo |= 1ULL << b; else hi |= 1ULL << (b - 64);
+    const uint32_t b = bit(y);
+    const uint64_t m = 1ULL << (b & 63);
+    lo |= b < 64 ? m : 0ULL;
+    hi |= b < 64 ? 0ULL : m;
   }
   __device__ __forceinline__ bool maybe(int32_t y) const {
     uint32_t b = bit(y);
@@ -517,8 +519,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sep_src(
               for (int r = 0; r < kH; r++) {
                 int32_t kk = atomicCAS(hk + h, -1, y);
                 if (kk == -1 || kk == y) {
-                  if (kk == -1) atomicAdd(s_fill + gi, 1);
-                  f2.add(y);
+                  if (kk == -1) {
+                    atomicAdd(s_fill + gi, 1);
+                    f2.add(y);
+                  }
                   atomicMin(hv + h, xi);  // BFS parent = smallest position reaching y
                   break;
                 }
@@ -541,8 +545,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sep_src(
               for (int r = 0; r < kH; r++) {
                 int32_t kk = atomicCAS(hk + h, -1, y);
                 if (kk == -1 || kk == y) {
-                  mine += kk == -1;
-                  f2.add(y);
+                  if (kk == -1) {  // a lane that finds y present: its inserter added it
+                    mine++;
+                    f2.add(y);
+                  }
                   atomicMin(hv + h, xi);  // BFS parent = smallest position reaching y
                   break;
                 }
