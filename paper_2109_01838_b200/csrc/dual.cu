@@ -368,6 +368,7 @@ struct SrcTier {
   static constexpr int kEdges = EDGES;        // max repulsive edges of the source
 };
 using SrcTier1 = SrcTier<8, 32, 6, 256, 1 << 30, false>;
+using SrcTier15 = SrcTier<8, 32, 7, 512, 64, false>;  // tier 1's overflow, twice the L2 table
 using SrcTier2 = SrcTier<32, 128, 10, 1024, 64, true>;
 constexpr int kSrcThreads1 = 256, kSrcThreads2 = 128;
 
@@ -564,9 +565,9 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sep_src(
       __syncwarp(mask);  // table complete before the lookups
     }
     if (over) {
-      if (!kListed) {
+      if (gover) {  // the next tier takes the source
         if (lane == 0) gover[k] = 1;
-      } else {
+      } else {  // last tier: its edges go to the row-intersection kernels
         for (int32_t i = e0 + lane; i < e1; i += kGrp) fb[i] = 1;
       }
       __syncwarp(mask);
@@ -866,18 +867,35 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
     RAMA_LAUNCH_CHECK();
     ctx.launches++;
   }
-  {  // sources too large for tier 1: a warp each, larger tables
-    Buf<int32_t> G2;
-    int64_t ng2 = compact_indices(ctx, gover.p, ng, G2);
-    if (ng2 > 0) {
-      constexpr int kPer = kSrcThreads2 / SrcTier2::kGrp;
-      int64_t blocks = std::min<int64_t>((ng2 + kPer - 1) / kPer, cap);
-      KernelScope ks(ctx.s, "k_sep_src_wide", 0.0);
-      k_sep_src<SrcTier2, kSrcThreads2, 6, true><<<(unsigned)blocks, kSrcThreads2, 0, ctx.s>>>(
-          gstart.p, gsrc.p, G2.p, ng2, ng, n2, Q2.p, qb.p, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p,
-          (uint8_t*)nullptr, fb.p, force == 1 ? 1 : 0);
-      RAMA_LAUNCH_CHECK();
-      ctx.launches++;
+  {  // sources too large for tier 1: 8 lanes with a 128-entry table, then a
+     // warp each with 4x/16x tables
+    Buf<int32_t> G15;
+    int64_t ng15 = compact_indices(ctx, gover.p, ng, G15);
+    if (ng15 > 0) {
+      Buf<uint8_t> gover2(ng, ctx);
+      gover2.zero();
+      {
+        constexpr int kPer = kSrcThreads1 / SrcTier15::kGrp;
+        int64_t blocks = std::min<int64_t>((ng15 + kPer - 1) / kPer, cap);
+        KernelScope ks(ctx.s, "k_sep_src_mid", 0.0);
+        k_sep_src<SrcTier15, kSrcThreads1, 6, true><<<(unsigned)blocks, kSrcThreads1, 0, ctx.s>>>(
+            gstart.p, gsrc.p, G15.p, ng15, ng, n2, Q2.p, qb.p, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p,
+            gover2.p, fb.p, force ? 1 : 0);
+        RAMA_LAUNCH_CHECK();
+        ctx.launches++;
+      }
+      Buf<int32_t> G2;
+      int64_t ng2 = compact_indices(ctx, gover2.p, ng, G2);
+      if (ng2 > 0) {
+        constexpr int kPer = kSrcThreads2 / SrcTier2::kGrp;
+        int64_t blocks = std::min<int64_t>((ng2 + kPer - 1) / kPer, cap);
+        KernelScope ks(ctx.s, "k_sep_src_wide", 0.0);
+        k_sep_src<SrcTier2, kSrcThreads2, 6, true><<<(unsigned)blocks, kSrcThreads2, 0, ctx.s>>>(
+            gstart.p, gsrc.p, G2.p, ng2, ng, n2, Q2.p, qb.p, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p,
+            (uint8_t*)nullptr, fb.p, force == 1 ? 1 : 0);
+        RAMA_LAUNCH_CHECK();
+        ctx.launches++;
+      }
     }
   }
   // sources that did not fit the tables: sorted-row intersections
