@@ -201,17 +201,6 @@ __device__ __forceinline__ int32_t warp_claim(int32_t* counter, bool take) {
   return take ? b + __popc(bal & lanes_below()) : -1;
 }
 
-// vote[x] = max(vote[x], key) over (hi, lo) as one unsigned 128-bit value
-__device__ __forceinline__ void vote_max(ulonglong2* p, unsigned long long hi, unsigned long long lo) {
-  unsigned __int128 key = ((unsigned __int128)hi << 64) | lo;
-  unsigned __int128 cur = 0;
-  while (key > cur) {
-    unsigned __int128 old = atomicCAS((unsigned __int128*)p, cur, key);
-    if (old == cur) return;
-    cur = old;
-  }
-}
-
 // the vote a node casts for neighbour y over a slot of cost bits `bits`:
 // larger cost first, then smaller canonical id (contraction.py:207)
 __device__ __forceinline__ unsigned long long vote_lo(int32_t minid_y) {
@@ -264,8 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cl_rounds(Args A) {
       int32_t s = LD(P + i);
       unsigned long long bits = dbits(LD(A.c + s));
       int32_t a = LD(A.u + s), b = LD(A.v + s);
-      vote_max(A.vote + a, bits, vote_lo(LD(A.minid + b)));
-      vote_max(A.vote + b, bits, vote_lo(LD(A.minid + a)));
+      vote_max_pair(A.vote + a, vote_lo(LD(A.minid + b)), A.vote + b, vote_lo(LD(A.minid + a)), bits);
     }
     grid.sync();
     PHASE_MARK(0);

@@ -425,4 +425,28 @@ __device__ __forceinline__ double seg_sum(const double* a, int64_t n) { return s
 
 __device__ __forceinline__ uint64_t dbits(double x) { return (uint64_t)__double_as_longlong(x); }
 
+// Handshake votes: *pa = max(*pa, (hi, lo_a)) and *pb = max(*pb, (hi, lo_b))
+// as unsigned 128-bit values (hi = cost bits, lo = ~neighbour id).  The two
+// CAS loops are interleaved so both atomics are in flight together.
+__device__ __forceinline__ void vote_max_pair(ulonglong2* pa, unsigned long long lo_a, ulonglong2* pb,
+                                              unsigned long long lo_b, unsigned long long hi) {
+  const unsigned __int128 ka = ((unsigned __int128)hi << 64) | lo_a;
+  const unsigned __int128 kb = ((unsigned __int128)hi << 64) | lo_b;
+  unsigned __int128 ca = 0, cb = 0;
+  bool da = !(ka > ca), db = !(kb > cb);
+  while (!(da && db)) {
+    unsigned __int128 oa = ca, ob = cb;
+    if (!da) oa = atomicCAS((unsigned __int128*)pa, ca, ka);
+    if (!db) ob = atomicCAS((unsigned __int128*)pb, cb, kb);
+    if (!da) {
+      if (oa == ca) da = true;
+      else { ca = oa; da = !(ka > ca); }
+    }
+    if (!db) {
+      if (ob == cb) db = true;
+      else { cb = ob; db = !(kb > cb); }
+    }
+  }
+}
+
 }  // namespace rama

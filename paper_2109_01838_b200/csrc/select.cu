@@ -56,19 +56,6 @@ __device__ __forceinline__ void sf_union(int32_t* p, int32_t a, int32_t b) {
 
 // ----------------------------------------------------------------- matching
 
-// one pass of votes: every unmatched endpoint keeps the max of
-// (cost bits, ~neighbour id) as one 128-bit value -- the best positive edge,
-// ties toward the smaller neighbour (contraction.py:207)
-__device__ __forceinline__ void vote_max128(ulonglong2* p, unsigned long long hi, unsigned long long lo) {
-  unsigned __int128 key = ((unsigned __int128)hi << 64) | lo;
-  unsigned __int128 cur = 0;
-  while (key > cur) {
-    unsigned __int128 old = atomicCAS((unsigned __int128*)p, cur, key);
-    if (old == cur) return;
-    cur = old;
-  }
-}
-
 __global__ void k_match_vote(const int32_t* __restrict__ P, int64_t np, const int32_t* __restrict__ u,
                              const int32_t* __restrict__ v, const double* __restrict__ c,
                              const uint8_t* __restrict__ matched, ulonglong2* __restrict__ vote) {
@@ -77,8 +64,7 @@ __global__ void k_match_vote(const int32_t* __restrict__ P, int64_t np, const in
     int32_t a = u[e], b = v[e];
     if (matched[a] | matched[b]) continue;
     unsigned long long bits = dbits(c[e]);
-    vote_max128(vote + a, bits, 0xffffffffULL - (uint32_t)b);
-    vote_max128(vote + b, bits, 0xffffffffULL - (uint32_t)a);
+    vote_max_pair(vote + a, 0xffffffffULL - (uint32_t)b, vote + b, 0xffffffffULL - (uint32_t)a, bits);
   }
 }
 
