@@ -56,6 +56,9 @@ __device__ __forceinline__ void sf_union(int32_t* p, int32_t a, int32_t b) {
 
 // ----------------------------------------------------------------- matching
 
+// one pass of votes: every unmatched endpoint keeps the max of
+// (cost bits, ~neighbour id) as one 128-bit value -- the best positive edge,
+// ties toward the smaller neighbour (contraction.py:207)
 __global__ void k_match_vote(const int32_t* __restrict__ P, int64_t np, const int32_t* __restrict__ u,
                              const int32_t* __restrict__ v, const double* __restrict__ c,
                              const uint8_t* __restrict__ matched, ulonglong2* __restrict__ vote) {
