@@ -468,26 +468,15 @@ void row_ptr_from_sorted(Ctx& ctx, const int32_t* u, int64_t m, int64_t n, int32
 
 // ---------------------------------------------------------- bucket sort
 
-// Warp-aggregated histogram: lanes of a warp that hit the same row share
-// one atomicAdd (__match_any_sync), and every item records its offset
-// inside its row so the scatter pass needs no atomics.  Items with row < 0
-// are dropped (used by contraction for merged edges).
+// Histogram of the rows: every item records its offset inside its row (the
+// atomicAdd's old value), so the scatter pass needs no atomics.  Items with
+// row < 0 are dropped (contraction's merged edges).  Plain atomics beat
+// warp aggregation with __match_any_sync here (C2: 1.23 -> 0.92 ms).
 __global__ void k_bucket_count(const int32_t* __restrict__ row, int64_t N, int32_t* __restrict__ cnt,
                                int32_t* __restrict__ off) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < N; base += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i = base + threadIdx.x;
-    int32_t r = i < N ? row[i] : -1;
-    unsigned active = __ballot_sync(0xffffffffu, r >= 0);
-    if (r >= 0) {
-      unsigned peers = __match_any_sync(active, r);
-      int leader = __ffs(peers) - 1;
-      int rank = __popc(peers & ((1u << lane) - 1u));
-      int32_t b = 0;
-      if (lane == leader) b = atomicAdd(&cnt[r], __popc(peers));
-      b = __shfl_sync(peers, b, leader);
-      off[i] = b + rank;
-    }
+  GRID_STRIDE(i, N) {
+    const int32_t r = row[i];
+    if (r >= 0) off[i] = atomicAdd(&cnt[r], 1);
   }
 }
 
