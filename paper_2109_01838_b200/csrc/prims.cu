@@ -319,7 +319,7 @@ bool trace_print() { return trace_level() >= 1; }
 
 unsigned capped_grid(int64_t work, int block) {
   int64_t g = (work + block - 1) / block;
-  int64_t cap = (int64_t)(g_num_sms > 0 ? g_num_sms : 148) * 16;  // 16 x 256 threads per SM
+  int64_t cap = (int64_t)(g_num_sms > 0 ? g_num_sms : 148) * 32;  // 32 x 256 threads per SM (more loads in flight than 16)
   if (g > cap) g = cap;
   if (g < 1) g = 1;
   return (unsigned)g;
