@@ -850,7 +850,7 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
   gover.zero();
   static const int64_t cap = [] {  // RAMA_SEP_BLOCKS overrides the grid cap (tests)
     const char* e = getenv("RAMA_SEP_BLOCKS");
-    return e ? (int64_t)atoll(e) : (int64_t)148 * 6 * 4;
+    return e ? (int64_t)atoll(e) : (int64_t)148 * 6 * 8;  // 8 waves of 6 CTAs per SM (measured best)
   }();
   const int force = sep_force_fallback();
   {
