@@ -404,7 +404,7 @@ static unsigned coop_blocks(const void* fn) {
 
 static void launch_coop(Ctx& ctx, const void* fn, const char* name, void** args, int64_t work) {
   KernelScope ks(ctx.s, name, 0.0);
-  int64_t want = (work + 4 * kBlock - 1) / (4 * kBlock);  // ~4 items per thread per level
+  int64_t want = (work + kBlock - 1) / kBlock;  // ~1 item per thread per level
   unsigned cap = coop_blocks(fn);
   unsigned blocks = (unsigned)(want < 1 ? 1 : (want < cap ? want : cap));
   RAMA_CUDA(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kBlock), args, 0, ctx.s));
