@@ -370,7 +370,7 @@ struct SrcTier {
 using SrcTier1 = SrcTier<8, 32, 6, 256, 1 << 30, false>;
 using SrcTier15 = SrcTier<8, 32, 7, 512, 64, false>;  // tier 1's overflow, twice the L2 table
 using SrcTier2 = SrcTier<32, 128, 10, 1024, 64, true>;
-constexpr int kSrcThreads1 = 256, kSrcThreads2 = 128;
+constexpr int kSrcThreads1 = 128, kSrcThreads2 = 128;
 
 template <int HBITS>
 __device__ __forceinline__ int32_t src_slot(int32_t y) {
@@ -850,7 +850,7 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
   gover.zero();
   static const int64_t cap = [] {  // RAMA_SEP_BLOCKS overrides the grid cap (tests)
     const char* e = getenv("RAMA_SEP_BLOCKS");
-    return e ? (int64_t)atoll(e) : (int64_t)148 * 6 * 8;  // 8 waves of 6 CTAs per SM (measured best)
+    return e ? (int64_t)atoll(e) : (int64_t)148 * 12 * 8;  // 8 waves of 12 CTAs per SM
   }();
   const int force = sep_force_fallback();
   {
@@ -861,7 +861,7 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
     // edges' endpoints, the cycle rows written
     KernelScope ks(ctx.s, "k_sep_src",
                    4.0 * (double)(g.n + 1) + 4.0 * (double)csr.arcs + (16.0 + 4.0 * L) * (double)n2);
-    k_sep_src<SrcTier1, kSrcThreads1, 6, false><<<(unsigned)blocks, kSrcThreads1, 0, ctx.s>>>(
+    k_sep_src<SrcTier1, kSrcThreads1, 12, false><<<(unsigned)blocks, kSrcThreads1, 0, ctx.s>>>(
         gstart.p, gsrc.p, (const int32_t*)nullptr, ng, ng, n2, Q2.p, qb.p, csr.ptr.p, csr.adj.p, L, out.len.p,
         out.nodes.p, gover.p, fb.p, force ? 1 : 0);
     RAMA_LAUNCH_CHECK();
@@ -878,7 +878,7 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
         constexpr int kPer = kSrcThreads1 / SrcTier15::kGrp;
         int64_t blocks = std::min<int64_t>((ng15 + kPer - 1) / kPer, cap);
         KernelScope ks(ctx.s, "k_sep_src_mid", 0.0);
-        k_sep_src<SrcTier15, kSrcThreads1, 6, true><<<(unsigned)blocks, kSrcThreads1, 0, ctx.s>>>(
+        k_sep_src<SrcTier15, kSrcThreads1, 12, true><<<(unsigned)blocks, kSrcThreads1, 0, ctx.s>>>(
             gstart.p, gsrc.p, G15.p, ng15, ng, n2, Q2.p, qb.p, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p,
             gover2.p, fb.p, force ? 1 : 0);
         RAMA_LAUNCH_CHECK();
