@@ -13,11 +13,13 @@ strides 2, 3; 2,097,152 nodes / 9,892,581 edges), BASELINE.json configs[1].
           (256 MiB write) between steps outside the events.
 * e2e   : edges/s through the C ABI with HOST buffers (rama_solve_host:
           H2D of u, v, c + solve + D2H of labels inside the timed region).
-* N > 1 : one process per GPU (torchrun), each rank solves its own
+* N > 1 : one process per GPU (bench.py re-execs itself under
+          torch.distributed.run when WORLD_SIZE is unset), each rank solves its own
           independent instance (seed = rank) and the labels/objectives are
           gathered over NCCL every step -- weak scaling, no other exchange.
 * --impl reference : the CPU oracle port of the reference solver
-          (oracle/, single-threaded like the reference) on a bounded sample.
+          (oracle/, single-threaded like the reference) on the full C2
+          instance, one solve per step, steps spread over the host cores.
 """
 
 import argparse
@@ -33,7 +35,6 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CPU_SAMPLE_ROWS = 256  # C2 crop for the CPU baseline: 256 x 2048 (~2.4M edges, ~11 s oracle)
 BATCH_INSTANCES = 64   # C5: 64 independent 512x512 grids per step
 BATCH_WORKERS = int(os.environ.get("RAMA_BATCH_WORKERS", "8"))  # concurrent streams (host threads) per GPU for a batch
 
@@ -71,23 +72,21 @@ def mode_of(workload):
 # ------------------------------------------------------------ CPU oracle
 
 def cpu_sample(workload):
-    """Bounded sample of the workload for the single-threaded CPU oracle."""
+    """The instance the CPU arms solve per step: the FULL workload where the
+    single-threaded port finishes it in ~20 s (C1, C2, C5), a crop where it
+    cannot (C3 ~2 min per solve; C4, whose reference run does not finish).
+    Returns ((n, u, v, c), description, same_config)."""
     from paper_2109_01838_b200 import instances
 
-    if workload == "c2":
-        n, u, v, c = instances.grid8_coo(CPU_SAMPLE_ROWS, 2048, strides=(2, 3), seed=0)
-        desc = "C2-shaped crop %dx2048 (+strides 2,3), seed 0, %d edges, full PD solve" % (CPU_SAMPLE_ROWS, u.size)
-    elif workload == "c3":
+    if workload == "c3":
         n, u, v, c = instances.grid3d_coo(16, 256, 256, stride=2, seed=0)
-        desc = "C3-shaped crop 16x256x256 (+stride 2), seed 0, %d edges, full PD solve" % u.size
-    elif workload == "c4":
+        return (n, u, v, c), "C3-shaped crop 16x256x256 (+stride 2), seed 0, %d raw edges, full PD solve" % u.size, False
+    if workload == "c4":
         n, u, v, c = instances.chung_lu_coo(10_000, 2.1, 260_000, seed=0)
-        desc = "C4-shaped Chung-Lu n=10k (m target 20n), seed 0, full PD solve"
-    elif workload == "c5batch":
-        return instances.make("c5", seed=0), "one instance of the batch (512x512, seed 0), full PD solve"
-    else:
-        return instances.make(workload), "full %s instance" % workload
-    return (n, u, v, c), desc
+        return (n, u, v, c), "C4-shaped Chung-Lu n=10k (26 n draws), seed 0, full PD solve", False
+    if workload == "c5batch":
+        return instances.make("c5", seed=0), "one instance of the batch (512x512, seed 0), full PD solve", False
+    return instances.make(workload), "the full %s instance (seed 0), full %s solve" % (workload, mode_of(workload)), True
 
 
 def run_oracle(sample, mode):
@@ -101,11 +100,39 @@ def run_oracle(sample, mode):
 
 
 def cpu_baseline(workload):
-    sample, desc = cpu_sample(workload)
+    """One single-threaded oracle solve of the sample, in-process."""
+    sample, desc, same = cpu_sample(workload)
     secs, m, _ = run_oracle(sample, mode_of(workload))
-    return {"value": m / secs, "unit": "edges/s", "cores": 1, "kind": "port",
-            "sample": desc + "; %.2f s on 1 host core (oracle/rama_oracle.c, the reference is single-threaded too)"
+    return {"value": m / secs, "unit": "edges/s", "cores": 1, "kind": "port", "same_config": same,
+            "sample": desc + "; %.2f s on 1 host core (oracle/rama_oracle.c; the reference is single-threaded too)"
             % secs}
+
+
+_POOL_SAMPLE = None  # set before the pool forks (shared copy-on-write)
+
+
+def _pool_warm(mode):
+    import oracle
+    from paper_2109_01838_b200 import instances
+
+    oracle.solve(oracle.Graph(*instances.grid_coo(64, 64, 0, seed=0)), mode=mode)
+    return os.getpid()
+
+
+def _pool_solve(mode):
+    secs, m, _ = run_oracle(_POOL_SAMPLE, mode)
+    return secs, m
+
+
+def _host_mem_gb():
+    try:
+        with open("/proc/meminfo") as fh:
+            for line in fh:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) / 1e6
+    except OSError:
+        pass
+    return 16.0
 
 
 # --------------------------------------------------------------- clocks
@@ -169,29 +196,42 @@ def traffic_from_profiles(kernel):
 # ---------------------------------------------------------------- arms
 
 def reference_arm(args):
+    """The reference's CPU algorithm (the oracle port: the reference itself is
+    Python+numba and single-threaded) on the box's host cores: every step is
+    one full solve of the sample, the steps run concurrently in a process
+    pool with one single-threaded solver per core, value = edges of all steps
+    / wall time of the timed steps."""
+    global _POOL_SAMPLE
+    import multiprocessing as mp
+
     rank, _, world = dist_env()
     if rank != 0:
         return
-    sample, desc = cpu_sample(args.workload)
     mode = mode_of(args.workload)
-    import oracle
-    from paper_2109_01838_b200 import instances
-
-    small = instances.grid_coo(64, 64, 0, seed=0)
-    for _ in range(args.warmup):  # warm caches / page in the library
-        oracle.solve(oracle.Graph(*small), mode=mode)
-    times, m = [], 0
-    for _ in range(args.steps):
-        secs, m, _ = run_oracle(sample, mode)
-        times.append(secs)
-    total = sum(times)
-    value = m * args.steps / total
+    _POOL_SAMPLE, desc, same = cpu_sample(args.workload)
+    cpus = os.cpu_count() or 1
+    per_solve_gb = 3.0 * max(1.0, _POOL_SAMPLE[1].size / 10e6)  # ~1.5 GB RSS per 10 M-edge solve, 2x margin
+    workers = max(1, min(args.steps, cpus, int(_host_mem_gb() / per_solve_gb)))
+    ctx = mp.get_context("fork")
+    with ctx.Pool(workers) as pool:
+        pool.map(_pool_warm, [mode] * max(workers, args.warmup))  # page in the library in every worker
+        t0 = time.perf_counter()
+        res = pool.map(_pool_solve, [mode] * args.steps, chunksize=1)
+        wall = time.perf_counter() - t0
+    m = res[0][1]
+    value = m * args.steps / wall
+    lat = [r[0] for r in res]
+    sample = "%s; %d steps over %d worker processes (1 thread each, %d host cores), solve latency %.2f s mean" % (
+        desc, args.steps, workers, cpus, statistics.mean(lat))
     line = {
         "impl": "reference", "metric": "multicut solve throughput (edges/s)", "value": value, "unit": "edges/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD_DESC[args.workload], "mode": mode, "sample": desc},
-        "cpu_baseline": {"value": value, "unit": "edges/s", "cores": 1, "kind": "port", "sample": desc},
+        "config": {"workload": WORKLOAD_DESC[args.workload], "edges": int(m), "mode": mode, "sample": desc,
+                   "same_config": same},
+        "solve_latency_s": statistics.mean(lat),
+        "cpu_baseline": {"value": value, "unit": "edges/s", "cores": workers, "kind": "port", "sample": sample,
+                         "same_config": same},
         "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -430,8 +470,24 @@ def b200_arm(args):
         torch.distributed.destroy_process_group()
 
 
+def spawn_ranks(args):
+    """--gpus N > 1 without a torchrun environment: re-exec under
+    torch.distributed.run (one process per GPU, NCCL, 127.0.0.1)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args)
     if args.impl == "reference":
         reference_arm(args)
     else:

@@ -645,14 +645,13 @@ int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc) {
   Buf<int32_t> eh;
   int64_t grow = 1;  // doubles when a launch could not run a single round
   Buf<int32_t> sc(SC_COUNT, ctx);
-  static const int max_blocks = [] {  // at most one CTA per SM (thread-safe init: batch workers)
-    int dev = 0, sms = 0, per_sm = 0;
-    RAMA_CUDA(cudaGetDevice(&dev));
-    RAMA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  static const bool resident = [] {  // thread-safe init (batch workers)
+    int per_sm = 0;
     RAMA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cl_rounds, kThreads, 0));
-    RAMA_REQUIRE(per_sm >= 1, "cleanup kernel cannot be resident");
-    return sms;
+    return per_sm >= 1;
   }();
+  RAMA_REQUIRE(resident, "cleanup kernel cannot be resident");
+  const int max_blocks = num_sms();  // at most one CTA per SM (per device)
   // sized by the quotient: a small cleanup (batch instances) leaves the
   // other SMs to concurrent solves instead of claiming the whole GPU
   const int grid_blocks = (int)std::min<int64_t>(max_blocks, std::max<int64_t>(8, (m + 8191) / 8192));

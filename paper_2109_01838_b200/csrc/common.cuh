@@ -55,6 +55,7 @@ struct Error : public std::runtime_error {
 struct Ctx {
   cudaStream_t s = nullptr;
   int64_t* pinned = nullptr;  // 64 int64 slots
+  cudaEvent_t ev = nullptr;   // asynchronous read-backs (recycled with `pinned`)
   int launches = 0;           // kernels launched through this context
 
   explicit Ctx(cudaStream_t st);
@@ -65,6 +66,8 @@ struct Ctx {
 };
 
 void ensure_pool_configured();
+// SM count of the current device (after ensure_pool_configured)
+int num_sms();
 // grow the stream-ordered pool to at least `bytes` up front (one mapping
 // instead of many growth steps in the middle of a solve)
 void reserve_pool(Ctx& ctx, size_t bytes);
@@ -168,6 +171,8 @@ void* dev_alloc(size_t bytes, cudaStream_t s);
 void dev_free(void* p, size_t bytes, cudaStream_t s);
 // return every cached block of stream s to the pool (before destroying s)
 void dev_release_stream(cudaStream_t s);
+// return every cached block (all devices, all streams) and trim the pools
+void dev_release_all();
 
 template <class T>
 struct Buf {

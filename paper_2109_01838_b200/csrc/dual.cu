@@ -23,6 +23,7 @@
 // nvcc cannot contract into FMAs and lam is bit-identical to numpy's.
 #include "internal.h"
 #include "compact.cuh"
+#include "sortreduce.cuh"
 
 namespace rama {
 
@@ -64,6 +65,16 @@ static void positive_csr(Ctx& ctx, const GraphView& g, PosCSR& out) {
   RAMA_KERNEL(ctx, k_key_lo, na, bs.key.p, na, out.adj.p);
   out.arcs = na;
 }
+
+// sorted item p -> adj[p]
+struct AdjEmit {
+  int32_t* adj;
+  __device__ __forceinline__ bool keep(int32_t, uint64_t) const { return true; }
+  template <class A>
+  __device__ __forceinline__ void out(int64_t idx, int32_t, uint64_t key, A, int64_t) const {
+    adj[idx] = (int32_t)(uint32_t)key;
+  }
+};
 
 // ----------------------------------------------------------- separation
 
@@ -272,7 +283,7 @@ __global__ void k_sep4(const int32_t* __restrict__ Q, int64_t nq, const int32_t*
 __global__ void k_sep5(const int32_t* __restrict__ Q, int64_t nq, const int32_t* __restrict__ NQ,
                        const int32_t* __restrict__ u, const int32_t* __restrict__ v,
                        const int32_t* __restrict__ ptr, const int32_t* __restrict__ adj, int L,
-                       int32_t* __restrict__ out_len, int32_t* __restrict__ out_nodes) {
+                       int32_t* __restrict__ out_len, int32_t* __restrict__ out_nodes, uint8_t* __restrict__ capped) {
   const int g = threadIdx.x % kSepLanes;
   const int64_t per_warp = 32 / kSepLanes;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -298,6 +309,7 @@ __global__ void k_sep5(const int32_t* __restrict__ Q, int64_t nq, const int32_t*
     int32_t bz = 0x7fffffff;
     // trip counts are warp-uniform: the group shuffles below use the full mask
     int32_t lbmax = warp_max(min(lb, kHubCap));
+    if (capped && live && g == 0 && lb > kHubCap) capped[q] = 1;  // D2 truncated this search
     for (int32_t k = 0; k < lbmax; k++) {
       bool zok = live && k < lb;
       int32_t z = zok ? adj[pb + k] : 0;
@@ -308,7 +320,12 @@ __global__ void k_sep5(const int32_t* __restrict__ Q, int64_t nq, const int32_t*
       if (zok) {
         pz = ptr[z];
         lz = ptr[z + 1] - pz;
-        if (lz > kHubCap || first_common(Na, la, adj + pz, lz) >= 0) zok = false;  // hub, or z at distance 2
+        if (lz > kHubCap) {  // hub candidate skipped (D2)
+          zok = false;
+          if (capped) capped[q] = 1;
+        } else if (first_common(Na, la, adj + pz, lz) >= 0) {
+          zok = false;  // z at distance 2
+        }
       }
       uint64_t zbest = ~0ULL;
       int32_t lzmax = warp_max(zok ? lz : 0);
@@ -463,7 +480,8 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sep_src(
     const int32_t* __restrict__ gstart, const int32_t* __restrict__ gsrc, const int32_t* __restrict__ glist,
     int64_t nlist, int64_t ng, int64_t n2, const int32_t* __restrict__ Q2, const int32_t* __restrict__ qb,
     const int32_t* __restrict__ ptr, const int32_t* __restrict__ adj, int L, int32_t* __restrict__ out_len,
-    int32_t* __restrict__ out_nodes, uint8_t* __restrict__ gover, uint8_t* __restrict__ fb, int force_fallback) {
+    int32_t* __restrict__ out_nodes, uint8_t* __restrict__ gover, uint8_t* __restrict__ fb, int force_fallback,
+    uint8_t* __restrict__ capped) {
   constexpr int kGrp = T::kGrp, kPer = THREADS / T::kGrp, kH = T::kHash;
   __shared__ int32_t s_l1[kPer][T::kL1];
   __shared__ int32_t s_hk[kPer][kH];
@@ -594,13 +612,17 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sep_src(
         uint64_t bk = ~0ULL;
         int32_t bz = 0x7fffffff;
         const int32_t lbc = min(lb, kHubCap);
+        if (capped && lane == 0 && lb > kHubCap) capped[q] = 1;  // D2 truncated this search
         for (int32_t t = lane; t < lbc; t += kGrp) {
           int32_t z = adj[pb + t];
           if (z == a || (f1.maybe(z) && src_in_l1(l1, la, z)) ||
               (f2.maybe(z) && src_lookup<T::kHashBits>(hk, hv, z) >= 0))
             continue;
           const int32_t pz = ptr[z], lz = ptr[z + 1] - pz;
-          if (lz > kHubCap) continue;
+          if (lz > kHubCap) {  // hub candidate skipped (D2)
+            if (capped) capped[q] = 1;
+            continue;
+          }
           uint64_t zb = ~0ULL;
           for (int32_t w = 0; w < lz; w++) {
             int32_t y = adj[pz + w];
@@ -663,7 +685,8 @@ __global__ void __launch_bounds__(256) k_sep_bfs(const int32_t* __restrict__ gst
                                                  const int32_t* __restrict__ ptr, const int32_t* __restrict__ adj,
                                                  int L, int32_t* __restrict__ out_len,
                                                  int32_t* __restrict__ out_nodes, unsigned long long* keys,
-                                                 int32_t* par, int32_t* pos, int32_t* queue, int64_t n) {
+                                                 int32_t* par, int32_t* pos, int32_t* queue, int32_t* depth,
+                                                 int64_t n) {
   const int lane = threadIdx.x & 31;
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t W = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -671,6 +694,7 @@ __global__ void __launch_bounds__(256) k_sep_bfs(const int32_t* __restrict__ gst
   int32_t* Pa = par + w * n;
   int32_t* Po = pos + w * n;
   int32_t* Qu = queue + w * n;
+  int32_t* Dp = depth + w * n;
   for (int64_t k = w; k < ng; k += W) {
     const uint32_t tick = (uint32_t)(k + 1);
     const uint64_t done = bfs_key(tick, 0);
@@ -681,14 +705,12 @@ __global__ void __launch_bounds__(256) k_sep_bfs(const int32_t* __restrict__ gst
       K[a] = done;
       Pa[a] = -1;
       Po[a] = 0;
+      Dp[a] = 0;
     }
     __syncwarp();
-    int32_t lstart[8], lend[8];
-    lstart[0] = 0;
-    lend[0] = 1;
+    int32_t s = 0, e = 1;  // current level's queue range
     int32_t qlen = 1;
-    for (int lev = 0; lev <= L - 3; lev++) {  // levels 1 .. L-2
-      const int32_t s = lstart[lev], e = lend[lev];
+    for (int lev = 0; lev <= L - 3 && s < e; lev++) {  // discover levels 1 .. L-2
       for (int32_t p = s; p < e; p++) {  // candidates: atomicMin over the position
         const int32_t x = __ldcg(Qu + p);
         const int32_t b0 = ptr[x], dx = ptr[x + 1] - b0;
@@ -711,15 +733,16 @@ __global__ void __launch_bounds__(256) k_sep_bfs(const int32_t* __restrict__ gst
             Qu[at] = y;
             Pa[y] = x;
             Po[y] = at;
+            Dp[y] = lev + 1;
           }
           qlen += __popc(bal);
         }
       }
       __syncwarp();
-      for (int32_t i = lend[lev] + lane; i < qlen; i += 32) K[__ldcg(Qu + i)] = done;
+      for (int32_t i = e + lane; i < qlen; i += 32) K[__ldcg(Qu + i)] = done;
       __syncwarp();
-      lstart[lev + 1] = e;
-      lend[lev + 1] = qlen;
+      s = e;
+      e = qlen;
     }
     const int32_t last = L - 2;  // deepest stored level
     for (int32_t i = i0; i < i1; i++) {
@@ -727,19 +750,14 @@ __global__ void __launch_bounds__(256) k_sep_bfs(const int32_t* __restrict__ gst
       const int32_t b = v[NQ[q]];
       int32_t tail = -1, len = 0;
       if (__ldcg(K + b) == done) {  // b itself reached at level <= L-2
-        int32_t pb = __ldcg(Po + b), lv = 0;
-        while (lv < last && pb >= lend[lv]) lv++;
-        len = lv + 1;
+        len = __ldcg(Dp + b) + 1;
         tail = b;
       } else {  // b at level L-1: parent = first queue position among N(b) at level L-2
         const int32_t b0 = ptr[b], db = ptr[b + 1] - b0;
         int32_t best = 0x7fffffff;
         for (int32_t j = lane; j < db; j += 32) {
           int32_t y = adj[b0 + j];
-          if (__ldcg(K + y) == done) {
-            int32_t py = __ldcg(Po + y);
-            if (py >= lstart[last] && py < lend[last]) best = min(best, py);
-          }
+          if (__ldcg(K + y) == done && __ldcg(Dp + y) == last) best = min(best, __ldcg(Po + y));
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
@@ -768,6 +786,48 @@ __global__ void __launch_bounds__(256) k_sep_bfs(const int32_t* __restrict__ gst
   }
 }
 
+// The exact BFS over the repulsive edges Qx (indices into NQ, ascending):
+// grouped by source, one warp per source with 24 n bytes of scratch per warp.
+__global__ void k_bfs_heads(const int32_t* __restrict__ Qx, int64_t nx, const int32_t* __restrict__ NQ,
+                            const int32_t* __restrict__ u, uint8_t* __restrict__ head) {
+  GRID_STRIDE(i, nx) head[i] = (i == 0) || u[NQ[Qx[i]]] != u[NQ[Qx[i - 1]]];
+}
+
+__global__ void k_clear_rows(const int32_t* __restrict__ Qx, int64_t nx, int L, int32_t* __restrict__ out_len,
+                             int32_t* __restrict__ out_nodes) {
+  GRID_STRIDE(i, nx) {
+    const int32_t q = Qx[i];
+    out_len[q] = 0;
+    for (int j = 0; j < L; j++) out_nodes[(int64_t)q * L + j] = 0;
+  }
+}
+
+static void run_sep_bfs(Ctx& ctx, const GraphView& g, const int32_t* ptr, const int32_t* adj, const int32_t* NQ,
+                        const int32_t* Qx, int64_t nx, int L, CycleRows& out) {
+  if (nx == 0) return;
+  Buf<uint8_t> head(nx, ctx);
+  RAMA_KERNEL(ctx, k_bfs_heads, nx, Qx, nx, NQ, g.u, head.p);
+  Buf<int32_t> gstart;
+  const int64_t ng = compact_indices(ctx, head.p, nx, gstart);
+  size_t free_b = 0, total_b = 0;
+  RAMA_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const int64_t per_warp = 24 * g.n;
+  int64_t W = (int64_t)(free_b / 4) / (per_warp > 0 ? per_warp : 1);
+  if (W > (int64_t)num_sms() * 8) W = (int64_t)num_sms() * 8;
+  if (W > ng) W = ng;
+  RAMA_REQUIRE(W >= 1, "not enough device memory for the exact separation scratch");
+  W = (W + 7) / 8 * 8;  // whole 8-warp blocks; every launched warp owns a scratch slice
+  Buf<unsigned long long> keys((size_t)W * g.n, ctx);
+  Buf<int32_t> par((size_t)W * g.n, ctx), pos((size_t)W * g.n, ctx), queue((size_t)W * g.n, ctx),
+      depth((size_t)W * g.n, ctx);
+  keys.fill_bytes(0xff);
+  KernelScope ks(ctx.s, "k_sep_bfs", 0.0);
+  k_sep_bfs<<<(unsigned)((W + 7) / 8), 256, 0, ctx.s>>>(gstart.p, ng, nx, Qx, NQ, g.u, g.v, ptr, adj, L, out.len.p,
+                                                        out.nodes.p, keys.p, par.p, pos.p, queue.p, depth.p, g.n);
+  RAMA_LAUNCH_CHECK();
+  ctx.launches++;
+}
+
 // RAMA_SEP_FALLBACK=1 routes every source through the row-intersection
 // kernels, =2 every source through the tier-2 tables (tests use them to
 // check all executions against the oracle)
@@ -791,10 +851,12 @@ __global__ void k_sep_stats(const int32_t* __restrict__ Q2, const int32_t* __res
   }
 }
 
-void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
+static void separate_tables(Ctx& ctx, const GraphView& g, int L, CycleRows& out, const PosCSR& csr,
+                            const Buf<int32_t>& NQ, int64_t nq, uint8_t* capped);
+
+void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out, bool exact) {
   ProfScope prof(ctx.s, kFamSeparate);
   RAMA_REQUIRE(L >= 3, "max_len must be at least 3");
-  RAMA_REQUIRE(L <= 8, "max_cycle_length > 8 is not supported by the B200 build");
   Buf<int32_t> NQ;
   int64_t nq = compact_if(ctx, g.m, NegCost{g.c}, NQ);
   out.rows = nq;
@@ -809,6 +871,34 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
     out.nodes.zero();
     return;
   }
+  if (L >= 6) {  // PD+ and longer: the exact source-grouped BFS for every edge without a triangle
+    Buf<uint8_t> miss(nq, ctx);
+    RAMA_KERNEL(ctx, k_sep3, nq, (const int32_t*)nullptr, nq, NQ.p, g.u, g.v, csr.ptr.p, csr.adj.p, L, out.len.p,
+                out.nodes.p, miss.p);
+    Buf<int32_t> Qx;
+    const int64_t nx = compact_indices(ctx, miss.p, nq, Qx);
+    run_sep_bfs(ctx, g, csr.ptr.p, csr.adj.p, NQ.p, Qx.p, nx, L, out);
+    return;
+  }
+  Buf<uint8_t> capped;
+  if (exact && L >= 5) {
+    capped.alloc(nq, ctx.s);
+    capped.zero();
+  }
+  separate_tables(ctx, g, L, out, csr, NQ, nq, capped.p);
+  if (capped.p) {  // exact opt-out of deviation D2: truncated searches rerun as the reference BFS
+    Buf<int32_t> Qx;
+    const int64_t nx = compact_indices(ctx, capped.p, nq, Qx);
+    if (nx > 0) {
+      RAMA_KERNEL(ctx, k_clear_rows, nx, Qx.p, nx, L, out.len.p, out.nodes.p);
+      run_sep_bfs(ctx, g, csr.ptr.p, csr.adj.p, NQ.p, Qx.p, nx, L, out);
+    }
+  }
+}
+
+// triangles, then 4/5-cycles from the source tables / row intersections
+static void separate_tables(Ctx& ctx, const GraphView& g, int L, CycleRows& out, const PosCSR& csr,
+                            const Buf<int32_t>& NQ, int64_t nq, uint8_t* capped) {
   // triangles: thread per edge, sorted-row intersection
   Buf<uint8_t> miss(nq, ctx);
   RAMA_KERNEL(ctx, k_sep3, nq, (const int32_t*)nullptr, nq, NQ.p, g.u, g.v, csr.ptr.p, csr.adj.p, L, out.len.p,
@@ -825,26 +915,6 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
   int64_t ng = compact_indices(ctx, head.p, n2, gstart);
   Buf<int32_t> gsrc(ng > 0 ? ng : 1, ctx);
   RAMA_KERNEL(ctx, k_gather_i32, ng, qa.p, gstart.p, ng, gsrc.p);
-  if (L >= 6) {  // PD+: the exact source-grouped BFS
-    size_t free_b = 0, total_b = 0;
-    RAMA_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    const int64_t per_warp = 20 * g.n;
-    int64_t W = (int64_t)(free_b / 4) / (per_warp > 0 ? per_warp : 1);
-    if (W > 148 * 8) W = 148 * 8;
-    if (W > ng) W = ng;
-    RAMA_REQUIRE(W >= 1, "not enough device memory for the PD+ separation scratch");
-    W = (W + 7) / 8 * 8;  // whole 8-warp blocks; every launched warp owns a scratch slice
-    Buf<unsigned long long> keys((size_t)W * g.n, ctx);
-    Buf<int32_t> par((size_t)W * g.n, ctx), pos((size_t)W * g.n, ctx), queue((size_t)W * g.n, ctx);
-    keys.fill_bytes(0xff);
-    KernelScope ks(ctx.s, "k_sep_bfs", 0.0);
-    k_sep_bfs<<<(unsigned)((W + 7) / 8), 256, 0, ctx.s>>>(gstart.p, ng, n2, Q2.p, NQ.p, g.u, g.v, csr.ptr.p,
-                                                          csr.adj.p, L, out.len.p, out.nodes.p, keys.p, par.p,
-                                                          pos.p, queue.p, g.n);
-    RAMA_LAUNCH_CHECK();
-    ctx.launches++;
-    return;
-  }
   Buf<uint8_t> fb(n2, ctx), gover(ng, ctx);
   fb.zero();
   gover.zero();
@@ -863,7 +933,7 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
                    4.0 * (double)(g.n + 1) + 4.0 * (double)csr.arcs + (16.0 + 4.0 * L) * (double)n2);
     k_sep_src<SrcTier1, kSrcThreads1, 12, false><<<(unsigned)blocks, kSrcThreads1, 0, ctx.s>>>(
         gstart.p, gsrc.p, (const int32_t*)nullptr, ng, ng, n2, Q2.p, qb.p, csr.ptr.p, csr.adj.p, L, out.len.p,
-        out.nodes.p, gover.p, fb.p, force ? 1 : 0);
+        out.nodes.p, gover.p, fb.p, force ? 1 : 0, capped);
     RAMA_LAUNCH_CHECK();
     ctx.launches++;
   }
@@ -880,7 +950,7 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
         KernelScope ks(ctx.s, "k_sep_src_mid", 0.0);
         k_sep_src<SrcTier15, kSrcThreads1, 12, true><<<(unsigned)blocks, kSrcThreads1, 0, ctx.s>>>(
             gstart.p, gsrc.p, G15.p, ng15, ng, n2, Q2.p, qb.p, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p,
-            gover2.p, fb.p, force ? 1 : 0);
+            gover2.p, fb.p, force ? 1 : 0, capped);
         RAMA_LAUNCH_CHECK();
         ctx.launches++;
       }
@@ -892,7 +962,7 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
         KernelScope ks(ctx.s, "k_sep_src_wide", 0.0);
         k_sep_src<SrcTier2, kSrcThreads2, 6, true><<<(unsigned)blocks, kSrcThreads2, 0, ctx.s>>>(
             gstart.p, gsrc.p, G2.p, ng2, ng, n2, Q2.p, qb.p, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p,
-            (uint8_t*)nullptr, fb.p, force == 1 ? 1 : 0);
+            (uint8_t*)nullptr, fb.p, force == 1 ? 1 : 0, capped);
         RAMA_LAUNCH_CHECK();
         ctx.launches++;
       }
@@ -922,7 +992,8 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
   if (n3 == 0) return;
   Buf<int32_t> Q4(n3, ctx);
   RAMA_KERNEL(ctx, k_gather_i32, n3, Q3.p, I3.p, n3, Q4.p);
-  RAMA_KERNEL(ctx, k_sep5, n3 * kSepLanes, Q4.p, n3, NQ.p, g.u, g.v, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p);
+  RAMA_KERNEL(ctx, k_sep5, n3 * kSepLanes, Q4.p, n3, NQ.p, g.u, g.v, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p,
+              capped);
 }
 
 // --------------------------------------------------------- triangulation

@@ -9,6 +9,7 @@
 // Merged (f(u) == f(v)) edges get row -1 and are dropped by the bucket sort,
 // which avoids a separate compaction pass.
 #include "internal.h"
+#include "sortreduce.cuh"
 
 namespace rama {
 
@@ -20,59 +21,81 @@ __global__ void k_iota(int32_t* x, int64_t n) {
 
 void iota(Ctx& ctx, int32_t* x, int64_t n) { RAMA_KERNEL(ctx, k_iota, n, x, n); }
 
-// head[p] = slot p starts a new (row, key-high) segment (p < limit)
-__global__ void k_seg_heads(const int32_t* __restrict__ row, const uint64_t* __restrict__ key, int64_t limit,
-                            uint8_t* __restrict__ head) {
-  GRID_STRIDE(p, limit) {
-    head[p] = (p == 0) || row[p] != row[p - 1] || (key[p] >> 32) != (key[p - 1] >> 32);
-  }
-}
-
-// out edge j = segment [heads[j], heads[j+1]) of the sorted slots
-__global__ void k_seg_reduce(const int32_t* __restrict__ heads, int64_t k, int64_t limit,
-                             const int32_t* __restrict__ row, const uint64_t* __restrict__ key,
-                             const double* __restrict__ c, const int32_t* __restrict__ src,
-                             int32_t* __restrict__ ou, int32_t* __restrict__ ov, double* __restrict__ oc) {
-  GRID_STRIDE(j, k) {
-    int64_t b = heads[j];
-    int64_t e = (j + 1 < k) ? heads[j + 1] : limit;
-    ou[j] = row[b];
-    ov[j] = (int32_t)(key[b] >> 32);
-    oc[j] = seg_sum(GatherF64{c, src + b}, e - b);  // c in sorted order, gathered in place
-  }
-}
-
-// reduce sorted slots [0, limit) into a canonical graph
-static Graph reduce_sorted(Ctx& ctx, int64_t n_out, int64_t limit, BucketSorted& bs, const double* c) {
-  Graph out;
-  out.n = n_out;
-  Buf<uint8_t> head(limit > 0 ? limit : 1, ctx);
-  RAMA_KERNEL(ctx, k_seg_heads, limit, bs.row.p, bs.key.p, limit, head.p);
-  Buf<int32_t> hp;
-  int64_t k = compact_indices(ctx, head.p, limit, hp);
-  out.m = k;
-  out.u.alloc(k > 0 ? k : 1, ctx.s);
-  out.v.alloc(k > 0 ? k : 1, ctx.s);
-  out.c.alloc(k > 0 ? k : 1, ctx.s);
-  RAMA_KERNEL(ctx, k_seg_reduce, k, hp.p, k, limit, bs.row.p, bs.key.p, c, bs.src.p, out.u.p, out.v.p, out.c.p);
-  return out;
-}
-
 // ---------------------------------------------------------- canonicalize
 
-__global__ void k_canon_prep(const int32_t* __restrict__ u, const int32_t* __restrict__ v, int64_t m, int64_t n,
-                             int32_t* __restrict__ row, uint64_t* __restrict__ key, int32_t* __restrict__ err) {
+// validation pass (graph.py:31-42): raised before any work
+__global__ void k_canon_check(const int32_t* __restrict__ u, const int32_t* __restrict__ v, int64_t m, int64_t n,
+                              int32_t* __restrict__ err) {
   GRID_STRIDE(i, m) {
-    int32_t a = u[i], b = v[i];
+    const int32_t a = u[i], b = v[i];
     if (a == b) atomicOr(err, 1);
-    if (a < 0 || b < 0 || a >= n || b >= n) {
-      atomicOr(err, 2);
-      a = 0; b = 0;
-    }
-    int32_t lo = a < b ? a : b, hi = a < b ? b : a;
-    row[i] = lo;
-    key[i] = ((uint64_t)(uint32_t)hi << 32) | (uint64_t)i;
+    if (a < 0 || b < 0 || a >= n || b >= n) atomicOr(err, 2);
   }
+}
+
+// items of a raw COO: row = min endpoint, key = (max << 32 | edge), pay = c
+struct CanonSrc {
+  static constexpr int kK = 1;
+  const int32_t* u;
+  const int32_t* v;
+  const double* c;
+  int64_t m;
+  __host__ __device__ __forceinline__ int64_t size() const { return m; }
+  __device__ __forceinline__ bool item(int64_t i, int, int32_t& row, uint64_t& key, double& pay) const {
+    const int32_t a = u[i], b = v[i];
+    row = a < b ? a : b;
+    key = ((uint64_t)(uint32_t)(a < b ? b : a) << 32) | (uint64_t)i;
+    pay = c[i];
+    return true;
+  }
+};
+
+// items of a contraction (contraction.py:148-160): row = min(f(u), f(v)),
+// key = (max << 32 | edge); merged edges (f(u) == f(v)) produce nothing
+struct ContractSrc {
+  static constexpr int kK = 1;
+  const int32_t* u;
+  const int32_t* v;
+  const double* c;
+  const int32_t* f;
+  int64_t m;
+  __host__ __device__ __forceinline__ int64_t size() const { return m; }
+  __device__ __forceinline__ bool item(int64_t i, int, int32_t& row, uint64_t& key, double& pay) const {
+    const int32_t a = __ldg(f + u[i]), b = __ldg(f + v[i]);
+    if (a == b) return false;
+    row = a < b ? a : b;
+    key = ((uint64_t)(uint32_t)(a < b ? b : a) << 32) | (uint64_t)i;
+    pay = c[i];
+    return true;
+  }
+};
+
+// one canonical edge per (row, hi) group: cost = np.add.reduceat order over
+// the group's source edges (keys embed the source index => source order)
+struct GraphEmit {
+  int32_t* ou;
+  int32_t* ov;
+  double* oc;
+  __device__ __forceinline__ bool keep(int32_t, uint64_t) const { return true; }
+  template <class A>
+  __device__ __forceinline__ void out(int64_t idx, int32_t row, uint64_t key, A pays, int64_t len) const {
+    ou[idx] = row;
+    ov[idx] = (int32_t)(key >> 32);
+    // reduceat: x0 + pairwise(x[1:]); two terms are x0 + x1 in either order
+    oc[idx] = len == 1 ? pays[0] : len == 2 ? __dadd_rn(pays[0], pays[1]) : seg_sum(pays, len);
+  }
+};
+
+template <class Src>
+static Graph sort_reduce_graph(Ctx& ctx, int64_t n_out, int64_t m_in, const Src& src) {
+  Graph out;
+  out.n = n_out;
+  out.u.alloc(m_in > 0 ? m_in : 1, ctx.s);
+  out.v.alloc(m_in > 0 ? m_in : 1, ctx.s);
+  out.c.alloc(m_in > 0 ? m_in : 1, ctx.s);
+  SrResult sr;
+  out.m = sort_reduce<32, true, true>(ctx, n_out, m_in, src, GraphEmit{out.u.p, out.v.p, out.c.p}, sr);
+  return out;
 }
 
 Graph canonicalize(Ctx& ctx, int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m) {
@@ -84,16 +107,13 @@ Graph canonicalize(Ctx& ctx, int64_t n, const int32_t* u, const int32_t* v, cons
     g.n = n;
     return g;
   }
-  Buf<int32_t> row(m, ctx), err(1, ctx);
-  Buf<uint64_t> key(m, ctx);
+  Buf<int32_t> err(1, ctx);
   err.zero();
-  RAMA_KERNEL(ctx, k_canon_prep, m, u, v, m, n, row.p, key.p, err.p);
+  RAMA_KERNEL(ctx, k_canon_check, m, u, v, m, n, err.p);
   int32_t e = read_scalar(ctx, err.p);
   RAMA_REQUIRE(!(e & 1), "self-loops are not allowed");
   RAMA_REQUIRE(!(e & 2), "edge endpoint out of range");
-  BucketSorted bs;
-  bucket_sort(ctx, n, m, row.p, key.p, bs);
-  return reduce_sorted(ctx, n, m, bs, c);
+  return sort_reduce_graph(ctx, n, m, CanonSrc{u, v, c, m});
 }
 
 // ------------------------------------------------------------ components
@@ -178,47 +198,29 @@ int64_t components(Ctx& ctx, int64_t n, const int32_t* su, const int32_t* sv, in
 
 // -------------------------------------------------------------- contract
 
-__global__ void k_contract_prep(const int32_t* __restrict__ u, const int32_t* __restrict__ v,
-                                const double* __restrict__ c, int64_t m, const int32_t* __restrict__ f,
-                                int32_t n_out, int32_t* __restrict__ row, uint64_t* __restrict__ key,
-                                double* __restrict__ jc) {
-  GRID_STRIDE(i, m) {
-    int32_t a = f[u[i]], b = f[v[i]];
-    if (a == b) {
-      row[i] = -1;  // merged edge: dropped by the bucket sort, joined mass
-      key[i] = (uint64_t)i;
-      if (jc) jc[i] = c[i];
-    } else {
-      int32_t lo = a < b ? a : b, hi = a < b ? b : a;
-      row[i] = lo;
-      key[i] = ((uint64_t)(uint32_t)hi << 32) | (uint64_t)i;
-      if (jc) jc[i] = 0.0;
-    }
-  }
+// mass of the merged edges (contraction.py:151): only when a caller asks
+__global__ void k_joined_mass(const int32_t* __restrict__ u, const int32_t* __restrict__ v,
+                              const double* __restrict__ c, int64_t m, const int32_t* __restrict__ f,
+                              double* __restrict__ jc) {
+  GRID_STRIDE(i, m) jc[i] = (f[u[i]] == f[v[i]]) ? c[i] : 0.0;
 }
 
 Graph contract(Ctx& ctx, const GraphView& g, const int32_t* map, int64_t n_targets, double* joined) {
   // algorithmic bytes: 24 m_in + 16 m_out
   ProfScope prof(ctx.s, kFamContract, 24.0 * (double)g.m);
-  int64_t m = g.m;
+  const int64_t m = g.m;
   if (m == 0) {
     if (joined) *joined = 0.0;
     Graph out;
     out.n = n_targets;
     return out;
   }
-  Buf<int32_t> row(m, ctx);
-  Buf<uint64_t> key(m, ctx);
-  Buf<double> jc;
-  if (joined) jc.alloc(m, ctx.s);
-  prof_set_bytes(36.0 * (double)m);
-  RAMA_KERNEL(ctx, k_contract_prep, m, g.u, g.v, g.c, m, map, (int32_t)n_targets, row.p, key.p,
-              joined ? jc.p : (double*)nullptr);
-  if (joined) *joined = device_sum(ctx, jc.p, m);
-  BucketSorted bs;
-  bucket_sort(ctx, n_targets, m, row.p, key.p, bs, true);
-  int64_t limit = bs.total;
-  Graph out = reduce_sorted(ctx, n_targets, limit, bs, g.c);
+  if (joined) {
+    Buf<double> jc(m, ctx);
+    RAMA_KERNEL(ctx, k_joined_mass, m, g.u, g.v, g.c, m, map, jc.p);
+    *joined = device_sum(ctx, jc.p, m);
+  }
+  Graph out = sort_reduce_graph(ctx, n_targets, m, ContractSrc{g.u, g.v, g.c, map, m});
   prof.add_bytes(16.0 * (double)out.m);
   return out;
 }

@@ -72,7 +72,9 @@ struct CycleRows {
   Buf<int32_t> nodes;  // rows * L
 };
 // a4/a5 _separate_arrays (dual.py:155-197)
-void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out);
+// exact: deviation D2's truncated 5-cycle searches (hub neighbourhoods) are
+// rerun as the reference BFS (SolverConfig.exact_separation)
+void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out, bool exact = false);
 
 struct DualState {
   int64_t n = 0, m_orig = 0, m_aug = 0, T = 0;
@@ -124,6 +126,7 @@ struct SolveConfig {
   double switch_fraction = 0.1;
   int max_rounds = 100;
   int separation_rounds = 1;
+  bool exact_separation = false;  // no D2 (rama_cfg.flags bit 0)
 };
 
 struct RoundInfo {

@@ -11,6 +11,7 @@
 // huge rows (power-law hubs) CUB's segmented sort.  CUB is used only
 // for generic scans/selection/segmented sorting, never for domain logic.
 #include "common.cuh"
+#include "sortreduce.cuh"
 
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
@@ -23,8 +24,6 @@
 
 namespace rama {
 
-static int g_num_sms = 0;
-
 HostStats& host_stats() {
   static thread_local HostStats hs;
   return hs;
@@ -34,7 +33,7 @@ HostStats& host_stats() {
 // cudaFreeHost cost milliseconds and cudaFreeHost synchronises the device.
 namespace {
 std::mutex g_pin_mu;
-std::vector<int64_t*> g_pin_free;
+std::vector<std::pair<int64_t*, cudaEvent_t>> g_pin_free;
 }  // namespace
 
 Ctx::Ctx(cudaStream_t st) : s(st) {
@@ -42,27 +41,38 @@ Ctx::Ctx(cudaStream_t st) : s(st) {
   {
     std::lock_guard<std::mutex> lk(g_pin_mu);
     if (!g_pin_free.empty()) {
-      pinned = g_pin_free.back();
+      pinned = g_pin_free.back().first;
+      ev = g_pin_free.back().second;
       g_pin_free.pop_back();
     }
   }
-  if (!pinned) RAMA_CUDA(cudaMallocHost((void**)&pinned, 64 * sizeof(int64_t)));
+  if (!pinned) {
+    RAMA_CUDA(cudaMallocHost((void**)&pinned, 64 * sizeof(int64_t)));
+    RAMA_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  }
 }
 
 Ctx::~Ctx() {
   if (pinned) {
     std::lock_guard<std::mutex> lk(g_pin_mu);
-    g_pin_free.push_back(pinned);
+    g_pin_free.emplace_back(pinned, ev);
   }
 }
 
 // ------------------------------------------------------ caching allocator
 
 namespace {
+// blocks are keyed by (device, stream, size class): the default stream's
+// handle is 0 on every device, so the stream alone does not identify memory
 struct CacheKey {
+  int dev;
   cudaStream_t s;
   size_t bytes;  // class size
-  bool operator<(const CacheKey& o) const { return s < o.s || (s == o.s && bytes < o.bytes); }
+  bool operator<(const CacheKey& o) const {
+    if (dev != o.dev) return dev < o.dev;
+    if (s != o.s) return s < o.s;
+    return bytes < o.bytes;
+  }
 };
 std::mutex g_cache_mu;
 std::map<CacheKey, std::vector<void*>> g_cache;
@@ -75,13 +85,20 @@ inline size_t class_bytes(size_t bytes) {
   size_t step = (size_t)1 << (e - 2);
   return (bytes + step - 1) / step * step;
 }
+
+inline int cur_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
 }  // namespace
 
 void* dev_alloc(size_t bytes, cudaStream_t s) {
   size_t b = class_bytes(bytes);
+  const int dev = cur_device();
   {
     std::lock_guard<std::mutex> lk(g_cache_mu);
-    auto it = g_cache.find(CacheKey{s, b});
+    auto it = g_cache.find(CacheKey{dev, s, b});
     if (it != g_cache.end() && !it->second.empty()) {
       void* p = it->second.back();
       it->second.pop_back();
@@ -102,24 +119,54 @@ void* dev_alloc(size_t bytes, cudaStream_t s) {
 
 void dev_free(void* p, size_t bytes, cudaStream_t s) {
   size_t b = class_bytes(bytes);
+  const int dev = cur_device();
   std::lock_guard<std::mutex> lk(g_cache_mu);
   if (g_cached_bytes + b > ((size_t)48 << 30)) {  // cap what the cache holds
     cudaFreeAsync(p, s);
     return;
   }
-  g_cache[CacheKey{s, b}].push_back(p);
+  g_cache[CacheKey{dev, s, b}].push_back(p);
   g_cached_bytes += b;
 }
 
 void dev_release_stream(cudaStream_t s) {
+  const int dev = cur_device();
   std::lock_guard<std::mutex> lk(g_cache_mu);
-  for (auto it = g_cache.lower_bound(CacheKey{s, 0}); it != g_cache.end() && it->first.s == s;) {
+  for (auto it = g_cache.begin(); it != g_cache.end();) {
+    if (it->first.dev != dev || it->first.s != s) {
+      ++it;
+      continue;
+    }
     for (void* p : it->second) {
       cudaFreeAsync(p, s);
       g_cached_bytes -= it->first.bytes;
     }
     it = g_cache.erase(it);
   }
+}
+
+void dev_release_all() {
+  std::vector<int> devs;
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    int cur = cur_device();
+    for (auto& kv : g_cache) {
+      cudaSetDevice(kv.first.dev);
+      for (void* p : kv.second) cudaFreeAsync(p, kv.first.s);
+      devs.push_back(kv.first.dev);
+    }
+    g_cache.clear();
+    g_cached_bytes = 0;
+    cudaSetDevice(cur);
+  }
+  int cur = cur_device();
+  for (int d : devs) {
+    cudaSetDevice(d);
+    cudaDeviceSynchronize();
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+  }
+  cudaSetDevice(cur);
 }
 
 void reserve_pool(Ctx& ctx, size_t bytes) {
@@ -142,17 +189,31 @@ void reserve_pool(Ctx& ctx, size_t bytes) {
   RAMA_CUDA(cudaFreeAsync(p, ctx.s));
 }
 
+namespace {
+constexpr int kMaxDevices = 64;
+std::mutex g_pool_mu;
+bool g_pool_done[kMaxDevices] = {false};
+int g_sms[kMaxDevices] = {0};
+}  // namespace
+
+// per device: the stream-ordered pool keeps freed memory (release threshold
+// raised), and the SM count sizes the grids of kernels launched there
 void ensure_pool_configured() {
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    RAMA_CUDA(cudaGetDevice(&dev));
-    cudaMemPool_t pool;
-    RAMA_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
-    uint64_t thr = UINT64_MAX;
-    RAMA_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-    RAMA_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-  });
+  const int dev = cur_device();
+  RAMA_REQUIRE(dev >= 0 && dev < kMaxDevices, "device ordinal out of range");
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (g_pool_done[dev]) return;
+  cudaMemPool_t pool;
+  RAMA_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t thr = UINT64_MAX;
+  RAMA_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  RAMA_CUDA(cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev));
+  g_pool_done[dev] = true;
+}
+
+int num_sms() {
+  const int dev = cur_device();
+  return (dev >= 0 && dev < kMaxDevices && g_sms[dev] > 0) ? g_sms[dev] : 148;
 }
 
 // ------------------------------------------------------------- profiling
@@ -319,7 +380,7 @@ bool trace_print() { return trace_level() >= 1; }
 
 unsigned capped_grid(int64_t work, int block) {
   int64_t g = (work + block - 1) / block;
-  int64_t cap = (int64_t)(g_num_sms > 0 ? g_num_sms : 148) * 32;  // 32 x 256 threads per SM (more loads in flight than 16)
+  int64_t cap = (int64_t)num_sms() * 32;  // 32 x 256 threads per SM (more loads in flight than 16)
   if (g > cap) g = cap;
   if (g < 1) g = 1;
   return (unsigned)g;
@@ -689,6 +750,58 @@ void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint6
   RAMA_CUDA(cub::DeviceSegmentedSort::SortPairs(tmp.p, tb, k1.p, k2.p, s1.p, s2.p, (int)tot, (int)nb, boff.p,
                                                 boff.p + 1, ctx.s));
   k_big_unstage<<<g, kBlock, 0, ctx.s>>>(huge_list, nb, out.row_ptr.p, boff.p, k2.p, s2.p, out.key.p, out.src.p);
+  RAMA_LAUNCH_CHECK();
+  ctx.launches += 3;
+}
+
+// ------------------------------------------------ sort-reduce: huge rows
+
+__global__ void k_sr_hlen(const int32_t* __restrict__ rows, int64_t nb, const int32_t* __restrict__ ptr,
+                          int32_t* __restrict__ len) {
+  GRID_STRIDE(i, nb) len[i] = ptr[rows[i] + 1] - ptr[rows[i]];
+}
+
+__global__ void k_sr_hstage(const int32_t* __restrict__ rows, int64_t nb, const int32_t* __restrict__ ptr,
+                            const int32_t* __restrict__ off, const SrItem* __restrict__ items,
+                            uint64_t* __restrict__ k, uint64_t* __restrict__ v) {
+  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    const int32_t base = ptr[rows[b]], len = ptr[rows[b] + 1] - base, o = off[b];
+    for (int32_t j = threadIdx.x; j < len; j += blockDim.x) {
+      k[o + j] = items[base + j].key;
+      v[o + j] = (uint64_t)__double_as_longlong(items[base + j].pay);
+    }
+  }
+}
+
+__global__ void k_sr_hunstage(const int32_t* __restrict__ rows, int64_t nb, const int32_t* __restrict__ ptr,
+                              const int32_t* __restrict__ off, const uint64_t* __restrict__ k,
+                              const uint64_t* __restrict__ v, SrItem* __restrict__ items) {
+  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    const int32_t base = ptr[rows[b]], len = ptr[rows[b] + 1] - base, o = off[b];
+    for (int32_t j = threadIdx.x; j < len; j += blockDim.x) {
+      SrItem it;
+      it.key = k[o + j];
+      it.pay = __longlong_as_double((long long)v[o + j]);
+      items[base + j] = it;
+    }
+  }
+}
+
+void sr_sort_huge(Ctx& ctx, const int32_t* rowptr, const int32_t* rows, int64_t nb, SrItem* items) {
+  Buf<int32_t> blen(nb, ctx), boff(nb + 1, ctx);
+  RAMA_KERNEL(ctx, k_sr_hlen, nb, rows, nb, rowptr, blen.p);
+  const int64_t tot = exclusive_scan(ctx, blen.p, boff.p, nb, true);
+  Buf<uint64_t> k1(tot, ctx), k2(tot, ctx), v1(tot, ctx), v2(tot, ctx);
+  const unsigned g = (unsigned)std::min<int64_t>(nb, 4096);
+  k_sr_hstage<<<g, kBlock, 0, ctx.s>>>(rows, nb, rowptr, boff.p, items, k1.p, v1.p);
+  RAMA_LAUNCH_CHECK();
+  size_t tb = 0;
+  RAMA_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, tb, k1.p, k2.p, v1.p, v2.p, (int)tot, (int)nb, boff.p,
+                                                boff.p + 1, ctx.s));
+  Buf<uint8_t> tmp(tb, ctx);
+  RAMA_CUDA(cub::DeviceSegmentedSort::SortPairs(tmp.p, tb, k1.p, k2.p, v1.p, v2.p, (int)tot, (int)nb, boff.p,
+                                                boff.p + 1, ctx.s));
+  k_sr_hunstage<<<g, kBlock, 0, ctx.s>>>(rows, nb, rowptr, boff.p, k2.p, v2.p, items);
   RAMA_LAUNCH_CHECK();
   ctx.launches += 3;
 }

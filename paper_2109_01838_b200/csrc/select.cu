@@ -391,12 +391,7 @@ __global__ void k_rank_coop(int64_t na, int steps, int32_t* d1, int32_t* n1, int
 }
 
 static unsigned coop_blocks(const void* fn) {
-  static const int sms = [] {  // thread-safe init (batch workers launch concurrently)
-    int dev = 0, v = 0;
-    RAMA_CUDA(cudaGetDevice(&dev));
-    RAMA_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
-    return v;
-  }();
+  const int sms = num_sms();  // per device
   int per_sm = 0;
   RAMA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBlock, 0));
   return (unsigned)(sms * (per_sm < 4 ? per_sm : 4));

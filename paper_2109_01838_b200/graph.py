@@ -161,6 +161,10 @@ def clustering_cost(g, labels):
     if g.num_edges == 0:
         return 0.0
     du, dv, dc = g.device()
+    if not (lab.dtype.kind in "iu" and (lab.size == 0 or (lab.min() >= 0 and lab.max() < 2 ** 31))):
+        # the kernel compares int32 labels: map arbitrary labels (any dtype,
+        # negative or >= 2^31) to dense ids first, equality is preserved
+        lab = np.unique(lab, return_inverse=True)[1].ravel()
     dl = L.i32(lab)
     out = L.ctypes.c_double()
     L.call("rama_clustering_cost", g.num_nodes, L.ptr(du), L.ptr(dv), L.ptr(dc), g.num_edges, L.ptr(dl),

@@ -117,18 +117,33 @@ def solve_device(n, du, dv, dc, m, cfg, labels=None):
     return labels, float(out[0]), float(out[1]), _records(trace, min(nr.value, k))
 
 
+def _empty_solution(cfg):
+    """The reference's result on a graph without nodes, trace included
+    (solver.py:93-240 run on n = 0: every loop makes one identity round)."""
+    lab = np.zeros(0, np.int64)
+    if cfg.mode == "GAEC":
+        return Solution(lab, 0.0, float("-inf"), [RoundRecord(1, "gaec", 0, 0, 0, None, False, 0, 0.0)])
+    if cfg.mode == "P":
+        return Solution(lab, 0.0, float("-inf"), [RoundRecord(1, "contract", 0, 0, 0, None, False, 0, 0.0)])
+    if cfg.mode == "D":
+        recs = [RoundRecord(r, "dual", 0, 0, 0, 0.0, True, 0, 0.0) for r in range(1, cfg.separation_rounds + 1)]
+        return Solution(lab, 0.0, 0.0, recs)
+    recs = [RoundRecord(1, "primal-dual", 0, 0, 0, 0.0, True, 0, 0.0),
+            RoundRecord(2, "cleanup", 0, 0, 0, None, False, 0, 0.0)]
+    return Solution(lab, 0.0, 0.0, recs)
+
+
 def solve(g, cfg):
     """Run the solver in the configured mode (solver.py:243-252)."""
     cfg.validate()
     n, m = g.num_nodes, g.num_edges
+    if n == 0:
+        return _empty_solution(cfg)
     if m:
         du, dv, dc = g.device()
     else:
         du = dv = L.empty_i32(1)
         dc = L.empty_f64(1)
-    if n == 0:
-        lb = float("-inf") if cfg.mode in ("P", "GAEC") else 0.0
-        return Solution(np.zeros(0, np.int64), 0.0, lb, [])
     labels, primal, lb, trace = solve_device(n, du, dv, dc, m, cfg)
     return Solution(L.host_i64(labels, n), primal, lb, trace)
 
