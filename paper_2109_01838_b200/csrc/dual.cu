@@ -163,11 +163,13 @@ __device__ __forceinline__ int32_t level2_parent(const int32_t* __restrict__ ptr
 // lexicographic argmin with shuffles (keys packed as (parent << 32 | node)).
 constexpr int kSepLanes = 8;
 
-// Deviation D2, dense / power-law neighbourhoods only: the
-// 5-cycle search looks at no more than kHubCap neighbours z of b and skips
-// candidates z with more than kHubCap positive neighbours, bounding the
-// per-edge work at kHubCap^2 lookups (the reference BFS spends ~12 ms per
-// edge on C4).  Grid-like graphs (C1-C3, C5) never reach the caps.
+// Dense / power-law neighbourhoods only: the pull-style 5-cycle search
+// (per z in N(b), scan N(z)) looks at no more than kHubCap neighbours z of b
+// and stops at candidates z with more than kHubCap positive neighbours,
+// bounding the per-edge work at kHubCap^2 lookups; a search that hit a cap
+// is flagged and answered again by the exact ordered search
+// (k_sep5_ordered), which stops at its first hit.  Grid-like graphs (C1-C3,
+// C5) never reach the caps.
 constexpr int32_t kHubCap = 128;
 
 __device__ __forceinline__ uint64_t group_min(uint64_t x) {
@@ -309,7 +311,7 @@ __global__ void k_sep5(const int32_t* __restrict__ Q, int64_t nq, const int32_t*
     int32_t bz = 0x7fffffff;
     // trip counts are warp-uniform: the group shuffles below use the full mask
     int32_t lbmax = warp_max(min(lb, kHubCap));
-    if (capped && live && g == 0 && lb > kHubCap) capped[q] = 1;  // D2 truncated this search
+    if (capped && live && g == 0 && lb > kHubCap) capped[q] = 1;  // truncated: answered again exactly
     for (int32_t k = 0; k < lbmax; k++) {
       bool zok = live && k < lb;
       int32_t z = zok ? adj[pb + k] : 0;
@@ -320,7 +322,7 @@ __global__ void k_sep5(const int32_t* __restrict__ Q, int64_t nq, const int32_t*
       if (zok) {
         pz = ptr[z];
         lz = ptr[z + 1] - pz;
-        if (lz > kHubCap) {  // hub candidate skipped (D2)
+        if (lz > kHubCap) {  // hub candidate skipped: flagged for the exact search
           zok = false;
           if (capped) capped[q] = 1;
         } else if (first_common(Na, la, adj + pz, lz) >= 0) {
@@ -350,6 +352,67 @@ __global__ void k_sep5(const int32_t* __restrict__ Q, int64_t nq, const int32_t*
       int32_t* row = out_nodes + q * (int64_t)L;
       out_len[q] = 5;
       row[0] = a; row[1] = (int32_t)(bx_y >> 32); row[2] = (int32_t)(uint32_t)bx_y; row[3] = bz; row[4] = b;
+    }
+  }
+}
+
+// Exact 5-cycles for the searches the capped passes truncated (hub
+// neighbourhoods).  At this stage (a, b) has no 3- or 4-cycle, so every
+// z in N(b) is at BFS level >= 3 and the reference's answer
+// z* = argmin_(z in N(b)) (px(py(z)), py(z), z) is the FIRST (x, y) in
+// lexicographic order -- x in N(a) ascending, y in N(x) ascending, y not in
+// {a} u N(a) -- with N(y) & N(b) non-empty, and z* = min(N(y) & N(b)).  (A y
+// met again under a larger x was already tested under px(y) and failed, so
+// the first hit has px(y) = x.)  One warp per edge, lanes over N(x) in
+// ascending chunks; the scan stops at the first hit, which on power-law
+// graphs comes within the first hub rows.
+__global__ void k_sep5_ordered(const int32_t* __restrict__ Qx, int64_t nx, const int32_t* __restrict__ NQ,
+                               const int32_t* __restrict__ u, const int32_t* __restrict__ v,
+                               const int32_t* __restrict__ ptr, const int32_t* __restrict__ adj, int L,
+                               int32_t* __restrict__ out_len, int32_t* __restrict__ out_nodes) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t W = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = w0; i < nx; i += W) {
+    const int32_t q = Qx[i];
+    const int32_t e = NQ[q];
+    const int32_t a = u[e], b = v[e];
+    const int32_t* Na = adj + ptr[a];
+    const int32_t la = ptr[a + 1] - ptr[a];
+    const int32_t* Nb = adj + ptr[b];
+    const int32_t lb = ptr[b + 1] - ptr[b];
+    int32_t hx = -1, hy = -1, hz = -1;
+    for (int32_t xi = 0; xi < la && hx < 0; xi++) {
+      const int32_t x = Na[xi];
+      const int32_t* Nx = adj + ptr[x];
+      const int32_t lx = ptr[x + 1] - ptr[x];
+      for (int32_t j0 = 0; j0 < lx; j0 += 32) {
+        const int32_t j = j0 + lane;
+        int32_t z = -1, y = -1;
+        if (j < lx) {
+          y = Nx[j];
+          if (y != a && !in_sorted(Na, la, y)) z = first_common(adj + ptr[y], ptr[y + 1] - ptr[y], Nb, lb);
+        }
+        const unsigned hit = __ballot_sync(0xffffffffu, z >= 0);
+        if (hit) {
+          const int src = __ffs(hit) - 1;
+          hx = x;
+          hy = __shfl_sync(0xffffffffu, y, src);
+          hz = __shfl_sync(0xffffffffu, z, src);
+          break;
+        }
+      }
+    }
+    if (lane == 0) {
+      int32_t* row = out_nodes + (int64_t)q * L;
+      if (hx >= 0) {
+        out_len[q] = 5;
+        row[0] = a; row[1] = hx; row[2] = hy; row[3] = hz; row[4] = b;
+        for (int j = 5; j < L; j++) row[j] = 0;
+      } else {
+        out_len[q] = 0;
+        for (int j = 0; j < L; j++) row[j] = 0;
+      }
     }
   }
 }
@@ -612,14 +675,14 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sep_src(
         uint64_t bk = ~0ULL;
         int32_t bz = 0x7fffffff;
         const int32_t lbc = min(lb, kHubCap);
-        if (capped && lane == 0 && lb > kHubCap) capped[q] = 1;  // D2 truncated this search
+        if (capped && lane == 0 && lb > kHubCap) capped[q] = 1;  // truncated: answered again exactly
         for (int32_t t = lane; t < lbc; t += kGrp) {
           int32_t z = adj[pb + t];
           if (z == a || (f1.maybe(z) && src_in_l1(l1, la, z)) ||
               (f2.maybe(z) && src_lookup<T::kHashBits>(hk, hv, z) >= 0))
             continue;
           const int32_t pz = ptr[z], lz = ptr[z + 1] - pz;
-          if (lz > kHubCap) {  // hub candidate skipped (D2)
+          if (lz > kHubCap) {  // hub candidate skipped: flagged for the exact search
             if (capped) capped[q] = 1;
             continue;
           }
@@ -793,15 +856,6 @@ __global__ void k_bfs_heads(const int32_t* __restrict__ Qx, int64_t nx, const in
   GRID_STRIDE(i, nx) head[i] = (i == 0) || u[NQ[Qx[i]]] != u[NQ[Qx[i - 1]]];
 }
 
-__global__ void k_clear_rows(const int32_t* __restrict__ Qx, int64_t nx, int L, int32_t* __restrict__ out_len,
-                             int32_t* __restrict__ out_nodes) {
-  GRID_STRIDE(i, nx) {
-    const int32_t q = Qx[i];
-    out_len[q] = 0;
-    for (int j = 0; j < L; j++) out_nodes[(int64_t)q * L + j] = 0;
-  }
-}
-
 static void run_sep_bfs(Ctx& ctx, const GraphView& g, const int32_t* ptr, const int32_t* adj, const int32_t* NQ,
                         const int32_t* Qx, int64_t nx, int L, CycleRows& out) {
   if (nx == 0) return;
@@ -854,7 +908,7 @@ __global__ void k_sep_stats(const int32_t* __restrict__ Q2, const int32_t* __res
 static void separate_tables(Ctx& ctx, const GraphView& g, int L, CycleRows& out, const PosCSR& csr,
                             const Buf<int32_t>& NQ, int64_t nq, uint8_t* capped);
 
-void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out, bool exact) {
+void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
   ProfScope prof(ctx.s, kFamSeparate);
   RAMA_REQUIRE(L >= 3, "max_len must be at least 3");
   Buf<int32_t> NQ;
@@ -881,17 +935,22 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out, bool exact) {
     return;
   }
   Buf<uint8_t> capped;
-  if (exact && L >= 5) {
+  if (L >= 5) {
     capped.alloc(nq, ctx.s);
     capped.zero();
   }
   separate_tables(ctx, g, L, out, csr, NQ, nq, capped.p);
-  if (capped.p) {  // exact opt-out of deviation D2: truncated searches rerun as the reference BFS
+  if (capped.p) {  // the truncated 5-cycle searches rerun exactly
     Buf<int32_t> Qx;
     const int64_t nx = compact_indices(ctx, capped.p, nq, Qx);
     if (nx > 0) {
-      RAMA_KERNEL(ctx, k_clear_rows, nx, Qx.p, nx, L, out.len.p, out.nodes.p);
-      run_sep_bfs(ctx, g, csr.ptr.p, csr.adj.p, NQ.p, Qx.p, nx, L, out);
+      if (trace_print()) fprintf(stderr, "[rama] exact 5-cycle searches %lld\n", (long long)nx);
+      const int64_t blocks = std::min<int64_t>((nx + 7) / 8, (int64_t)num_sms() * 16);
+      KernelScope ks(ctx.s, "k_sep5_ordered", 0.0);
+      k_sep5_ordered<<<(unsigned)blocks, 256, 0, ctx.s>>>(Qx.p, nx, NQ.p, g.u, g.v, csr.ptr.p, csr.adj.p, L,
+                                                          out.len.p, out.nodes.p);
+      RAMA_LAUNCH_CHECK();
+      ctx.launches++;
     }
   }
 }

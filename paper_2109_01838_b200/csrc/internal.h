@@ -72,9 +72,9 @@ struct CycleRows {
   Buf<int32_t> nodes;  // rows * L
 };
 // a4/a5 _separate_arrays (dual.py:155-197)
-// exact: deviation D2's truncated 5-cycle searches (hub neighbourhoods) are
-// rerun as the reference BFS (SolverConfig.exact_separation)
-void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out, bool exact = false);
+// (the 5-cycle searches the capped table passes truncate -- hub
+// neighbourhoods -- are rerun by the exact ordered search)
+void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out);
 
 struct DualState {
   int64_t n = 0, m_orig = 0, m_aug = 0, T = 0;
@@ -126,7 +126,6 @@ struct SolveConfig {
   double switch_fraction = 0.1;
   int max_rounds = 100;
   int separation_rounds = 1;
-  bool exact_separation = false;  // no D2 (rama_cfg.flags bit 0)
 };
 
 struct RoundInfo {

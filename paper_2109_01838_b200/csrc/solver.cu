@@ -81,7 +81,7 @@ void solve(Ctx& ctx, const GraphView& g, const SolveConfig& cfg, int32_t* labels
       auto t0 = clk::now();
       if (rnd == 1) {
         CycleRows cyc;
-        separate(ctx, g, cfg.max_cycle_length, cyc, cfg.exact_separation);
+        separate(ctx, g, cfg.max_cycle_length, cyc);
         triangulate(ctx, g, cyc, st);
       } else {
         extend_separation(ctx, st, cfg.max_cycle_length);
@@ -136,7 +136,7 @@ void solve(Ctx& ctx, const GraphView& g, const SolveConfig& cfg, int32_t* labels
         tp = clk::now();
       };
       CycleRows cyc;
-      separate(ctx, cur.view(), cfg.max_cycle_length, cyc, cfg.exact_separation);
+      separate(ctx, cur.view(), cfg.max_cycle_length, cyc);
       mark(0);
       DualState st;
       triangulate(ctx, cur.view(), cyc, st);

@@ -194,10 +194,11 @@ def test_separation_dense_and_hub_sources_match_oracle():
     """Sources too large for the 8-lane tables (dense neighbourhoods: tier-2
     tables) and power-law hubs (row-intersection kernels, including the
     4-cycle search from the target's side when |N(a)| > 4 |N(b)|) give the
-    reference's cycles.  Power-law graphs are compared up to L = 4: the
-    5-cycle search caps hub neighbourhoods (DESIGN.md deviation D2)."""
+    reference's cycles.  On the power-law graphs the 5-cycle searches the
+    capped passes truncate are answered by the exact ordered search."""
     cases = [(instances.random_coo(300, 0.15, seed=s), (3, 4, 5)) for s in range(2)]
-    cases += [(instances.chung_lu_coo(3000, 2.1, 40000, seed=s), (3, 4)) for s in range(2)]
+    cases += [(instances.chung_lu_coo(3000, 2.1, 40000, seed=s), (3, 4, 5)) for s in range(3)]
+    cases += [(instances.chung_lu_coo(1000, 1.8, 30000, seed=s), (5,)) for s in range(2)]
     for (n, u, v, c), lengths in cases:
         g, og = _both(n, u, v, c)
         for L in lengths:
