@@ -36,7 +36,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 BATCH_INSTANCES = 64   # C5: 64 independent 512x512 grids per step
-BATCH_WORKERS = int(os.environ.get("RAMA_BATCH_WORKERS", "8"))  # concurrent streams (host threads) per GPU for a batch
+BATCH_WORKERS = int(os.environ.get("RAMA_BATCH_WORKERS", "1"))  # union groups (streams) per GPU for a batch
 
 
 def parse():
@@ -303,7 +303,7 @@ def b200_arm(args):
 
         e2e_h2d, e2e_d2h = int(m * 16), int(labels.numel() * 4 + 16 * (hi - lo))
         job = {"instances_per_step": count, "instances_per_gpu": hi - lo, "nodes_per_instance": n,
-               "edges_per_instance": m_inst, "concurrent_streams_per_gpu": BATCH_WORKERS}
+               "edges_per_instance": m_inst, "union_groups_per_gpu": BATCH_WORKERS}
     else:
         n, u, v, c = instances.make(args.workload, seed=rank)
         g = P.WeightedGraph(n, u, v, c)  # canonicalised on the GPU (not timed)

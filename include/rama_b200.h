@@ -115,18 +115,23 @@ int rama_solve_host(int64_t n, const int32_t* u, const int32_t* v, const double*
                     const rama_cfg* cfg, int32_t* labels, double* primal_lb, rama_round* trace,
                     int32_t max_trace, int32_t* n_rounds, void* stream);
 
-/* Batch of independent instances, solved
- * concurrently on `workers` internal streams (one host thread each; 0 = 8).
- * Instance i is the COO slice [edge_off[i], edge_off[i+1]) of u, v, c with
- * node ids local to the instance, n_i = node_off[i+1] - node_off[i] nodes;
- * its labels go to labels + node_off[i].  node_off, edge_off (count + 1
- * entries) and primal_lb (2 * count: {primal, lower_bound} per instance)
- * are HOST arrays; u, v, c, labels are device arrays.  All work is ordered
- * after prior work on `stream` and the call returns when it is done.
- * Replaces a Python loop of solve() calls (solver.py:243-252). */
+/* Batch of independent instances; replaces a
+ * Python loop of solve() calls (solver.py:243-252).  Instance i is the COO
+ * slice [edge_off[i], edge_off[i+1]) of u, v, c with node ids local to the
+ * instance, n_i = node_off[i+1] - node_off[i] nodes; its labels go to
+ * labels + node_off[i].  node_off, edge_off (count + 1 entries), primal_lb
+ * (2 * count: {primal, lower_bound} per instance), trace (count x max_trace
+ * records, instance-major; may be NULL) and n_rounds (count; may be NULL)
+ * are HOST arrays; u, v, c, labels are device arrays.
+ * Modes P / PD / PD+: the instances are split into `workers` contiguous
+ * groups (0 = 1), each solved as ONE disjoint-union graph on its own
+ * internal stream -- every round's kernels run once for the whole group, and
+ * each instance's labels, objectives and trace equal its single solve bit for
+ * bit.  Modes D / GAEC: one solve per instance on `workers` streams.  All work
+ * is ordered after prior work on `stream`; the call returns when it is done. */
 int rama_solve_batch(int64_t count, const int64_t* node_off, const int64_t* edge_off, const int32_t* u,
                      const int32_t* v, const double* c, const rama_cfg* cfg, int32_t* labels, double* primal_lb,
-                     int32_t workers, void* stream);
+                     rama_round* trace, int32_t max_trace, int32_t* n_rounds, int32_t workers, void* stream);
 
 /* ---- graph core ----------------------------------------------------------- */
 

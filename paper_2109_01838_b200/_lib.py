@@ -74,7 +74,8 @@ _SIGS = {
                    _I32P, _vp],
     "rama_solve_host": [_i64, _vp, _vp, _vp, _i64, ctypes.POINTER(RamaCfg), _vp, _F64P, ctypes.POINTER(RamaRound),
                         _i32, _I32P, _vp],
-    "rama_solve_batch": [_i64, _I64P, _I64P, _vp, _vp, _vp, ctypes.POINTER(RamaCfg), _vp, _F64P, _i32, _vp],
+    "rama_solve_batch": [_i64, _I64P, _I64P, _vp, _vp, _vp, ctypes.POINTER(RamaCfg), _vp, _F64P,
+                         ctypes.POINTER(RamaRound), _i32, _I32P, _i32, _vp],
     "rama_canonicalize": [_i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _I64P, _vp],
     "rama_clustering_cost": [_i64, _vp, _vp, _vp, _i64, _vp, _F64P, _vp],
     "rama_components": [_i64, _vp, _vp, _i64, _vp, _I64P, _vp],

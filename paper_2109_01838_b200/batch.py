@@ -53,7 +53,7 @@ def gather_results(labels, objectives, nodes_per_instance, count, group=None):
     return torch.cat(keep_l), torch.cat(keep_o)
 
 
-def solve_sharded(instances, cfg, workers=8, group=None):
+def solve_sharded(instances, cfg, workers=1, group=None):
     """Solve a batch of equally sized instances across all ranks.
 
     instances: list of (n, u, v, cost) raw COO (every rank holds the list;

@@ -66,15 +66,6 @@ void export_graph(Ctx& ctx, const Graph& g, int32_t* ou, int32_t* ov, double* oc
   *om = g.m;
 }
 
-__global__ void k_is_canonical(const int32_t* __restrict__ u, const int32_t* __restrict__ v, int64_t m, int64_t n,
-                               int32_t* bad) {
-  GRID_STRIDE(i, m) {
-    bool ok = u[i] >= 0 && u[i] < v[i] && v[i] < n;
-    if (ok && i > 0) ok = u[i - 1] < u[i] || (u[i - 1] == u[i] && v[i - 1] < v[i]);
-    if (!ok) atomicOr(bad, 1);
-  }
-}
-
 SolveConfig to_cfg(const rama_cfg* cfg) {
   RAMA_REQUIRE(cfg != nullptr, "cfg is NULL");
   SolveConfig c;
@@ -94,6 +85,21 @@ SolveConfig to_cfg(const rama_cfg* cfg) {
   return c;
 }
 
+rama_round to_round(const RoundInfo& r) {
+  rama_round o;
+  o.round_index = r.round_index;
+  o.phase = r.phase;
+  o.nodes = r.nodes;
+  o.edges = r.edges;
+  o.triplets = r.triplets;
+  o.lb = r.lb;
+  o.lb_valid = r.lb_valid;
+  o.reserved = 0;
+  o.contracted = r.contracted;
+  o.time_ms = r.time_ms;
+  return o;
+}
+
 void run_solve(Ctx& ctx, int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m,
                const rama_cfg* cfg, int32_t* labels, double* primal_lb, rama_round* trace, int32_t max_trace,
                int32_t* n_rounds) {
@@ -101,14 +107,9 @@ void run_solve(Ctx& ctx, int64_t n, const int32_t* u, const int32_t* v, const do
   SolveConfig sc = to_cfg(cfg);
   GraphView g = view_of(n, u, v, c, m);
   Graph canon;
-  if (m > 0) {
-    Buf<int32_t> bad(1, ctx);
-    bad.zero();
-    RAMA_KERNEL(ctx, k_is_canonical, m, u, v, m, n, bad.p);
-    if (read_scalar(ctx, bad.p)) {
-      canon = canonicalize(ctx, n, u, v, c, m);
-      g = canon.view();
-    }
+  if (m > 0 && !is_canonical(ctx, g)) {
+    canon = canonicalize(ctx, n, u, v, c, m);
+    g = canon.view();
   }
   std::vector<RoundInfo> tr(max_trace > 0 ? max_trace : 0);
   SolveResult res;
@@ -116,20 +117,7 @@ void run_solve(Ctx& ctx, int64_t n, const int32_t* u, const int32_t* v, const do
   primal_lb[0] = res.primal;
   primal_lb[1] = res.lb_finite ? res.lb : -std::numeric_limits<double>::infinity();
   int written = res.n_rounds < max_trace ? res.n_rounds : max_trace;
-  for (int i = 0; trace && i < written; i++) {
-    const RoundInfo& r = tr[i];
-    rama_round& o = trace[i];
-    o.round_index = r.round_index;
-    o.phase = r.phase;
-    o.nodes = r.nodes;
-    o.edges = r.edges;
-    o.triplets = r.triplets;
-    o.lb = r.lb;
-    o.lb_valid = r.lb_valid;
-    o.reserved = 0;
-    o.contracted = r.contracted;
-    o.time_ms = r.time_ms;
-  }
+  for (int i = 0; trace && i < written; i++) trace[i] = to_round(tr[i]);
   if (n_rounds) *n_rounds = res.n_rounds;
 }
 
@@ -426,20 +414,36 @@ int rama_lower_bound(int64_t m_aug, const double* base, int64_t T, const int32_t
 
 int rama_solve_batch(int64_t count, const int64_t* node_off, const int64_t* edge_off, const int32_t* u,
                      const int32_t* v, const double* c, const rama_cfg* cfg, int32_t* labels, double* primal_lb,
-                     int32_t workers, void* stream) {
+                     rama_round* trace, int32_t max_trace, int32_t* n_rounds, int32_t workers, void* stream) {
   return guarded(stream, [&](Ctx& ctx) {
     RAMA_REQUIRE(count >= 0, "count must be non-negative");
     if (count == 0) return;
     RAMA_REQUIRE(node_off && edge_off && primal_lb, "offset / result arrays must not be NULL");
-    to_cfg(cfg);
+    const SolveConfig sc = to_cfg(cfg);
     for (int64_t i = 0; i < count; i++) {
       RAMA_REQUIRE(node_off[i + 1] >= node_off[i] && edge_off[i + 1] >= edge_off[i], "offsets must be non-decreasing");
       check_sizes(node_off[i + 1] - node_off[i], edge_off[i + 1] - edge_off[i]);
     }
+    if (max_trace < 0 || !trace) max_trace = 0;
+    // modes P / PD / PD+: contiguous groups of instances, each solved as one
+    // disjoint union (batch.cu); modes D / GAEC: one instance per job
+    const bool uni = sc.mode <= 2;
+    int W = workers > 0 ? workers : 1;
+    if (W > count) W = (int)count;
+    std::vector<int64_t> job_lo, job_hi;
+    if (uni) {
+      for (int w = 0; w < W; w++) {
+        job_lo.push_back(count * w / W);
+        job_hi.push_back(count * (w + 1) / W);
+      }
+    } else {
+      for (int64_t i = 0; i < count; i++) {
+        job_lo.push_back(i);
+        job_hi.push_back(i + 1);
+      }
+    }
     int dev = 0;
     RAMA_CUDA(cudaGetDevice(&dev));
-    int W = workers > 0 ? workers : 8;
-    if (W > count) W = (int)count;
     cudaEvent_t start;
     RAMA_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
     RAMA_CUDA(cudaEventRecord(start, ctx.s));
@@ -449,6 +453,7 @@ int rama_solve_batch(int64_t count, const int64_t* node_off, const int64_t* edge
       RAMA_CUDA(cudaStreamWaitEvent(streams[w], start, 0));
     }
     std::atomic<int64_t> next(0), launches(0);
+    const int64_t njobs = (int64_t)job_lo.size();
     std::mutex mu;
     int err_code = 0;
     std::string err_msg;
@@ -456,23 +461,39 @@ int rama_solve_batch(int64_t count, const int64_t* node_off, const int64_t* edge
       try {
         RAMA_CUDA(cudaSetDevice(dev));
         Ctx wc(streams[w]);
+        std::vector<RoundInfo> tr;
         while (true) {
-          int64_t i = next.fetch_add(1);
-          if (i >= count) break;
-          int64_t no = node_off[i], eo = edge_off[i];
-          run_solve(wc, node_off[i + 1] - no, u + eo, v + eo, c + eo, edge_off[i + 1] - eo, cfg, labels + no,
-                    primal_lb + 2 * i, nullptr, 0, nullptr);
+          const int64_t j = next.fetch_add(1);
+          if (j >= njobs) break;
+          const int64_t lo = job_lo[j], hi = job_hi[j], k = hi - lo;
+          const int64_t no = node_off[lo], eo = edge_off[lo];
+          if (uni) {
+            tr.assign((size_t)k * max_trace, RoundInfo());
+            std::vector<int32_t> nr(k, 0);
+            solve_union(wc, k, node_off + lo, edge_off + lo, u + eo, v + eo, c + eo, sc, labels + no,
+                        primal_lb + 2 * lo, max_trace ? tr.data() : nullptr, max_trace, nr.data());
+            for (int64_t i = 0; i < k; i++) {
+              const int written = nr[i] < max_trace ? nr[i] : max_trace;
+              for (int r = 0; r < written; r++)
+                trace[(lo + i) * max_trace + r] = to_round(tr[(size_t)i * max_trace + r]);
+              if (n_rounds) n_rounds[lo + i] = nr[i];
+            }
+          } else {
+            run_solve(wc, node_off[lo + 1] - no, u + eo, v + eo, c + eo, edge_off[lo + 1] - eo, cfg, labels + no,
+                      primal_lb + 2 * lo, max_trace ? trace + lo * max_trace : nullptr, max_trace,
+                      n_rounds ? n_rounds + lo : nullptr);
+          }
         }
         wc.sync();
         launches += wc.launches;
       } catch (const Error& e) {
         std::lock_guard<std::mutex> lk(mu);
         if (!err_code) { err_code = e.code; err_msg = e.what(); }
-        next = count;
+        next = njobs;
       } catch (const std::exception& e) {
         std::lock_guard<std::mutex> lk(mu);
         if (!err_code) { err_code = kInternal; err_msg = e.what(); }
-        next = count;
+        next = njobs;
       }
     };
     std::vector<std::thread> pool;

@@ -340,6 +340,9 @@ int64_t compact_indices(Ctx& ctx, const uint8_t* flags, int64_t n, Buf<int32_t>&
 
 // deterministic fp64 sum (fixed block order, not numpy's order)
 double device_sum(Ctx& ctx, const double* x, int64_t n);
+// out[j] (device) = device_sum of x[start[j], start[j] + len[j]), bit for
+// bit (start, len: device int64[K]); 0.0 for an empty segment
+void device_sums(Ctx& ctx, const double* x, const int64_t* start, const int64_t* len, int64_t K, double* out);
 
 // row pointers of a (u, v)-sorted edge list: ptr[x] = first edge with u >= x
 void row_ptr_from_sorted(Ctx& ctx, const int32_t* u, int64_t m, int64_t n, int32_t* ptr);

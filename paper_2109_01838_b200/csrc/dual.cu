@@ -1536,20 +1536,19 @@ __global__ void k_tri_min(int64_t T, const double* __restrict__ lam, double* __r
   }
 }
 
+void lower_bound_terms(Ctx& ctx, const DualState& st, double* cl_out, double* neg, double* tm) {
+  RAMA_KERNEL(ctx, k_reparam, st.m_aug, st.m_aug, st.base.p, st.T ? st.slot_ptr.p : (const int32_t*)nullptr,
+              st.slots.p, st.lam.p, cl_out, neg);
+  RAMA_KERNEL(ctx, k_tri_min, st.T, st.T, st.lam.p, tm);
+}
+
 double lower_bound(Ctx& ctx, const DualState& st, double* cl_out) {
   ProfScope prof(ctx.s, kFamBound);
   double total = 0.0;
-  if (st.m_aug > 0) {
-    Buf<double> neg(st.m_aug, ctx);
-    RAMA_KERNEL(ctx, k_reparam, st.m_aug, st.m_aug, st.base.p, st.T ? st.slot_ptr.p : (const int32_t*)nullptr,
-                st.slots.p, st.lam.p, cl_out, neg.p);
-    total = device_sum(ctx, neg.p, st.m_aug);
-  }
-  if (st.T > 0) {
-    Buf<double> tm(st.T, ctx);
-    RAMA_KERNEL(ctx, k_tri_min, st.T, st.T, st.lam.p, tm.p);
-    total += device_sum(ctx, tm.p, st.T);
-  }
+  Buf<double> neg(st.m_aug > 0 ? st.m_aug : 1, ctx), tm(st.T > 0 ? st.T : 1, ctx);
+  lower_bound_terms(ctx, st, cl_out, neg.p, tm.p);
+  if (st.m_aug > 0) total = device_sum(ctx, neg.p, st.m_aug);
+  if (st.T > 0) total += device_sum(ctx, tm.p, st.T);
   return total;
 }
 

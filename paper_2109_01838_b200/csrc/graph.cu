@@ -196,6 +196,23 @@ int64_t components(Ctx& ctx, int64_t n, const int32_t* su, const int32_t* sv, in
   return nt;
 }
 
+__global__ void k_is_canonical(const int32_t* __restrict__ u, const int32_t* __restrict__ v, int64_t m, int64_t n,
+                               int32_t* bad) {
+  GRID_STRIDE(i, m) {
+    bool ok = u[i] >= 0 && u[i] < v[i] && v[i] < n;
+    if (ok && i > 0) ok = u[i - 1] < u[i] || (u[i - 1] == u[i] && v[i - 1] < v[i]);
+    if (!ok) atomicOr(bad, 1);
+  }
+}
+
+bool is_canonical(Ctx& ctx, const GraphView& g) {
+  if (g.m == 0) return true;
+  Buf<int32_t> bad(1, ctx);
+  bad.zero();
+  RAMA_KERNEL(ctx, k_is_canonical, g.m, g.u, g.v, g.m, g.n, bad.p);
+  return read_scalar(ctx, bad.p) == 0;
+}
+
 // -------------------------------------------------------------- contract
 
 // mass of the merged edges (contraction.py:151): only when a caller asks
@@ -243,10 +260,14 @@ __global__ void k_cut_costs(const int32_t* __restrict__ u, const int32_t* __rest
   GRID_STRIDE(i, m) x[i] = (lab[u[i]] != lab[v[i]]) ? c[i] : 0.0;
 }
 
+void cut_costs(Ctx& ctx, const GraphView& g, const int32_t* labels, double* x) {
+  RAMA_KERNEL(ctx, k_cut_costs, g.m, g.u, g.v, g.c, g.m, labels, x);
+}
+
 double clustering_cost(Ctx& ctx, const GraphView& g, const int32_t* labels) {
   if (g.m == 0) return 0.0;
   Buf<double> x(g.m, ctx);
-  RAMA_KERNEL(ctx, k_cut_costs, g.m, g.u, g.v, g.c, g.m, labels, x.p);
+  cut_costs(ctx, g, labels, x.p);
   return device_sum(ctx, x.p, g.m);
 }
 

@@ -29,6 +29,8 @@ struct Graph {
 // ---- graph core (graph.cu) --------------------------------------------------
 // a3  WeightedGraph.__init__ (graph.py:29-57)
 Graph canonicalize(Ctx& ctx, int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m);
+// the WeightedGraph invariant: ids in range, u < v, (u, v) strictly ascending
+bool is_canonical(Ctx& ctx, const GraphView& g);
 // a17 connected_components (contraction.py:101-111); returns num_targets
 // (check: validate endpoint ranges first -- the C ABI entry; internal callers
 // pass edges that are valid by construction)
@@ -40,6 +42,8 @@ Graph contract(Ctx& ctx, const GraphView& g, const int32_t* map, int64_t n_targe
 void compose(Ctx& ctx, int32_t* f_total, int64_t n0, const int32_t* f);
 // a21 clustering_cost (graph.py:134-145)
 double clustering_cost(Ctx& ctx, const GraphView& g, const int32_t* labels);
+// per-edge cut cost x[e] = c[e] if labels differ else 0 (the summands of clustering_cost)
+void cut_costs(Ctx& ctx, const GraphView& g, const int32_t* labels, double* x);
 void iota(Ctx& ctx, int32_t* x, int64_t n);
 
 // ---- contraction-set selection (select.cu) ---------------------------------
@@ -106,6 +110,9 @@ bool check_edge_triangle_agreement(Ctx& ctx, const DualState& st, double eps);
 // (cl_out: optional m_aug buffer receiving c^lambda for a following
 // reparametrized_graph call)
 double lower_bound(Ctx& ctx, const DualState& st, double* cl_out = nullptr);
+// the summands of lower_bound: neg[m_aug] = min(0, c^lambda_e), tm[T] = the
+// triplets' minimal pattern costs (cl_out optional)
+void lower_bound_terms(Ctx& ctx, const DualState& st, double* cl_out, double* neg, double* tm);
 // a12 reparametrized_graph (dual.py:408-411): canonical merge of originals
 // and chords carrying c^lambda
 Graph reparametrized_graph(Ctx& ctx, const DualState& st, const double* cl = nullptr);
@@ -147,5 +154,17 @@ struct SolveResult {
 
 void solve(Ctx& ctx, const GraphView& g, const SolveConfig& cfg, int32_t* labels, SolveResult& res,
            RoundInfo* trace, int max_trace);
+
+// ---- batch (batch.cu) -----------------------------------------------------------
+// K independent instances (modes P, PD, PD+) solved as one disjoint union:
+// instance i = COO slice [edge_off[i], edge_off[i+1]) of u, v, c (device,
+// local ids), n_i = node_off[i+1] - node_off[i] (host offsets).  labels
+// (device, node_off layout) receive each instance's canonical labeling;
+// primal_lb[2i], [2i+1] (host); traces (host, K x max_trace, may be null)
+// and n_rounds[K] (host, may be null) each instance's RoundRecords.  Every
+// instance's result equals its single solve bit for bit.
+void solve_union(Ctx& ctx, int64_t K, const int64_t* node_off, const int64_t* edge_off, const int32_t* u,
+                 const int32_t* v, const double* c, const SolveConfig& cfg, int32_t* labels, double* primal_lb,
+                 RoundInfo* traces, int max_trace, int32_t* n_rounds);
 
 }  // namespace rama

@@ -498,6 +498,57 @@ double device_sum(Ctx& ctx, const double* x, int64_t n) {
   return read_scalar(ctx, part.p + kSumBlocks);
 }
 
+// K independent sums in one launch pair, each in exactly device_sum's order
+// (segment j = x[start[j], start[j] + len[j]) takes grid row j): the batch
+// solve's per-instance objectives are bit-identical to single solves
+__global__ void k_partial_sum_seg(const double* __restrict__ x, const int64_t* __restrict__ start,
+                                  const int64_t* __restrict__ len, double* __restrict__ part) {
+  __shared__ double sh[kBlock];
+  const double* xs = x + start[blockIdx.y];
+  const int64_t n = len[blockIdx.y];
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    acc += xs[i];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = sh[0];
+}
+
+__global__ void k_final_sum_seg(const double* part, int np, const int64_t* __restrict__ len, double* out) {
+  __shared__ double sh[1024];
+  const double* ps = part + (int64_t)blockIdx.x * np;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) acc += ps[i];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = len[blockIdx.x] > 0 ? sh[0] : 0.0;
+}
+
+void device_sums(Ctx& ctx, const double* x, const int64_t* start, const int64_t* len, int64_t K, double* out) {
+  if (K <= 0) return;
+  RAMA_REQUIRE(K < 65536, "too many segments");
+  Buf<double> part((size_t)K * kSumBlocks, ctx);
+  {
+    KernelScope ks(ctx.s, "k_partial_sum_seg", 0.0);
+    k_partial_sum_seg<<<dim3(kSumBlocks, (unsigned)K), kBlock, 0, ctx.s>>>(x, start, len, part.p);
+  }
+  RAMA_LAUNCH_CHECK();
+  {
+    KernelScope ks(ctx.s, "k_final_sum_seg", 0.0);
+    k_final_sum_seg<<<(unsigned)K, 1024, 0, ctx.s>>>(part.p, kSumBlocks, len, out);
+  }
+  RAMA_LAUNCH_CHECK();
+  ctx.launches += 2;
+}
+
 // ----------------------------------------------------------- row ptrs
 
 // dense lists (m >= n): one pass over the sorted u, edge i opens the rows

@@ -176,12 +176,13 @@ def dual_bound(g, cfg):
     return solve(g, cfg).lower_bound
 
 
-def solve_batch(graphs, cfg, workers=8):
-    """Solve independent instances concurrently on one GPU (SURVEY.md 8(e),
-    config C5): one ``rama_solve_batch`` call, ``workers`` streams.
+def solve_batch(graphs, cfg, workers=1):
+    """Solve independent instances on one GPU:
+    one ``rama_solve_batch`` call.  Modes P / PD / PD+ solve ``workers``
+    contiguous groups, each as one disjoint-union graph; every Solution
+    (labels, objectives, trace) equals the single solve's.
 
-    ``graphs``: WeightedGraph list.  Returns a list of Solution (trace
-    omitted: batch solves record no per-round trace).
+    ``graphs``: WeightedGraph list.  Returns a list of Solution.
     """
     cfg.validate()
     t = L.torch()
@@ -199,16 +200,27 @@ def solve_batch(graphs, cfg, workers=8):
     else:
         du = dv = L.empty_i32(1)
         dc = L.empty_f64(1)
-    labels, out = solve_batch_device(node_off, edge_off, du, dv, dc, cfg, workers)
+    k = max(_max_trace(cfg, g.num_nodes) for g in graphs)
+    trace = (L.RamaRound * (count * k))()
+    nr = np.zeros(count, np.int32)
+    labels, out = solve_batch_device(node_off, edge_off, du, dv, dc, cfg, workers, trace=(trace, k, nr))
     lab = labels.cpu().numpy().astype(np.int64)
-    return [Solution(lab[node_off[i]:node_off[i + 1]], float(out[2 * i]), float(out[2 * i + 1]), [])
-            for i in range(count)]
+    sols = []
+    for i, g in enumerate(graphs):
+        if g.num_nodes == 0:
+            sols.append(_empty_solution(cfg))
+            continue
+        recs = _records(trace[i * k:(i + 1) * k], min(int(nr[i]), k))
+        sols.append(Solution(lab[node_off[i]:node_off[i + 1]], float(out[2 * i]), float(out[2 * i + 1]), recs))
+    return sols
 
 
-def solve_batch_device(node_off, edge_off, du, dv, dc, cfg, workers=8, labels=None):
+def solve_batch_device(node_off, edge_off, du, dv, dc, cfg, workers=1, labels=None, trace=None):
     """Device entry of the batch solve: concatenated canonical COO slices
     (int32 u, v; float64 c CUDA tensors) with host offset arrays.  Returns
-    (labels int32 CUDA tensor, numpy float64[2 * count] of (primal, lb))."""
+    (labels int32 CUDA tensor, numpy float64[2 * count] of (primal, lb)).
+    ``trace``: optional (ctypes RamaRound array of count * k, k, int32
+    numpy n_rounds[count]) receiving every instance's RoundRecords."""
     cfg.validate()
     node_off = np.ascontiguousarray(node_off, np.int64)
     edge_off = np.ascontiguousarray(edge_off, np.int64)
@@ -217,7 +229,11 @@ def solve_batch_device(node_off, edge_off, du, dv, dc, cfg, workers=8, labels=No
         labels = L.empty_i32(int(node_off[-1]))
     out = np.zeros(max(2 * count, 1), np.float64)
     c = cfg.to_c()
+    if trace is None:
+        tbuf, k, nr = None, 0, None
+    else:
+        tbuf, k, nr = trace
     L.call("rama_solve_batch", count, node_off.ctypes.data_as(L._I64P), edge_off.ctypes.data_as(L._I64P), L.ptr(du),
-           L.ptr(dv), L.ptr(dc), L.ctypes.byref(c), L.ptr(labels), out.ctypes.data_as(L._F64P), int(workers),
-           L.stream())
+           L.ptr(dv), L.ptr(dc), L.ctypes.byref(c), L.ptr(labels), out.ctypes.data_as(L._F64P), tbuf, int(k),
+           nr.ctypes.data_as(L._I32P) if nr is not None else None, int(workers), L.stream())
     return labels, out

@@ -64,21 +64,52 @@ def test_gather_results_gloo_world2(count):
         assert np.array_equal(O[:, 0], np.arange(count)) and np.array_equal(O[:, 1], -np.arange(count))
 
 
+def _trace_key(sol):
+    return [(r.round_index, r.phase, r.nodes, r.edges, r.triplets, r.lb, r.lb_valid, r.contracted) for r in sol.trace]
+
+
 @pytest.mark.gpu
 def test_batch_solve_equals_single_solves():
+    """The union batch solve (batch.cu) reproduces every instance's single
+    solve bit for bit: labels, primal, LB and the whole trace -- across
+    instances that stop in different rounds, switch to the forest policy in
+    different rounds, or have no positive edge at all."""
     import paper_2109_01838_b200 as P
     from paper_2109_01838_b200 import instances
 
-    graphs = [P.WeightedGraph(*instances.grid_coo(96, 128, 0, seed=s)) for s in range(6)]
+    graphs = [P.WeightedGraph(*instances.grid_coo(96, 128, 0, seed=s)) for s in range(4)]
     graphs.append(P.WeightedGraph(*instances.grid8_coo(40, 50, strides=(2, 3), seed=9)))
     graphs.append(P.WeightedGraph(5))  # no edges
-    for mode in ("PD", "P"):
+    graphs.append(P.WeightedGraph(1))  # one node
+    graphs += [P.WeightedGraph(*instances.random_coo(120, 0.08, seed=s)) for s in range(3)]
+    n, u, v, c = instances.grid_coo(20, 30, 0, seed=3)
+    graphs.append(P.WeightedGraph(n, u, v, -np.abs(c)))  # all repulsive: stops in round 1
+    graphs += [P.WeightedGraph(*instances.chung_lu_coo(800, 2.1, 9000, seed=s)) for s in range(2)]
+    graphs.append(P.WeightedGraph(*instances.grid_coo(64, 64, 3, seed=5)))
+    for mode in ("PD", "P", "PD+"):
         cfg = P.SolverConfig(mode=mode)
-        got = P.solve_batch(graphs, cfg, workers=3)
+        singles = [P.solve(g, cfg) for g in graphs]
+        for workers in (1, 3):
+            got = P.solve_batch(graphs, cfg, workers=workers)
+            for i, (a, b) in enumerate(zip(singles, got)):
+                assert np.array_equal(a.labeling, b.labeling), (mode, workers, i)
+                assert a.primal_cost == b.primal_cost and a.lower_bound == b.lower_bound, (mode, workers, i)
+                assert _trace_key(a) == _trace_key(b), (mode, workers, i)
+
+
+@pytest.mark.gpu
+def test_batch_solve_modes_d_and_gaec():
+    import paper_2109_01838_b200 as P
+    from paper_2109_01838_b200 import instances
+
+    graphs = [P.WeightedGraph(*instances.grid_coo(24, 32, 0, seed=s)) for s in range(3)]
+    for cfg in (P.SolverConfig(mode="D", separation_rounds=2), P.SolverConfig(mode="GAEC")):
+        got = P.solve_batch(graphs, cfg, workers=2)
         for g, b in zip(graphs, got):
             a = P.solve(g, cfg)
             assert np.array_equal(a.labeling, b.labeling)
             assert a.primal_cost == b.primal_cost and a.lower_bound == b.lower_bound
+            assert _trace_key(a) == _trace_key(b)
 
 
 @pytest.mark.gpu
