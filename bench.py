@@ -302,6 +302,7 @@ def b200_arm(args):
             torch.cuda.current_stream().synchronize()
 
         e2e_h2d, e2e_d2h = int(m * 16), int(labels.numel() * 4 + 16 * (hi - lo))
+        e2e_host = "pinned torch tensors copied by the caller, labels copied back"
         job = {"instances_per_step": count, "instances_per_gpu": hi - lo, "nodes_per_instance": n,
                "edges_per_instance": m_inst, "union_groups_per_gpu": BATCH_WORKERS}
     else:
@@ -324,15 +325,18 @@ def b200_arm(args):
                 torch.distributed.all_gather_into_tensor(objs, mine)
             return primal, lb, trace
 
-        hu = torch.from_numpy(g.edges_u.astype(np.int32)).pin_memory().numpy()
-        hv = torch.from_numpy(g.edges_v.astype(np.int32)).pin_memory().numpy()
-        hc = torch.from_numpy(g.costs.astype(np.float64)).pin_memory().numpy()
-        hlab = torch.empty(max(n, 1), dtype=torch.int32).pin_memory().numpy()
+        # plain (pageable) numpy arrays, as the parcut-side binding of
+        # INTEGRATION.md passes them; rama_solve_host stages them itself
+        hu = np.ascontiguousarray(g.edges_u, dtype=np.int32)
+        hv = np.ascontiguousarray(g.edges_v, dtype=np.int32)
+        hc = np.ascontiguousarray(g.costs, dtype=np.float64)
+        hlab = np.empty(max(n, 1), dtype=np.int32)
 
         def e2e_step():  # rama_solve_host: H2D + solve + D2H inside the C ABI call
             P.solve_host(n, hu, hv, hc, cfg, labels=hlab)
 
         e2e_h2d, e2e_d2h = int(m * (4 + 4 + 8)), int(n * 4 + 16)
+        e2e_host = "pageable numpy arrays (rama_solve_host stages them through pinned chunks)"
         job = {"instances_per_step": world, "seed": "rank"}
 
     for _ in range(args.warmup):
@@ -400,7 +404,7 @@ def b200_arm(args):
             torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
         e2e = {"value": m_step * args.steps / (float(te.item()) / 1e3), "unit": "edges/s",
                "h2d_bytes_per_step": e2e_h2d, "d2h_bytes_per_step": e2e_d2h,
-               "ms_per_step": float(te.item()) / args.steps}
+               "ms_per_step": float(te.item()) / args.steps, "host_memory": e2e_host}
 
     if rank != 0:
         if world > 1:

@@ -109,8 +109,10 @@ int rama_solve(int64_t n, const int32_t* u, const int32_t* v, const double* c, i
  * 2, solver.py:211-240); PD+ (max_cycle_length 6..8) uses the exact
  * source-grouped BFS separation. */
 
-/* Same with HOST arrays (u, v, c, labels); copies in and out through pinned
- * staging inside the call.  The end-to-end entry for non-CUDA callers. */
+/* Same with HOST arrays (u, v, c, labels): the end-to-end entry for
+ * non-CUDA callers (numpy through ctypes).  Pinned host buffers are copied
+ * directly; pageable ones through a cached pinned staging area (16 MiB
+ * chunks, parallel host memcpy overlapped with the DMA). */
 int rama_solve_host(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m,
                     const rama_cfg* cfg, int32_t* labels, double* primal_lb, rama_round* trace,
                     int32_t max_trace, int32_t* n_rounds, void* stream);

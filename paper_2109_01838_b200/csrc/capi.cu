@@ -185,12 +185,12 @@ int rama_solve_host(int64_t n, const int32_t* u, const int32_t* v, const double*
     Buf<int32_t> du(m > 0 ? m : 1, ctx), dv(m > 0 ? m : 1, ctx), dl(n > 0 ? n : 1, ctx);
     Buf<double> dc(m > 0 ? m : 1, ctx);
     if (m > 0) {
-      RAMA_CUDA(cudaMemcpyAsync(du.p, u, sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx.s));
-      RAMA_CUDA(cudaMemcpyAsync(dv.p, v, sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx.s));
-      RAMA_CUDA(cudaMemcpyAsync(dc.p, c, sizeof(double) * m, cudaMemcpyHostToDevice, ctx.s));
+      copy_h2d(ctx, du.p, u, sizeof(int32_t) * m);
+      copy_h2d(ctx, dv.p, v, sizeof(int32_t) * m);
+      copy_h2d(ctx, dc.p, c, sizeof(double) * m);
     }
     run_solve(ctx, n, du.p, dv.p, dc.p, m, cfg, dl.p, primal_lb, trace, max_trace, n_rounds);
-    if (n > 0) RAMA_CUDA(cudaMemcpyAsync(labels, dl.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx.s));
+    if (n > 0) copy_d2h(ctx, labels, dl.p, sizeof(int32_t) * n);
   });
 }
 

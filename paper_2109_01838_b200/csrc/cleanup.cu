@@ -610,8 +610,9 @@ static int64_t pool_slack_override() {
 }
 
 int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc) {
-  ProfScope prof(ctx.s, kFamCleanup);
   const int64_t n = q.n, m = q.m;
+  // algorithmic bytes: the quotient read once, the map written
+  ProfScope prof(ctx.s, kFamCleanup, 16.0 * (double)m + 4.0 * (double)n);
   if (n == 0) return 0;
   if (m == 0) {
     iota(ctx, fc, n);

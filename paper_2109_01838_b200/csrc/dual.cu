@@ -909,10 +909,14 @@ static void separate_tables(Ctx& ctx, const GraphView& g, int L, CycleRows& out,
                             const Buf<int32_t>& NQ, int64_t nq, uint8_t* capped);
 
 void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
-  ProfScope prof(ctx.s, kFamSeparate);
+  // algorithmic bytes: the graph read once (16 m),
+  // the positive CSR written and read once (2 x (4 (n + 1) + 4 arcs)), one
+  // cycle row per repulsive edge written (4 + 4 L)
+  ProfScope prof(ctx.s, kFamSeparate, 16.0 * (double)g.m + 8.0 * (double)(g.n + 1));
   RAMA_REQUIRE(L >= 3, "max_len must be at least 3");
   Buf<int32_t> NQ;
   int64_t nq = compact_if(ctx, g.m, NegCost{g.c}, NQ);
+  prof.add_bytes((4.0 + 4.0 * L) * (double)nq);
   out.rows = nq;
   out.L = L;
   out.len.alloc(nq > 0 ? nq : 1, ctx.s);
@@ -920,6 +924,7 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
   if (nq == 0) return;
   PosCSR csr;
   positive_csr(ctx, g, csr);
+  prof.add_bytes(8.0 * (double)csr.arcs);
   if (csr.arcs == 0) {
     out.len.zero();
     out.nodes.zero();
@@ -1249,6 +1254,12 @@ void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& 
   st.lam.alloc(T > 0 ? 3 * T : 1, ctx.s);
   st.lam.zero();
   build_slot_lists(ctx, st);
+  // algorithmic bytes: cycle rows read (4 + 4 L), the
+  // originals' (u, v) read for the handles (8 m), augmented edges written
+  // (eu, ev, base, coverage, slot pointer: 24 m_aug), triplets written
+  // (nodes 12, handles 12, lambda 24, slot list 12: 60 T)
+  prof.add_bytes((4.0 + 4.0 * cyc.L) * (double)rows + 8.0 * (double)m + 24.0 * (double)st.m_aug +
+                 60.0 * (double)st.T);
 }
 
 
@@ -1543,7 +1554,9 @@ void lower_bound_terms(Ctx& ctx, const DualState& st, double* cl_out, double* ne
 }
 
 double lower_bound(Ctx& ctx, const DualState& st, double* cl_out) {
-  ProfScope prof(ctx.s, kFamBound);
+  // algorithmic bytes: lambda (24 T) and the slot lists (12 T + 4 m_aug)
+  // read once, base read (8 m_aug), c^lambda written (8 m_aug)
+  ProfScope prof(ctx.s, kFamBound, 36.0 * (double)st.T + 20.0 * (double)st.m_aug);
   double total = 0.0;
   Buf<double> neg(st.m_aug > 0 ? st.m_aug : 1, ctx), tm(st.T > 0 ? st.T : 1, ctx);
   lower_bound_terms(ctx, st, cl_out, neg.p, tm.p);
@@ -1694,7 +1707,7 @@ __global__ void k_sorted_edges_out(const int32_t* __restrict__ row, const uint64
 }
 
 Graph reparametrized_graph(Ctx& ctx, const DualState& st, const double* cl_in) {
-  ProfScope prof(ctx.s, kFamBound);
+  ProfScope prof(ctx.s, kFamBound, 32.0 * (double)st.m_aug);  // (eu, ev, c^lambda) read, canonical COO written
   Graph g;
   g.n = st.n;
   g.m = st.m_aug;

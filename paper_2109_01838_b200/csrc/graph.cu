@@ -99,7 +99,8 @@ static Graph sort_reduce_graph(Ctx& ctx, int64_t n_out, int64_t m_in, const Src&
 }
 
 Graph canonicalize(Ctx& ctx, int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m) {
-  ProfScope prof(ctx.s, kFamCanon);
+  // algorithmic bytes: raw COO read once, canonical COO written (<= m)
+  ProfScope prof(ctx.s, kFamCanon, 32.0 * (double)m);
   RAMA_REQUIRE(n >= 0, "num_nodes must be non-negative");
   RAMA_REQUIRE(n < (1LL << 31) && m < (1LL << 31), "graph too large for int32 ids");
   if (m == 0) {
@@ -179,7 +180,8 @@ __global__ void k_cc_label(const int32_t* __restrict__ parent, const int32_t* __
 }
 
 int64_t components(Ctx& ctx, int64_t n, const int32_t* su, const int32_t* sv, int64_t k, int32_t* map, bool check) {
-  ProfScope prof(ctx.s, kFamComponents);
+  // algorithmic bytes: the pairs read once, the map written
+  ProfScope prof(ctx.s, kFamComponents, 8.0 * (double)k + 4.0 * (double)n);
   if (n == 0) return 0;
   if (check && k > 0) {
     Buf<int32_t> err(1, ctx);

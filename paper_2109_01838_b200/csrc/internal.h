@@ -26,6 +26,13 @@ struct Graph {
   }
 };
 
+// ---- host buffers (staging.cu) ------------------------------------------------
+// host -> device (ordered on ctx.s; the host buffer may be reused on return)
+// and device -> host (complete on return); pageable host memory goes through
+// pinned staging chunks with a parallel memcpy overlapped with the DMA
+void copy_h2d(Ctx& ctx, void* dst, const void* src, size_t bytes);
+void copy_d2h(Ctx& ctx, void* dst, const void* src, size_t bytes);
+
 // ---- graph core (graph.cu) --------------------------------------------------
 // a3  WeightedGraph.__init__ (graph.py:29-57)
 Graph canonicalize(Ctx& ctx, int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m);

@@ -106,6 +106,9 @@ int64_t select_matching(Ctx& ctx, const GraphView& g, int rounds, Buf<int32_t>& 
   if (n == 0 || m == 0) return 0;
   Buf<int32_t> P;
   int64_t np = compact_if(ctx, m, PosCost{g.c}, P);
+  // algorithmic bytes: costs scanned once (8 m), then SURVEY.md 8(d)'s
+  // 34 m+ + 17 n per handshake round (every positive edge is visited)
+  prof.add_bytes(8.0 * (double)m + (double)rounds * (34.0 * (double)np + 17.0 * (double)n));
   if (np == 0) return 0;
   Buf<uint8_t> matched(n, ctx);
   matched.zero();
@@ -518,8 +521,9 @@ __global__ void k_gather_pairs(const int32_t* __restrict__ idx, int64_t k, const
 }
 
 int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_t>& sv) {
-  ProfScope prof(ctx.s, kFamForest);
   int64_t n = g.n, m = g.m;
+  // algorithmic bytes: the graph read once, the selected pairs written
+  ProfScope prof(ctx.s, kFamForest, 16.0 * (double)m + 8.0 * (double)n);
   su.alloc(1, ctx.s);
   sv.alloc(1, ctx.s);
   if (n == 0 || m == 0) return 0;

@@ -433,7 +433,7 @@ void sr_sort_huge(Ctx& ctx, const int32_t* rowptr, const int32_t* rows, int64_t 
 
 struct SrResult {
   Buf<int32_t> rowptr;  // R + 1 (rowptr[R] = items kept)
-  Buf<int64_t> total;   // device: outputs written (kUnique) / items (else)
+  Buf<int64_t> total;   // device: outputs written (kUnique; else rowptr[R] counts them)
 };
 
 // One sort-reduce over `src` into `R` rows.  N_max: upper bound of the
@@ -514,6 +514,7 @@ int64_t sort_reduce(Ctx& ctx, int64_t R, int64_t N_max, const Src& src, const Em
   RAMA_LAUNCH_CHECK();
   ctx.launches++;
   if (!want) return -1;
+  if (!kUnique) return read_scalar(ctx, res.rowptr.p + R);  // every item is an output
   return read_scalar(ctx, res.total.p);
 }
 

@@ -120,3 +120,28 @@ def test_batch_solve_reports_bad_instance():
     with pytest.raises(ValueError):
         P.solve_batch_device(np.array([0, 4, 2]), np.array([0, 0, 0]), P._lib.empty_i32(1), P._lib.empty_i32(1),
                              P._lib.empty_f64(1), cfg)
+
+
+@pytest.mark.gpu
+def test_solve_sharded_over_nccl_single_rank():
+    """batch.solve_sharded end to end through a real NCCL process group (one
+    rank: the box has one GPU; the gather is the same all_gather_into_tensor
+    the 2/4/8-GPU runs use): every instance equals its single solve."""
+    import paper_2109_01838_b200 as P
+    from paper_2109_01838_b200 import instances
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        insts = [instances.grid_coo(64, 80, 0, seed=s) for s in range(5)]
+        cfg = P.SolverConfig(mode="PD")
+        labels, objs = batch.solve_sharded(insts, cfg)
+        assert labels.is_cuda and labels.shape == (5, 64 * 80) and objs.shape == (5, 2)
+        for s, inst in enumerate(insts):
+            one = P.solve(P.WeightedGraph(*inst), cfg)
+            assert np.array_equal(labels[s].cpu().numpy(), one.labeling)
+            assert objs[s, 0].item() == one.primal_cost and objs[s, 1].item() == one.lower_bound
+    finally:
+        dist.destroy_process_group()

@@ -115,6 +115,24 @@ def test_determinism_and_host_entry():
     assert np.array_equal(lab, a.labeling) and primal == a.primal_cost and lb == a.lower_bound
 
 
+def test_host_entry_staging_pageable_and_pinned():
+    """rama_solve_host with buffers larger than one 16 MiB staging chunk,
+    from pageable numpy and from pinned memory, equals the device entry."""
+    import torch
+
+    n, u, v, c = instances.grid_coo(1500, 1500, 0, seed=2)  # 4.5 M edges: c is 36 MB
+    g = P.WeightedGraph(n, u, v, c)
+    cfg = P.SolverConfig(mode="P")
+    a = P.solve(g, cfg)
+    hu, hv, hc = (np.ascontiguousarray(x) for x in (g.edges_u.astype(np.int32), g.edges_v.astype(np.int32), g.costs))
+    lab, primal, _, _ = P.solve_host(n, hu, hv, hc, cfg)
+    assert np.array_equal(lab, a.labeling) and primal == a.primal_cost
+    pu, pv, pc = (torch.from_numpy(x).pin_memory().numpy() for x in (hu, hv, hc))
+    pl = torch.empty(n, dtype=torch.int32).pin_memory().numpy()
+    lab, primal, _, _ = P.solve_host(n, pu, pv, pc, cfg, labels=pl)
+    assert np.array_equal(lab, a.labeling) and primal == a.primal_cost
+
+
 def test_c2_full_size_parity():
     with open(os.path.join(DIR, "c2_reference.json")) as fh:
         ref = json.load(fh)
