@@ -133,10 +133,23 @@ def _empty_solution(cfg):
     return Solution(lab, 0.0, 0.0, recs)
 
 
+GAEC_WARN_NODES = 50_000
+
+
+def _warn_gaec(cfg, n):
+    if cfg.mode == "GAEC" and n > GAEC_WARN_NODES:
+        import warnings
+
+        warnings.warn("mode GAEC joins one edge per round on the GPU (O(n) rounds of O(m) work: exact, but slow "
+                      "beyond ~1e5 nodes); it is the paper's baseline -- use mode PD or P for large graphs",
+                      RuntimeWarning, stacklevel=3)
+
+
 def solve(g, cfg):
     """Run the solver in the configured mode (solver.py:243-252)."""
     cfg.validate()
     n, m = g.num_nodes, g.num_edges
+    _warn_gaec(cfg, n)
     if n == 0:
         return _empty_solution(cfg)
     if m:

@@ -85,3 +85,19 @@ def test_canonical_labels_and_parse_host():  # graph.py:148-157, test_graph.py
         P.parse_instance("0 1 2.5\n")
     with pytest.raises(P.ParseError, match="line 2"):
         P.parse_instance("MULTICUT\n0 0 1.0\n")
+
+
+def test_gaec_mode_warns_on_large_graphs():
+    """Mode GAEC is exact but joins one edge per round:
+    large inputs get a RuntimeWarning before any work, small ones do not."""
+    import warnings
+
+    from paper_2109_01838_b200 import solver as S
+
+    cfg = S.SolverConfig(mode="GAEC")
+    with pytest.warns(RuntimeWarning, match="one edge per round"):
+        S._warn_gaec(cfg, S.GAEC_WARN_NODES + 1)
+    with warnings.catch_warnings():
+        warnings.simplefilter("error")
+        S._warn_gaec(cfg, 1000)
+        S._warn_gaec(S.SolverConfig(mode="PD"), 10 ** 7)
