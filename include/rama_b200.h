@@ -105,6 +105,26 @@ int rama_solve(int64_t n, const int32_t* u, const int32_t* v, const double* c, i
                const rama_cfg* cfg, int32_t* labels, double* primal_lb, rama_round* trace,
                int32_t max_trace, int32_t* n_rounds, void* stream);
 
+/* Caller-owned scratch (SURVEY.md 8(b) ownership): rama_solve with every
+ * scratch buffer carved from the caller's DEVICE block ws[ws_bytes] (e.g. a
+ * tensor from torch's caching allocator) instead of the library's cached
+ * stream-ordered pool.  ws must stay valid until the call returns and must
+ * not be used by other work on other streams meanwhile.  A block too small
+ * fails with RAMA_ERR_NOMEM (nothing written); *ws_peak (host, may be NULL)
+ * receives the high-water mark the call used. */
+int rama_solve_ws(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m,
+                  const rama_cfg* cfg, int32_t* labels, double* primal_lb, rama_round* trace,
+                  int32_t max_trace, int32_t* n_rounds, void* ws, uint64_t ws_bytes, uint64_t* ws_peak,
+                  void* stream);
+
+/* Workspace estimate for rama_solve_ws on a graph of n nodes and m edges:
+ * 400 B per edge + 96 B per node + 64 MiB (measured high-water marks per
+ * edge: C5 143, C2 189, C3 209, C4 267 bytes). */
+uint64_t rama_ws_bytes(int64_t n, int64_t m, const rama_cfg* cfg);
+
+/* Return every block the library's own pool caches (all devices). */
+int rama_release_cache(void);
+
 /* Mode D runs cfg->separation_rounds rounds (extend_separation from round
  * 2, solver.py:211-240); PD+ (max_cycle_length 6..8) uses the exact
  * source-grouped BFS separation. */

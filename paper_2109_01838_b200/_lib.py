@@ -72,6 +72,10 @@ _SIGS = {
     "rama_serialize_multicut": [_i64, _vp, _vp, _vp, _i64, _vp, _i64, _I64P, _i32],
     "rama_solve": [_i64, _vp, _vp, _vp, _i64, ctypes.POINTER(RamaCfg), _vp, _F64P, ctypes.POINTER(RamaRound), _i32,
                    _I32P, _vp],
+    "rama_solve_ws": [_i64, _vp, _vp, _vp, _i64, ctypes.POINTER(RamaCfg), _vp, _F64P, ctypes.POINTER(RamaRound), _i32,
+                      _I32P, _vp, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64), _vp],
+    "rama_ws_bytes": [_i64, _i64, ctypes.POINTER(RamaCfg)],
+    "rama_release_cache": [],
     "rama_solve_host": [_i64, _vp, _vp, _vp, _i64, ctypes.POINTER(RamaCfg), _vp, _F64P, ctypes.POINTER(RamaRound),
                         _i32, _I32P, _vp],
     "rama_solve_batch": [_i64, _I64P, _I64P, _vp, _vp, _vp, ctypes.POINTER(RamaCfg), _vp, _F64P,
@@ -95,7 +99,7 @@ _SIGS = {
     "rama_lower_bound": [_i64, _vp, _i64, _vp, _vp, _F64P, _vp],
 }
 _RESTYPES = {"rama_last_error": ctypes.c_char_p, "rama_io_last_error": ctypes.c_char_p, "rama_last_launch_count": ctypes.c_int64,
-             "rama_profile_kernels": ctypes.c_int64}
+             "rama_profile_kernels": ctypes.c_int64, "rama_ws_bytes": ctypes.c_uint64}
 
 EXPORTED = tuple(_SIGS)
 

@@ -177,6 +177,31 @@ int rama_solve(int64_t n, const int32_t* u, const int32_t* v, const double* c, i
   });
 }
 
+int rama_solve_ws(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m, const rama_cfg* cfg,
+                  int32_t* labels, double* primal_lb, rama_round* trace, int32_t max_trace, int32_t* n_rounds,
+                  void* ws, uint64_t ws_bytes, uint64_t* ws_peak, void* stream) {
+  return guarded(stream, [&](Ctx& ctx) {
+    RAMA_REQUIRE(ws != nullptr || ws_bytes == 0, "workspace pointer is NULL");
+    Arena arena(ws, (size_t)ws_bytes);
+    {
+      ArenaScope scope(&arena);
+      run_solve(ctx, n, u, v, c, m, cfg, labels, primal_lb, trace, max_trace, n_rounds);
+      ctx.sync();  // the workspace's ranges are in use until the stream drains
+    }
+    if (ws_peak) *ws_peak = arena.peak;
+  });
+}
+
+uint64_t rama_ws_bytes(int64_t n, int64_t m, const rama_cfg* cfg) {
+  const int L = cfg ? cfg->max_cycle_length : 5;
+  const double per_edge = 400.0 + 96.0 * (L > 5 ? L - 5 : 0);
+  return (uint64_t)(per_edge * (double)(m > 0 ? m : 0) + 96.0 * (double)(n > 0 ? n : 0)) + ((uint64_t)64 << 20);
+}
+
+int rama_release_cache(void) {
+  return guarded(nullptr, [&](Ctx&) { dev_release_all(); });
+}
+
 int rama_solve_host(int64_t n, const int32_t* u, const int32_t* v, const double* c, int64_t m, const rama_cfg* cfg,
                     int32_t* labels, double* primal_lb, rama_round* trace, int32_t max_trace, int32_t* n_rounds,
                     void* stream) {

@@ -13,6 +13,7 @@
 #include <chrono>
 #include <cstdint>
 #include <cstdio>
+#include <map>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -168,6 +169,28 @@ inline double host_ms_since(std::chrono::steady_clock::time_point t0) {
 // (same-stream reuse is ordered, no events needed).  After the first solve
 // of a shape every scratch buffer comes from the cache.
 void* dev_alloc(size_t bytes, cudaStream_t s);
+
+// Caller-owned workspace (rama_solve_ws, SURVEY.md 8(b) ownership): while
+// an ArenaScope is open on a thread, dev_alloc carves every buffer from the
+// caller's device block (first fit, 256-byte aligned, coalescing free list;
+// the call's work is on one stream, so a freed range is reusable at once)
+// and nothing reaches the CUDA pool.  Exhaustion throws kNoMemory.
+struct Arena {
+  char* base;
+  size_t size;
+  size_t used = 0, peak = 0;
+  std::map<size_t, size_t> free_, live_;  // offset -> length
+  Arena(void* p, size_t n);
+  void* alloc(size_t bytes);
+  void release(void* p);
+  bool owns(const void* p) const;
+};
+struct ArenaScope {
+  Arena* prev;
+  explicit ArenaScope(Arena* a);
+  ~ArenaScope();
+};
+bool arena_active();
 void dev_free(void* p, size_t bytes, cudaStream_t s);
 // return every cached block of stream s to the pool (before destroying s)
 void dev_release_stream(cudaStream_t s);

@@ -93,7 +93,66 @@ inline int cur_device() {
 }
 }  // namespace
 
+// ------------------------------------------------- caller-owned workspace
+
+namespace {
+thread_local Arena* g_arena = nullptr;
+}
+
+Arena::Arena(void* p, size_t n) : base((char*)p), size(n) {
+  const size_t skew = (256 - ((uintptr_t)base & 255)) & 255;  // first 256-byte boundary
+  if (n > skew) free_[skew] = n - skew;
+}
+
+void* Arena::alloc(size_t bytes) {
+  const size_t b = (bytes + 255) & ~(size_t)255;
+  for (auto it = free_.begin(); it != free_.end(); ++it) {  // first fit
+    if (it->second < b) continue;
+    const size_t off = it->first, len = it->second;
+    free_.erase(it);
+    if (len > b) free_[off + b] = len - b;
+    live_[off] = b;
+    used += b;
+    if (used > peak) peak = used;
+    return base + off;
+  }
+  throw Error(kNoMemory, "workspace exhausted: " + std::to_string(b) + " bytes requested with " +
+                             std::to_string(used) + " of " + std::to_string(size) +
+                             " in use (give a larger workspace; rama_ws_bytes is an estimate)");
+}
+
+bool Arena::owns(const void* p) const { return (const char*)p >= base && (const char*)p < base + size; }
+
+void Arena::release(void* p) {
+  const size_t off = (size_t)((char*)p - base);
+  auto lv = live_.find(off);
+  if (lv == live_.end()) return;
+  size_t len = lv->second;
+  live_.erase(lv);
+  used -= len;
+  size_t start = off;
+  auto nx = free_.lower_bound(off);
+  if (nx != free_.end() && nx->first == off + len) {  // merge with the next free block
+    len += nx->second;
+    nx = free_.erase(nx);
+  }
+  if (nx != free_.begin()) {  // and with the previous one
+    auto pv = std::prev(nx);
+    if (pv->first + pv->second == off) {
+      start = pv->first;
+      len += pv->second;
+      free_.erase(pv);
+    }
+  }
+  free_[start] = len;
+}
+
+ArenaScope::ArenaScope(Arena* a) : prev(g_arena) { g_arena = a; }
+ArenaScope::~ArenaScope() { g_arena = prev; }
+bool arena_active() { return g_arena != nullptr; }
+
 void* dev_alloc(size_t bytes, cudaStream_t s) {
+  if (g_arena) return g_arena->alloc(bytes);  // stream-ordered: one stream per workspace call
   size_t b = class_bytes(bytes);
   const int dev = cur_device();
   {
@@ -118,6 +177,10 @@ void* dev_alloc(size_t bytes, cudaStream_t s) {
 }
 
 void dev_free(void* p, size_t bytes, cudaStream_t s) {
+  if (g_arena && g_arena->owns(p)) {
+    g_arena->release(p);
+    return;
+  }
   size_t b = class_bytes(bytes);
   const int dev = cur_device();
   std::lock_guard<std::mutex> lk(g_cache_mu);
@@ -170,6 +233,7 @@ void dev_release_all() {
 }
 
 void reserve_pool(Ctx& ctx, size_t bytes) {
+  if (g_arena) return;  // scratch comes from the caller's workspace
   int dev = 0;
   RAMA_CUDA(cudaGetDevice(&dev));
   cudaMemPool_t pool;

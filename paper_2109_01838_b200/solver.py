@@ -98,11 +98,23 @@ def _max_trace(cfg, n):
     return max(min(cfg.max_rounds, max(n, 1) + 1), cfg.separation_rounds) + 2
 
 
-def solve_device(n, du, dv, dc, m, cfg, labels=None):
+def workspace_bytes(n, m, cfg):
+    """Workspace estimate for a caller-owned scratch block (``rama_ws_bytes``)."""
+    cfg.validate()
+    c = cfg.to_c()
+    return int(L.load().rama_ws_bytes(int(n), int(m), L.ctypes.byref(c)))
+
+
+def solve_device(n, du, dv, dc, m, cfg, labels=None, workspace=None):
     """Device-resident solve on CUDA tensors (int32 u, v; float64 c).
 
     Returns (labels int32 CUDA tensor, primal, lower_bound, trace).  This is
     the in-HBM entry the benchmark times; ``solve`` wraps it for host data.
+
+    ``workspace``: None (the library's cached scratch pool), ``"torch"``
+    (scratch carved from one uint8 tensor of ``workspace_bytes`` from torch's
+    caching allocator, grown and retried if a solve needs more), or a CUDA
+    uint8 tensor to carve it from (``rama_solve_ws``).
     """
     cfg.validate()
     if labels is None:
@@ -112,8 +124,28 @@ def solve_device(n, du, dv, dc, m, cfg, labels=None):
     out = (L.ctypes.c_double * 2)()
     nr = L.ctypes.c_int32()
     c = cfg.to_c()
-    L.call("rama_solve", int(n), L.ptr(du), L.ptr(dv), L.ptr(dc), int(m), L.ctypes.byref(c), L.ptr(labels), out,
-           trace, k, L.ctypes.byref(nr), L.stream())
+    if workspace is None:
+        L.call("rama_solve", int(n), L.ptr(du), L.ptr(dv), L.ptr(dc), int(m), L.ctypes.byref(c), L.ptr(labels), out,
+               trace, k, L.ctypes.byref(nr), L.stream())
+    else:
+        t = L.torch()
+        grow = isinstance(workspace, str)
+        if grow:
+            if workspace != "torch":
+                raise ValueError("workspace must be None, 'torch' or a CUDA uint8 tensor")
+            workspace = t.empty(workspace_bytes(n, m, cfg), dtype=t.uint8, device="cuda")
+        peak = L.ctypes.c_uint64()
+        while True:
+            try:
+                L.call("rama_solve_ws", int(n), L.ptr(du), L.ptr(dv), L.ptr(dc), int(m), L.ctypes.byref(c),
+                       L.ptr(labels), out, trace, k, L.ctypes.byref(nr), L.ptr(workspace), int(workspace.numel()),
+                       L.ctypes.byref(peak), L.stream())
+                break
+            except MemoryError:
+                if not grow:
+                    raise
+                workspace = t.empty(2 * workspace.numel(), dtype=t.uint8, device="cuda")
+        solve_device.last_workspace_peak = int(peak.value)
     return labels, float(out[0]), float(out[1]), _records(trace, min(nr.value, k))
 
 

@@ -300,3 +300,27 @@ def test_edge_cases_all_modes():
                 assert sol.lower_bound == float("-inf")
             else:
                 assert sol.lower_bound == pytest.approx(ref.lower_bound, abs=1e-12)
+
+
+def test_caller_workspace_solve():
+    """rama_solve_ws (SURVEY.md 8(b) ownership): every scratch buffer from a
+    caller block -- here a tensor from torch's caching allocator -- gives the
+    same solve; a block too small fails with MemoryError before writing
+    anything; the reported high-water mark fits the estimate."""
+    import torch
+
+    n, u, v, c = instances.grid8_coo(96, 160, strides=(2, 3), seed=3)
+    g = P.WeightedGraph(n, u, v, c)
+    du, dv, dc = g.device()
+    cfg = P.SolverConfig(mode="PD")
+    a = P.solve_device(n, du, dv, dc, g.num_edges, cfg)
+    b = P.solve_device(n, du, dv, dc, g.num_edges, cfg, workspace="torch")
+    assert torch.equal(a[0], b[0]) and a[1] == b[1] and a[2] == b[2]
+    peak = P.solve_device.last_workspace_peak
+    assert 0 < peak <= P.workspace_bytes(n, g.num_edges, cfg)
+    ws = torch.empty(2 * peak, dtype=torch.uint8, device="cuda")  # first fit: some fragmentation slack
+    d = P.solve_device(n, du, dv, dc, g.num_edges, cfg, workspace=ws)
+    assert torch.equal(a[0], d[0]) and a[1] == d[1]
+    with pytest.raises(MemoryError, match="workspace exhausted"):
+        P.solve_device(n, du, dv, dc, g.num_edges, cfg, workspace=torch.empty(1 << 16, dtype=torch.uint8,
+                                                                                 device="cuda"))
