@@ -18,7 +18,7 @@ HEADER = os.path.join(ROOT, "include", "rama_b200.h")
 
 def declared_symbols():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*|int64_t)\s+(rama_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*|int64_t|uint64_t)\s+(rama_\w+)\s*\(", text, re.M)))
 
 
 def test_library_builds_and_exports_every_declared_symbol():
