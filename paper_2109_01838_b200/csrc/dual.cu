@@ -118,6 +118,43 @@ __device__ __forceinline__ int32_t first_common(const int32_t* a, int32_t la, co
   return -1;
 }
 
+// position in a of the smallest common element of two ascending lists, or -1
+__device__ __forceinline__ int32_t first_common_pos(const int32_t* a, int32_t la, const int32_t* b, int32_t lb) {
+  if (la > 16 * lb) {  // short b: binary-search its elements in a
+    int32_t lo = 0;
+    for (int32_t k = 0; k < lb; k++) {
+      int32_t y = b[k], hi = la;
+      while (lo < hi) {
+        int32_t mid = (lo + hi) >> 1;
+        if (a[mid] < y) lo = mid + 1; else hi = mid;
+      }
+      if (lo == la) return -1;
+      if (a[lo] == y) return lo;
+    }
+    return -1;
+  }
+  if (lb > 16 * la) {  // short a: binary-search its elements in b
+    int32_t lo = 0;
+    for (int32_t k = 0; k < la; k++) {
+      int32_t y = a[k], hi = lb;
+      while (lo < hi) {
+        int32_t mid = (lo + hi) >> 1;
+        if (b[mid] < y) lo = mid + 1; else hi = mid;
+      }
+      if (lo == lb) return -1;
+      if (b[lo] == y) return k;
+    }
+    return -1;
+  }
+  int32_t i = 0, j = 0;
+  while (i < la && j < lb) {
+    int32_t x = a[i], y = b[j];
+    if (x == y) return i;
+    if (x < y) i++; else j++;
+  }
+  return -1;
+}
+
 __global__ void k_gather_i32(const int32_t* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
                              int32_t* __restrict__ dst) {
   GRID_STRIDE(i, n) dst[i] = src[idx[i]];
@@ -227,19 +264,33 @@ __global__ void k_sep4(const int32_t* __restrict__ Q, int64_t nq, const int32_t*
     const bool bside = live && la > 4 * lb;
     const int32_t lb_max = warp_max(bside ? lb : 0);
     if (lb_max > 0) {
+      // keys (position of px(y) in N(a), y).  px(y) is searched in a growing
+      // prefix of N(a) (64, 512, ... positions): if any y has a parent in the
+      // prefix, the minimum does, so the walks never pass it (hub rows: two
+      // long rows are never merged end to end); a prefix with no parent
+      // for any y grows x8 for all of them.
       uint64_t bb = ~0ULL;
-      for (int32_t k0 = 0; k0 < lb_max; k0 += kSepLanes) {
-        const int32_t k = k0 + g;
-        if (bside && k < lb) {
-          const int32_t y = adj[pb + k];
-          const int32_t p = level2_parent(ptr, adj, a, Na, la, y);
-          if (p >= 0) {
-            const uint64_t key = pack2(p, y);
-            bb = key < bb ? key : bb;
+      int32_t lim = min(la, 64);
+      bool need = bside;
+      while (__any_sync(0xffffffffu, need)) {
+        for (int32_t k0 = 0; k0 < lb_max; k0 += kSepLanes) {
+          const int32_t k = k0 + g;
+          if (need && k < lb) {
+            const int32_t y = adj[pb + k];
+            if (y != a && !in_sorted(Na, la, y)) {
+              const int32_t p = first_common_pos(Na, lim, adj + ptr[y], ptr[y + 1] - ptr[y]);
+              if (p >= 0) {
+                const uint64_t key = pack2(p, y);
+                bb = key < bb ? key : bb;
+              }
+            }
           }
         }
+        bb = group_min(bb);
+        if (need && (bb != ~0ULL || lim >= la)) need = false;
+        if (need) lim = (int32_t)min((int64_t)la, (int64_t)lim * 8);
       }
-      bb = group_min(bb);
+      if (bb != ~0ULL) bb = pack2(Na[(int32_t)(bb >> 32)], (int32_t)(uint32_t)bb);  // position -> node
       if (bside) {
         best = bb;
         done = true;
