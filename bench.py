@@ -182,11 +182,12 @@ def peak_hbm():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def traffic_from_profiles(kernel):
+def traffic_from_profiles(kernel, workload):
     """dram read+write bytes of one launch of `kernel` from the committed ncu
-    --set full summary (profiles/ncu_summary.json, round-1 launch of C2)."""
+    --set full summary (profiles/ncu_summary.json: launches of a C2 solve,
+    so only C2 lines carry it)."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if not os.path.exists(p):
+    if workload != "c2" or not os.path.exists(p):
         return None
     with open(p) as fh:
         d = json.load(fh)
@@ -425,7 +426,7 @@ def b200_arm(args):
                 name, (k_ms, k_bytes, k_cnt) = with_bytes[0]
         achieved = k_bytes / (k_ms / 1e3) / 1e9 if k_ms > 0 else 0.0
         roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "peak_source": peak_src, "traffic": traffic_from_profiles(name),
+                "frac": achieved / peak, "peak_source": peak_src, "traffic": traffic_from_profiles(name, args.workload),
                 "algorithmic_bytes_per_launch": k_bytes / max(k_cnt, 1), "launches_per_step": k_cnt / args.steps,
                 "avg_launch_us": 1e3 * k_ms / max(k_cnt, 1), "share_of_step": k_ms / p_ms,
                 "dominant_kernel": dominant}
