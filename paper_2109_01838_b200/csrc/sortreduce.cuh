@@ -43,9 +43,14 @@ struct __align__(16) SrItem {
   double pay;
 };
 
-constexpr int kSrThreads = 512;
-constexpr int kSrTile = 4096;           // row window per tile (items)
-constexpr int kSrHuge = 768;            // longer rows: pre-sorted in global memory (2 CTAs per SM fit)
+#ifndef RAMA_SR_THREADS
+#define RAMA_SR_THREADS 512
+#define RAMA_SR_TILE 4096
+#define RAMA_SR_HUGE 768
+#endif
+constexpr int kSrThreads = RAMA_SR_THREADS;
+constexpr int kSrTile = RAMA_SR_TILE;   // row window per tile (items)
+constexpr int kSrHuge = RAMA_SR_HUGE;   // longer rows: pre-sorted in global memory
 constexpr int kSrCap = kSrTile + kSrHuge;  // staged items per tile (max)
 constexpr int kSrPer = (kSrCap + kSrThreads - 1) / kSrThreads;
 // dynamic shared memory of a tile: keys, payloads, rows, sort permutation
