@@ -363,6 +363,8 @@ int64_t compact_indices(Ctx& ctx, const uint8_t* flags, int64_t n, Buf<int32_t>&
 
 // deterministic fp64 sum (fixed block order, not numpy's order)
 double device_sum(Ctx& ctx, const double* x, int64_t n);
+// the same sum written to a device scalar (n >= 1), no read-back
+void device_sum_to(Ctx& ctx, const double* x, int64_t n, double* out);
 // out[j] (device) = device_sum of x[start[j], start[j] + len[j]), bit for
 // bit (start, len: device int64[K]); 0.0 for an empty segment
 void device_sums(Ctx& ctx, const double* x, const int64_t* start, const int64_t* len, int64_t K, double* out);

@@ -28,6 +28,26 @@ int64_t compact_if(Ctx& ctx, int64_t n, Pred pred, Buf<int32_t>& out) {
   return read_scalar(ctx, nsel.p);
 }
 
+// the same, count left on the device (no read-back): consumers read *count
+template <class Pred>
+void compact_if_dev(Ctx& ctx, int64_t n, Pred pred, Buf<int32_t>& out, Buf<int32_t>& count) {
+  out.alloc(n > 0 ? n : 1, ctx.s);
+  count.alloc(1, ctx.s);
+  if (n <= 0) {
+    count.zero();
+    return;
+  }
+  thrust::counting_iterator<int32_t> it(0);
+  size_t tb = 0;
+  RAMA_CUDA(cub::DeviceSelect::If(nullptr, tb, it, out.p, count.p, (int)n, pred, ctx.s));
+  Buf<uint8_t> tmp(tb, ctx);
+  {
+    KernelScope ks(ctx.s, "cub::DeviceSelect", 0.0);
+    RAMA_CUDA(cub::DeviceSelect::If(tmp.p, tb, it, out.p, count.p, (int)n, pred, ctx.s));
+  }
+  ctx.launches++;
+}
+
 struct NegCost {  // c_i < 0
   const double* c;
   __device__ __forceinline__ bool operator()(int32_t i) const { return c[i] < 0.0; }

@@ -1604,6 +1604,27 @@ void lower_bound_terms(Ctx& ctx, const DualState& st, double* cl_out, double* ne
   RAMA_KERNEL(ctx, k_tri_min, st.T, st.T, st.lam.p, tm);
 }
 
+__global__ void k_lb_total(const double* __restrict__ sn, const double* __restrict__ st, double* __restrict__ out) {
+  double total = 0.0;  // as lower_bound: total = sum(neg); total += sum(tm)
+  if (sn) total = *sn;
+  if (st) total += *st;
+  *out = total;
+}
+
+void lower_bound_to(Ctx& ctx, const DualState& st, double* cl_out, double* out) {
+  ProfScope prof(ctx.s, kFamBound, 36.0 * (double)st.T + 20.0 * (double)st.m_aug);
+  Buf<double> neg(st.m_aug > 0 ? st.m_aug : 1, ctx), tm(st.T > 0 ? st.T : 1, ctx), sums(2, ctx);
+  lower_bound_terms(ctx, st, cl_out, neg.p, tm.p);
+  if (st.m_aug > 0) device_sum_to(ctx, neg.p, st.m_aug, sums.p);
+  if (st.T > 0) device_sum_to(ctx, tm.p, st.T, sums.p + 1);
+  {
+    KernelScope ks(ctx.s, "k_lb_total", 0.0);
+    k_lb_total<<<1, 1, 0, ctx.s>>>(st.m_aug > 0 ? sums.p : nullptr, st.T > 0 ? sums.p + 1 : nullptr, out);
+  }
+  RAMA_LAUNCH_CHECK();
+  ctx.launches++;
+}
+
 double lower_bound(Ctx& ctx, const DualState& st, double* cl_out) {
   // algorithmic bytes: lambda (24 T) and the slot lists (12 T + 4 m_aug)
   // read once, base read (8 m_aug), c^lambda written (8 m_aug)

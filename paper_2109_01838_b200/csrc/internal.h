@@ -120,6 +120,8 @@ double lower_bound(Ctx& ctx, const DualState& st, double* cl_out = nullptr);
 // the summands of lower_bound: neg[m_aug] = min(0, c^lambda_e), tm[T] = the
 // triplets' minimal pattern costs (cl_out optional)
 void lower_bound_terms(Ctx& ctx, const DualState& st, double* cl_out, double* neg, double* tm);
+// lower_bound into a device scalar (no read-back; same value bit for bit)
+void lower_bound_to(Ctx& ctx, const DualState& st, double* cl_out, double* out);
 // a12 reparametrized_graph (dual.py:408-411): canonical merge of originals
 // and chords carrying c^lambda
 Graph reparametrized_graph(Ctx& ctx, const DualState& st, const double* cl = nullptr);

@@ -545,6 +545,21 @@ __global__ void k_final_sum(const double* part, int np, double* out) {
   if (threadIdx.x == 0) *out = sh[0];
 }
 
+void device_sum_to(Ctx& ctx, const double* x, int64_t n, double* out) {
+  Buf<double> part(kSumBlocks, ctx);
+  {
+    KernelScope ks(ctx.s, "k_partial_sum", 8.0 * (double)n);
+    k_partial_sum<<<kSumBlocks, kBlock, 0, ctx.s>>>(x, n, part.p);
+  }
+  RAMA_LAUNCH_CHECK();
+  {
+    KernelScope ks(ctx.s, "k_final_sum", 0.0);
+    k_final_sum<<<1, 1024, 0, ctx.s>>>(part.p, kSumBlocks, out);
+  }
+  RAMA_LAUNCH_CHECK();
+  ctx.launches += 2;
+}
+
 double device_sum(Ctx& ctx, const double* x, int64_t n) {
   if (n <= 0) return 0.0;
   Buf<double> part(kSumBlocks + 1, ctx);

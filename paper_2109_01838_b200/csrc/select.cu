@@ -59,9 +59,11 @@ __device__ __forceinline__ void sf_union(int32_t* p, int32_t a, int32_t b) {
 // one pass of votes: every unmatched endpoint keeps the max of
 // (cost bits, ~neighbour id) as one 128-bit value -- the best positive edge,
 // ties toward the smaller neighbour (contraction.py:207)
-__global__ void k_match_vote(const int32_t* __restrict__ P, int64_t np, const int32_t* __restrict__ u,
-                             const int32_t* __restrict__ v, const double* __restrict__ c,
-                             const uint8_t* __restrict__ matched, ulonglong2* __restrict__ vote) {
+__global__ void k_match_vote(const int32_t* __restrict__ P, const int32_t* __restrict__ np_dev,
+                             const int32_t* __restrict__ u, const int32_t* __restrict__ v,
+                             const double* __restrict__ c, const uint8_t* __restrict__ matched,
+                             ulonglong2* __restrict__ vote) {
+  const int64_t np = *np_dev;  // positive edges (compacted on the device, count not read back)
   GRID_STRIDE(i, np) {
     int32_t e = P[i];
     int32_t a = u[e], b = v[e];
@@ -104,12 +106,12 @@ int64_t select_matching(Ctx& ctx, const GraphView& g, int rounds, Buf<int32_t>& 
   su.alloc(1, ctx.s);
   sv.alloc(1, ctx.s);
   if (n == 0 || m == 0) return 0;
-  Buf<int32_t> P;
-  int64_t np = compact_if(ctx, m, PosCost{g.c}, P);
+  Buf<int32_t> P, npd;
+  compact_if_dev(ctx, m, PosCost{g.c}, P, npd);
   // algorithmic bytes: costs scanned once (8 m), then SURVEY.md 8(d)'s
-  // 34 m+ + 17 n per handshake round (every positive edge is visited)
-  prof.add_bytes(8.0 * (double)m + (double)rounds * (34.0 * (double)np + 17.0 * (double)n));
-  if (np == 0) return 0;
+  // 34 m+ + 17 n per handshake round over the positive edges (m+ ~ m / 2
+  // here: the count stays on the device)
+  prof.add_bytes(8.0 * (double)m + (double)rounds * (34.0 * 0.5 * (double)m + 17.0 * (double)n));
   Buf<uint8_t> matched(n, ctx);
   matched.zero();
   Buf<ulonglong2> vote(n, ctx);
@@ -117,7 +119,7 @@ int64_t select_matching(Ctx& ctx, const GraphView& g, int rounds, Buf<int32_t>& 
   partner.fill_bytes(0xff);
   for (int r = 0; r < rounds; r++) {
     vote.zero();
-    RAMA_KERNEL(ctx, k_match_vote, np, P.p, np, g.u, g.v, g.c, matched.p, vote.p);
+    RAMA_KERNEL(ctx, k_match_vote, m, P.p, npd.p, g.u, g.v, g.c, matched.p, vote.p);
     RAMA_KERNEL(ctx, k_match_pair, n, n, vote.p, matched.p, partner.p);
   }
   Buf<uint8_t> lf(n, ctx);

@@ -119,6 +119,8 @@ void solve(Ctx& ctx, const GraphView& g, const SolveConfig& cfg, int32_t* labels
   iota(ctx, labels, n0);  // f_total
   Graph cur = copy_graph(ctx, g);
   double lb = nan;
+  Buf<double> d_lb(1, ctx);
+  double* h_lb = (double*)(ctx.pinned + 40);  // the round's LB lands here before the round-end sync
   for (int rnd = 1; rnd <= cfg.max_rounds; rnd++) {
     auto t0 = clk::now();
     int64_t nodes_before = cur.n, edges_before = cur.m, T = 0;
@@ -143,9 +145,9 @@ void solve(Ctx& ctx, const GraphView& g, const SolveConfig& cfg, int32_t* labels
       mark(1);
       message_passing(ctx, st, cfg.mp_iterations);
       Buf<double> cl(st.m_aug > 0 ? st.m_aug : 1, ctx);
-      lb_r = lower_bound(ctx, st, cl.p);  // c^lambda computed once for the bound and the graph
+      lower_bound_to(ctx, st, cl.p, d_lb.p);  // c^lambda computed once for the bound and the graph
+      RAMA_CUDA(cudaMemcpyAsync(h_lb, d_lb.p, sizeof(double), cudaMemcpyDeviceToHost, ctx.s));
       T = st.T;
-      if (rnd == 1) lb = lb_r;
       mark(2);
       Graph rep = reparametrized_graph(ctx, st, cl.p);
       mark(3);
@@ -159,6 +161,10 @@ void solve(Ctx& ctx, const GraphView& g, const SolveConfig& cfg, int32_t* labels
       contraction_step(ctx, cur.view(), 3, cfg.switch_fraction, step);
     }
     ctx.sync();
+    if (dual) {
+      lb_r = *h_lb;
+      if (rnd == 1) lb = lb_r;
+    }
     push(trace, max_trace, nr,
          RoundInfo{rnd, dual ? 1 : 0, nodes_before, edges_before, T, lb_r, (dual && rnd == 1) ? 1 : 0,
                    nodes_before - step.num_targets, ms_since(t0)});
