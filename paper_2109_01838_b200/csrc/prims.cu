@@ -630,31 +630,56 @@ void device_sums(Ctx& ctx, const double* x, const int64_t* start, const int64_t*
 
 // ----------------------------------------------------------- row ptrs
 
-// dense lists (m >= n): one pass over the sorted u, edge i opens the rows
-// (u[i-1], u[i]] -- the gaps are short; sparse lists: one binary search per
-// row (a long gap would serialise a thread)
-__global__ void k_row_ptr_fill(const int32_t* __restrict__ u, int64_t m, int64_t n, int32_t* __restrict__ ptr) {
+// Row pointers of a (u, v)-sorted list: edge i opens the rows (u[i-1],
+// u[i]].  Gaps of up to kShortGap rows are filled by the edge's own thread;
+// longer ones (empty stretches: isolated nodes, a batch's finished
+// instances) are listed and filled by whole blocks, so no thread walks a
+// long gap and no row needs a binary search.  The list's length stays on
+// the device.
+constexpr int kShortGap = 32;
+constexpr int64_t kGapPiece = 2048;
+
+__global__ void k_row_ptr_open(const int32_t* __restrict__ u, int64_t m, int64_t n, int32_t* __restrict__ ptr,
+                               int64_t* __restrict__ gaps, int32_t* __restrict__ ngaps) {
   GRID_STRIDE(i, m + 1) {
-    int64_t prev = i > 0 ? (int64_t)u[i - 1] : -1;
-    int64_t cur = i < m ? (int64_t)u[i] : n;
-    for (int64_t x = prev + 1; x <= cur; x++) ptr[x] = (int32_t)i;
+    const int64_t prev = i > 0 ? (int64_t)u[i - 1] : -1;
+    const int64_t cur = i < m ? (int64_t)u[i] : n;
+    if (cur - prev <= kShortGap) {
+      for (int64_t x = prev + 1; x <= cur; x++) ptr[x] = (int32_t)i;
+    } else {  // listed in pieces of kGapPiece rows (one block each)
+      const int64_t pieces = (cur - prev + kGapPiece - 1) / kGapPiece;
+      const int64_t k = atomicAdd(ngaps, (int32_t)pieces);
+      for (int64_t p = 0; p < pieces; p++) {
+        const int64_t lo = prev + 1 + p * kGapPiece;
+        gaps[3 * (k + p)] = lo;
+        gaps[3 * (k + p) + 1] = min(cur, lo + kGapPiece - 1);
+        gaps[3 * (k + p) + 2] = i;
+      }
+    }
   }
 }
 
-__global__ void k_row_ptr_search(const int32_t* __restrict__ u, int64_t m, int64_t n, int32_t* __restrict__ ptr) {
-  GRID_STRIDE(x, n + 1) {
-    int64_t lo = 0, hi = m;
-    while (lo < hi) {
-      int64_t mid = (lo + hi) >> 1;
-      if (u[mid] < x) lo = mid + 1; else hi = mid;
-    }
-    ptr[x] = (int32_t)lo;
+__global__ void k_row_ptr_gaps(const int64_t* __restrict__ gaps, const int32_t* __restrict__ ngaps,
+                               int32_t* __restrict__ ptr) {
+  const int32_t ng = *ngaps;
+  for (int32_t g = blockIdx.x; g < ng; g += gridDim.x) {
+    const int64_t lo = gaps[3 * (int64_t)g], hi = gaps[3 * (int64_t)g + 1];
+    const int32_t val = (int32_t)gaps[3 * (int64_t)g + 2];
+    for (int64_t x = lo + threadIdx.x; x <= hi; x += blockDim.x) ptr[x] = val;
   }
 }
 
 void row_ptr_from_sorted(Ctx& ctx, const int32_t* u, int64_t m, int64_t n, int32_t* ptr) {
-  if (m >= 4 * n) RAMA_KERNEL(ctx, k_row_ptr_fill, m + 1, u, m, n, ptr);
-  else RAMA_KERNEL(ctx, k_row_ptr_search, n + 1, u, m, n, ptr);
+  Buf<int32_t> ng(1, ctx);
+  Buf<int64_t> gaps(3 * ((n + 1) / (kShortGap + 1) + (n + 1) / kGapPiece + 2), ctx);
+  ng.zero();
+  RAMA_KERNEL(ctx, k_row_ptr_open, m + 1, u, m, n, ptr, gaps.p, ng.p);
+  {
+    KernelScope ks(ctx.s, "k_row_ptr_gaps", 0.0);
+    k_row_ptr_gaps<<<(unsigned)num_sms() * 4, kBlock, 0, ctx.s>>>(gaps.p, ng.p, ptr);
+  }
+  RAMA_LAUNCH_CHECK();
+  ctx.launches++;
 }
 
 // ---------------------------------------------------------- bucket sort
