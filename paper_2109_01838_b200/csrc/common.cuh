@@ -347,6 +347,7 @@ struct BucketSorted {
   Buf<uint64_t> key;     // N
   Buf<int32_t> src;      // N
   int64_t total = 0;     // kept items (row >= 0) = row_ptr[R]
+  int64_t big_rows = 0;  // rows longer than 256 items
 };
 // Items with row < 0 are dropped.  Only rows < sort_rows are sorted
 // (default all); later rows keep scatter order.

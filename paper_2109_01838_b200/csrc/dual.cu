@@ -27,6 +27,15 @@
 
 namespace rama {
 
+// slot lists longer than kLongCov (hub edges) are summed a warp per edge
+// (message passing section)
+constexpr int32_t kLongCov = 64;
+
+struct LongCov {  // edge with more than kLongCov slots
+  const int32_t* ptr;
+  __device__ __forceinline__ bool operator()(int32_t e) const { return ptr[e + 1] - ptr[e] > kLongCov; }
+};
+
 // ---------------------------------------------------------------- CSR
 
 __global__ void k_pos_arcs(const int32_t* __restrict__ P, int64_t np, const int32_t* __restrict__ u,
@@ -1237,6 +1246,10 @@ void build_slot_lists(Ctx& ctx, DualState& st) {
   st.slot_ptr = std::move(bs.row_ptr);
   RAMA_KERNEL(ctx, k_key_lo, S, bs.key.p, S, st.slots.p);
   RAMA_KERNEL(ctx, k_coverage, st.m_aug, st.slot_ptr.p, st.m_aug, st.coverage.p);
+  // hub slot lists (only when the sort saw rows > 256: grids never have them)
+  st.long_e.release();
+  st.n_long.release();
+  if (bs.big_rows > 0) compact_if_dev(ctx, st.m_aug, LongCov{st.slot_ptr.p}, st.long_e, st.n_long);
 }
 
 void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& st) {
@@ -1498,15 +1511,68 @@ __device__ __forceinline__ double edge_sum(const int32_t* __restrict__ ptr, cons
   return acc;
 }
 
+// Edges covered by more than kLongCov slots (power-law hubs: C4 round 1 has
+// edges covered ~1e5 times) would serialise one thread over a long chain of
+// dependent gathers.  Their sum must stay sequential in slot order
+// (np.bincount), so a warp gathers 32 multipliers at a time -- the next
+// chunk's loads in flight while the current one is folded -- and every lane
+// folds them in order from registers: the critical path is one fp64 add per
+// slot instead of a dependent load.
+__device__ __forceinline__ double warp_edge_sum(const int32_t* __restrict__ ptr, const int32_t* __restrict__ slots,
+                                                const double* __restrict__ lam, int32_t e, int32_t& cov) {
+  const int lane = threadIdx.x & 31;
+  const int32_t b = ptr[e], en = ptr[e + 1];
+  cov = en - b;
+  double acc = 0.0;
+  double x = b + lane < en ? lam[slots[b + lane]] : 0.0;
+  for (int32_t p0 = b; p0 < en; p0 += 32) {
+    const int32_t pn = p0 + 32 + lane;
+    const double xn = pn < en ? lam[slots[pn]] : 0.0;  // next chunk in flight
+    const int32_t cnt = min(32, en - p0);
+    for (int32_t j = 0; j < cnt; j++) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, x, j));
+    x = xn;
+  }
+  return acc;
+}
+
 __global__ void k_mp_edge(int64_t m, const double* __restrict__ base, const int32_t* __restrict__ ptr,
                           const int32_t* __restrict__ slots, const double* __restrict__ lam,
-                          double* __restrict__ delta) {
+                          double* __restrict__ delta, int32_t long_cov) {
   GRID_STRIDE(e, m) {
+    if (ptr[e + 1] - ptr[e] > long_cov) continue;  // k_mp_edge_long
     int32_t cov;
     double acc = edge_sum(ptr, slots, lam, e, &cov);
     if (cov == 0) continue;
     double cl = __dadd_rn(base[e], acc);
     delta[e] = __ddiv_rn(cl, (double)cov);
+  }
+}
+
+__global__ void k_mp_edge_long(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
+                               const double* __restrict__ base, const int32_t* __restrict__ ptr,
+                               const int32_t* __restrict__ slots, const double* __restrict__ lam,
+                               double* __restrict__ delta) {
+  const int32_t nl = *count;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t W = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = w0; i < nl; i += W) {
+    const int32_t e = list[i];
+    int32_t cov;
+    const double acc = warp_edge_sum(ptr, slots, lam, e, cov);
+    if ((threadIdx.x & 31) == 0) delta[e] = __ddiv_rn(__dadd_rn(base[e], acc), (double)cov);
+  }
+}
+
+// the edge phase: short lists a thread per edge, hub lists a warp per edge
+static void edge_phase(Ctx& ctx, const DualState& st, double* delta) {
+  RAMA_KERNEL(ctx, k_mp_edge, st.m_aug, st.m_aug, st.base.p, st.slot_ptr.p, st.slots.p, st.lam.p, delta,
+              st.n_long.p ? kLongCov : INT32_MAX);
+  if (st.n_long.p) {
+    KernelScope ks(ctx.s, "k_mp_edge_long", 0.0);
+    k_mp_edge_long<<<(unsigned)num_sms() * 8, kBlock, 0, ctx.s>>>(st.long_e.p, st.n_long.p, st.base.p,
+                                                                  st.slot_ptr.p, st.slots.p, st.lam.p, delta);
+    RAMA_LAUNCH_CHECK();
+    ctx.launches++;
   }
 }
 
@@ -1546,15 +1612,15 @@ __global__ void k_mp_triplet(int64_t T, const int32_t* __restrict__ te, const do
   }
 }
 
-void mp_phases(Ctx& ctx, DualState& st, bool edge_phase, bool triplet_phase) {
+void mp_phases(Ctx& ctx, DualState& st, bool do_edge, bool do_triplet) {
   if (st.T == 0) return;
   Buf<double> delta;
-  if (edge_phase) {
+  if (do_edge) {
     delta.alloc(st.m_aug, ctx.s);
-    RAMA_KERNEL(ctx, k_mp_edge, st.m_aug, st.m_aug, st.base.p, st.slot_ptr.p, st.slots.p, st.lam.p, delta.p);
+    edge_phase(ctx, st, delta.p);
   }
-  RAMA_KERNEL(ctx, k_mp_triplet, st.T, st.T, st.tri_edges.p, delta.p, st.lam.p, edge_phase ? 1 : 0,
-              triplet_phase ? 1 : 0);
+  RAMA_KERNEL(ctx, k_mp_triplet, st.T, st.T, st.tri_edges.p, delta.p, st.lam.p, do_edge ? 1 : 0,
+              do_triplet ? 1 : 0);
 }
 
 void message_passing(Ctx& ctx, DualState& st, int iters) {
@@ -1564,7 +1630,7 @@ void message_passing(Ctx& ctx, DualState& st, int iters) {
   Buf<double> delta(st.m_aug, ctx);
   for (int it = 0; it < iters; it++) {
     prof_set_bytes(20.0 * (double)st.m_aug + 36.0 * (double)st.T);
-    RAMA_KERNEL(ctx, k_mp_edge, st.m_aug, st.m_aug, st.base.p, st.slot_ptr.p, st.slots.p, st.lam.p, delta.p);
+    edge_phase(ctx, st, delta.p);
     prof_set_bytes(84.0 * (double)st.T);
     RAMA_KERNEL(ctx, k_mp_triplet, st.T, st.T, st.tri_edges.p, delta.p, st.lam.p, 1, 1);
   }
@@ -1572,8 +1638,9 @@ void message_passing(Ctx& ctx, DualState& st, int iters) {
 
 __global__ void k_reparam(int64_t m, const double* __restrict__ base, const int32_t* __restrict__ ptr,
                           const int32_t* __restrict__ slots, const double* __restrict__ lam,
-                          double* __restrict__ cl, double* __restrict__ negpart) {
+                          double* __restrict__ cl, double* __restrict__ negpart, int32_t long_cov) {
   GRID_STRIDE(e, m) {
+    if (ptr != nullptr && ptr[e + 1] - ptr[e] > long_cov) continue;  // k_reparam_long
     int32_t cov;
     double acc = (ptr != nullptr) ? edge_sum(ptr, slots, lam, e, &cov) : 0.0;
     double x = __dadd_rn(base[e], acc);
@@ -1582,10 +1649,38 @@ __global__ void k_reparam(int64_t m, const double* __restrict__ base, const int3
   }
 }
 
-void reparam_costs(Ctx& ctx, const DualState& st, double* cl) {
-  RAMA_KERNEL(ctx, k_reparam, st.m_aug, st.m_aug, st.base.p, st.T ? st.slot_ptr.p : (const int32_t*)nullptr,
-              st.slots.p, st.lam.p, cl, (double*)nullptr);
+__global__ void k_reparam_long(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
+                               const double* __restrict__ base, const int32_t* __restrict__ ptr,
+                               const int32_t* __restrict__ slots, const double* __restrict__ lam,
+                               double* __restrict__ cl, double* __restrict__ negpart) {
+  const int32_t nl = *count;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t W = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = w0; i < nl; i += W) {
+    const int32_t e = list[i];
+    int32_t cov;
+    const double x = __dadd_rn(base[e], warp_edge_sum(ptr, slots, lam, e, cov));
+    if ((threadIdx.x & 31) == 0) {
+      if (cl) cl[e] = x;
+      if (negpart) negpart[e] = mn2(x, 0.0);
+    }
+  }
 }
+
+// c^lambda (and its negative part): short slot lists a thread per edge, hub lists a warp per edge
+static void reparam_pass(Ctx& ctx, const DualState& st, double* cl, double* neg) {
+  RAMA_KERNEL(ctx, k_reparam, st.m_aug, st.m_aug, st.base.p, st.T ? st.slot_ptr.p : (const int32_t*)nullptr,
+              st.slots.p, st.lam.p, cl, neg, st.n_long.p ? kLongCov : INT32_MAX);
+  if (st.T && st.n_long.p) {
+    KernelScope ks(ctx.s, "k_reparam_long", 0.0);
+    k_reparam_long<<<(unsigned)num_sms() * 8, kBlock, 0, ctx.s>>>(st.long_e.p, st.n_long.p, st.base.p,
+                                                                  st.slot_ptr.p, st.slots.p, st.lam.p, cl, neg);
+    RAMA_LAUNCH_CHECK();
+    ctx.launches++;
+  }
+}
+
+void reparam_costs(Ctx& ctx, const DualState& st, double* cl) { reparam_pass(ctx, st, cl, nullptr); }
 
 __global__ void k_tri_min(int64_t T, const double* __restrict__ lam, double* __restrict__ out) {
   GRID_STRIDE(t, T) {
@@ -1599,8 +1694,7 @@ __global__ void k_tri_min(int64_t T, const double* __restrict__ lam, double* __r
 }
 
 void lower_bound_terms(Ctx& ctx, const DualState& st, double* cl_out, double* neg, double* tm) {
-  RAMA_KERNEL(ctx, k_reparam, st.m_aug, st.m_aug, st.base.p, st.T ? st.slot_ptr.p : (const int32_t*)nullptr,
-              st.slots.p, st.lam.p, cl_out, neg);
+  reparam_pass(ctx, st, cl_out, neg);
   RAMA_KERNEL(ctx, k_tri_min, st.T, st.T, st.lam.p, tm);
 }
 

@@ -100,6 +100,8 @@ struct DualState {
   Buf<int32_t> slot_ptr;    // m_aug + 1 : edge -> ascending slot list
   Buf<int32_t> slots;       // 3T
   Buf<double> lam;          // 3T
+  Buf<int32_t> long_e;      // edges with more than kLongCov slots (hubs), count on the device in n_long
+  Buf<int32_t> n_long;
 };
 // a6/a7 _triangulate_arrays (dual.py:216-290)
 void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& st);

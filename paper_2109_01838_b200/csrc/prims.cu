@@ -885,6 +885,7 @@ void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint6
   const int64_t total = hp[0];
   const int32_t nbig = hp[1], nb = hp[2];
   out.total = total;
+  out.big_rows = nbig;
   if (getenv("RAMA_SORT_STATS") && (nbig || nb))
     fprintf(stderr, "[rama] bucket_sort R %lld N %lld kept %lld: %d rows > %d, %d rows > %d\n", (long long)R,
             (long long)N, (long long)total, nbig, kSmallRow, nb, kBlockRow);
