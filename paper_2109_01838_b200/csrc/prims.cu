@@ -480,7 +480,10 @@ void exclusive_scan64(Ctx& ctx, const int64_t* in, int64_t* out, int64_t n) {
   size_t tb = 0;
   RAMA_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, (int)n, ctx.s));
   Buf<uint8_t> tmp(tb, ctx);
-  RAMA_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, in, out, (int)n, ctx.s));
+  {
+    KernelScope ks(ctx.s, "cub::DeviceScan", 0.0);
+    RAMA_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, in, out, (int)n, ctx.s));
+  }
   ctx.launches++;
 }
 
@@ -810,6 +813,64 @@ __global__ void k_big_lens(const int32_t* __restrict__ rows, int64_t nb, const i
 }
 
 // move huge rows between the row layout and a contiguous staging area
+// Segmented sort of the hub rows by key, as two device-wide stable radix
+// sorts: by the 64-bit key, then (stable) by the segment id -- the result
+// is ordered by (segment, key).  CUB's DeviceSegmentedSort gives each long
+// segment to one CTA, which serialised power-law hubs (C4: 128 ms per solve
+// for rows of up to ~4e5 items); here every pass uses the whole GPU.
+__global__ void k_seg_of(const int32_t* __restrict__ off, int64_t nb, int64_t tot, uint32_t* __restrict__ seg,
+                         int32_t* __restrict__ idx) {
+  GRID_STRIDE(p, tot) {
+    int64_t lo = 0, hi = nb - 1;  // last segment whose offset <= p
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (off[mid] <= p) lo = mid; else hi = mid - 1;
+    }
+    seg[p] = (uint32_t)lo;
+    idx[p] = (int32_t)p;
+  }
+}
+
+__global__ void k_gather_seg(const uint32_t* __restrict__ seg, const int32_t* __restrict__ perm, int64_t tot,
+                             uint32_t* __restrict__ out) {
+  GRID_STRIDE(p, tot) out[p] = seg[perm[p]];
+}
+
+template <class V>
+__global__ void k_permute_pairs(const int32_t* __restrict__ perm, int64_t tot, const uint64_t* __restrict__ k_in,
+                                const V* __restrict__ v_in, uint64_t* __restrict__ k_out, V* __restrict__ v_out) {
+  GRID_STRIDE(p, tot) {
+    const int32_t q = perm[p];
+    k_out[p] = k_in[q];
+    v_out[p] = v_in[q];
+  }
+}
+
+template <class V>
+static void seg_sort_pairs(Ctx& ctx, const uint64_t* k1, uint64_t* k2, const V* v1, V* v2, int64_t tot, int64_t nb,
+                           const int32_t* off) {
+  if (tot <= 0) return;
+  Buf<uint32_t> seg(tot, ctx), seg2(tot, ctx), seg3(tot, ctx);
+  Buf<int32_t> idx(tot, ctx), perm1(tot, ctx), perm2(tot, ctx);
+  Buf<uint64_t> ks(tot, ctx);
+  RAMA_KERNEL(ctx, k_seg_of, tot, off, nb, tot, seg.p, idx.p);
+  radix_sort_pairs(ctx, k1, idx.p, ks.p, perm1.p, tot, 0, 64);  // stable by key
+  RAMA_KERNEL(ctx, k_gather_seg, tot, seg.p, perm1.p, tot, seg2.p);
+  int bits = 1;
+  while (((int64_t)1 << bits) < nb) bits++;
+  size_t tb = 0;
+  RAMA_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, seg2.p, seg3.p, perm1.p, perm2.p, (int)tot, 0, bits,
+                                            ctx.s));
+  Buf<uint8_t> tmp(tb, ctx);
+  {
+    KernelScope ks2(ctx.s, "cub::DeviceRadixSort", 0.0);
+    RAMA_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, seg2.p, seg3.p, perm1.p, perm2.p, (int)tot, 0, bits,
+                                              ctx.s));  // stable by segment: (segment, key) order
+  }
+  ctx.launches++;
+  RAMA_KERNEL(ctx, k_permute_pairs<V>, tot, perm2.p, tot, k1, v1, k2, v2);
+}
+
 __global__ void k_big_stage(const int32_t* __restrict__ rows, int64_t nb, const int32_t* __restrict__ ptr,
                             const int32_t* __restrict__ off, const BItem* __restrict__ items,
                             uint64_t* __restrict__ key_out, int32_t* __restrict__ src_out) {
@@ -899,12 +960,7 @@ void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint6
   unsigned g = (unsigned)std::min<int64_t>(nb, 4096);
   k_big_stage<<<g, kBlock, 0, ctx.s>>>(huge_list, nb, out.row_ptr.p, boff.p, items.p, k1.p, s1.p);
   RAMA_LAUNCH_CHECK();
-  size_t tb = 0;
-  RAMA_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, tb, k1.p, k2.p, s1.p, s2.p, (int)tot, (int)nb, boff.p,
-                                                boff.p + 1, ctx.s));
-  Buf<uint8_t> tmp(tb, ctx);
-  RAMA_CUDA(cub::DeviceSegmentedSort::SortPairs(tmp.p, tb, k1.p, k2.p, s1.p, s2.p, (int)tot, (int)nb, boff.p,
-                                                boff.p + 1, ctx.s));
+  seg_sort_pairs<int32_t>(ctx, k1.p, k2.p, s1.p, s2.p, tot, nb, boff.p);
   k_big_unstage<<<g, kBlock, 0, ctx.s>>>(huge_list, nb, out.row_ptr.p, boff.p, k2.p, s2.p, out.key.p, out.src.p);
   RAMA_LAUNCH_CHECK();
   ctx.launches += 3;
@@ -951,12 +1007,7 @@ void sr_sort_huge(Ctx& ctx, const int32_t* rowptr, const int32_t* rows, int64_t 
   const unsigned g = (unsigned)std::min<int64_t>(nb, 4096);
   k_sr_hstage<<<g, kBlock, 0, ctx.s>>>(rows, nb, rowptr, boff.p, items, k1.p, v1.p);
   RAMA_LAUNCH_CHECK();
-  size_t tb = 0;
-  RAMA_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, tb, k1.p, k2.p, v1.p, v2.p, (int)tot, (int)nb, boff.p,
-                                                boff.p + 1, ctx.s));
-  Buf<uint8_t> tmp(tb, ctx);
-  RAMA_CUDA(cub::DeviceSegmentedSort::SortPairs(tmp.p, tb, k1.p, k2.p, v1.p, v2.p, (int)tot, (int)nb, boff.p,
-                                                boff.p + 1, ctx.s));
+  seg_sort_pairs<uint64_t>(ctx, k1.p, k2.p, v1.p, v2.p, tot, nb, boff.p);
   k_sr_hunstage<<<g, kBlock, 0, ctx.s>>>(rows, nb, rowptr, boff.p, k2.p, v2.p, items);
   RAMA_LAUNCH_CHECK();
   ctx.launches += 3;
