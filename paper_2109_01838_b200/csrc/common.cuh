@@ -459,6 +459,31 @@ __device__ __forceinline__ double seg_sum(const double* a, int64_t n) { return s
 
 __device__ __forceinline__ uint64_t dbits(double x) { return (uint64_t)__double_as_longlong(x); }
 
+// atomicAdd(cnt + r, delta) for every lane with r >= 0, aggregated over runs
+// of equal r in consecutive lanes: histogram inputs grouped by row (sorted
+// edge lists, power-law hub rows) take one atomic per run instead of one per
+// item.  Returns the value the lane's own atomic would have returned in
+// lane order (old + delta x rank in the run): distinct offsets per item.
+// All 32 lanes of the warp must call it.
+__device__ __forceinline__ int32_t run_atomic_add(int32_t* cnt, int32_t r, int32_t delta) {
+  const int lane = threadIdx.x & 31;
+  const int32_t prev = __shfl_up_sync(0xffffffffu, r, 1);
+  const bool act = r >= 0;
+  const bool head = act && (lane == 0 || prev != r);
+  const unsigned heads = __ballot_sync(0xffffffffu, head);
+  const unsigned stops = heads | __ballot_sync(0xffffffffu, !act);  // a run ends at the next head or inactive lane
+  const unsigned upto = 0xffffffffu >> (31 - lane);                  // lanes 0..lane
+  const int h = act ? 31 - __clz(heads & upto) : lane;
+  int32_t old = 0;
+  if (head) {
+    const unsigned above = stops & ~upto;
+    const int end = above ? __ffs(above) - 1 : 32;
+    old = atomicAdd(cnt + r, delta * (end - lane));
+  }
+  old = __shfl_sync(0xffffffffu, old, h);
+  return old + delta * (lane - h);
+}
+
 // Handshake votes: *pa = max(*pa, (hi, lo_a)) and *pb = max(*pb, (hi, lo_b))
 // as unsigned 128-bit values (hi = cost bits, lo = ~neighbour id).  The two
 // CAS loops are interleaved so both atomics are in flight together.

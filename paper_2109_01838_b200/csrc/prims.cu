@@ -693,9 +693,13 @@ void row_ptr_from_sorted(Ctx& ctx, const int32_t* u, int64_t m, int64_t n, int32
 // warp aggregation with __match_any_sync here (C2: 1.23 -> 0.92 ms).
 __global__ void k_bucket_count(const int32_t* __restrict__ row, int64_t N, int32_t* __restrict__ cnt,
                                int32_t* __restrict__ off) {
-  GRID_STRIDE(i, N) {
-    const int32_t r = row[i];
-    if (r >= 0) off[i] = atomicAdd(&cnt[r], 1);
+  const int lane = threadIdx.x & 31;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x - lane; i0 < N;
+       i0 += (int64_t)gridDim.x * blockDim.x) {  // warp-uniform trip count
+    const int64_t i = i0 + lane;
+    const int32_t r = i < N ? row[i] : -1;
+    const int32_t o = run_atomic_add(cnt, r, 1);
+    if (r >= 0) off[i] = o;
   }
 }
 

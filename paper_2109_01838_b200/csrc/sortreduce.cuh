@@ -162,16 +162,22 @@ __device__ __forceinline__ int64_t sr_lookback_block(uint64_t* st, int64_t t, in
 // ---- K1 / K3 -------------------------------------------------------------------
 // Src functor: `int64_t size() const` inputs, up to Src::kK items each;
 // `bool item(int64_t i, int k, int32_t& row, uint64_t& key, double& pay) const`.
+// (counts and slots aggregated over runs of equal rows in consecutive lanes,
+// run_atomic_add: sorted inputs and hub rows take one atomic per run)
 template <class Src>
 __global__ void k_sr_count(Src src, int32_t* __restrict__ cnt) {
   const int64_t n = src.size();
-  GRID_STRIDE(i, n) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x - lane; i0 < n;
+       i0 += (int64_t)gridDim.x * blockDim.x) {  // warp-uniform trip count
+    const int64_t i = i0 + lane;
 #pragma unroll
     for (int k = 0; k < Src::kK; k++) {
-      int32_t row;
+      int32_t row = -1;
       uint64_t key;
       double pay;
-      if (src.item(i, k, row, key, pay)) atomicAdd(cnt + row, 1);
+      if (!(i < n && src.item(i, k, row, key, pay))) row = -1;
+      run_atomic_add(cnt, row, 1);
     }
   }
 }
@@ -180,14 +186,19 @@ template <class Src>
 __global__ void k_sr_scatter(Src src, const int32_t* __restrict__ rowptr, int32_t* __restrict__ cnt,
                              SrItem* __restrict__ items) {
   const int64_t n = src.size();
-  GRID_STRIDE(i, n) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x - lane; i0 < n;
+       i0 += (int64_t)gridDim.x * blockDim.x) {  // warp-uniform trip count
+    const int64_t i = i0 + lane;
 #pragma unroll
     for (int k = 0; k < Src::kK; k++) {
-      int32_t row;
-      uint64_t key;
-      double pay;
-      if (src.item(i, k, row, key, pay)) {
-        const int32_t p = rowptr[row] + atomicSub(cnt + row, 1) - 1;
+      int32_t row = -1;
+      uint64_t key = 0;
+      double pay = 0.0;
+      if (!(i < n && src.item(i, k, row, key, pay))) row = -1;
+      const int32_t left = run_atomic_add(cnt, row, -1);  // count-down: slots left before this item's
+      if (row >= 0) {
+        const int32_t p = rowptr[row] + left - 1;
         SrItem it;
         it.key = key;
         it.pay = pay;
