@@ -218,6 +218,7 @@ constexpr int kSepLanes = 8;
 // C5) never reach the caps.
 constexpr int32_t kHubCap = 128;
 
+
 __device__ __forceinline__ uint64_t group_min(uint64_t x) {
 #pragma unroll
   for (int o = kSepLanes / 2; o > 0; o >>= 1) {
@@ -243,10 +244,13 @@ __device__ __forceinline__ uint64_t pack2(int32_t hi, int32_t lo) {
 // such y has px(y) = x because no smaller x qualifies), and y* is the
 // smallest of those.  Scanning x ascending usually stops at the first x, so
 // the cost is one row intersection instead of |N(b)| of them.
-__global__ void k_sep4(const int32_t* __restrict__ Q, int64_t nq, const int32_t* __restrict__ NQ,
-                       const int32_t* __restrict__ u, const int32_t* __restrict__ v,
+// (Q: repulsive edge ids, *nq_dev of them; the misses are appended to miss_list)
+__global__ void k_sep4(const int32_t* __restrict__ Q, const int32_t* __restrict__ nq_dev,
+                       const int32_t* __restrict__ NQ, const int32_t* __restrict__ u, const int32_t* __restrict__ v,
                        const int32_t* __restrict__ ptr, const int32_t* __restrict__ adj, int L,
-                       int32_t* __restrict__ out_len, int32_t* __restrict__ out_nodes, uint8_t* __restrict__ miss) {
+                       int32_t* __restrict__ out_len, int32_t* __restrict__ out_nodes, int32_t* __restrict__ miss_list,
+                       int32_t* __restrict__ miss_cnt) {
+  const int64_t nq = *nq_dev;
   const int g = threadIdx.x % kSepLanes;
   const int64_t per_warp = 32 / kSepLanes;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -337,15 +341,16 @@ __global__ void k_sep4(const int32_t* __restrict__ Q, int64_t nq, const int32_t*
         out_len[q] = 4;
         row[0] = a; row[1] = (int32_t)(best >> 32); row[2] = (int32_t)(uint32_t)best; row[3] = b;
       }
-      if (miss) miss[i] = !found;
+      if (miss_list && !found) miss_list[atomicAdd(miss_cnt, 1)] = q;
     }
   }
 }
 
-__global__ void k_sep5(const int32_t* __restrict__ Q, int64_t nq, const int32_t* __restrict__ NQ,
-                       const int32_t* __restrict__ u, const int32_t* __restrict__ v,
+__global__ void k_sep5(const int32_t* __restrict__ Q, const int32_t* __restrict__ nq_dev,
+                       const int32_t* __restrict__ NQ, const int32_t* __restrict__ u, const int32_t* __restrict__ v,
                        const int32_t* __restrict__ ptr, const int32_t* __restrict__ adj, int L,
                        int32_t* __restrict__ out_len, int32_t* __restrict__ out_nodes, uint8_t* __restrict__ capped) {
+  const int64_t nq = *nq_dev;
   const int g = threadIdx.x % kSepLanes;
   const int64_t per_warp = 32 / kSepLanes;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -426,52 +431,56 @@ __global__ void k_sep5(const int32_t* __restrict__ Q, int64_t nq, const int32_t*
 // the first hit has px(y) = x.)  One warp per edge, lanes over N(x) in
 // ascending chunks; the scan stops at the first hit, which on power-law
 // graphs comes within the first hub rows.
-__global__ void k_sep5_ordered(const int32_t* __restrict__ Qx, int64_t nx, const int32_t* __restrict__ NQ,
+__global__ void k_sep5_ordered(const uint8_t* __restrict__ flags, int64_t nq, const int32_t* __restrict__ NQ,
                                const int32_t* __restrict__ u, const int32_t* __restrict__ v,
                                const int32_t* __restrict__ ptr, const int32_t* __restrict__ adj, int L,
                                int32_t* __restrict__ out_len, int32_t* __restrict__ out_nodes) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t W = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = w0; i < nx; i += W) {
-    const int32_t q = Qx[i];
-    const int32_t e = NQ[q];
-    const int32_t a = u[e], b = v[e];
-    const int32_t* Na = adj + ptr[a];
-    const int32_t la = ptr[a + 1] - ptr[a];
-    const int32_t* Nb = adj + ptr[b];
-    const int32_t lb = ptr[b + 1] - ptr[b];
-    int32_t hx = -1, hy = -1, hz = -1;
-    for (int32_t xi = 0; xi < la && hx < 0; xi++) {
-      const int32_t x = Na[xi];
-      const int32_t* Nx = adj + ptr[x];
-      const int32_t lx = ptr[x + 1] - ptr[x];
-      for (int32_t j0 = 0; j0 < lx; j0 += 32) {
-        const int32_t j = j0 + lane;
-        int32_t z = -1, y = -1;
-        if (j < lx) {
-          y = Nx[j];
-          if (y != a && !in_sorted(Na, la, y)) z = first_common(adj + ptr[y], ptr[y + 1] - ptr[y], Nb, lb);
-        }
-        const unsigned hit = __ballot_sync(0xffffffffu, z >= 0);
-        if (hit) {
-          const int src = __ffs(hit) - 1;
-          hx = x;
-          hy = __shfl_sync(0xffffffffu, y, src);
-          hz = __shfl_sync(0xffffffffu, z, src);
-          break;
+  for (int64_t c0 = w0 * 32; c0 < nq; c0 += W * 32) {  // a warp scans 32 flags, then takes the flagged edges
+    unsigned todo = __ballot_sync(0xffffffffu, c0 + lane < nq && flags[c0 + lane]);
+    while (todo) {
+      const int32_t q = (int32_t)(c0 + __ffs(todo) - 1);
+      todo &= todo - 1;
+      const int32_t e = NQ[q];
+      const int32_t a = u[e], b = v[e];
+      const int32_t* Na = adj + ptr[a];
+      const int32_t la = ptr[a + 1] - ptr[a];
+      const int32_t* Nb = adj + ptr[b];
+      const int32_t lb = ptr[b + 1] - ptr[b];
+      int32_t hx = -1, hy = -1, hz = -1;
+      for (int32_t xi = 0; xi < la && hx < 0; xi++) {
+        const int32_t x = Na[xi];
+        const int32_t* Nx = adj + ptr[x];
+        const int32_t lx = ptr[x + 1] - ptr[x];
+        for (int32_t j0 = 0; j0 < lx; j0 += 32) {
+          const int32_t j = j0 + lane;
+          int32_t z = -1, y = -1;
+          if (j < lx) {
+            y = Nx[j];
+            if (y != a && !in_sorted(Na, la, y)) z = first_common(adj + ptr[y], ptr[y + 1] - ptr[y], Nb, lb);
+          }
+          const unsigned hit = __ballot_sync(0xffffffffu, z >= 0);
+          if (hit) {
+            const int src = __ffs(hit) - 1;
+            hx = x;
+            hy = __shfl_sync(0xffffffffu, y, src);
+            hz = __shfl_sync(0xffffffffu, z, src);
+            break;
+          }
         }
       }
-    }
-    if (lane == 0) {
-      int32_t* row = out_nodes + (int64_t)q * L;
-      if (hx >= 0) {
-        out_len[q] = 5;
-        row[0] = a; row[1] = hx; row[2] = hy; row[3] = hz; row[4] = b;
-        for (int j = 5; j < L; j++) row[j] = 0;
-      } else {
-        out_len[q] = 0;
-        for (int j = 0; j < L; j++) row[j] = 0;
+      if (lane == 0) {
+        int32_t* row = out_nodes + (int64_t)q * L;
+        if (hx >= 0) {
+          out_len[q] = 5;
+          row[0] = a; row[1] = hx; row[2] = hy; row[3] = hz; row[4] = b;
+          for (int j = 5; j < L; j++) row[j] = 0;
+        } else {
+          out_len[q] = 0;
+          for (int j = 0; j < L; j++) row[j] = 0;
+        }
       }
     }
   }
@@ -598,13 +607,19 @@ __device__ __forceinline__ int32_t grp_sum_i32(int32_t x, unsigned mask) {
 // Table values are POSITIONS in N+(a) (ascending = node order), so the
 // parent is the atomicMin over the positions that reach y and every row of
 // the level can be walked at once (no sequential x loop).
+// Lists are appended on the device (no host read-back between the tiers):
+// the next tier reads *over_cnt groups of over_list, the row-intersection
+// kernels *fb_cnt repulsive edges of fb_list.
 template <class T, int THREADS, int MINB, bool kListed>
 __global__ void __launch_bounds__(THREADS, MINB) k_sep_src(
     const int32_t* __restrict__ gstart, const int32_t* __restrict__ gsrc, const int32_t* __restrict__ glist,
-    int64_t nlist, int64_t ng, int64_t n2, const int32_t* __restrict__ Q2, const int32_t* __restrict__ qb,
-    const int32_t* __restrict__ ptr, const int32_t* __restrict__ adj, int L, int32_t* __restrict__ out_len,
-    int32_t* __restrict__ out_nodes, uint8_t* __restrict__ gover, uint8_t* __restrict__ fb, int force_fallback,
-    uint8_t* __restrict__ capped) {
+    int64_t nlist_host, const int32_t* __restrict__ nlist_dev, int64_t ng, int64_t n2,
+    const int32_t* __restrict__ Q2, const int32_t* __restrict__ qb, const int32_t* __restrict__ ptr,
+    const int32_t* __restrict__ adj, int L, int32_t* __restrict__ out_len, int32_t* __restrict__ out_nodes,
+    int32_t* __restrict__ over_list, int32_t* __restrict__ over_cnt, int32_t* __restrict__ fb_list,
+    int32_t* __restrict__ fb_cnt, int force_fallback, uint8_t* __restrict__ capped) {
+  int64_t nlist = nlist_host;
+  if constexpr (kListed) nlist = *nlist_dev;
   constexpr int kGrp = T::kGrp, kPer = THREADS / T::kGrp, kH = T::kHash;
   __shared__ int32_t s_l1[kPer][T::kL1];
   __shared__ int32_t s_hk[kPer][kH];
@@ -706,10 +721,13 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sep_src(
       __syncwarp(mask);  // table complete before the lookups
     }
     if (over) {
-      if (gover) {  // the next tier takes the source
-        if (lane == 0) gover[k] = 1;
+      if constexpr (!T::kAbort) {  // tiers 1 / 1.5: the next tier takes the source
+        if (lane == 0) over_list[atomicAdd(over_cnt, 1)] = (int32_t)k;
       } else {  // last tier: its edges go to the row-intersection kernels
-        for (int32_t i = e0 + lane; i < e1; i += kGrp) fb[i] = 1;
+        int32_t at = 0;
+        if (lane == 0) at = atomicAdd(fb_cnt, e1 - e0);
+        at = __shfl_sync(mask, at, 0, kGrp);
+        for (int32_t i = e0 + lane; i < e1; i += kGrp) fb_list[at + (i - e0)] = Q2[i];
       }
       __syncwarp(mask);
       continue;
@@ -999,24 +1017,22 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
     run_sep_bfs(ctx, g, csr.ptr.p, csr.adj.p, NQ.p, Qx.p, nx, L, out);
     return;
   }
+  // searches the capped 5-cycle passes truncate are flagged and rerun
+  // exactly; the exact pass scans the flags itself (no compaction, no read-back)
   Buf<uint8_t> capped;
   if (L >= 5) {
     capped.alloc(nq, ctx.s);
     capped.zero();
   }
   separate_tables(ctx, g, L, out, csr, NQ, nq, capped.p);
-  if (capped.p) {  // the truncated 5-cycle searches rerun exactly
-    Buf<int32_t> Qx;
-    const int64_t nx = compact_indices(ctx, capped.p, nq, Qx);
-    if (nx > 0) {
-      if (trace_print()) fprintf(stderr, "[rama] exact 5-cycle searches %lld\n", (long long)nx);
-      const int64_t blocks = std::min<int64_t>((nx + 7) / 8, (int64_t)num_sms() * 16);
-      KernelScope ks(ctx.s, "k_sep5_ordered", 0.0);
-      k_sep5_ordered<<<(unsigned)blocks, 256, 0, ctx.s>>>(Qx.p, nx, NQ.p, g.u, g.v, csr.ptr.p, csr.adj.p, L,
-                                                          out.len.p, out.nodes.p);
-      RAMA_LAUNCH_CHECK();
-      ctx.launches++;
-    }
+  if (capped.p) {
+    KernelScope ks(ctx.s, "k_sep5_ordered", 0.0);
+    const int64_t warps = (nq + 31) / 32;
+    const unsigned blocks = (unsigned)std::min<int64_t>((warps + 7) / 8, (int64_t)num_sms() * 16);
+    k_sep5_ordered<<<blocks, 256, 0, ctx.s>>>(capped.p, nq, NQ.p, g.u, g.v, csr.ptr.p, csr.adj.p, L, out.len.p,
+                                              out.nodes.p);
+    RAMA_LAUNCH_CHECK();
+    ctx.launches++;
   }
 }
 
@@ -1039,9 +1055,11 @@ static void separate_tables(Ctx& ctx, const GraphView& g, int L, CycleRows& out,
   int64_t ng = compact_indices(ctx, head.p, n2, gstart);
   Buf<int32_t> gsrc(ng > 0 ? ng : 1, ctx);
   RAMA_KERNEL(ctx, k_gather_i32, ng, qa.p, gstart.p, ng, gsrc.p);
-  Buf<uint8_t> fb(n2, ctx), gover(ng, ctx);
-  fb.zero();
-  gover.zero();
+  // overflow lists, appended on the device: tier 1 -> 1.5 -> 2 sources, then
+  // the fall-back edges and the 4-cycle misses of the row-intersection pass
+  Buf<int32_t> cnt(4, ctx);  // G15 | G2 | fall-back | misses
+  cnt.zero();
+  Buf<int32_t> G15(ng, ctx), G2(ng, ctx), FB(n2, ctx), M4(n2, ctx);
   static const int64_t cap = [] {  // RAMA_SEP_BLOCKS overrides the grid cap (tests)
     const char* e = getenv("RAMA_SEP_BLOCKS");
     return e ? (int64_t)atoll(e) : (int64_t)148 * 12 * 8;  // 8 waves of 12 CTAs per SM
@@ -1056,68 +1074,50 @@ static void separate_tables(Ctx& ctx, const GraphView& g, int L, CycleRows& out,
     KernelScope ks(ctx.s, "k_sep_src",
                    4.0 * (double)(g.n + 1) + 4.0 * (double)csr.arcs + (16.0 + 4.0 * L) * (double)n2);
     k_sep_src<SrcTier1, kSrcThreads1, 12, false><<<(unsigned)blocks, kSrcThreads1, 0, ctx.s>>>(
-        gstart.p, gsrc.p, (const int32_t*)nullptr, ng, ng, n2, Q2.p, qb.p, csr.ptr.p, csr.adj.p, L, out.len.p,
-        out.nodes.p, gover.p, fb.p, force ? 1 : 0, capped);
+        gstart.p, gsrc.p, (const int32_t*)nullptr, ng, (const int32_t*)nullptr, ng, n2, Q2.p, qb.p, csr.ptr.p,
+        csr.adj.p, L, out.len.p, out.nodes.p, G15.p, cnt.p, (int32_t*)nullptr, (int32_t*)nullptr, force ? 1 : 0,
+        capped);
     RAMA_LAUNCH_CHECK();
     ctx.launches++;
   }
-  {  // sources too large for tier 1: 8 lanes with a 128-entry table, then a
-     // warp each with 4x/16x tables
-    Buf<int32_t> G15;
-    int64_t ng15 = compact_indices(ctx, gover.p, ng, G15);
-    if (ng15 > 0) {
-      Buf<uint8_t> gover2(ng, ctx);
-      gover2.zero();
-      {
-        constexpr int kPer = kSrcThreads1 / SrcTier15::kGrp;
-        int64_t blocks = std::min<int64_t>((ng15 + kPer - 1) / kPer, cap);
-        KernelScope ks(ctx.s, "k_sep_src_mid", 0.0);
-        k_sep_src<SrcTier15, kSrcThreads1, 12, true><<<(unsigned)blocks, kSrcThreads1, 0, ctx.s>>>(
-            gstart.p, gsrc.p, G15.p, ng15, ng, n2, Q2.p, qb.p, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p,
-            gover2.p, fb.p, force ? 1 : 0, capped);
-        RAMA_LAUNCH_CHECK();
-        ctx.launches++;
-      }
-      Buf<int32_t> G2;
-      int64_t ng2 = compact_indices(ctx, gover2.p, ng, G2);
-      if (ng2 > 0) {
-        constexpr int kPer = kSrcThreads2 / SrcTier2::kGrp;
-        int64_t blocks = std::min<int64_t>((ng2 + kPer - 1) / kPer, cap);
-        KernelScope ks(ctx.s, "k_sep_src_wide", 0.0);
-        k_sep_src<SrcTier2, kSrcThreads2, 6, true><<<(unsigned)blocks, kSrcThreads2, 0, ctx.s>>>(
-            gstart.p, gsrc.p, G2.p, ng2, ng, n2, Q2.p, qb.p, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p,
-            (uint8_t*)nullptr, fb.p, force == 1 ? 1 : 0, capped);
-        RAMA_LAUNCH_CHECK();
-        ctx.launches++;
-      }
-    }
+  // sources too large for tier 1: 8 lanes with a 128-entry table, then a warp
+  // each with 4x/16x tables (grids of one wave: the lists are short or empty)
+  const unsigned wave = (unsigned)num_sms() * 12;
+  {
+    KernelScope ks(ctx.s, "k_sep_src_mid", 0.0);
+    k_sep_src<SrcTier15, kSrcThreads1, 12, true><<<wave, kSrcThreads1, 0, ctx.s>>>(
+        gstart.p, gsrc.p, G15.p, 0, cnt.p, ng, n2, Q2.p, qb.p, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p,
+        G2.p, cnt.p + 1, (int32_t*)nullptr, (int32_t*)nullptr, force ? 1 : 0, capped);
+    RAMA_LAUNCH_CHECK();
+    ctx.launches++;
   }
-  // sources that did not fit the tables: sorted-row intersections
-  Buf<int32_t> I2;
-  int64_t nf = compact_indices(ctx, fb.p, n2, I2);
+  {
+    KernelScope ks(ctx.s, "k_sep_src_wide", 0.0);
+    k_sep_src<SrcTier2, kSrcThreads2, 6, true><<<(unsigned)num_sms() * 6, kSrcThreads2, 0, ctx.s>>>(
+        gstart.p, gsrc.p, G2.p, 0, cnt.p + 1, ng, n2, Q2.p, qb.p, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p,
+        (int32_t*)nullptr, (int32_t*)nullptr, FB.p, cnt.p + 2, force == 1 ? 1 : 0, capped);
+    RAMA_LAUNCH_CHECK();
+    ctx.launches++;
+  }
   if (getenv("RAMA_SEP_STATS")) {
     Buf<unsigned long long> st(5, ctx);
     st.zero();
     RAMA_KERNEL(ctx, k_sep_stats, n2, Q2.p, qa.p, qb.p, n2, csr.ptr.p, out.len.p, st.p);
     unsigned long long h[5];
+    int32_t nf = 0;
     RAMA_CUDA(cudaMemcpy(h, st.p, sizeof(h), cudaMemcpyDeviceToHost));
-    fprintf(stderr, "[rama] sep n=%lld m=%lld arcs+=%lld nq=%lld n2=%lld sources=%lld fallback=%lld | none %llu c4 %llu c5 %llu | avg deg+ a %.2f b %.2f\n",
+    RAMA_CUDA(cudaMemcpy(&nf, cnt.p + 2, sizeof(nf), cudaMemcpyDeviceToHost));
+    fprintf(stderr, "[rama] sep n=%lld m=%lld arcs+=%lld nq=%lld n2=%lld sources=%lld fallback=%d | none %llu c4 %llu c5 %llu (before the fall-back) | avg deg+ a %.2f b %.2f\n",
             (long long)g.n, (long long)g.m, (long long)csr.arcs, (long long)nq, (long long)n2, (long long)ng,
-            (long long)nf, h[0], h[1], h[2], (double)h[3] / n2, (double)h[4] / n2);
+            nf, h[0], h[1], h[2], (double)h[3] / n2, (double)h[4] / n2);
   }
-  if (nf == 0) return;
-  Buf<int32_t> Q3(nf, ctx);
-  RAMA_KERNEL(ctx, k_gather_i32, nf, Q2.p, I2.p, nf, Q3.p);
-  RAMA_KERNEL(ctx, k_sep4, nf * kSepLanes, Q3.p, nf, NQ.p, g.u, g.v, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p,
-              L >= 5 ? miss.p : (uint8_t*)nullptr);
+  // sources that did not fit the tables: sorted-row intersections over the
+  // device lists (4-cycles, then 5-cycles for the misses)
+  RAMA_KERNEL(ctx, k_sep4, n2 * kSepLanes, FB.p, cnt.p + 2, NQ.p, g.u, g.v, csr.ptr.p, csr.adj.p, L, out.len.p,
+              out.nodes.p, L >= 5 ? M4.p : (int32_t*)nullptr, cnt.p + 3);
   if (L < 5) return;
-  Buf<int32_t> I3;
-  int64_t n3 = compact_indices(ctx, miss.p, nf, I3);
-  if (n3 == 0) return;
-  Buf<int32_t> Q4(n3, ctx);
-  RAMA_KERNEL(ctx, k_gather_i32, n3, Q3.p, I3.p, n3, Q4.p);
-  RAMA_KERNEL(ctx, k_sep5, n3 * kSepLanes, Q4.p, n3, NQ.p, g.u, g.v, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p,
-              capped);
+  RAMA_KERNEL(ctx, k_sep5, n2 * kSepLanes, M4.p, cnt.p + 3, NQ.p, g.u, g.v, csr.ptr.p, csr.adj.p, L, out.len.p,
+              out.nodes.p, capped);
 }
 
 // --------------------------------------------------------- triangulation
