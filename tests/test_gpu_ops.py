@@ -269,3 +269,42 @@ def test_agreement_matches_reference_and_oracle():
             O.message_passing(ost, iters - (0 if iters == 10 else 10))
         for eps in (1e-6, 1e-3, 0.5):
             assert P.check_edge_triangle_agreement(st, eps) == O.check_edge_triangle_agreement(ost, eps)
+
+
+def test_hub_rows_sort_paths_match_oracle():
+    """Rows far beyond the shared-memory tiles (a hub with 9k neighbours, a
+    second with 2.5k, plus duplicates): canonicalisation and contraction take
+    the device-wide (key, segment) radix path for them, the histograms the
+    run-aggregated atomics; results equal the oracle bit for bit."""
+    rng = np.random.default_rng(5)
+    n = 16000
+    hub1 = np.arange(1, 9001)
+    hub2 = rng.choice(np.arange(9001, n), 2500, replace=False)
+    ru = rng.integers(0, n, 30000)
+    rv = rng.integers(0, n, 30000)
+    keep = ru != rv
+    u = np.concatenate([np.zeros(hub1.size, np.int64), np.full(hub2.size, 9000), ru[keep], hub1[:3000]])
+    v = np.concatenate([hub1, hub2, rv[keep], np.zeros(3000, np.int64)])  # last block: duplicates, flipped
+    c = rng.standard_normal(u.size)
+    g, og = _both(n, u, v, c)
+    assert np.array_equal(g.edges_u, og.edges_u) and np.array_equal(g.edges_v, og.edges_v)
+    assert np.array_equal(g.costs, og.costs)
+    # contract along a matching-like map that folds many hub edges together
+    fmap = np.arange(n, dtype=np.int64) // 2  # canonical: pairs (2k, 2k + 1), the hubs' rows merge
+    nt = n // 2
+    og2, ojoined = O.contract_graph(og, fmap, nt)
+    g2, joined = P.contract_graph(g, P.ContractionMapping(np.asarray(fmap, np.int64), nt))
+    assert np.array_equal(g2.edges_u, og2.edges_u) and np.array_equal(g2.edges_v, og2.edges_v)
+    assert np.array_equal(g2.costs, og2.costs)
+    # separation and triangulation over the hub rows (positive CSR, slot lists)
+    for L in (3, 4, 5):
+        a1, b1 = P.dual._separate(g, L)
+        a2, b2 = O.separate(og, L)
+        assert np.array_equal(a1, a2) and np.array_equal(b1, b2), L
+    lengths, nodes = O.separate(og, 5)
+    st = P.dual._triangulate_arrays(g, lengths, nodes)
+    ost = O.triangulate(og, lengths, nodes)
+    assert np.array_equal(st.tri_edges, ost.tri_edges) and np.array_equal(st.coverage, ost.coverage)
+    P.message_passing(st, 3)
+    O.message_passing(ost, 3)
+    assert np.array_equal(st.lam, ost.lam)
