@@ -8,6 +8,7 @@
 
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/discard_iterator.h>
 
 namespace rama {
 
@@ -46,6 +47,30 @@ void compact_if_dev(Ctx& ctx, int64_t n, Pred pred, Buf<int32_t>& out, Buf<int32
     RAMA_CUDA(cub::DeviceSelect::If(tmp.p, tb, it, out.p, count.p, (int)n, pred, ctx.s));
   }
   ctx.launches++;
+}
+
+// indices with c < 0 and with c > 0, each ascending, in ONE pass over the
+// costs (CUB three-way partition; zero-cost edges are discarded) and one
+// read-back of both counts
+template <class PredA, class PredB>
+void partition2(Ctx& ctx, int64_t n, PredA pa, PredB pb, Buf<int32_t>& out_a, Buf<int32_t>& out_b, int64_t& na,
+                int64_t& nb) {
+  out_a.alloc(n > 0 ? n : 1, ctx.s);
+  out_b.alloc(n > 0 ? n : 1, ctx.s);
+  na = nb = 0;
+  if (n <= 0) return;
+  Buf<int32_t> cnt(2, ctx);
+  thrust::counting_iterator<int32_t> it(0);
+  thrust::discard_iterator<> none;
+  size_t tb = 0;
+  RAMA_CUDA(cub::DevicePartition::If(nullptr, tb, it, out_a.p, out_b.p, none, cnt.p, (int)n, pa, pb, ctx.s));
+  Buf<uint8_t> tmp(tb, ctx);
+  {
+    KernelScope ks(ctx.s, "cub::DevicePartition", 0.0);
+    RAMA_CUDA(cub::DevicePartition::If(tmp.p, tb, it, out_a.p, out_b.p, none, cnt.p, (int)n, pa, pb, ctx.s));
+  }
+  ctx.launches++;
+  read_pair(ctx, cnt.p, cnt.p + 1, na, nb);
 }
 
 struct NegCost {  // c_i < 0

@@ -60,9 +60,8 @@ struct PosCSR {
 };
 
 // _positive_csr (dual.py:155-166): symmetric CSR of E+ sorted by (head, tail)
-static void positive_csr(Ctx& ctx, const GraphView& g, PosCSR& out) {
-  Buf<int32_t> P;
-  int64_t np = compact_if(ctx, g.m, PosCost{g.c}, P);
+// (P: the np positive edges, ascending)
+static void positive_csr(Ctx& ctx, const GraphView& g, const Buf<int32_t>& P, int64_t np, PosCSR& out) {
   int64_t na = 2 * np;
   Buf<int32_t> row(na > 0 ? na : 1, ctx);
   Buf<uint64_t> key(na > 0 ? na : 1, ctx);
@@ -992,8 +991,9 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
   // cycle row per repulsive edge written (4 + 4 L)
   ProfScope prof(ctx.s, kFamSeparate, 16.0 * (double)g.m + 8.0 * (double)(g.n + 1));
   RAMA_REQUIRE(L >= 3, "max_len must be at least 3");
-  Buf<int32_t> NQ;
-  int64_t nq = compact_if(ctx, g.m, NegCost{g.c}, NQ);
+  Buf<int32_t> NQ, PE;
+  int64_t nq = 0, npos = 0;
+  partition2(ctx, g.m, NegCost{g.c}, PosCost{g.c}, NQ, PE, nq, npos);  // repulsive and attractive edges, one pass
   prof.add_bytes((4.0 + 4.0 * L) * (double)nq);
   out.rows = nq;
   out.L = L;
@@ -1001,7 +1001,7 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
   out.nodes.alloc(nq > 0 ? nq * L : 1, ctx.s);
   if (nq == 0) return;
   PosCSR csr;
-  positive_csr(ctx, g, csr);
+  positive_csr(ctx, g, PE, npos, csr);
   prof.add_bytes(8.0 * (double)csr.arcs);
   if (csr.arcs == 0) {
     out.len.zero();
@@ -1285,7 +1285,7 @@ void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& 
     BucketSorted cs;
     bucket_sort(ctx, n, craw, crow.p, ckey.p, cs, true);
     Buf<int32_t> hp;
-    int64_t nh = compact_if(ctx, craw, SortedHead{cs.row.p, cs.key.p}, hp);
+    int64_t nh = compact_if(ctx, cs.total, SortedHead{cs.row.p, cs.key.p}, hp);  // kept chords only
     Buf<uint8_t> isnew(nh > 0 ? nh : 1, ctx);
     RAMA_KERNEL(ctx, k_chord_new, nh, hp.p, nh, cs.row.p, cs.key.p, rptr_p, g.v, isnew.p);
     Buf<int32_t> sel;
@@ -1304,7 +1304,7 @@ void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& 
     BucketSorted ts;
     bucket_sort(ctx, n, traw, trow.p, tkey.p, ts, true);
     Buf<int32_t> hp;
-    T = compact_if(ctx, traw, SortedHead{ts.row.p, ts.key.p}, hp);
+    T = compact_if(ctx, ts.total, SortedHead{ts.row.p, ts.key.p}, hp);  // kept triplets only
     st.tri_nodes.alloc(3 * T, ctx.s);
     st.tri_edges.alloc(3 * T, ctx.s);
     RAMA_KERNEL(ctx, k_tri_out, T, hp.p, T, ts.row.p, ts.key.p, st.tri_nodes.p);
