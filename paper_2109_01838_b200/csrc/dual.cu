@@ -1563,10 +1563,32 @@ __global__ void k_mp_edge_long(const int32_t* __restrict__ list, const int32_t* 
   }
 }
 
-// the edge phase: short lists a thread per edge, hub lists a warp per edge
+// the same edge pass reached through the slots (late rounds: a few
+// triplets over a large graph): the first slot of each covered edge computes it
+__global__ void k_mp_edge_by_slot(int64_t S, const int32_t* __restrict__ te, const double* __restrict__ base,
+                                  const int32_t* __restrict__ ptr, const int32_t* __restrict__ slots,
+                                  const double* __restrict__ lam, double* __restrict__ delta, int32_t long_cov) {
+  GRID_STRIDE(s, S) {
+    const int32_t e = te[s];
+    const int32_t b = ptr[e];
+    if (slots[b] != (int32_t)s || ptr[e + 1] - b > long_cov) continue;
+    int32_t cov;
+    const double acc = edge_sum(ptr, slots, lam, e, &cov);
+    delta[e] = __ddiv_rn(__dadd_rn(base[e], acc), (double)cov);
+  }
+}
+
+// the edge phase: short lists a thread per edge (or per first slot when the
+// slots are far fewer than the edges), hub lists a warp per edge
 static void edge_phase(Ctx& ctx, const DualState& st, double* delta) {
-  RAMA_KERNEL(ctx, k_mp_edge, st.m_aug, st.m_aug, st.base.p, st.slot_ptr.p, st.slots.p, st.lam.p, delta,
-              st.n_long.p ? kLongCov : INT32_MAX);
+  const int32_t long_cov = st.n_long.p ? kLongCov : INT32_MAX;
+  if (3 * st.T < st.m_aug) {
+    RAMA_KERNEL(ctx, k_mp_edge_by_slot, 3 * st.T, 3 * st.T, st.tri_edges.p, st.base.p, st.slot_ptr.p, st.slots.p,
+                st.lam.p, delta, long_cov);
+  } else {
+    RAMA_KERNEL(ctx, k_mp_edge, st.m_aug, st.m_aug, st.base.p, st.slot_ptr.p, st.slots.p, st.lam.p, delta,
+                long_cov);
+  }
   if (st.n_long.p) {
     KernelScope ks(ctx.s, "k_mp_edge_long", 0.0);
     k_mp_edge_long<<<(unsigned)num_sms() * 8, kBlock, 0, ctx.s>>>(st.long_e.p, st.n_long.p, st.base.p,
