@@ -52,8 +52,14 @@ def test_small_exact_modes():
 
 
 def test_small_pd_matches_oracle_and_reference():
+    """PD equals the oracle with the handshake cleanup (deviation D1) bit for
+    bit, and the reference's LB; the primal against the reference's GAEC
+    cleanup: 1 of the 60 small graphs is worse (by 1.08 %, 0.17 in absolute
+    cost), and the 60 together by 0.013 %."""
     fx = load("solve_small.npz")
     worse = 0
+    diff = ref_total = 0.0
+    worst = 0.0
     for i in range(fx.count("edges")):
         g = _pg(fx, i)
         n, u, v, c = fx.graph_arrays(i)
@@ -65,8 +71,12 @@ def test_small_pd_matches_oracle_and_reference():
         assert sol.primal_cost == pytest.approx(P.clustering_cost(g, sol.labeling), abs=1e-12)
         assert sol.lower_bound <= sol.primal_cost + 1e-9
         assert sol.trace[-1].phase == "cleanup"
-        worse += sol.primal_cost > fx.scalar("primal_PD", i) + 1e-9
-    assert worse <= 3  # handshake cleanup ~= GAEC on tiny graphs
+        ref_primal = fx.scalar("primal_PD", i)
+        worse += sol.primal_cost > ref_primal + 1e-9
+        diff += sol.primal_cost - ref_primal
+        ref_total += abs(ref_primal)
+        worst = max(worst, (sol.primal_cost - ref_primal) / max(abs(ref_primal), 1e-12))
+    assert worse <= 1 and worst <= 0.011 and diff / ref_total <= 2e-4, (worse, worst, diff / ref_total)
 
 
 def test_c1_mode_p_bit_exact():
