@@ -819,7 +819,235 @@ __device__ __forceinline__ uint64_t bfs_key(uint32_t tick, uint32_t c) {
   return ((uint64_t)(0xffffffffu - tick) << 32) | c;
 }
 
+// BFS state of one warp, per node: the candidate key K (atomicMin), BFS
+// parent, queue position and depth.  Dense: node-indexed arrays of n
+// entries (any graph).  Hashed: tick-tagged open addressing over H slots --
+// a slot whose tag carries another source's tick is free, so nothing is
+// cleared between sources, and stale keys (older ticks) compare above any
+// current one; a source whose BFS outgrows H/2 slots is handed to the dense
+// pass.
+struct BfsDense {
+  unsigned long long* K;
+  int32_t *Pa, *Po, *Dp;
+  __device__ __forceinline__ int32_t ins(int32_t y, uint32_t) { return y; }
+  __device__ __forceinline__ int32_t find(int32_t y, uint32_t) const { return y; }
+};
+
+struct BfsHash {
+  unsigned long long* tag;  // (tick << 32) | node
+  unsigned long long* K;
+  int32_t *Pa, *Po, *Dp;
+  uint32_t mask;
+  int32_t* claims;          // slots claimed for the current source (shared memory)
+  __device__ __forceinline__ static uint32_t slot(int32_t y) {  // mixed: the low bits index the table
+    uint32_t x = (uint32_t)y * 0x9E3779B1u;
+    x ^= x >> 15;
+    x *= 0x85EBCA6Bu;
+    return x ^ (x >> 13);
+  }
+  __device__ __forceinline__ int32_t ins(int32_t y, uint32_t tick) {
+    const unsigned long long want = ((unsigned long long)tick << 32) | (uint32_t)y;
+    uint32_t h = slot(y) & mask;
+    for (uint32_t probes = 0; probes <= mask;) {
+      const unsigned long long t = __ldcg(tag + h);
+      if (t == want) return (int32_t)h;
+      if ((uint32_t)(t >> 32) != tick) {  // free for this source
+        const unsigned long long old = atomicCAS(tag + h, t, want);
+        if (old == t) {
+          atomicAdd(claims, 1);
+          return (int32_t)h;
+        }
+        if (old == want) return (int32_t)h;
+        if ((uint32_t)(old >> 32) != tick) continue;  // another stale value: retry the slot
+      }
+      h = (h + 1) & mask;
+      probes++;
+    }
+    return -1;
+  }
+  __device__ __forceinline__ int32_t find(int32_t y, uint32_t tick) const {
+    const unsigned long long want = ((unsigned long long)tick << 32) | (uint32_t)y;
+    uint32_t h = slot(y) & mask;
+    for (uint32_t probes = 0; probes <= mask; probes++) {
+      const unsigned long long t = __ldcg(tag + h);
+      if (t == want) return (int32_t)h;
+      if ((uint32_t)(t >> 32) != tick) return -1;
+      h = (h + 1) & mask;
+    }
+    return -1;
+  }
+};
+
+// One warp per source group (glist: the groups to run, *gcount of them; else
+// all ng).  qcap: queue capacity per warp; limit: claimed slots after which a
+// source is abandoned to `over` (hashed state only).
+constexpr int32_t kBfsLaneRow = 12;  // rows up to this long are walked by one lane (longer: the whole warp)
+
+// tick: this source's stamp, increasing along each warp's sources (stale
+// keys of earlier sources must compare above the current ones)
+template <class S>
+__device__ __forceinline__ void bfs_source(S& st, int32_t* Qu, int64_t k, uint32_t tick, int64_t ng, int64_t n2,
+                                           const int32_t* __restrict__ gstart, const int32_t* __restrict__ Q2,
+                                           const int32_t* __restrict__ NQ, const int32_t* __restrict__ u,
+                                           const int32_t* __restrict__ v, const int32_t* __restrict__ ptr,
+                                           const int32_t* __restrict__ adj, int L, int32_t* __restrict__ out_len,
+                                           int32_t* __restrict__ out_nodes, int32_t limit, int32_t* claims,
+                                           int32_t* __restrict__ over_list, int32_t* __restrict__ over_cnt) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t done = bfs_key(tick, 0);
+  const int32_t i0 = gstart[k], i1 = (k + 1 < ng) ? gstart[k + 1] : (int32_t)n2;
+  const int32_t a = u[NQ[Q2[i0]]];
+  if (lane == 0) {
+    *claims = 0;
+    const int32_t sa = st.ins(a, tick);
+    Qu[0] = a;
+    st.K[sa] = done;
+    st.Pa[sa] = -1;
+    st.Po[sa] = 0;
+    st.Dp[sa] = 0;
+  }
+  __syncwarp();
+  int32_t s = 0, e = 1;  // current level's queue range
+  int32_t qlen = 1;
+  for (int lev = 0; lev <= L - 3 && s < e; lev++) {  // discover levels 1 .. L-2
+    // 32 queue positions at a time: a lane per position walks its row (grid
+    // degrees: most lanes busy), or, when a row in the chunk is long, the
+    // whole warp walks one row after the other
+    bool full = false;
+    for (int32_t p0 = s; p0 < e; p0 += 32) {  // candidates: atomicMin over the position
+      const int32_t p = p0 + lane;
+      const int32_t x = p < e ? __ldcg(Qu + p) : 0;
+      const int32_t b0 = p < e ? ptr[x] : 0, dx = p < e ? ptr[x + 1] - b0 : 0;
+      if (!__any_sync(0xffffffffu, dx > kBfsLaneRow)) {
+        for (int32_t j = 0; j < dx; j++) {
+          const int32_t sy = st.ins(adj[b0 + j], tick);
+          if (sy < 0) full = true;
+          else atomicMin(st.K + sy, (unsigned long long)bfs_key(tick, (uint32_t)p + 1));
+        }
+        continue;
+      }
+      for (int32_t pp = p0; pp < min(p0 + 32, e); pp++) {
+        const int32_t xx = __ldcg(Qu + pp);
+        const int32_t bb = ptr[xx], dd = ptr[xx + 1] - bb;
+        for (int32_t j = lane; j < dd; j += 32) {
+          const int32_t sy = st.ins(adj[bb + j], tick);
+          if (sy < 0) full = true;
+          else atomicMin(st.K + sy, (unsigned long long)bfs_key(tick, (uint32_t)pp + 1));
+        }
+      }
+    }
+    __syncwarp();
+    if (__any_sync(0xffffffffu, full) || *(volatile int32_t*)claims > limit) {  // hashed state outgrown
+      if (lane == 0) over_list[atomicAdd(over_cnt, 1)] = (int32_t)k;
+      return;
+    }
+    for (int32_t p0 = s; p0 < e; p0 += 32) {  // winners in (position, row) order
+      const int32_t p = p0 + lane;
+      const int32_t x = p < e ? __ldcg(Qu + p) : 0;
+      const int32_t b0 = p < e ? ptr[x] : 0, dx = p < e ? ptr[x + 1] - b0 : 0;
+      if (!__any_sync(0xffffffffu, dx > kBfsLaneRow)) {
+        // a lane per position: count its winners, offsets by a warp scan
+        // (lane order = position order), then write them in row order
+        const unsigned long long mine = bfs_key(tick, (uint32_t)p + 1);
+        int32_t cnt = 0;
+        for (int32_t j = 0; j < dx; j++) {
+          const int32_t sy = st.find(adj[b0 + j], tick);
+          cnt += sy >= 0 && __ldcg(st.K + sy) == mine;
+        }
+        int32_t incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        int32_t at = qlen + incl - cnt;
+        for (int32_t j = 0; j < dx && cnt > 0; j++) {
+          const int32_t y = adj[b0 + j];
+          const int32_t sy = st.find(y, tick);
+          if (sy >= 0 && __ldcg(st.K + sy) == mine) {
+            Qu[at] = y;
+            st.Pa[sy] = x;
+            st.Po[sy] = at;
+            st.Dp[sy] = lev + 1;
+            at++;
+            cnt--;
+          }
+        }
+        qlen += __shfl_sync(0xffffffffu, incl, 31);
+        continue;
+      }
+      for (int32_t pp = p0; pp < min(p0 + 32, e); pp++) {
+        const int32_t xx = __ldcg(Qu + pp);
+        const int32_t bb = ptr[xx], dd = ptr[xx + 1] - bb;
+        for (int32_t j0 = 0; j0 < dd; j0 += 32) {
+          const int32_t j = j0 + lane;
+          const int32_t y = j < dd ? adj[bb + j] : 0;
+          const int32_t sy = j < dd ? st.find(y, tick) : -1;
+          const bool win = sy >= 0 && __ldcg(st.K + sy) == bfs_key(tick, (uint32_t)pp + 1);
+          const unsigned bal = __ballot_sync(0xffffffffu, win);
+          if (win) {
+            const int32_t at = qlen + __popc(bal & ((1u << lane) - 1u));
+            Qu[at] = y;
+            st.Pa[sy] = xx;
+            st.Po[sy] = at;
+            st.Dp[sy] = lev + 1;
+          }
+          qlen += __popc(bal);
+        }
+      }
+    }
+    __syncwarp();
+    for (int32_t i = e + lane; i < qlen; i += 32) st.K[st.find(__ldcg(Qu + i), tick)] = done;
+    __syncwarp();
+    s = e;
+    e = qlen;
+  }
+  const int32_t last = L - 2;  // deepest stored level
+  for (int32_t i = i0; i < i1; i++) {
+    const int32_t q = Q2[i];
+    const int32_t b = v[NQ[q]];
+    int32_t tail = -1, len = 0;
+    const int32_t sb = st.find(b, tick);
+    if (sb >= 0 && __ldcg(st.K + sb) == done) {  // b itself reached at level <= L-2
+      len = __ldcg(st.Dp + sb) + 1;
+      tail = b;
+    } else {  // b at level L-1: parent = first queue position among N(b) at level L-2
+      const int32_t b0 = ptr[b], db = ptr[b + 1] - b0;
+      int32_t best = 0x7fffffff;
+      for (int32_t j = lane; j < db; j += 32) {
+        const int32_t sy = st.find(adj[b0 + j], tick);
+        if (sy >= 0 && __ldcg(st.K + sy) == done && __ldcg(st.Dp + sy) == last) best = min(best, __ldcg(st.Po + sy));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+      if (best != 0x7fffffff) {
+        len = L;
+        tail = -2 - best;  // marks: b appended after the queue node at `best`
+      }
+    }
+    if (lane == 0 && len >= 3) {
+      int32_t* row = out_nodes + (int64_t)q * L;
+      out_len[q] = len;
+      int32_t idx = len - 1, x;
+      if (tail >= 0) {
+        x = tail;
+      } else {
+        row[idx--] = b;
+        x = __ldcg(Qu + (-2 - tail));
+      }
+      for (; idx >= 0; idx--) {
+        row[idx] = x;
+        x = __ldcg(st.Pa + st.find(x, tick));
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// dense state: n-sized slices per warp (glist: an overflow list, *gcount
+// groups; else every group)
 __global__ void __launch_bounds__(256) k_sep_bfs(const int32_t* __restrict__ gstart, int64_t ng, int64_t n2,
+                                                 const int32_t* __restrict__ glist, const int32_t* __restrict__ gcount,
                                                  const int32_t* __restrict__ Q2, const int32_t* __restrict__ NQ,
                                                  const int32_t* __restrict__ u, const int32_t* __restrict__ v,
                                                  const int32_t* __restrict__ ptr, const int32_t* __restrict__ adj,
@@ -827,102 +1055,52 @@ __global__ void __launch_bounds__(256) k_sep_bfs(const int32_t* __restrict__ gst
                                                  int32_t* __restrict__ out_nodes, unsigned long long* keys,
                                                  int32_t* par, int32_t* pos, int32_t* queue, int32_t* depth,
                                                  int64_t n) {
-  const int lane = threadIdx.x & 31;
+  __shared__ int32_t s_claims[8];
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t W = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  unsigned long long* K = keys + w * n;
-  int32_t* Pa = par + w * n;
-  int32_t* Po = pos + w * n;
-  int32_t* Qu = queue + w * n;
-  int32_t* Dp = depth + w * n;
-  for (int64_t k = w; k < ng; k += W) {
-    const uint32_t tick = (uint32_t)(k + 1);
-    const uint64_t done = bfs_key(tick, 0);
-    const int32_t i0 = gstart[k], i1 = (k + 1 < ng) ? gstart[k + 1] : (int32_t)n2;
-    const int32_t a = u[NQ[Q2[i0]]];
-    if (lane == 0) {
-      Qu[0] = a;
-      K[a] = done;
-      Pa[a] = -1;
-      Po[a] = 0;
-      Dp[a] = 0;
-    }
-    __syncwarp();
-    int32_t s = 0, e = 1;  // current level's queue range
-    int32_t qlen = 1;
-    for (int lev = 0; lev <= L - 3 && s < e; lev++) {  // discover levels 1 .. L-2
-      for (int32_t p = s; p < e; p++) {  // candidates: atomicMin over the position
-        const int32_t x = __ldcg(Qu + p);
-        const int32_t b0 = ptr[x], dx = ptr[x + 1] - b0;
-        for (int32_t j = lane; j < dx; j += 32) {
-          int32_t y = adj[b0 + j];
-          atomicMin(K + y, (unsigned long long)bfs_key(tick, (uint32_t)p + 1));
-        }
-      }
-      __syncwarp();
-      for (int32_t p = s; p < e; p++) {  // winners in (position, row) order
-        const int32_t x = __ldcg(Qu + p);
-        const int32_t b0 = ptr[x], dx = ptr[x + 1] - b0;
-        for (int32_t j0 = 0; j0 < dx; j0 += 32) {
-          int32_t j = j0 + lane;
-          int32_t y = j < dx ? adj[b0 + j] : 0;
-          bool win = j < dx && __ldcg(K + y) == bfs_key(tick, (uint32_t)p + 1);
-          unsigned bal = __ballot_sync(0xffffffffu, win);
-          if (win) {
-            int32_t at = qlen + __popc(bal & ((1u << lane) - 1u));
-            Qu[at] = y;
-            Pa[y] = x;
-            Po[y] = at;
-            Dp[y] = lev + 1;
-          }
-          qlen += __popc(bal);
-        }
-      }
-      __syncwarp();
-      for (int32_t i = e + lane; i < qlen; i += 32) K[__ldcg(Qu + i)] = done;
-      __syncwarp();
-      s = e;
-      e = qlen;
-    }
-    const int32_t last = L - 2;  // deepest stored level
-    for (int32_t i = i0; i < i1; i++) {
-      const int32_t q = Q2[i];
-      const int32_t b = v[NQ[q]];
-      int32_t tail = -1, len = 0;
-      if (__ldcg(K + b) == done) {  // b itself reached at level <= L-2
-        len = __ldcg(Dp + b) + 1;
-        tail = b;
-      } else {  // b at level L-1: parent = first queue position among N(b) at level L-2
-        const int32_t b0 = ptr[b], db = ptr[b + 1] - b0;
-        int32_t best = 0x7fffffff;
-        for (int32_t j = lane; j < db; j += 32) {
-          int32_t y = adj[b0 + j];
-          if (__ldcg(K + y) == done && __ldcg(Dp + y) == last) best = min(best, __ldcg(Po + y));
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
-        if (best != 0x7fffffff) {
-          len = L;
-          tail = -2 - best;  // marks: b appended after the queue node at `best`
-        }
-      }
-      if (lane == 0 && len >= 3) {
-        int32_t* row = out_nodes + (int64_t)q * L;
-        out_len[q] = len;
-        int32_t idx = len - 1, x;
-        if (tail >= 0) {
-          x = tail;
-        } else {
-          row[idx--] = b;
-          x = __ldcg(Qu + (-2 - tail));
-        }
-        for (; idx >= 0; idx--) {
-          row[idx] = x;
-          x = __ldcg(Pa + x);
-        }
-      }
-      __syncwarp();
-    }
+  BfsDense st{keys + w * n, par + w * n, pos + w * n, depth + w * n};
+  const int64_t nl = glist ? (int64_t)*gcount : ng;
+  for (int64_t j = w; j < nl; j += W) {
+    const int64_t k = glist ? glist[j] : j;  // the list is unordered: stamp by position j
+    bfs_source(st, queue + w * n, k, (uint32_t)(j + 1), ng, n2, gstart, Q2, NQ, u, v, ptr, adj, L, out_len, out_nodes, 0x7fffffff,
+               s_claims + (threadIdx.x >> 5), nullptr, nullptr);
+  }
+}
+
+// hashed state: H = mask + 1 slots per warp; sources that outgrow H / 2 go
+// to over_list for the dense kernel
+__global__ void __launch_bounds__(256) k_sep_bfs_hash(const int32_t* __restrict__ gstart, int64_t ng, int64_t n2,
+                                                      const int32_t* __restrict__ glist,
+                                                      const int32_t* __restrict__ gcount,
+                                                      const int32_t* __restrict__ Q2, const int32_t* __restrict__ NQ,
+                                                      const int32_t* __restrict__ u, const int32_t* __restrict__ v,
+                                                      const int32_t* __restrict__ ptr,
+                                                      const int32_t* __restrict__ adj, int L,
+                                                      int32_t* __restrict__ out_len, int32_t* __restrict__ out_nodes,
+                                                      unsigned long long* tags, unsigned long long* keys,
+                                                      int32_t* par, int32_t* pos, int32_t* queue, int32_t* depth,
+                                                      uint32_t mask, int32_t* __restrict__ over_list,
+                                                      int32_t* __restrict__ over_cnt) {
+  __shared__ int32_t s_claims[8];
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t W = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t H = (int64_t)mask + 1;
+  BfsHash st{tags + w * H, keys + w * H, par + w * H, pos + w * H, depth + w * H, mask, s_claims + (threadIdx.x >> 5)};
+  const int64_t nl = glist ? (int64_t)*gcount : ng;
+  for (int64_t j = w; j < nl; j += W) {
+    const int64_t k = glist ? glist[j] : j;
+    bfs_source(st, queue + w * H, k, (uint32_t)(j + 1), ng, n2, gstart, Q2, NQ, u, v, ptr, adj, L, out_len,
+               out_nodes, (int32_t)(H / 2), st.claims, over_list, over_cnt);
+  }
+}
+
+// no cycle of up to 5 edges found, and both ends have attractive neighbours
+__global__ void k_needs_bfs(const int32_t* __restrict__ len, int64_t nq, const int32_t* __restrict__ NQ,
+                            const int32_t* __restrict__ u, const int32_t* __restrict__ v,
+                            const int32_t* __restrict__ ptr, uint8_t* __restrict__ deep) {
+  GRID_STRIDE(q, nq) {
+    const int32_t e = NQ[q], a = u[e], b = v[e];
+    deep[q] = len[q] == 0 && ptr[a + 1] > ptr[a] && ptr[b + 1] > ptr[b];
   }
 }
 
@@ -940,21 +1118,56 @@ static void run_sep_bfs(Ctx& ctx, const GraphView& g, const int32_t* ptr, const 
   RAMA_KERNEL(ctx, k_bfs_heads, nx, Qx, nx, NQ, g.u, head.p);
   Buf<int32_t> gstart;
   const int64_t ng = compact_indices(ctx, head.p, nx, gstart);
-  size_t free_b = 0, total_b = 0;
-  RAMA_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  // hashed pass, one warp per source, 1 K slots (32 KB) per warp: the small
+  // balls of grid-like graphs stay in L2-resident tables; the balls that
+  // outgrow them take the dense pass (measured, PD+: C2 293 -> 152 ms and
+  // 83 -> 6 GB; C3 34.6 s with the dense pass alone -> 29 s; 16 K-slot tables:
+  // C2 162 ms, C3 83 s) -- RAMA_BFS_HASH_BITS resizes the table (tests)
+  static const int kHashBits = [] {
+    const char* e = getenv("RAMA_BFS_HASH_BITS");
+    const int b = e ? atoi(e) : 10;
+    return b < 4 ? 4 : (b > 20 ? 20 : b);
+  }();
+  Buf<int32_t> over(ng, ctx), ocnt(1, ctx);
+  ocnt.zero();
+  for (int pass = 0; pass < 1; pass++) {
+    const int bits = kHashBits;
+    const int64_t H = (int64_t)1 << bits;
+    const int64_t budget = std::max<int64_t>(8, ((int64_t)4 << 30) / (32 * H));  // ~4 GB of tables at most
+    int64_t W = std::min<int64_t>(std::min<int64_t>((int64_t)num_sms() * 8, ng), budget);
+    W = (W + 7) / 8 * 8;  // whole 8-warp blocks
+    Buf<unsigned long long> tags((size_t)W * H, ctx), keys((size_t)W * H, ctx);
+    Buf<int32_t> par((size_t)W * H, ctx), pos((size_t)W * H, ctx), queue((size_t)W * H, ctx),
+        depth((size_t)W * H, ctx);
+    tags.fill_bytes(0xff);
+    keys.fill_bytes(0xff);
+    KernelScope ks(ctx.s, "k_sep_bfs_hash", 0.0);
+    k_sep_bfs_hash<<<(unsigned)(W / 8), 256, 0, ctx.s>>>(
+        gstart.p, ng, nx, (const int32_t*)nullptr, ocnt.p, Qx, NQ, g.u, g.v, ptr, adj, L, out.len.p, out.nodes.p,
+        tags.p, keys.p, par.p, pos.p, queue.p, depth.p, (uint32_t)(H - 1), over.p, ocnt.p);
+    RAMA_LAUNCH_CHECK();
+    ctx.launches++;
+  }
+  const int64_t no = read_scalar(ctx, ocnt.p);
+  if (getenv("RAMA_SEP_STATS"))
+    fprintf(stderr, "[rama] sep bfs: %lld edges, %lld sources, %lld beyond the hashed table\n", (long long)nx,
+            (long long)ng, (long long)no);
+  if (no == 0) return;
+  // dense pass for the sources whose ball outgrew the table: n-sized slices,
+  // at most ~16 GB of them
   const int64_t per_warp = 24 * g.n;
-  int64_t W = (int64_t)(free_b / 4) / (per_warp > 0 ? per_warp : 1);
-  if (W > (int64_t)num_sms() * 8) W = (int64_t)num_sms() * 8;
-  if (W > ng) W = ng;
-  RAMA_REQUIRE(W >= 1, "not enough device memory for the exact separation scratch");
-  W = (W + 7) / 8 * 8;  // whole 8-warp blocks; every launched warp owns a scratch slice
-  Buf<unsigned long long> keys((size_t)W * g.n, ctx);
-  Buf<int32_t> par((size_t)W * g.n, ctx), pos((size_t)W * g.n, ctx), queue((size_t)W * g.n, ctx),
-      depth((size_t)W * g.n, ctx);
+  int64_t Wd = std::min<int64_t>((int64_t)num_sms() * 8, no);
+  const int64_t budget = std::max<int64_t>(8, ((int64_t)16 << 30) / (per_warp > 0 ? per_warp : 1));
+  if (Wd > budget) Wd = budget;
+  Wd = (Wd + 7) / 8 * 8;
+  Buf<unsigned long long> keys((size_t)Wd * g.n, ctx);
+  Buf<int32_t> par((size_t)Wd * g.n, ctx), pos((size_t)Wd * g.n, ctx), queue((size_t)Wd * g.n, ctx),
+      depth((size_t)Wd * g.n, ctx);
   keys.fill_bytes(0xff);
   KernelScope ks(ctx.s, "k_sep_bfs", 0.0);
-  k_sep_bfs<<<(unsigned)((W + 7) / 8), 256, 0, ctx.s>>>(gstart.p, ng, nx, Qx, NQ, g.u, g.v, ptr, adj, L, out.len.p,
-                                                        out.nodes.p, keys.p, par.p, pos.p, queue.p, depth.p, g.n);
+  k_sep_bfs<<<(unsigned)(Wd / 8), 256, 0, ctx.s>>>(gstart.p, ng, nx, over.p, ocnt.p, Qx, NQ, g.u, g.v, ptr, adj, L,
+                                                   out.len.p, out.nodes.p, keys.p, par.p, pos.p, queue.p, depth.p,
+                                                   g.n);
   RAMA_LAUNCH_CHECK();
   ctx.launches++;
 }
@@ -1008,15 +1221,6 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
     out.nodes.zero();
     return;
   }
-  if (L >= 6) {  // PD+ and longer: the exact source-grouped BFS for every edge without a triangle
-    Buf<uint8_t> miss(nq, ctx);
-    RAMA_KERNEL(ctx, k_sep3, nq, (const int32_t*)nullptr, nq, NQ.p, g.u, g.v, csr.ptr.p, csr.adj.p, L, out.len.p,
-                out.nodes.p, miss.p);
-    Buf<int32_t> Qx;
-    const int64_t nx = compact_indices(ctx, miss.p, nq, Qx);
-    run_sep_bfs(ctx, g, csr.ptr.p, csr.adj.p, NQ.p, Qx.p, nx, L, out);
-    return;
-  }
   // searches the capped 5-cycle passes truncate are flagged and rerun
   // exactly; the exact pass scans the flags itself (no compaction, no read-back)
   Buf<uint8_t> capped;
@@ -1033,6 +1237,17 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
                                               out.nodes.p);
     RAMA_LAUNCH_CHECK();
     ctx.launches++;
+  }
+  if (L >= 6) {
+    // PD+ and longer: cycles of up to 5 edges came from the passes above --
+    // the BFS reaches b at the same level with the same parents whatever L
+    // is -- so only the edges without one (both ends on E+) run the exact
+    // source-grouped BFS for lengths 6..L
+    Buf<uint8_t> deep(nq, ctx);
+    RAMA_KERNEL(ctx, k_needs_bfs, nq, out.len.p, nq, NQ.p, g.u, g.v, csr.ptr.p, deep.p);
+    Buf<int32_t> Qx;
+    const int64_t nx = compact_indices(ctx, deep.p, nq, Qx);
+    run_sep_bfs(ctx, g, csr.ptr.p, csr.adj.p, NQ.p, Qx.p, nx, L, out);
   }
 }
 

@@ -207,6 +207,27 @@ def test_separation_tiers_agree():
     assert outs[0] == outs[1] == outs[2]
 
 
+def test_pd_plus_hashed_and_dense_bfs_agree_with_oracle():
+    """PD+ (cycles of 6-7 edges): the source-grouped BFS keeps each warp's
+    state in a tick-tagged hash table and hands the sources whose ball
+    outgrows it to the dense pass; a 16-slot table (RAMA_BFS_HASH_BITS=4)
+    sends most sources there.  Both executions equal the oracle's PD+ solve."""
+    code = ("import sys, hashlib; sys.path.insert(0, '..')\n"
+            "import paper_2109_01838_b200 as P\nfrom paper_2109_01838_b200 import instances\n"
+            "for coo in [instances.grid3d_coo(12, 24, 24, stride=2, seed=4), instances.grid_coo(48, 64, 3, seed=2),\n"
+            "            instances.random_coo(200, 0.05, seed=3)]:\n"
+            "    s = P.solve(P.WeightedGraph(*coo), P.SolverConfig(mode='PD+'))\n"
+            "    t = [(r.nodes, r.edges, r.triplets, r.contracted, r.lb) for r in s.trace]\n"
+            "    print(repr(s.primal_cost), repr(s.lower_bound), hashlib.md5(s.labeling.tobytes()).hexdigest(), t)\n")
+    outs = [_solve_env({"RAMA_BFS_HASH_BITS": k}, code) for k in ("10", "4")]
+    assert outs[0] == outs[1]
+    lines = outs[0].strip().splitlines()
+    for line, coo in zip(lines, [instances.grid3d_coo(12, 24, 24, stride=2, seed=4), instances.grid_coo(48, 64, 3, seed=2),
+                                 instances.random_coo(200, 0.05, seed=3)]):
+        ref = O.solve(O.Graph(*coo), mode="PD+", cleanup="handshake")
+        assert line.split()[0] == repr(ref.primal_cost), (line, ref.primal_cost)
+
+
 # Reference per-round statistics of C3 (SURVEY.md Appendix A, measured with
 # the reference parcut solver): (nodes, edges, triplets, |S|) per PD round,
 # and its primal / lower bound (BASELINE.md section 2).
