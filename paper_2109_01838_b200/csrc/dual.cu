@@ -74,16 +74,6 @@ static void positive_csr(Ctx& ctx, const GraphView& g, const Buf<int32_t>& P, in
   out.arcs = na;
 }
 
-// sorted item p -> adj[p]
-struct AdjEmit {
-  int32_t* adj;
-  __device__ __forceinline__ bool keep(int32_t, uint64_t) const { return true; }
-  template <class A>
-  __device__ __forceinline__ void out(int64_t idx, int32_t, uint64_t key, A, int64_t) const {
-    adj[idx] = (int32_t)(uint32_t)key;
-  }
-};
-
 // ----------------------------------------------------------- separation
 
 __device__ __forceinline__ bool in_sorted(const int32_t* a, int32_t len, int32_t y) {

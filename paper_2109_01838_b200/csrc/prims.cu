@@ -1,7 +1,8 @@
 // Generic device primitives: prefix scans, compaction, deterministic sums,
-// and the bucket sort that every canonical-order step of the solver is
-// built on (canonicalisation, contraction, positive CSR, triplet and chord
-// dedupe, edge->slot lists).
+// row pointers, the caching allocator / caller workspace, and the bucket
+// sort behind the positive CSR, the triplet and chord dedupe and the
+// edge->slot lists (canonicalisation and contraction use the fused
+// sort-reduce of sortreduce.cuh).
 //
 // Bucket sort = counting sort on a 32-bit row id (warp-aggregated atomic
 // histogram + scan + scatter) followed by an in-row sort on a 64-bit key.

@@ -1,11 +1,12 @@
 // Fused row sort + unique + reduce ("sort-reduce"): the canonical-order
-// primitive behind contraction (a18), canonicalisation (a3), the positive
-// CSR (a4), triangulation's chord/triplet dedupe (a6/a7) and the edge->slot
-// lists (a8).
+// primitive behind contraction (a18) and canonicalisation (a3).  (The
+// positive CSR, triangulation's dedupes and the slot lists keep the bucket
+// sort of prims.cu: their rows hold 1-3 items, for which this tile kernel
+// measured slower -- DESIGN.md section 4.)
 //
 // Items are produced on the fly by a functor over an input index space (so
-// relabelling, orientation, predicates and fan expansion are fused into the
-// passes instead of materialising row/key arrays), grouped by a 32-bit row
+// relabelling and orientation are fused into the passes instead of
+// materialising row/key arrays), grouped by a 32-bit row
 // and ordered by a 64-bit key inside the row:
 //
 //   K1 count    one pass over the inputs: row histogram (L2-resident atomics)
