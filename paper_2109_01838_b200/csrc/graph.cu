@@ -1,13 +1,14 @@
 // Graph core kernels: canonicalisation (a3), connected components (a17),
 // contraction (a18), composition (a19) and the clustering objective (a21).
 //
-// Contraction = relabel + bucket sort by the contracted row u' with key
-// (v' << 32 | edge index) + segmented reduce.  Sorting within a (u', v')
-// segment by source edge index reproduces numpy's stable lexsort, and the
-// segment sum reproduces np.add.reduceat's x0 + pairwise(x[1:]) order, so
-// contracted costs are bit-identical to the reference (contraction.py:155-162).
-// Merged (f(u) == f(v)) edges get row -1 and are dropped by the bucket sort,
-// which avoids a separate compaction pass.
+// Contraction = one fused sort-reduce (sortreduce.cuh): the relabel by f
+// happens inside its count and scatter passes, items are grouped by the
+// contracted row u' with key (v' << 32 | edge index), and each unique
+// (u', v') group is written at its final position with its segment sum.
+// Sorting within a group by source edge index reproduces numpy's stable
+// lexsort, and the sum reproduces np.add.reduceat's x0 + pairwise(x[1:])
+// order, so contracted costs are bit-identical to the reference
+// (contraction.py:155-162).  Merged (f(u) == f(v)) edges produce no item.
 #include "internal.h"
 #include "sortreduce.cuh"
 
