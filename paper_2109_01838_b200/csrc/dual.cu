@@ -1436,24 +1436,81 @@ __global__ void k_slot_items(const int32_t* __restrict__ te, int64_t S, uint64_t
   GRID_STRIDE(s, S) key[s] = (uint64_t)s;
 }
 
-__global__ void k_coverage(const int32_t* __restrict__ ptr, int64_t m, int32_t* __restrict__ cov) {
-  GRID_STRIDE(e, m) cov[e] = ptr[e + 1] - ptr[e];
+// edge -> slot lists without a general sort: count the slots per edge (the
+// run-aggregated atomics also hand every slot its offset in the row), scan,
+// scatter the slot ids, then order each row -- rows hold 1-3 slots on grids,
+// so an insertion sort per row in registers replaces the bucket sort's
+// 16-byte items, key arrays and ranking.  If any row exceeds kSlotFastRow the
+// bucket sort (with its hub paths) builds the lists instead.
+constexpr int32_t kSlotFastRow = 32;
+
+__global__ void k_slot_count(const int32_t* __restrict__ te, int64_t S, int32_t* __restrict__ cov,
+                             int32_t* __restrict__ off, int32_t* __restrict__ long_flag) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x - lane; i0 < S;
+       i0 += (int64_t)gridDim.x * blockDim.x) {  // warp-uniform trip count
+    const int64_t s = i0 + lane;
+    const int32_t e = s < S ? te[s] : -1;
+    const int32_t o = run_atomic_add(cov, e, 1);
+    if (e >= 0) {
+      off[s] = o;
+      if (o >= kSlotFastRow) *long_flag = 1;
+    }
+  }
+}
+
+__global__ void k_slot_scatter(const int32_t* __restrict__ te, int64_t S, const int32_t* __restrict__ ptr,
+                               const int32_t* __restrict__ off, int32_t* __restrict__ slots) {
+  GRID_STRIDE(s, S) slots[ptr[te[s]] + off[s]] = (int32_t)s;
+}
+
+__global__ void k_slot_rowsort(const int32_t* __restrict__ ptr, int64_t m, int32_t* __restrict__ slots) {
+  GRID_STRIDE(e, m) {
+    const int32_t b = ptr[e], len = ptr[e + 1] - b;
+    if (len < 2) continue;
+    int32_t x[kSlotFastRow];
+#pragma unroll 4
+    for (int32_t k = 0; k < len; k++) x[k] = slots[b + k];
+    for (int32_t k = 1; k < len; k++) {  // ascending slot order (np.bincount's summation order)
+      const int32_t y = x[k];
+      int32_t h = k - 1;
+      while (h >= 0 && x[h] > y) {
+        x[h + 1] = x[h];
+        h--;
+      }
+      x[h + 1] = y;
+    }
+    for (int32_t k = 0; k < len; k++) slots[b + k] = x[k];
+  }
 }
 
 void build_slot_lists(Ctx& ctx, DualState& st) {
   int64_t S = 3 * st.T;
   st.coverage.alloc(st.m_aug > 0 ? st.m_aug : 1, ctx.s);
   st.slots.alloc(S > 0 ? S : 1, ctx.s);
+  st.long_e.release();
+  st.n_long.release();
+  st.coverage.zero();
+  {
+    Buf<int32_t> off(S > 0 ? S : 1, ctx), flag(1, ctx);
+    flag.zero();
+    RAMA_KERNEL(ctx, k_slot_count, S, st.tri_edges.p, S, st.coverage.p, off.p, flag.p);
+    st.slot_ptr.alloc(st.m_aug + 1, ctx.s);
+    exclusive_scan(ctx, st.coverage.p, st.slot_ptr.p, st.m_aug, false);
+    if (read_scalar(ctx, flag.p) == 0) {
+      RAMA_KERNEL(ctx, k_slot_scatter, S, st.tri_edges.p, S, st.slot_ptr.p, off.p, st.slots.p);
+      RAMA_KERNEL(ctx, k_slot_rowsort, st.m_aug, st.slot_ptr.p, st.m_aug, st.slots.p);
+      return;
+    }
+  }
+  // rows beyond kSlotFastRow (power-law hubs): the bucket sort
   Buf<uint64_t> key(S > 0 ? S : 1, ctx);
   RAMA_KERNEL(ctx, k_slot_items, S, st.tri_edges.p, S, key.p);
   BucketSorted bs;
   bucket_sort(ctx, st.m_aug, S, st.tri_edges.p, key.p, bs, false);
   st.slot_ptr = std::move(bs.row_ptr);
   RAMA_KERNEL(ctx, k_key_lo, S, bs.key.p, S, st.slots.p);
-  RAMA_KERNEL(ctx, k_coverage, st.m_aug, st.slot_ptr.p, st.m_aug, st.coverage.p);
   // hub slot lists (only when the sort saw rows > 256: grids never have them)
-  st.long_e.release();
-  st.n_long.release();
   if (bs.big_rows > 0) compact_if_dev(ctx, st.m_aug, LongCov{st.slot_ptr.p}, st.long_e, st.n_long);
 }
 
