@@ -38,6 +38,65 @@ struct LongCov {  // edge with more than kLongCov slots
 
 // ---------------------------------------------------------------- CSR
 
+// Rows of at most kSmallRow int32 values (grid-like graphs: the positive
+// CSR, the edge->slot lists) are built without a general sort: a
+// run-aggregated count hands every item its offset in its row, the values
+// are scattered into place and each row is insertion-sorted in registers.
+// A row beyond kSmallRow (power-law hubs) sends the build to the bucket sort.
+constexpr int32_t kSmallRow = 32;
+
+__global__ void k_rowsort_i32(const int32_t* __restrict__ ptr, int64_t m, int32_t* __restrict__ slots) {
+  GRID_STRIDE(e, m) {
+    const int32_t b = ptr[e], len = ptr[e + 1] - b;
+    if (len < 2) continue;
+    int32_t x[kSmallRow];
+#pragma unroll 4
+    for (int32_t k = 0; k < len; k++) x[k] = slots[b + k];
+    for (int32_t k = 1; k < len; k++) {
+      const int32_t y = x[k];
+      int32_t h = k - 1;
+      while (h >= 0 && x[h] > y) {
+        x[h + 1] = x[h];
+        h--;
+      }
+      x[h + 1] = y;
+    }
+    for (int32_t k = 0; k < len; k++) slots[b + k] = x[k];
+  }
+}
+
+// both arcs of every positive edge: counts per node with offsets
+__global__ void k_pcsr_count(const int32_t* __restrict__ P, int64_t np, const int32_t* __restrict__ u,
+                             const int32_t* __restrict__ v, int32_t* __restrict__ cnt, int32_t* __restrict__ off,
+                             int32_t* __restrict__ long_flag) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x - lane; i0 < np;
+       i0 += (int64_t)gridDim.x * blockDim.x) {  // warp-uniform trip count
+    const int64_t i = i0 + lane;
+    const int32_t e = i < np ? P[i] : -1;
+    const int32_t a = e >= 0 ? u[e] : -1, b = e >= 0 ? v[e] : -1;
+    const int32_t oa = run_atomic_add(cnt, a, 1);  // sorted by u: runs aggregate
+    const int32_t ob = run_atomic_add(cnt, b, 1);
+    if (e >= 0) {
+      off[2 * i] = oa;
+      off[2 * i + 1] = ob;
+      if (oa >= kSmallRow || ob >= kSmallRow) *long_flag = 1;
+    }
+  }
+}
+
+__global__ void k_pcsr_scatter(const int32_t* __restrict__ P, int64_t np, const int32_t* __restrict__ u,
+                               const int32_t* __restrict__ v, const int32_t* __restrict__ ptr,
+                               const int32_t* __restrict__ off, int32_t* __restrict__ adj) {
+  GRID_STRIDE(i, np) {
+    const int32_t e = P[i], a = u[e], b = v[e];
+    adj[ptr[a] + off[2 * i]] = b;
+    adj[ptr[b] + off[2 * i + 1]] = a;
+  }
+}
+
+
+
 __global__ void k_pos_arcs(const int32_t* __restrict__ P, int64_t np, const int32_t* __restrict__ u,
                            const int32_t* __restrict__ v, int32_t* __restrict__ row, uint64_t* __restrict__ key) {
   GRID_STRIDE(i, np) {
@@ -63,6 +122,21 @@ struct PosCSR {
 // (P: the np positive edges, ascending)
 static void positive_csr(Ctx& ctx, const GraphView& g, const Buf<int32_t>& P, int64_t np, PosCSR& out) {
   int64_t na = 2 * np;
+  if (np > 0) {  // short rows: count, scatter, sort each row in registers
+    Buf<int32_t> cnt(g.n, ctx), off(na, ctx), flag(1, ctx);
+    cnt.zero();
+    flag.zero();
+    RAMA_KERNEL(ctx, k_pcsr_count, np, P.p, np, g.u, g.v, cnt.p, off.p, flag.p);
+    out.ptr.alloc(g.n + 1, ctx.s);
+    exclusive_scan(ctx, cnt.p, out.ptr.p, g.n, false);
+    if (read_scalar(ctx, flag.p) == 0) {
+      out.adj.alloc(na, ctx.s);
+      RAMA_KERNEL(ctx, k_pcsr_scatter, np, P.p, np, g.u, g.v, out.ptr.p, off.p, out.adj.p);
+      RAMA_KERNEL(ctx, k_rowsort_i32, g.n, out.ptr.p, g.n, out.adj.p);
+      out.arcs = na;
+      return;
+    }
+  }
   Buf<int32_t> row(na > 0 ? na : 1, ctx);
   Buf<uint64_t> key(na > 0 ? na : 1, ctx);
   RAMA_KERNEL(ctx, k_pos_arcs, np, P.p, np, g.u, g.v, row.p, key.p);
@@ -1440,9 +1514,8 @@ __global__ void k_slot_items(const int32_t* __restrict__ te, int64_t S, uint64_t
 // run-aggregated atomics also hand every slot its offset in the row), scan,
 // scatter the slot ids, then order each row -- rows hold 1-3 slots on grids,
 // so an insertion sort per row in registers replaces the bucket sort's
-// 16-byte items, key arrays and ranking.  If any row exceeds kSlotFastRow the
+// 16-byte items, key arrays and ranking.  If any row exceeds kSmallRow the
 // bucket sort (with its hub paths) builds the lists instead.
-constexpr int32_t kSlotFastRow = 32;
 
 __global__ void k_slot_count(const int32_t* __restrict__ te, int64_t S, int32_t* __restrict__ cov,
                              int32_t* __restrict__ off, int32_t* __restrict__ long_flag) {
@@ -1454,7 +1527,7 @@ __global__ void k_slot_count(const int32_t* __restrict__ te, int64_t S, int32_t*
     const int32_t o = run_atomic_add(cov, e, 1);
     if (e >= 0) {
       off[s] = o;
-      if (o >= kSlotFastRow) *long_flag = 1;
+      if (o >= kSmallRow) *long_flag = 1;
     }
   }
 }
@@ -1462,26 +1535,6 @@ __global__ void k_slot_count(const int32_t* __restrict__ te, int64_t S, int32_t*
 __global__ void k_slot_scatter(const int32_t* __restrict__ te, int64_t S, const int32_t* __restrict__ ptr,
                                const int32_t* __restrict__ off, int32_t* __restrict__ slots) {
   GRID_STRIDE(s, S) slots[ptr[te[s]] + off[s]] = (int32_t)s;
-}
-
-__global__ void k_slot_rowsort(const int32_t* __restrict__ ptr, int64_t m, int32_t* __restrict__ slots) {
-  GRID_STRIDE(e, m) {
-    const int32_t b = ptr[e], len = ptr[e + 1] - b;
-    if (len < 2) continue;
-    int32_t x[kSlotFastRow];
-#pragma unroll 4
-    for (int32_t k = 0; k < len; k++) x[k] = slots[b + k];
-    for (int32_t k = 1; k < len; k++) {  // ascending slot order (np.bincount's summation order)
-      const int32_t y = x[k];
-      int32_t h = k - 1;
-      while (h >= 0 && x[h] > y) {
-        x[h + 1] = x[h];
-        h--;
-      }
-      x[h + 1] = y;
-    }
-    for (int32_t k = 0; k < len; k++) slots[b + k] = x[k];
-  }
 }
 
 void build_slot_lists(Ctx& ctx, DualState& st) {
@@ -1499,11 +1552,11 @@ void build_slot_lists(Ctx& ctx, DualState& st) {
     exclusive_scan(ctx, st.coverage.p, st.slot_ptr.p, st.m_aug, false);
     if (read_scalar(ctx, flag.p) == 0) {
       RAMA_KERNEL(ctx, k_slot_scatter, S, st.tri_edges.p, S, st.slot_ptr.p, off.p, st.slots.p);
-      RAMA_KERNEL(ctx, k_slot_rowsort, st.m_aug, st.slot_ptr.p, st.m_aug, st.slots.p);
+      RAMA_KERNEL(ctx, k_rowsort_i32, st.m_aug, st.slot_ptr.p, st.m_aug, st.slots.p);
       return;
     }
   }
-  // rows beyond kSlotFastRow (power-law hubs): the bucket sort
+  // rows beyond kSmallRow (power-law hubs): the bucket sort
   Buf<uint64_t> key(S > 0 ? S : 1, ctx);
   RAMA_KERNEL(ctx, k_slot_items, S, st.tri_edges.p, S, key.p);
   BucketSorted bs;
