@@ -45,13 +45,39 @@ struct LongCov {  // edge with more than kLongCov slots
 // A row beyond kSmallRow (power-law hubs) sends the build to the bucket sort.
 constexpr int32_t kSmallRow = 32;
 
-__global__ void k_rowsort_i32(const int32_t* __restrict__ ptr, int64_t m, int32_t* __restrict__ slots) {
+__device__ __forceinline__ void cswap(int32_t& a, int32_t& b) {
+  const int32_t lo = min(a, b), hi = max(a, b);
+  a = lo;
+  b = hi;
+}
+
+__global__ void k_rowsort_i32(const int32_t* __restrict__ ptr, int64_t m, int32_t* __restrict__ vals) {
   GRID_STRIDE(e, m) {
     const int32_t b = ptr[e], len = ptr[e + 1] - b;
     if (len < 2) continue;
+    if (len <= 8) {  // registers: an 8-wide sorting network, padded
+      int32_t x0 = vals[b], x1 = vals[b + 1];
+      int32_t x2 = len > 2 ? vals[b + 2] : INT32_MAX, x3 = len > 3 ? vals[b + 3] : INT32_MAX;
+      int32_t x4 = len > 4 ? vals[b + 4] : INT32_MAX, x5 = len > 5 ? vals[b + 5] : INT32_MAX;
+      int32_t x6 = len > 6 ? vals[b + 6] : INT32_MAX, x7 = len > 7 ? vals[b + 7] : INT32_MAX;
+      cswap(x0, x2); cswap(x1, x3); cswap(x4, x6); cswap(x5, x7);
+      cswap(x0, x4); cswap(x1, x5); cswap(x2, x6); cswap(x3, x7);
+      cswap(x0, x1); cswap(x2, x3); cswap(x4, x5); cswap(x6, x7);
+      cswap(x2, x4); cswap(x3, x5);
+      cswap(x1, x4); cswap(x3, x6);
+      cswap(x1, x2); cswap(x3, x4); cswap(x5, x6);
+      vals[b] = x0;
+      vals[b + 1] = x1;
+      if (len > 2) vals[b + 2] = x2;
+      if (len > 3) vals[b + 3] = x3;
+      if (len > 4) vals[b + 4] = x4;
+      if (len > 5) vals[b + 5] = x5;
+      if (len > 6) vals[b + 6] = x6;
+      if (len > 7) vals[b + 7] = x7;
+      continue;
+    }
     int32_t x[kSmallRow];
-#pragma unroll 4
-    for (int32_t k = 0; k < len; k++) x[k] = slots[b + k];
+    for (int32_t k = 0; k < len; k++) x[k] = vals[b + k];
     for (int32_t k = 1; k < len; k++) {
       const int32_t y = x[k];
       int32_t h = k - 1;
@@ -61,7 +87,7 @@ __global__ void k_rowsort_i32(const int32_t* __restrict__ ptr, int64_t m, int32_
       }
       x[h + 1] = y;
     }
-    for (int32_t k = 0; k < len; k++) slots[b + k] = x[k];
+    for (int32_t k = 0; k < len; k++) vals[b + k] = x[k];
   }
 }
 
