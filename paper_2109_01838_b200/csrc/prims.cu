@@ -616,20 +616,22 @@ __global__ void k_final_sum_seg(const double* part, int np, const int64_t* __res
 }
 
 void device_sums(Ctx& ctx, const double* x, const int64_t* start, const int64_t* len, int64_t K, double* out) {
-  if (K <= 0) return;
-  RAMA_REQUIRE(K < 65536, "too many segments");
-  Buf<double> part((size_t)K * kSumBlocks, ctx);
-  {
-    KernelScope ks(ctx.s, "k_partial_sum_seg", 0.0);
-    k_partial_sum_seg<<<dim3(kSumBlocks, (unsigned)K), kBlock, 0, ctx.s>>>(x, start, len, part.p);
+  constexpr int64_t kMaxY = 65535;  // grid y limit: segments in slices
+  for (int64_t k0 = 0; k0 < K; k0 += kMaxY) {
+    const int64_t k = std::min<int64_t>(kMaxY, K - k0);
+    Buf<double> part((size_t)k * kSumBlocks, ctx);
+    {
+      KernelScope ks(ctx.s, "k_partial_sum_seg", 0.0);
+      k_partial_sum_seg<<<dim3(kSumBlocks, (unsigned)k), kBlock, 0, ctx.s>>>(x, start + k0, len + k0, part.p);
+    }
+    RAMA_LAUNCH_CHECK();
+    {
+      KernelScope ks(ctx.s, "k_final_sum_seg", 0.0);
+      k_final_sum_seg<<<(unsigned)k, 1024, 0, ctx.s>>>(part.p, kSumBlocks, len + k0, out + k0);
+    }
+    RAMA_LAUNCH_CHECK();
+    ctx.launches += 2;
   }
-  RAMA_LAUNCH_CHECK();
-  {
-    KernelScope ks(ctx.s, "k_final_sum_seg", 0.0);
-    k_final_sum_seg<<<(unsigned)K, 1024, 0, ctx.s>>>(part.p, kSumBlocks, len, out);
-  }
-  RAMA_LAUNCH_CHECK();
-  ctx.launches += 2;
 }
 
 // ----------------------------------------------------------- row ptrs

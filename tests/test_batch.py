@@ -145,3 +145,20 @@ def test_solve_sharded_over_nccl_single_rank():
             assert objs[s, 0].item() == one.primal_cost and objs[s, 1].item() == one.lower_bound
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_union_batch_many_small_instances():
+    """A few hundred tiny instances in one union (per-instance segments of
+    every reduction and bound): each equals its single solve."""
+    import paper_2109_01838_b200 as P
+    from paper_2109_01838_b200 import instances
+
+    graphs = [P.WeightedGraph(*instances.grid_coo(5 + s % 4, 6 + s % 3, 0, seed=s)) for s in range(300)]
+    cfg = P.SolverConfig(mode="PD")
+    got = P.solve_batch(graphs, cfg)
+    for s in (0, 1, 77, 150, 299):
+        a = P.solve(graphs[s], cfg)
+        assert np.array_equal(a.labeling, got[s].labeling)
+        assert a.primal_cost == got[s].primal_cost and a.lower_bound == got[s].lower_bound
+        assert _trace_key(a) == _trace_key(got[s])
