@@ -35,6 +35,8 @@
 
 #include "common.cuh"
 
+#include <atomic>
+
 #include <cub/cub.cuh>
 
 namespace rama {
@@ -517,12 +519,17 @@ int64_t sort_reduce(Ctx& ctx, int64_t R, int64_t N_max, const Src& src, const Em
   }
   RAMA_LAUNCH_CHECK();
   ctx.launches++;
-  static bool smem_set = [] {
-    RAMA_CUDA(cudaFuncSetAttribute(k_sr_tiles<GS, kUnique, kDistinct, Emit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)kSrSmem));
-    return true;
-  }();
-  (void)smem_set;
+  {  // the dynamic shared memory opt-in is per device
+    static std::atomic<uint64_t> set_on{0};
+    int dev = 0;
+    RAMA_CUDA(cudaGetDevice(&dev));
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(set_on.load() & bit)) {
+      RAMA_CUDA(cudaFuncSetAttribute(k_sr_tiles<GS, kUnique, kDistinct, Emit>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSrSmem));
+      set_on.fetch_or(bit);
+    }
+  }
   {
     KernelScope ks(ctx.s, "k_sr_tiles");
     k_sr_tiles<GS, kUnique, kDistinct, Emit><<<(unsigned)tiles, kSrThreads, kSrSmem, ctx.s>>>(
