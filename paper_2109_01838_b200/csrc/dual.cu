@@ -588,10 +588,14 @@ __global__ void k_sep5_ordered(const uint8_t* __restrict__ flags, int64_t nq, co
 //   4-cycle  y* = argmin_(y in N(b) & L2) (px(y), y)
 //   5-cycle  z* = argmin_(z in N(b), z not in {a} u L1 u L2) (px(py), py, z)
 //            with py(z) = argmin_(y in N(z) & L2) (px(y), y).
-// Two table sizes: tier 1 (8 lanes per source, 32 sources per block) fits
-// grid-like neighbourhoods; the sources it cannot hold go to tier 2 (a warp
-// per source, 4x the L1, 16x the L2 table); what overflows tier 2 (hubs)
-// is flagged for the row-intersection kernels above.
+// Table sizes: tier 1 (8 lanes per source, 16 sources per block, |N+(a)|
+// <= 16) fits grid-like neighbourhoods; tier 1.5 takes its overflow with
+// twice the L1 and L2 tables; the rest go to tier 2 (a warp per source, 128
+// L1 entries, 16x the L2 table); what overflows tier 2 (hubs) is flagged for
+// the row-intersection kernels above.  Tiers 1 / 1.5 walk the build's
+// (x, y in N+(x)) pairs and each 5-cycle candidate batch's (z, y in N+(z))
+// pairs flattened over the group's lanes (row offsets in shared memory), so
+// short and uneven rows do not leave lanes idle.
 // A group answers its source's edges one after another, so sources with
 // very many repulsive edges (power-law hubs' neighbours) would serialize a
 // whole launch behind one group: tier 2 passes those to the per-edge kernels.
@@ -605,7 +609,10 @@ struct SrcTier {
   static constexpr int kBuild = BUILD;        // max sum of |N+(x)| over x in N+(a)
   static constexpr int kEdges = EDGES;        // max repulsive edges of the source
 };
-using SrcTier1 = SrcTier<8, 32, 6, 256, 1 << 30, false>;
+#ifndef RAMA_T1_L1
+#define RAMA_T1_L1 16
+#endif
+using SrcTier1 = SrcTier<8, RAMA_T1_L1, 6, 256, 1 << 30, false>;
 using SrcTier15 = SrcTier<8, 32, 7, 512, 64, false>;  // tier 1's overflow, twice the L2 table
 using SrcTier2 = SrcTier<32, 128, 10, 1024, 64, true>;
 constexpr int kSrcThreads1 = 128, kSrcThreads2 = 128;
@@ -714,11 +721,20 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sep_src(
   __shared__ int32_t s_hk[kPer][kH];
   __shared__ int32_t s_hv[kPer][kH];
   __shared__ int32_t s_fill[kPer];
+  // flattened walks: row starts and cumulative row lengths of the build's
+  // N+(x) rows (tiers 1 / 1.5), reused for one batch of 5-cycle candidates z
+  constexpr int kFlat = T::kAbort ? kGrp : T::kL1;  // tier 2 builds row by row (it stops early)
+  __shared__ int32_t s_rs[kPer][kFlat];
+  __shared__ int32_t s_cum[kPer][kFlat + 1];
+  __shared__ int32_t s_zz[kPer][kGrp];
   const int gi = threadIdx.x / kGrp, lane = threadIdx.x % kGrp;
   const unsigned mask = kGrp == 32 ? 0xffffffffu : ((1u << kGrp) - 1u) << ((threadIdx.x & 31) & ~(kGrp - 1));
   int32_t* l1 = s_l1[gi];
   int32_t* hk = s_hk[gi];
   int32_t* hv = s_hv[gi];
+  int32_t* rs = s_rs[gi];
+  int32_t* cum = s_cum[gi];
+  int32_t* zz = s_zz[gi];
   const int64_t ngroups = (int64_t)gridDim.x * kPer;
   for (int64_t j = (int64_t)blockIdx.x * kPer + gi; j < nlist; j += ngroups) {
     const int64_t k = kListed ? glist[j] : j;
@@ -729,25 +745,52 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sep_src(
     Bloom128 f1, f2;  // L1 and L2 members
     __syncwarp(mask);  // the previous source's lookups are done before the table is reset
     if (!over) {
-      for (int32_t t = lane; t < la; t += kGrp) {
-        const int32_t x = adj[pa + t];
-        l1[t] = x;
-        f1.add(x);
+      // lane owns kL1 / kGrp consecutive positions of N+(a): x, row start,
+      // row length (cum, turned into exclusive offsets below)
+      constexpr int kOwn = T::kL1 / kGrp;
+      int32_t own = 0;
+#pragma unroll
+      for (int r = 0; r < kOwn; r++) {
+        const int32_t xi = lane * kOwn + r;
+        if (xi < la) {
+          const int32_t x = adj[pa + xi];
+          l1[xi] = x;
+          f1.add(x);
+          const int32_t px = ptr[x], lx = ptr[x + 1] - px;
+          if constexpr (!T::kAbort) {
+            rs[xi] = px;
+            cum[xi] = lx;
+          }
+          own += lx;
+        }
       }
       f1.group_or<kGrp>(mask);
+      int32_t incl = own;
+#pragma unroll
+      for (int o = 1; o < kGrp; o <<= 1) {
+        const int32_t t = __shfl_up_sync(mask, incl, o, kGrp);
+        if (lane >= o) incl += t;
+      }
+      const int32_t work = __shfl_sync(mask, incl, kGrp - 1, kGrp);
+      if constexpr (!T::kAbort) {
+        int32_t run = incl - own;
+#pragma unroll
+        for (int r = 0; r < kOwn; r++) {
+          const int32_t xi = lane * kOwn + r;
+          if (xi < la) {
+            const int32_t lx = cum[xi];
+            cum[xi] = run;
+            run += lx;
+          }
+        }
+        if (lane == 0) cum[la] = work;
+      }
       for (int32_t t = lane; t < kH; t += kGrp) {
         hk[t] = -1;
         hv[t] = 0x7fffffff;
       }
       if (T::kAbort && lane == 0) s_fill[gi] = 0;
       __syncwarp(mask);
-      // each lane walks whole rows N+(x) for its x positions (independent load chains)
-      int32_t work = 0;
-      for (int32_t xi = lane; xi < la; xi += kGrp) {
-        const int32_t x = l1[xi];
-        work += ptr[x + 1] - ptr[x];
-      }
-      work = grp_sum_i32<kGrp>(work, mask);
       over = work > T::kBuild;
       if (!over) {
         if (T::kAbort) {
@@ -780,26 +823,26 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sep_src(
           __syncwarp(mask);
           over = *fill > kH / 2;
         } else {
+          // the (x, y in N+(x)) pairs flattened over the group's lanes:
+          // pair w lies in row xi with cum[xi] <= w < cum[xi + 1]
           int32_t mine = 0;
-          for (int32_t xi = lane; xi < la; xi += kGrp) {
-            const int32_t x = l1[xi];
-            const int32_t px = ptr[x], lx = ptr[x + 1] - px;
-            for (int32_t t = 0; t < lx; t++) {
-              const int32_t y = adj[px + t];
-              if (y == a || (f1.maybe(y) && src_in_l1(l1, la, y))) continue;
-              int32_t h = src_slot<T::kHashBits>(y);
-              for (int r = 0; r < kH; r++) {
-                int32_t kk = atomicCAS(hk + h, -1, y);
-                if (kk == -1 || kk == y) {
-                  if (kk == -1) {  // a lane that finds y present: its inserter added it
-                    mine++;
-                    f2.add(y);
-                  }
-                  atomicMin(hv + h, xi);  // BFS parent = smallest position reaching y
-                  break;
+          int32_t xi = 0;
+          for (int32_t w = lane; w < work; w += kGrp) {
+            while (cum[xi + 1] <= w) xi++;
+            const int32_t y = adj[rs[xi] + (w - cum[xi])];
+            if (y == a || (f1.maybe(y) && src_in_l1(l1, la, y))) continue;
+            int32_t h = src_slot<T::kHashBits>(y);
+            for (int r = 0; r < kH; r++) {
+              int32_t kk = atomicCAS(hk + h, -1, y);
+              if (kk == -1 || kk == y) {
+                if (kk == -1) {  // a lane that finds y present: its inserter added it
+                  mine++;
+                  f2.add(y);
                 }
-                h = (h + 1) & (kH - 1);
+                atomicMin(hv + h, xi);  // BFS parent = smallest position reaching y
+                break;
               }
+              h = (h + 1) & (kH - 1);
             }
           }
           mine = grp_sum_i32<kGrp>(mine, mask);
@@ -839,30 +882,54 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sep_src(
       if (best != ~0ULL) {
         len = 4; r1 = l1[(int32_t)(best >> 32)]; r2 = (int32_t)(uint32_t)best;
       } else if (L >= 5) {
+        // min over the pairs (z, y in N+(z) & L2) of ((px(y), y), z), which
+        // is the per-z minimum followed by the (key, z) minimum over z; a
+        // batch of kGrp candidates z is filtered, then its pairs are walked
+        // flattened over the lanes
         uint64_t bk = ~0ULL;
         int32_t bz = 0x7fffffff;
         const int32_t lbc = min(lb, kHubCap);
         if (capped && lane == 0 && lb > kHubCap) capped[q] = 1;  // truncated: answered again exactly
-        for (int32_t t = lane; t < lbc; t += kGrp) {
-          int32_t z = adj[pb + t];
-          if (z == a || (f1.maybe(z) && src_in_l1(l1, la, z)) ||
-              (f2.maybe(z) && src_lookup<T::kHashBits>(hk, hv, z) >= 0))
-            continue;
-          const int32_t pz = ptr[z], lz = ptr[z + 1] - pz;
-          if (lz > kHubCap) {  // hub candidate skipped: flagged for the exact search
-            if (capped) capped[q] = 1;
-            continue;
-          }
-          uint64_t zb = ~0ULL;
-          for (int32_t w = 0; w < lz; w++) {
-            int32_t y = adj[pz + w];
-            int32_t p = f2.maybe(y) ? src_lookup<T::kHashBits>(hk, hv, y) : -1;
-            if (p >= 0) {
-              uint64_t key = ((uint64_t)(uint32_t)p << 32) | (uint32_t)y;
-              zb = key < zb ? key : zb;
+        for (int32_t base = 0; base < lbc; base += kGrp) {
+          const int32_t t = base + lane;
+          int32_t z = 0, pz = 0, lz = 0;
+          if (t < lbc) {
+            z = adj[pb + t];
+            if (!(z == a || (f1.maybe(z) && src_in_l1(l1, la, z)) ||
+                  (f2.maybe(z) && src_lookup<T::kHashBits>(hk, hv, z) >= 0))) {
+              pz = ptr[z];
+              lz = ptr[z + 1] - pz;
+              if (lz > kHubCap) {  // hub candidate skipped: flagged for the exact search
+                if (capped) capped[q] = 1;
+                lz = 0;
+              }
             }
           }
-          if (zb < bk || (zb == bk && z < bz)) { bk = zb; bz = z; }
+          int32_t zi = lz;
+#pragma unroll
+          for (int o = 1; o < kGrp; o <<= 1) {
+            const int32_t v = __shfl_up_sync(mask, zi, o, kGrp);
+            if (lane >= o) zi += v;
+          }
+          const int32_t tot = __shfl_sync(mask, zi, kGrp - 1, kGrp);
+          if (tot == 0) continue;
+          cum[lane] = zi - lz;
+          rs[lane] = pz;
+          zz[lane] = z;
+          if (lane == 0) cum[kGrp] = tot;
+          __syncwarp(mask);
+          int32_t c = 0;
+          for (int32_t w = lane; w < tot; w += kGrp) {
+            while (cum[c + 1] <= w) c++;
+            const int32_t y = adj[rs[c] + (w - cum[c])];
+            const int32_t p = f2.maybe(y) ? src_lookup<T::kHashBits>(hk, hv, y) : -1;
+            if (p >= 0) {
+              const uint64_t key = ((uint64_t)(uint32_t)p << 32) | (uint32_t)y;
+              const int32_t zc = zz[c];
+              if (key < bk || (key == bk && zc < bz)) { bk = key; bz = zc; }
+            }
+          }
+          __syncwarp(mask);  // the batch is read before the next one is written
         }
         uint64_t mn = grp_min_u64<kGrp>(bk, mask);
         int32_t zc = grp_min_i32<kGrp>(bk == mn ? bz : 0x7fffffff, mask);
