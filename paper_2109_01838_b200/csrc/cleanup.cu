@@ -720,9 +720,7 @@ int64_t handshake_cleanup(Ctx& ctx, const GraphView& q, int32_t* fc) {
     ctx.launches++;
     launches++;
     int32_t st[SC_COUNT];
-    RAMA_CUDA(cudaMemcpyAsync(ctx.pinned, sc.p, sizeof(st), cudaMemcpyDeviceToHost, ctx.s));
-    ctx.sync();
-    memcpy(st, ctx.pinned, sizeof(st));
+    memcpy(st, fetch(ctx, {{sc.p, (int)sizeof(st)}}), sizeof(st));
     total = st[SC_NPAIRS];
     if (round_trace) {
       const int32_t k0 = std::min(rounds, kTraceCap), k1 = std::min(st[SC_ROUNDS], kTraceCap);

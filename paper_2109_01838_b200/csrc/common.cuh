@@ -13,6 +13,7 @@
 #include <chrono>
 #include <cstdint>
 #include <cstdio>
+#include <initializer_list>
 #include <map>
 #include <stdexcept>
 #include <string>
@@ -52,10 +53,17 @@ struct Error : public std::runtime_error {
   } while (0)
 
 // Per-call context: the stream everything is ordered on plus a small pinned
+// RAMA_HOST_STATS=2: count host syncs per call chain (backtrace), printed
+// after each solve
+void note_sync();
+void dump_sync_sites();
+
 // staging area for scalar read-backs (the only host syncs in a solve).
 struct Ctx {
   cudaStream_t s = nullptr;
-  int64_t* pinned = nullptr;  // 64 int64 slots
+  int64_t* pinned = nullptr;  // 64 int64 slots (slot 63: the read-back flag)
+  int64_t* pinned_dev = nullptr;  // the same block, mapped into the device
+  uint32_t seq = 0;           // last read-back sequence number published
   cudaEvent_t ev = nullptr;   // asynchronous read-backs (recycled with `pinned`)
   int launches = 0;           // kernels launched through this context
 
@@ -63,7 +71,10 @@ struct Ctx {
   ~Ctx();
   Ctx(const Ctx&) = delete;
   Ctx& operator=(const Ctx&) = delete;
-  void sync() { RAMA_CUDA(cudaStreamSynchronize(s)); }
+  void sync() {
+    note_sync();
+    RAMA_CUDA(cudaStreamSynchronize(s));
+  }
 };
 
 void ensure_pool_configured();
@@ -286,34 +297,30 @@ bool trace_print();     // RAMA_TRACE=1 or 2: print launches and sync points
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)(n); i += (int64_t)gridDim.x * blockDim.x)
 
 // ---- scalar read-back -----------------------------------------------------
+// fetch(): up to four small device ranges (whole 4-byte words, <= 128 words
+// in all) are copied by a one-warp kernel into the pinned block at byte
+// offset `at`, which then publishes a sequence number in slot 63 (system
+// fence first); the host spins on that flag.  Measured on the B200: 8.7 us
+// per read-back round trip against 12.4 us for cudaMemcpyAsync +
+// cudaStreamSynchronize (tools/readback_probe.cu).  Returns a pointer to the
+// fetched bytes.
+struct FetchPart {
+  const void* src;
+  int bytes;
+};
+void* fetch(Ctx& ctx, std::initializer_list<FetchPart> parts, int at = 0);
+
 template <class T>
 T read_scalar(Ctx& ctx, const T* dev) {
-  static_assert(sizeof(T) <= 8, "scalar");
-  if (trace_print()) {
-    fprintf(stderr, "[rama] sync\n");
-    fflush(stderr);
-  }
-  auto t0 = std::chrono::steady_clock::now();
-  RAMA_CUDA(cudaMemcpyAsync(ctx.pinned, dev, sizeof(T), cudaMemcpyDeviceToHost, ctx.s));
-  ctx.sync();
-  HostStats& hs = host_stats();
-  hs.sync_ms += host_ms_since(t0);
-  hs.syncs++;
+  static_assert(sizeof(T) % 4 == 0 && sizeof(T) <= 8, "scalar");
   T v;
-  memcpy(&v, ctx.pinned, sizeof(T));
+  memcpy(&v, fetch(ctx, {{dev, (int)sizeof(T)}}), sizeof(T));
   return v;
 }
 
 // two int32 device scalars in one round trip
 inline void read_pair(Ctx& ctx, const int32_t* a, const int32_t* b, int64_t& x, int64_t& y) {
-  auto t0 = std::chrono::steady_clock::now();
-  int32_t* hp = (int32_t*)ctx.pinned;
-  RAMA_CUDA(cudaMemcpyAsync(hp, a, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx.s));
-  RAMA_CUDA(cudaMemcpyAsync(hp + 1, b, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx.s));
-  ctx.sync();
-  HostStats& hs = host_stats();
-  hs.sync_ms += host_ms_since(t0);
-  hs.syncs++;
+  const int32_t* hp = (const int32_t*)fetch(ctx, {{a, 4}, {b, 4}});
   x = hp[0];
   y = hp[1];
 }

@@ -18,6 +18,13 @@
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
 
+#include <cxxabi.h>
+#include <execinfo.h>
+
+#include <immintrin.h>
+
+#include <algorithm>
+#include <atomic>
 #include <mutex>
 #include <map>
 #include <string>
@@ -28,6 +35,55 @@ namespace rama {
 HostStats& host_stats() {
   static thread_local HostStats hs;
   return hs;
+}
+
+namespace {
+std::map<std::string, int64_t>& sync_sites() {
+  static thread_local std::map<std::string, int64_t> m;
+  return m;
+}
+bool sync_sites_on() {
+  static const bool on = [] {
+    const char* e = getenv("RAMA_HOST_STATS");
+    return e && atoi(e) >= 2;
+  }();
+  return on;
+}
+}  // namespace
+
+void note_sync() {
+  if (!sync_sites_on()) return;
+  void* bt[10];
+  const int k = backtrace(bt, 10);
+  char** sy = backtrace_symbols(bt, k);
+  std::string key;
+  for (int i = 1; i < k && i < 7; i++) {
+    std::string f = sy ? sy[i] : "?";
+    const size_t a = f.find('('), b = f.find('+', a == std::string::npos ? 0 : a);
+    std::string name = (a != std::string::npos && b != std::string::npos && b > a + 1) ? f.substr(a + 1, b - a - 1) : "?";
+    int st = 0;
+    char* dm = abi::__cxa_demangle(name.c_str(), nullptr, nullptr, &st);
+    if (st == 0 && dm) {
+      name = dm;
+      const size_t p = name.find('(');
+      if (p != std::string::npos) name = name.substr(0, p);
+    }
+    free(dm);
+    if (!key.empty()) key += " < ";
+    key += name;
+    if (name.find("solve") != std::string::npos) break;
+  }
+  free(sy);
+  sync_sites()[key]++;
+}
+
+void dump_sync_sites() {
+  if (!sync_sites_on()) return;
+  std::vector<std::pair<int64_t, std::string>> v;
+  for (auto& kv : sync_sites()) v.push_back({kv.second, kv.first});
+  std::sort(v.rbegin(), v.rend());
+  for (auto& x : v) fprintf(stderr, "[rama] syncs %4lld  %s\n", (long long)x.first, x.second.c_str());
+  sync_sites().clear();
 }
 
 // Pinned staging blocks are recycled across calls: cudaMallocHost /
@@ -48,9 +104,67 @@ Ctx::Ctx(cudaStream_t st) : s(st) {
     }
   }
   if (!pinned) {
-    RAMA_CUDA(cudaMallocHost((void**)&pinned, 64 * sizeof(int64_t)));
+    RAMA_CUDA(cudaHostAlloc((void**)&pinned, 64 * sizeof(int64_t), cudaHostAllocMapped | cudaHostAllocPortable));
+    memset(pinned, 0, 64 * sizeof(int64_t));
     RAMA_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }
+  RAMA_CUDA(cudaHostGetDevicePointer((void**)&pinned_dev, pinned, 0));
+  seq = *(volatile uint32_t*)(pinned + 63);  // a recycled block continues its sequence
+}
+
+namespace {
+struct FetchArgs {
+  const uint32_t* src[4];
+  int words[4];
+  int n;
+};
+__global__ void k_fetch(FetchArgs a, uint32_t* dst, volatile uint32_t* flag, uint32_t s) {
+  int o = 0;
+  for (int k = 0; k < a.n; k++) {
+    for (int i = threadIdx.x; i < a.words[k]; i += blockDim.x) dst[o + i] = __ldcg(a.src[k] + i);
+    o += a.words[k];
+  }
+  __threadfence_system();
+  __syncwarp();
+  if (threadIdx.x == 0) *flag = s;
+}
+}  // namespace
+
+void* fetch(Ctx& ctx, std::initializer_list<FetchPart> parts, int at) {
+  if (trace_print()) {
+    fprintf(stderr, "[rama] sync\n");
+    fflush(stderr);
+  }
+  note_sync();
+  auto t0 = std::chrono::steady_clock::now();
+  FetchArgs a{};
+  int words = 0;
+  for (const FetchPart& p : parts) {
+    RAMA_REQUIRE(a.n < 4 && p.bytes % 4 == 0, "fetch: at most four word-sized parts");
+    a.src[a.n] = (const uint32_t*)p.src;
+    a.words[a.n] = p.bytes / 4;
+    words += a.words[a.n];
+    a.n++;
+  }
+  RAMA_REQUIRE(at % 4 == 0 && at + 4 * words <= 63 * 8, "fetch: range exceeds the pinned block");
+  const uint32_t s = ++ctx.seq;
+  volatile uint32_t* flag = (volatile uint32_t*)(ctx.pinned + 63);
+  k_fetch<<<1, 32, 0, ctx.s>>>(a, (uint32_t*)((char*)ctx.pinned_dev + at), (volatile uint32_t*)(ctx.pinned_dev + 63),
+                               s);
+  RAMA_LAUNCH_CHECK();
+  for (uint32_t spins = 1; *flag != s; spins++) {
+    _mm_pause();
+    if ((spins & 1023) == 0) {  // a failed kernel never publishes: surface its error
+      const cudaError_t e = cudaStreamQuery(ctx.s);
+      if (e != cudaSuccess && e != cudaErrorNotReady) RAMA_CUDA(e);
+      if (e == cudaSuccess && *flag != s) RAMA_REQUIRE(false, "read-back flag not published");
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  HostStats& hs = host_stats();
+  hs.sync_ms += host_ms_since(t0);
+  hs.syncs++;
+  return (char*)ctx.pinned + at;
 }
 
 Ctx::~Ctx() {
@@ -946,10 +1060,7 @@ void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint6
     ctx.launches++;
   }
   // one read-back: the kept count and the number of hub rows
-  int32_t* hp = (int32_t*)ctx.pinned;
-  RAMA_CUDA(cudaMemcpyAsync(hp, out.row_ptr.p + R, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx.s));
-  RAMA_CUDA(cudaMemcpyAsync(hp + 1, counters, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx.s));
-  ctx.sync();
+  const int32_t* hp = (const int32_t*)fetch(ctx, {{out.row_ptr.p + R, 4}, {counters, 8}});
   const int64_t total = hp[0];
   const int32_t nbig = hp[1], nb = hp[2];
   out.total = total;

@@ -49,6 +49,7 @@ void solve(Ctx& ctx, const GraphView& g, const SolveConfig& cfg, int32_t* labels
     clk::time_point t0;
     ~Report() {
       if (!getenv("RAMA_HOST_STATS")) return;
+      dump_sync_sites();
       HostStats& hs = host_stats();
       int dev = 0;
       cudaGetDevice(&dev);
@@ -120,7 +121,6 @@ void solve(Ctx& ctx, const GraphView& g, const SolveConfig& cfg, int32_t* labels
   Graph cur = copy_graph(ctx, g);
   double lb = nan;
   Buf<double> d_lb(1, ctx);
-  double* h_lb = (double*)(ctx.pinned + 40);  // the round's LB lands here before the round-end sync
   for (int rnd = 1; rnd <= cfg.max_rounds; rnd++) {
     auto t0 = clk::now();
     int64_t nodes_before = cur.n, edges_before = cur.m, T = 0;
@@ -146,7 +146,6 @@ void solve(Ctx& ctx, const GraphView& g, const SolveConfig& cfg, int32_t* labels
       message_passing(ctx, st, cfg.mp_iterations);
       Buf<double> cl(st.m_aug > 0 ? st.m_aug : 1, ctx);
       lower_bound_to(ctx, st, cl.p, d_lb.p);  // c^lambda computed once for the bound and the graph
-      RAMA_CUDA(cudaMemcpyAsync(h_lb, d_lb.p, sizeof(double), cudaMemcpyDeviceToHost, ctx.s));
       T = st.T;
       mark(2);
       Graph rep = reparametrized_graph(ctx, st, cl.p);
@@ -160,10 +159,12 @@ void solve(Ctx& ctx, const GraphView& g, const SolveConfig& cfg, int32_t* labels
     } else {
       contraction_step(ctx, cur.view(), 3, cfg.switch_fraction, step);
     }
-    ctx.sync();
+    // round end: the LB comes back (the wait also closes the round's timing)
     if (dual) {
-      lb_r = *h_lb;
+      lb_r = read_scalar(ctx, d_lb.p);
       if (rnd == 1) lb = lb_r;
+    } else {
+      ctx.sync();
     }
     push(trace, max_trace, nr,
          RoundInfo{rnd, dual ? 1 : 0, nodes_before, edges_before, T, lb_r, (dual && rnd == 1) ? 1 : 0,
