@@ -1547,7 +1547,19 @@ __device__ __forceinline__ int32_t find_in_row(const int32_t* __restrict__ rptr,
   return -1;
 }
 
-// unique chords that are not already edges of g
+// unique chords that are not already edges of g, as one selection predicate
+// over the sorted chord list (run head, and no edge (row, key) in g)
+struct NewChordHead {
+  const int32_t* row;
+  const uint64_t* key;
+  const int32_t* rptr;
+  const int32_t* gv;
+  __device__ __forceinline__ bool operator()(int32_t p) const {
+    if (!(p == 0 || row[p] != row[p - 1] || key[p] != key[p - 1])) return false;
+    return find_in_row(rptr, gv, row[p], (int32_t)key[p]) < 0;
+  }
+};
+
 __global__ void k_chord_new(const int32_t* __restrict__ heads, int64_t nh, const int32_t* __restrict__ row,
                             const uint64_t* __restrict__ key, const int32_t* __restrict__ rptr,
                             const int32_t* __restrict__ gv, uint8_t* __restrict__ is_new) {
@@ -1562,7 +1574,7 @@ __global__ void k_chord_out(const int32_t* __restrict__ sel, int64_t C, const in
                             int32_t* __restrict__ eu, int32_t* __restrict__ ev, double* __restrict__ base,
                             uint64_t* __restrict__ ckeys) {
   GRID_STRIDE(i, C) {
-    int32_t p = heads[sel[i]];
+    int32_t p = heads[sel ? sel[i] : (int32_t)i];
     int32_t a = row[p], b = (int32_t)key[p];
     eu[m + i] = a;
     ev[m + i] = b;
@@ -1596,6 +1608,25 @@ __global__ void k_tri_handles(const int32_t* __restrict__ tn, int64_t T, const i
     te[3 * t] = edge_handle(rptr, gv, crptr, cv, m, i, j);
     te[3 * t + 1] = edge_handle(rptr, gv, crptr, cv, m, i, k);
     te[3 * t + 2] = edge_handle(rptr, gv, crptr, cv, m, j, k);
+  }
+}
+
+// k_tri_out + k_tri_handles in one pass over the kept triplets
+__global__ void k_tri_out_handles(const int32_t* __restrict__ heads, int64_t T, const int32_t* __restrict__ row,
+                                  const uint64_t* __restrict__ key, const int32_t* __restrict__ rptr,
+                                  const int32_t* __restrict__ gv, const int32_t* __restrict__ crptr,
+                                  const int32_t* __restrict__ cv, int64_t m, int32_t* __restrict__ tn,
+                                  int32_t* __restrict__ te) {
+  GRID_STRIDE(t, T) {
+    const int32_t p = heads[t];
+    const uint64_t k = key[p];
+    const int32_t i = row[p], j = (int32_t)(k >> 32), l = (int32_t)(uint32_t)k;
+    tn[3 * t] = i;
+    tn[3 * t + 1] = j;
+    tn[3 * t + 2] = l;
+    te[3 * t] = edge_handle(rptr, gv, crptr, cv, m, i, j);
+    te[3 * t + 1] = edge_handle(rptr, gv, crptr, cv, m, i, l);
+    te[3 * t + 2] = edge_handle(rptr, gv, crptr, cv, m, j, l);
   }
 }
 
@@ -1692,14 +1723,11 @@ void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& 
   if (craw > 0) {
     BucketSorted cs;
     bucket_sort(ctx, n, craw, crow.p, ckey.p, cs, true);
-    Buf<int32_t> hp;
-    int64_t nh = compact_if(ctx, cs.total, SortedHead{cs.row.p, cs.key.p}, hp);  // kept chords only
-    Buf<uint8_t> isnew(nh > 0 ? nh : 1, ctx);
-    RAMA_KERNEL(ctx, k_chord_new, nh, hp.p, nh, cs.row.p, cs.key.p, rptr_p, g.v, isnew.p);
-    Buf<int32_t> sel;
-    C = compact_indices(ctx, isnew.p, nh, sel);
+    Buf<int32_t> hp;  // first of each run of equal chords, not an edge of g: one selection, one read-back
+    C = compact_if(ctx, cs.total, NewChordHead{cs.row.p, cs.key.p, rptr_p, g.v}, hp);
     ckeys.alloc(C > 0 ? C : 1, ctx.s);
-    RAMA_KERNEL(ctx, k_chord_out, C, sel.p, C, hp.p, cs.row.p, cs.key.p, m, st.eu.p, st.ev.p, st.base.p, ckeys.p);
+    RAMA_KERNEL(ctx, k_chord_out, C, (const int32_t*)nullptr, C, hp.p, cs.row.p, cs.key.p, m, st.eu.p, st.ev.p,
+                st.base.p, ckeys.p);
   }
   st.m_aug = m + C;
   st.chords_sorted = true;
@@ -1715,9 +1743,8 @@ void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& 
     T = compact_if(ctx, ts.total, SortedHead{ts.row.p, ts.key.p}, hp);  // kept triplets only
     st.tri_nodes.alloc(3 * T, ctx.s);
     st.tri_edges.alloc(3 * T, ctx.s);
-    RAMA_KERNEL(ctx, k_tri_out, T, hp.p, T, ts.row.p, ts.key.p, st.tri_nodes.p);
-    RAMA_KERNEL(ctx, k_tri_handles, T, st.tri_nodes.p, T, rptr_p, g.v, st.chord_ptr.p, st.ev.p + m, m,
-                st.tri_edges.p);
+    RAMA_KERNEL(ctx, k_tri_out_handles, T, hp.p, T, ts.row.p, ts.key.p, rptr_p, g.v, st.chord_ptr.p, st.ev.p + m, m,
+                st.tri_nodes.p, st.tri_edges.p);
   } else {
     st.tri_nodes.alloc(1, ctx.s);
     st.tri_edges.alloc(1, ctx.s);

@@ -507,6 +507,109 @@ __global__ void k_mark_removed(const int32_t* __restrict__ qe, const uint8_t* __
   }
 }
 
+// ---- small trees: the reference's sequential loop, one thread per tree ----
+// When every tree of the forest has at most kSmallTree nodes (grid-like
+// graphs' late forest rounds), the conflict loop of _remove_conflict_edges
+// (contraction.py:231-284) runs as written, per tree: a repulsive edge only
+// meets removals inside its own tree, so each tree's queries in ascending
+// (u, v) order are independent of every other tree's.  A thread holds its
+// tree (<= 32 nodes, <= 31 edges) in registers / local memory, finds the
+// unique path of each query by relaxation sweeps over the not-yet-removed
+// edges and cuts the path's cheapest edge (ties: smallest (u, v)).  This
+// replaces the Euler tour, the lifting tables and the dependency passes of
+// the general path (~40 launches and ~6 read-backs per forest round).
+constexpr int kSmallTree = 32;
+
+// combined items per tree: its forest edges (key i) then its queries (key 2^32 + q)
+__global__ void k_tree_items(const int32_t* __restrict__ Fi, int64_t kf, const int32_t* __restrict__ Q, int64_t nq,
+                             const int32_t* __restrict__ P, const int32_t* __restrict__ u,
+                             const int32_t* __restrict__ loc, const int32_t* __restrict__ comp_loc,
+                             int32_t* __restrict__ row, uint64_t* __restrict__ key) {
+  GRID_STRIDE(i, kf + nq) {
+    if (i < kf) {
+      row[i] = comp_loc[loc[u[P[Fi[i]]]]];
+      key[i] = (uint64_t)i;
+    } else {
+      const int64_t q = i - kf;
+      row[i] = comp_loc[loc[u[Q[q]]]];
+      key[i] = (1ull << 32) | (uint64_t)q;
+    }
+  }
+}
+
+__device__ __forceinline__ int tree_slot(int32_t* node, int& nn, int32_t x, bool add) {
+  for (int i = 0; i < nn; i++)
+    if (node[i] == x) return i;
+  if (!add) return -1;
+  node[nn] = x;
+  return nn++;
+}
+
+__global__ void k_tree_resolve(const int32_t* __restrict__ rptr, const uint64_t* __restrict__ key, int64_t R,
+                               const int32_t* __restrict__ Fi, const int32_t* __restrict__ P,
+                               const int32_t* __restrict__ Q, const int32_t* __restrict__ u,
+                               const int32_t* __restrict__ v, const double* __restrict__ c,
+                               uint8_t* __restrict__ removed) {
+  GRID_STRIDE(r, R) {
+    const int32_t b = rptr[r], e = rptr[r + 1];
+    if (e - b < 2 || (key[e - 1] >> 32) == 0) continue;  // no edge or no query
+    int32_t node[kSmallTree];
+    int8_t ea[kSmallTree], eb[kSmallTree];
+    int32_t fid[kSmallTree];
+    int nn = 0, ne = 0;
+    int32_t p = b;
+    for (; p < e && (key[p] >> 32) == 0; p++) {
+      const int32_t i = (int32_t)(uint32_t)key[p];
+      const int32_t ed = P[Fi[i]];
+      ea[ne] = (int8_t)tree_slot(node, nn, u[ed], true);
+      eb[ne] = (int8_t)tree_slot(node, nn, v[ed], true);
+      fid[ne] = i;
+      ne++;
+    }
+    uint32_t rem = 0;  // removed tree edges
+    for (; p < e; p++) {
+      const int32_t ed = Q[(int32_t)(uint32_t)key[p]];
+      const int sa = tree_slot(node, nn, u[ed], false), sb = tree_slot(node, nn, v[ed], false);
+      if (sa < 0 || sb < 0) continue;
+      uint32_t vis = 1u << sa;
+      int8_t pe[kSmallTree];  // tree edge that reached each node
+      bool grew = true;
+      while (!((vis >> sb) & 1u) && grew) {
+        grew = false;
+        for (int k = 0; k < ne; k++) {
+          if ((rem >> k) & 1u) continue;
+          const bool ia = (vis >> ea[k]) & 1u, ib = (vis >> eb[k]) & 1u;
+          if (ia != ib) {
+            const int y = ia ? eb[k] : ea[k];
+            vis |= 1u << y;
+            pe[y] = (int8_t)k;
+            grew = true;
+          }
+        }
+      }
+      if (!((vis >> sb) & 1u)) continue;  // already separated
+      int best = -1;
+      double bc = 0.0;
+      int32_t bu = 0, bv = 0;
+      for (int x = sb; x != sa;) {
+        const int k = pe[x];
+        const int32_t fe = P[Fi[fid[k]]];
+        const double ck = c[fe];
+        const int32_t uk = u[fe], vk = v[fe];
+        if (best < 0 || ck < bc || (ck == bc && (uk < bu || (uk == bu && vk < bv)))) {
+          best = k;
+          bc = ck;
+          bu = uk;
+          bv = vk;
+        }
+        x = ea[k] == x ? eb[k] : ea[k];
+      }
+      rem |= 1u << best;
+      removed[fid[best]] = 1;
+    }
+  }
+}
+
 __global__ void k_forest_keep(const int32_t* __restrict__ Fi, int64_t kf, const uint8_t* __restrict__ removed,
                               uint8_t* __restrict__ keep_pos) {
   GRID_STRIDE(i, kf) keep_pos[Fi[i]] = !removed[i];
@@ -599,6 +702,21 @@ int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_
       RAMA_KERNEL(ctx, k_tree_sizes, nf, comp_loc.p, nf, sz.p, sz.p + nf);
       maxsz = (int64_t)read_scalar(ctx, sz.p + nf);
     }
+    static const bool tour_only = getenv("RAMA_FOREST_TOUR") != nullptr;  // A/B: always the general path
+    if (maxsz <= kSmallTree && !tour_only) {
+      const int64_t ni = kf + nq;
+      Buf<int32_t> irow(ni, ctx);
+      Buf<uint64_t> ikey(ni, ctx);
+      RAMA_KERNEL(ctx, k_tree_items, ni, Fi.p, kf, Q.p, nq, P.p, g.u, loc.p, comp_loc.p, irow.p, ikey.p);
+      BucketSorted ts;
+      bucket_sort(ctx, nf, ni, irow.p, ikey.p, ts, false);
+      RAMA_KERNEL(ctx, k_tree_resolve, nf, ts.row_ptr.p, ts.key.p, nf, Fi.p, P.p, Q.p, g.u, g.v, g.c, removed.p);
+      mark(4);
+      if (phase_prof)
+        fprintf(stderr, "[rama]   forest n %lld m+ %lld kf %lld conflicts %lld trees <= %lld nodes: rank sort %.2f "
+                "boruvka %.2f (%d) per-tree resolve %.2f ms\n", (long long)n, (long long)np, (long long)kf,
+                (long long)nq, (long long)maxsz, ph[0], ph[1], bv_iters, ph[4]);
+    } else {
     const int64_t maxdepth = maxsz - 1;
     Buf<int32_t> fu(kf, ctx), fv(kf, ctx), fval(kf, ctx), fsorted(kf, ctx), fkey(kf, ctx);
     Buf<uint64_t> fbits(kf, ctx), fbits2(kf, ctx);
@@ -686,6 +804,7 @@ int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_
       fprintf(stderr, "[rama]   forest n %lld m+ %lld kf %lld conflicts %lld LOG %d: rank sort %.2f boruvka %.2f (%d) "
               "euler %.2f lift+paths %.2f resolve %.2f (%d) ms\n", (long long)n, (long long)np, (long long)kf,
               (long long)nq, LOG, ph[0], ph[1], bv_iters, ph[2], ph[3], ph[4], rs_iters);
+    }
   }
   RAMA_KERNEL(ctx, k_forest_keep, kf, Fi.p, kf, removed.p, keep.p);
   Buf<int32_t> idx;

@@ -220,6 +220,19 @@ def test_forest_conflict_resolution_exact():
     assert np.array_equal(P.select_spanning_forest_no_conflicts(g), O.select_spanning_forest_no_conflicts(og))
 
 
+def test_forest_small_trees_exact():
+    # forests whose trees have <= 32 nodes take the per-tree sequential
+    # conflict loop (select.cu k_tree_resolve); 33-50 node trees the general
+    # Euler-tour path -- both must match the reference's loop exactly
+    cases = [(instances.grid_coo(120, 150, 2, seed=3), 1.0), (instances.grid_coo(120, 150, 2, seed=3), 1.2),
+             (instances.grid_coo(120, 150, 2, seed=3), 0.8)]  # max tree 29 / 16 / 50 nodes
+    cases += [(instances.grid8_coo(100, 120, strides=(2,), seed=s), sh)
+              for s, sh in ((0, 1.4), (1, 1.3), (2, 1.3), (3, 1.4), (0, 1.3))]  # 25, 26, 32, 30, 38 nodes
+    for (n, u, v, c), shift in cases:
+        g, og = _both(n, u, v, c - shift)
+        assert np.array_equal(P.select_spanning_forest_no_conflicts(g), O.select_spanning_forest_no_conflicts(og))
+
+
 def test_clustering_cost_matches_oracle():
     n, u, v, c = instances.grid_coo(300, 300, 0, seed=2)
     g, og = _both(n, u, v, c)
