@@ -1507,7 +1507,7 @@ __global__ void k_fan_counts(const int32_t* __restrict__ len, int64_t rows, int3
 __global__ void k_fan_emit(const int32_t* __restrict__ len, const int32_t* __restrict__ nodes, int64_t rows, int L,
                            const int32_t* __restrict__ toff, const int32_t* __restrict__ coff,
                            int32_t* __restrict__ trow, uint64_t* __restrict__ tkey, int32_t* __restrict__ crow,
-                           uint64_t* __restrict__ ckey) {
+                           uint64_t* __restrict__ ckey, uint64_t ctag) {
   GRID_STRIDE(r, rows) {
     int32_t l = len[r];
     if (l < 3) continue;
@@ -1528,7 +1528,7 @@ __global__ void k_fan_emit(const int32_t* __restrict__ len, const int32_t* __res
       int32_t a = v0 < row[j] ? v0 : row[j];
       int32_t b = v0 < row[j] ? row[j] : v0;
       crow[h] = a;
-      ckey[h] = (uint64_t)(uint32_t)b;
+      ckey[h] = ctag | (uint64_t)(uint32_t)b;
       h++;
     }
   }
@@ -1557,6 +1557,30 @@ struct NewChordHead {
   __device__ __forceinline__ bool operator()(int32_t p) const {
     if (!(p == 0 || row[p] != row[p - 1] || key[p] != key[p - 1])) return false;
     return find_in_row(rptr, gv, row[p], (int32_t)key[p]) < 0;
+  }
+};
+
+// triangulate's combined sort: chords carry kChordTag in the key (after the
+// row's triplets), triplets (b << 32 | c) with b < 2^31
+constexpr uint64_t kChordTag = 1ull << 63;
+struct NewChordHeadTagged {
+  const int32_t* row;
+  const uint64_t* key;
+  const int32_t* rptr;
+  const int32_t* gv;
+  __device__ __forceinline__ bool operator()(int32_t p) const {
+    const uint64_t k = key[p];
+    if (!(k & kChordTag)) return false;
+    if (!(p == 0 || row[p] != row[p - 1] || k != key[p - 1])) return false;
+    return find_in_row(rptr, gv, row[p], (int32_t)(uint32_t)k) < 0;
+  }
+};
+struct TripletHead {
+  const int32_t* row;
+  const uint64_t* key;
+  __device__ __forceinline__ bool operator()(int32_t p) const {
+    const uint64_t k = key[p];
+    return !(k & kChordTag) && (p == 0 || row[p] != row[p - 1] || k != key[p - 1]);
   }
 };
 
@@ -1703,16 +1727,20 @@ void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& 
   exclusive_scan(ctx, nc.p, coff.p, rows, false);
   int64_t traw = 0, craw = 0;
   read_pair(ctx, toff.p + rows, coff.p + rows, traw, craw);
-  Buf<int32_t> trow(traw > 0 ? traw : 1, ctx), crow(craw > 0 ? craw : 1, ctx);
-  Buf<uint64_t> tkey(traw > 0 ? traw : 1, ctx), ckey(craw > 0 ? craw : 1, ctx);
-  RAMA_KERNEL(ctx, k_fan_emit, rows, cyc.len.p, cyc.nodes.p, rows, cyc.L, toff.p, coff.p, trow.p, tkey.p, crow.p,
-              ckey.p);
+  // triplets and chords in one list, sorted once (chords tagged after each
+  // row's triplets); one partition then keeps the first triplet of each run
+  // and the first chord of each run that is not an edge of g, both in
+  // sorted order, with one read-back for both counts
+  const int64_t N = traw + craw;
+  Buf<int32_t> irow(N > 0 ? N : 1, ctx);
+  Buf<uint64_t> ikey(N > 0 ? N : 1, ctx);
+  RAMA_KERNEL(ctx, k_fan_emit, rows, cyc.len.p, cyc.nodes.p, rows, cyc.L, toff.p, coff.p, irow.p, ikey.p,
+              irow.p + traw, ikey.p + traw, kChordTag);
 
-  // chords: dedupe, drop existing edges
   st.orig_ptr.alloc(n + 1, ctx.s);
   int32_t* rptr_p = st.orig_ptr.p;
   row_ptr_from_sorted(ctx, g.u, m, n, rptr_p);
-  int64_t C = 0;
+  int64_t C = 0, T = 0;
   Buf<uint64_t> ckeys(1, ctx);
   st.eu.alloc(m + craw > 0 ? m + craw : 1, ctx.s);
   st.ev.alloc(m + craw > 0 ? m + craw : 1, ctx.s);
@@ -1720,13 +1748,18 @@ void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& 
   copy_d2d(ctx, st.eu.p, g.u, m);
   copy_d2d(ctx, st.ev.p, g.v, m);
   copy_d2d(ctx, st.base.p, g.c, m);
-  if (craw > 0) {
-    BucketSorted cs;
-    bucket_sort(ctx, n, craw, crow.p, ckey.p, cs, true);
-    Buf<int32_t> hp;  // first of each run of equal chords, not an edge of g: one selection, one read-back
-    C = compact_if(ctx, cs.total, NewChordHead{cs.row.p, cs.key.p, rptr_p, g.v}, hp);
-    ckeys.alloc(C > 0 ? C : 1, ctx.s);
-    RAMA_KERNEL(ctx, k_chord_out, C, (const int32_t*)nullptr, C, hp.p, cs.row.p, cs.key.p, m, st.eu.p, st.ev.p,
+  BucketSorted bs;
+  Buf<int32_t> hc, ht;
+  if (N > 0) {
+    bucket_sort(ctx, n, N, irow.p, ikey.p, bs, true);
+    partition2(ctx, bs.total, NewChordHeadTagged{bs.row.p, bs.key.p, rptr_p, g.v}, TripletHead{bs.row.p, bs.key.p},
+               hc, ht, C, T);
+  }
+  irow.release();
+  ikey.release();
+  if (C > 0) {
+    ckeys.alloc(C, ctx.s);
+    RAMA_KERNEL(ctx, k_chord_out, C, (const int32_t*)nullptr, C, hc.p, bs.row.p, bs.key.p, m, st.eu.p, st.ev.p,
                 st.base.p, ckeys.p);
   }
   st.m_aug = m + C;
@@ -1734,16 +1767,11 @@ void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& 
   st.chord_ptr.alloc(n + 1, ctx.s);
   row_ptr_from_sorted(ctx, st.eu.p + m, C, n, st.chord_ptr.p);
 
-  // triplets: dedupe (lexicographic), handles
-  int64_t T = 0;
-  if (traw > 0) {
-    BucketSorted ts;
-    bucket_sort(ctx, n, traw, trow.p, tkey.p, ts, true);
-    Buf<int32_t> hp;
-    T = compact_if(ctx, ts.total, SortedHead{ts.row.p, ts.key.p}, hp);  // kept triplets only
+  // triplets: handles
+  if (T > 0) {
     st.tri_nodes.alloc(3 * T, ctx.s);
     st.tri_edges.alloc(3 * T, ctx.s);
-    RAMA_KERNEL(ctx, k_tri_out_handles, T, hp.p, T, ts.row.p, ts.key.p, rptr_p, g.v, st.chord_ptr.p, st.ev.p + m, m,
+    RAMA_KERNEL(ctx, k_tri_out_handles, T, ht.p, T, bs.row.p, bs.key.p, rptr_p, g.v, st.chord_ptr.p, st.ev.p + m, m,
                 st.tri_nodes.p, st.tri_edges.p);
   } else {
     st.tri_nodes.alloc(1, ctx.s);
@@ -1865,7 +1893,7 @@ int64_t extend_separation(Ctx& ctx, DualState& st, int L) {
   Buf<int32_t> trow(traw, ctx), crow(craw > 0 ? craw : 1, ctx);
   Buf<uint64_t> tkey(traw, ctx), ckey(craw > 0 ? craw : 1, ctx);
   RAMA_KERNEL(ctx, k_fan_emit, rows, cyc.len.p, cyc.nodes.p, rows, cyc.L, toff.p, coff.p, trow.p, tkey.p, crow.p,
-              ckey.p);
+              ckey.p, 0ull);
   // new chords (sorted, unique, not yet augmented edges) join at base 0
   int64_t C = 0;
   Buf<int32_t> sel_c, hp_c;
