@@ -86,6 +86,10 @@ struct PosAlive {  // alive slot with c_i > 0
   const uint8_t* alive;
   __device__ __forceinline__ bool operator()(int32_t i) const { return alive[i] && c[i] > 0.0; }
 };
+struct FlagSet {  // flags[i] != 0
+  const uint8_t* f;
+  __device__ __forceinline__ bool operator()(int32_t i) const { return f[i] != 0; }
+};
 struct SortedHead {  // first item of each (row, key) run of a sorted list
   const int32_t* row;
   const uint64_t* key;

@@ -253,6 +253,12 @@ __device__ __forceinline__ int32_t first_common_pos(const int32_t* a, int32_t la
   return -1;
 }
 
+__global__ void k_gather_i32_dev(const int32_t* __restrict__ src, const int32_t* __restrict__ idx,
+                                 const int32_t* __restrict__ n_dev, int32_t* __restrict__ out) {
+  const int64_t n = *n_dev;
+  GRID_STRIDE(i, n) out[i] = src[idx[i]];
+}
+
 __global__ void k_gather_i32(const int32_t* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
                              int32_t* __restrict__ dst) {
   GRID_STRIDE(i, n) dst[i] = src[idx[i]];
@@ -709,12 +715,13 @@ __device__ __forceinline__ int32_t grp_sum_i32(int32_t x, unsigned mask) {
 template <class T, int THREADS, int MINB, bool kListed>
 __global__ void __launch_bounds__(THREADS, MINB) k_sep_src(
     const int32_t* __restrict__ gstart, const int32_t* __restrict__ gsrc, const int32_t* __restrict__ glist,
-    int64_t nlist_host, const int32_t* __restrict__ nlist_dev, int64_t ng, int64_t n2,
-    const int32_t* __restrict__ Q2, const int32_t* __restrict__ qb, const int32_t* __restrict__ ptr,
+    int64_t nlist_host, const int32_t* __restrict__ nlist_dev, const int32_t* __restrict__ ng_dev,
+    const int32_t* __restrict__ n2_dev, const int32_t* __restrict__ Q2, const int32_t* __restrict__ qb, const int32_t* __restrict__ ptr,
     const int32_t* __restrict__ adj, int L, int32_t* __restrict__ out_len, int32_t* __restrict__ out_nodes,
     int32_t* __restrict__ over_list, int32_t* __restrict__ over_cnt, int32_t* __restrict__ fb_list,
     int32_t* __restrict__ fb_cnt, int force_fallback, uint8_t* __restrict__ capped) {
-  int64_t nlist = nlist_host;
+  const int64_t ng = *ng_dev, n2 = *n2_dev;  // source groups, listed repulsive edges (counts on the device)
+  int64_t nlist = nlist_host < 0 ? ng : nlist_host;
   if constexpr (kListed) nlist = *nlist_dev;
   constexpr int kGrp = T::kGrp, kPer = THREADS / T::kGrp, kH = T::kHash;
   __shared__ int32_t s_l1[kPer][T::kL1];
@@ -949,10 +956,17 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sep_src(
   }
 }
 
-__global__ void k_src_heads(const int32_t* __restrict__ Q2, int64_t n2, const int32_t* __restrict__ NQ,
-                            const int32_t* __restrict__ u, const int32_t* __restrict__ v, uint8_t* __restrict__ head,
-                            int32_t* __restrict__ qa, int32_t* __restrict__ qb) {
-  GRID_STRIDE(i, n2) {
+// over the first *n2_dev of cap list entries (heads of the rest cleared)
+__global__ void k_src_heads(const int32_t* __restrict__ Q2, const int32_t* __restrict__ n2_dev, int64_t cap,
+                            const int32_t* __restrict__ NQ, const int32_t* __restrict__ u,
+                            const int32_t* __restrict__ v, uint8_t* __restrict__ head, int32_t* __restrict__ qa,
+                            int32_t* __restrict__ qb) {
+  const int64_t n2 = *n2_dev;
+  GRID_STRIDE(i, cap) {
+    if (i >= n2) {
+      head[i] = 0;
+      continue;
+    }
     int32_t e = NQ[Q2[i]];
     int32_t a = u[e];
     qa[i] = a;
@@ -1416,17 +1430,18 @@ static void separate_tables(Ctx& ctx, const GraphView& g, int L, CycleRows& out,
   RAMA_KERNEL(ctx, k_sep3, nq, (const int32_t*)nullptr, nq, NQ.p, g.u, g.v, csr.ptr.p, csr.adj.p, L, out.len.p,
               out.nodes.p, L >= 4 ? miss.p : (uint8_t*)nullptr);
   if (L < 4) return;
-  Buf<int32_t> Q2;
-  int64_t n2 = compact_indices(ctx, miss.p, nq, Q2);
-  if (n2 == 0) return;
+  // the edges without a triangle and their sources' group starts stay on
+  // the device (counts n2c / ngc): grids are sized by nq, no read-back
+  Buf<int32_t> Q2, n2c, gstart, ngc;
+  compact_if_dev(ctx, nq, FlagSet{miss.p}, Q2, n2c);
   // 4/5-cycles: source-grouped BFS levels in shared memory
-  Buf<uint8_t> head(n2, ctx);
-  Buf<int32_t> qa(n2, ctx), qb(n2, ctx);
-  RAMA_KERNEL(ctx, k_src_heads, n2, Q2.p, n2, NQ.p, g.u, g.v, head.p, qa.p, qb.p);
-  Buf<int32_t> gstart;
-  int64_t ng = compact_indices(ctx, head.p, n2, gstart);
-  Buf<int32_t> gsrc(ng > 0 ? ng : 1, ctx);
-  RAMA_KERNEL(ctx, k_gather_i32, ng, qa.p, gstart.p, ng, gsrc.p);
+  Buf<uint8_t> head(nq, ctx);
+  Buf<int32_t> qa(nq, ctx), qb(nq, ctx);
+  RAMA_KERNEL(ctx, k_src_heads, nq, Q2.p, n2c.p, nq, NQ.p, g.u, g.v, head.p, qa.p, qb.p);
+  compact_if_dev(ctx, nq, FlagSet{head.p}, gstart, ngc);
+  Buf<int32_t> gsrc(nq, ctx);
+  RAMA_KERNEL(ctx, k_gather_i32_dev, nq, qa.p, gstart.p, ngc.p, gsrc.p);
+  const int64_t n2 = nq, ng = nq;  // upper bounds of both counts (grid sizes, list capacities)
   // overflow lists, appended on the device: tier 1 -> 1.5 -> 2 sources, then
   // the fall-back edges and the 4-cycle misses of the row-intersection pass
   Buf<int32_t> cnt(4, ctx);  // G15 | G2 | fall-back | misses
@@ -1446,7 +1461,7 @@ static void separate_tables(Ctx& ctx, const GraphView& g, int L, CycleRows& out,
     KernelScope ks(ctx.s, "k_sep_src",
                    4.0 * (double)(g.n + 1) + 4.0 * (double)csr.arcs + (16.0 + 4.0 * L) * (double)n2);
     k_sep_src<SrcTier1, kSrcThreads1, 12, false><<<(unsigned)blocks, kSrcThreads1, 0, ctx.s>>>(
-        gstart.p, gsrc.p, (const int32_t*)nullptr, ng, (const int32_t*)nullptr, ng, n2, Q2.p, qb.p, csr.ptr.p,
+        gstart.p, gsrc.p, (const int32_t*)nullptr, -1, (const int32_t*)nullptr, ngc.p, n2c.p, Q2.p, qb.p, csr.ptr.p,
         csr.adj.p, L, out.len.p, out.nodes.p, G15.p, cnt.p, (int32_t*)nullptr, (int32_t*)nullptr, force ? 1 : 0,
         capped);
     RAMA_LAUNCH_CHECK();
@@ -1458,7 +1473,7 @@ static void separate_tables(Ctx& ctx, const GraphView& g, int L, CycleRows& out,
   {
     KernelScope ks(ctx.s, "k_sep_src_mid", 0.0);
     k_sep_src<SrcTier15, kSrcThreads1, 12, true><<<wave, kSrcThreads1, 0, ctx.s>>>(
-        gstart.p, gsrc.p, G15.p, 0, cnt.p, ng, n2, Q2.p, qb.p, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p,
+        gstart.p, gsrc.p, G15.p, 0, cnt.p, ngc.p, n2c.p, Q2.p, qb.p, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p,
         G2.p, cnt.p + 1, (int32_t*)nullptr, (int32_t*)nullptr, force ? 1 : 0, capped);
     RAMA_LAUNCH_CHECK();
     ctx.launches++;
@@ -1466,7 +1481,7 @@ static void separate_tables(Ctx& ctx, const GraphView& g, int L, CycleRows& out,
   {
     KernelScope ks(ctx.s, "k_sep_src_wide", 0.0);
     k_sep_src<SrcTier2, kSrcThreads2, 6, true><<<(unsigned)num_sms() * 6, kSrcThreads2, 0, ctx.s>>>(
-        gstart.p, gsrc.p, G2.p, 0, cnt.p + 1, ng, n2, Q2.p, qb.p, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p,
+        gstart.p, gsrc.p, G2.p, 0, cnt.p + 1, ngc.p, n2c.p, Q2.p, qb.p, csr.ptr.p, csr.adj.p, L, out.len.p, out.nodes.p,
         (int32_t*)nullptr, (int32_t*)nullptr, FB.p, cnt.p + 2, force == 1 ? 1 : 0, capped);
     RAMA_LAUNCH_CHECK();
     ctx.launches++;
@@ -1474,6 +1489,7 @@ static void separate_tables(Ctx& ctx, const GraphView& g, int L, CycleRows& out,
   if (getenv("RAMA_SEP_STATS")) {
     Buf<unsigned long long> st(5, ctx);
     st.zero();
+    const int64_t n2 = read_scalar(ctx, n2c.p), ng = read_scalar(ctx, ngc.p);
     RAMA_KERNEL(ctx, k_sep_stats, n2, Q2.p, qa.p, qb.p, n2, csr.ptr.p, out.len.p, st.p);
     unsigned long long h[5];
     int32_t nf = 0;
