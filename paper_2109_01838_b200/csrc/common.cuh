@@ -52,16 +52,19 @@ struct Error : public std::runtime_error {
     if (!(cond)) throw ::rama::Error(::rama::kInvalid, (msg));    \
   } while (0)
 
-// Per-call context: the stream everything is ordered on plus a small pinned
 // RAMA_HOST_STATS=2: count host syncs per call chain (backtrace), printed
 // after each solve
 void note_sync();
 void dump_sync_sites();
 
+constexpr int kPinSlots = 512;   // pinned read-back block (int64 slots)
+constexpr int kPinTagged = 256;  // first slot of fetch()'s tagged words
+
+// Per-call context: the stream everything is ordered on plus a small pinned
 // staging area for scalar read-backs (the only host syncs in a solve).
 struct Ctx {
   cudaStream_t s = nullptr;
-  int64_t* pinned = nullptr;  // 64 int64 slots (slot 63: the read-back flag)
+  int64_t* pinned = nullptr;  // kPinSlots int64 slots: 0-62 read-back data, 63 the sequence, kPinTagged.. tagged words
   int64_t* pinned_dev = nullptr;  // the same block, mapped into the device
   uint32_t seq = 0;           // last read-back sequence number published
   cudaEvent_t ev = nullptr;   // asynchronous read-backs (recycled with `pinned`)
@@ -297,13 +300,14 @@ bool trace_print();     // RAMA_TRACE=1 or 2: print launches and sync points
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)(n); i += (int64_t)gridDim.x * blockDim.x)
 
 // ---- scalar read-back -----------------------------------------------------
-// fetch(): up to four small device ranges (whole 4-byte words, <= 128 words
-// in all) are copied by a one-warp kernel into the pinned block at byte
-// offset `at`, which then publishes a sequence number in slot 63 (system
-// fence first); the host spins on that flag.  Measured on the B200: 8.7 us
-// per read-back round trip against 12.4 us for cudaMemcpyAsync +
-// cudaStreamSynchronize (tools/readback_probe.cu).  Returns a pointer to the
-// fetched bytes.
+// fetch(): up to four small device ranges (whole 4-byte words, <= 126 words
+// in all) are written by a one-warp kernel into the mapped pinned block, each
+// word in one 8-byte store together with the call's sequence number; the
+// host spins until every word carries it (no system-scope fence on the
+// device) and copies the words to byte offset `at` of the block.  Measured
+// on the B200 with a flag-after-fence variant: 8.7 us per read-back round
+// trip against 12.4 us for cudaMemcpyAsync + cudaStreamSynchronize
+// (tools/readback_probe.cu).  Returns a pointer to the fetched bytes.
 struct FetchPart {
   const void* src;
   int bytes;

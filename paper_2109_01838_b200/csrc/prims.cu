@@ -104,8 +104,8 @@ Ctx::Ctx(cudaStream_t st) : s(st) {
     }
   }
   if (!pinned) {
-    RAMA_CUDA(cudaHostAlloc((void**)&pinned, 64 * sizeof(int64_t), cudaHostAllocMapped | cudaHostAllocPortable));
-    memset(pinned, 0, 64 * sizeof(int64_t));
+    RAMA_CUDA(cudaHostAlloc((void**)&pinned, kPinSlots * sizeof(int64_t), cudaHostAllocMapped | cudaHostAllocPortable));
+    memset(pinned, 0, kPinSlots * sizeof(int64_t));
     RAMA_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }
   RAMA_CUDA(cudaHostGetDevicePointer((void**)&pinned_dev, pinned, 0));
@@ -118,15 +118,18 @@ struct FetchArgs {
   int words[4];
   int n;
 };
-__global__ void k_fetch(FetchArgs a, uint32_t* dst, volatile uint32_t* flag, uint32_t s) {
+// Every word travels with the call's sequence number in one 8-byte store
+// (sequence << 32 | word), so the host waits for all tags instead of a flag
+// published after a system-scope fence (the same self-validating 8-byte
+// protocol as NCCL's LL transport): no fence round trip on the device.
+__global__ void k_fetch(FetchArgs a, volatile unsigned long long* tagged, uint32_t s) {
   int o = 0;
   for (int k = 0; k < a.n; k++) {
-    for (int i = threadIdx.x; i < a.words[k]; i += blockDim.x) dst[o + i] = __ldcg(a.src[k] + i);
+    for (int i = threadIdx.x; i < a.words[k]; i += blockDim.x)
+      tagged[o + i] = ((unsigned long long)s << 32) | (unsigned long long)__ldcg(a.src[k] + i);
     o += a.words[k];
   }
-  __threadfence_system();
-  __syncwarp();
-  if (threadIdx.x == 0) *flag = s;
+  if (o == 0 && threadIdx.x == 0) tagged[0] = (unsigned long long)s << 32;  // a pure sync point
 }
 }  // namespace
 
@@ -148,18 +151,24 @@ void* fetch(Ctx& ctx, std::initializer_list<FetchPart> parts, int at) {
   }
   RAMA_REQUIRE(at % 4 == 0 && at + 4 * words <= 63 * 8, "fetch: range exceeds the pinned block");
   const uint32_t s = ++ctx.seq;
-  volatile uint32_t* flag = (volatile uint32_t*)(ctx.pinned + 63);
-  k_fetch<<<1, 32, 0, ctx.s>>>(a, (uint32_t*)((char*)ctx.pinned_dev + at), (volatile uint32_t*)(ctx.pinned_dev + 63),
-                               s);
+  k_fetch<<<1, 32, 0, ctx.s>>>(a, (volatile unsigned long long*)(ctx.pinned_dev + kPinTagged), s);
   RAMA_LAUNCH_CHECK();
-  for (uint32_t spins = 1; *flag != s; spins++) {
-    _mm_pause();
-    if ((spins & 1023) == 0) {  // a failed kernel never publishes: surface its error
-      const cudaError_t e = cudaStreamQuery(ctx.s);
-      if (e != cudaSuccess && e != cudaErrorNotReady) RAMA_CUDA(e);
-      if (e == cudaSuccess && *flag != s) RAMA_REQUIRE(false, "read-back flag not published");
+  volatile unsigned long long* tg = (volatile unsigned long long*)(ctx.pinned + kPinTagged);
+  uint32_t* out = (uint32_t*)((char*)ctx.pinned + at);
+  const int wait = words > 0 ? words : 1;
+  for (int i = 0; i < wait; i++) {
+    unsigned long long w;
+    for (uint32_t spins = 1; (uint32_t)((w = tg[i]) >> 32) != s; spins++) {
+      _mm_pause();
+      if ((spins & 1023) == 0) {  // a failed kernel never publishes: surface its error
+        const cudaError_t e = cudaStreamQuery(ctx.s);
+        if (e != cudaSuccess && e != cudaErrorNotReady) RAMA_CUDA(e);
+        if (e == cudaSuccess && (uint32_t)(tg[i] >> 32) != s) RAMA_REQUIRE(false, "read-back word not published");
+      }
     }
+    if (i < words) out[i] = (uint32_t)w;
   }
+  *(volatile uint32_t*)(ctx.pinned + 63) = s;  // the sequence survives recycling of the block
   std::atomic_thread_fence(std::memory_order_acquire);
   HostStats& hs = host_stats();
   hs.sync_ms += host_ms_since(t0);
