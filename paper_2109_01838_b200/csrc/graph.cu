@@ -88,14 +88,18 @@ struct GraphEmit {
 };
 
 template <class Src>
-static Graph sort_reduce_graph(Ctx& ctx, int64_t n_out, int64_t m_in, const Src& src) {
+static Graph sort_reduce_graph(Ctx& ctx, int64_t n_out, int64_t m_in, const Src& src,
+                               const int32_t* nt_dev = nullptr) {
   Graph out;
   out.n = n_out;
   out.u.alloc(m_in > 0 ? m_in : 1, ctx.s);
   out.v.alloc(m_in > 0 ? m_in : 1, ctx.s);
   out.c.alloc(m_in > 0 ? m_in : 1, ctx.s);
   SrResult sr;
-  out.m = sort_reduce<32, true, true>(ctx, n_out, m_in, src, GraphEmit{out.u.p, out.v.p, out.c.p}, sr);
+  int64_t nt = n_out;
+  out.m = sort_reduce<32, true, true>(ctx, n_out, m_in, src, GraphEmit{out.u.p, out.v.p, out.c.p}, sr, true, "sr",
+                                      nt_dev, &nt);
+  out.n = nt;
   return out;
 }
 
@@ -180,7 +184,8 @@ __global__ void k_cc_label(const int32_t* __restrict__ parent, const int32_t* __
   GRID_STRIDE(x, n) map[x] = rank[parent[x]];
 }
 
-int64_t components(Ctx& ctx, int64_t n, const int32_t* su, const int32_t* sv, int64_t k, int32_t* map, bool check) {
+int64_t components(Ctx& ctx, int64_t n, const int32_t* su, const int32_t* sv, int64_t k, int32_t* map, bool check,
+                   Buf<int32_t>* keep_rank) {
   // algorithmic bytes: the pairs read once, the map written
   ProfScope prof(ctx.s, kFamComponents, 8.0 * (double)k + 4.0 * (double)n);
   if (n == 0) return 0;
@@ -190,13 +195,15 @@ int64_t components(Ctx& ctx, int64_t n, const int32_t* su, const int32_t* sv, in
     RAMA_KERNEL(ctx, k_cc_check, k, su, sv, k, n, err.p);
     RAMA_REQUIRE(read_scalar(ctx, err.p) == 0, "contraction edge endpoint out of range");
   }
-  Buf<int32_t> parent(n, ctx), flag(n, ctx), rank(n + 1, ctx);
+  Buf<int32_t> parent(n, ctx), flag(n, ctx), own_rank;
+  Buf<int32_t>& rank = keep_rank ? *keep_rank : own_rank;
+  rank.alloc(n + 1, ctx.s);
   iota(ctx, parent.p, n);
   RAMA_KERNEL(ctx, k_cc_hook, k, su, sv, k, parent.p);
   RAMA_KERNEL(ctx, k_cc_flatten, n, parent.p, n, flag.p);
-  int64_t nt = exclusive_scan(ctx, flag.p, rank.p, n, true);
+  int64_t nt = exclusive_scan(ctx, flag.p, rank.p, n, !keep_rank);  // rank[n] = number of components
   RAMA_KERNEL(ctx, k_cc_label, n, parent.p, rank.p, n, map);
-  return nt;
+  return keep_rank ? -1 : nt;
 }
 
 __global__ void k_is_canonical(const int32_t* __restrict__ u, const int32_t* __restrict__ v, int64_t m, int64_t n,
@@ -225,14 +232,15 @@ __global__ void k_joined_mass(const int32_t* __restrict__ u, const int32_t* __re
   GRID_STRIDE(i, m) jc[i] = (f[u[i]] == f[v[i]]) ? c[i] : 0.0;
 }
 
-Graph contract(Ctx& ctx, const GraphView& g, const int32_t* map, int64_t n_targets, double* joined) {
+Graph contract(Ctx& ctx, const GraphView& g, const int32_t* map, int64_t n_targets, double* joined,
+               const int32_t* nt_dev) {
   // algorithmic bytes: 24 m_in + 16 m_out
   ProfScope prof(ctx.s, kFamContract, 24.0 * (double)g.m);
   const int64_t m = g.m;
   if (m == 0) {
     if (joined) *joined = 0.0;
     Graph out;
-    out.n = n_targets;
+    out.n = nt_dev ? (int64_t)read_scalar(ctx, nt_dev) : n_targets;
     return out;
   }
   if (joined) {
@@ -240,7 +248,7 @@ Graph contract(Ctx& ctx, const GraphView& g, const int32_t* map, int64_t n_targe
     RAMA_KERNEL(ctx, k_joined_mass, m, g.u, g.v, g.c, m, map, jc.p);
     *joined = device_sum(ctx, jc.p, m);
   }
-  Graph out = sort_reduce_graph(ctx, n_targets, m, ContractSrc{g.u, g.v, g.c, map, m});
+  Graph out = sort_reduce_graph(ctx, n_targets, m, ContractSrc{g.u, g.v, g.c, map, m}, nt_dev);
   prof.add_bytes(16.0 * (double)out.m);
   return out;
 }

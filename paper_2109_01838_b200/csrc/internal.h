@@ -41,10 +41,15 @@ bool is_canonical(Ctx& ctx, const GraphView& g);
 // a17 connected_components (contraction.py:101-111); returns num_targets
 // (check: validate endpoint ranges first -- the C ABI entry; internal callers
 // pass edges that are valid by construction)
+// keep_rank: the count stays on the device at keep_rank[n] (no read-back;
+// returns -1)
 int64_t components(Ctx& ctx, int64_t n, const int32_t* su, const int32_t* sv, int64_t k, int32_t* map,
-                   bool check = false);
-// a18 contract_graph (contraction.py:142-163); *joined (host) may be null
-Graph contract(Ctx& ctx, const GraphView& g, const int32_t* map, int64_t n_targets, double* joined);
+                   bool check = false, Buf<int32_t>* keep_rank = nullptr);
+// a18 contract_graph (contraction.py:142-163); *joined (host) may be null.
+// nt_dev: the target count is on the device (n_targets only bounds it); it is
+// read back together with the edge count
+Graph contract(Ctx& ctx, const GraphView& g, const int32_t* map, int64_t n_targets, double* joined,
+               const int32_t* nt_dev = nullptr);
 // a19 ContractionMapping.then (contraction.py:45-52): f_total = f[f_total]
 void compose(Ctx& ctx, int32_t* f_total, int64_t n0, const int32_t* f);
 // a21 clustering_cost (graph.py:134-145)

@@ -852,8 +852,12 @@ void contraction_step(Ctx& ctx, const GraphView& g, int policy, double switch_fr
   }
   out.identity = false;
   out.map.alloc(g.n, ctx.s);
-  out.num_targets = components(ctx, g.n, su.p, sv.p, k, out.map.p);
-  out.next = contract(ctx, g, out.map.p, out.num_targets, want_joined ? &out.joined : nullptr);
+  // the component count stays on the device and returns with the
+  // contraction's edge count (one read-back for both)
+  Buf<int32_t> rank;
+  components(ctx, g.n, su.p, sv.p, k, out.map.p, false, &rank);
+  out.next = contract(ctx, g, out.map.p, g.n, want_joined ? &out.joined : nullptr, rank.p + g.n);
+  out.num_targets = out.next.n;
 }
 
 }  // namespace rama

@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(kSrThreads) k_sr_tiles(const SrItem* __restric
                                                          int64_t tiles, const int32_t* __restrict__ tile_row,
                                                          uint64_t* __restrict__ status,
                                                          int32_t* __restrict__ tile_ctr, int64_t* __restrict__ total,
-                                                         Emit emit) {
+                                                         Emit emit, const int32_t* __restrict__ R_dev) {
   // staged items as SoA; the row order is a permutation (sorted position ->
   // staged index), so items never move
   extern __shared__ __align__(16) unsigned char s_dyn[];
@@ -274,7 +274,10 @@ __global__ void __launch_bounds__(kSrThreads) k_sr_tiles(const SrItem* __restric
   // tiles in launch order (blocks are dispatched in index order, as in CUB's
   // single-pass scans)
   const int32_t t = blockIdx.x;
-  const int32_t r0 = __ldg(tile_row + t), r1 = __ldg(tile_row + t + 1);
+  // R_dev: the rows actually used when R only bounds them (the rest are
+  // empty; the last tile must not walk them)
+  const int32_t r0 = __ldg(tile_row + t), r1 = R_dev ? min(__ldg(tile_row + t + 1), max(*R_dev, r0))
+                                                     : __ldg(tile_row + t + 1);
   const int32_t s0 = __ldg(rowptr + r0), s1 = __ldg(rowptr + r1);
   int32_t se = s1, rh = -1;  // staged end, huge (last) row
   if (r1 > r0) {
@@ -460,12 +463,16 @@ struct SrResult {
 // read-back), else -1 (the count stays in res.total on the device).
 template <int GS, bool kUnique, bool kDistinct, class Src, class Emit>
 int64_t sort_reduce(Ctx& ctx, int64_t R, int64_t N_max, const Src& src, const Emit& emit, SrResult& res,
-                    bool want = true, const char* tag = "sr") {
+                    bool want = true, const char* tag = "sr", const int32_t* extra_dev = nullptr,
+                    int64_t* extra_out = nullptr) {
+  // extra_dev: one more device word read back with the output count (want);
+  // it is also the number of rows in use (R bounds it; rows beyond are empty)
   res.rowptr.alloc(R + 1, ctx.s);
   res.total.alloc(1, ctx.s);
   RAMA_CUDA(cudaMemsetAsync(res.total.p, 0, sizeof(int64_t), ctx.s));
   if (R == 0 || N_max == 0) {
     RAMA_CUDA(cudaMemsetAsync(res.rowptr.p, 0, sizeof(int32_t) * (R + 1), ctx.s));
+    if (want && extra_dev) *extra_out = read_scalar(ctx, extra_dev);
     return want ? 0 : -1;
   }
   Buf<int32_t> cnt(R + 2, ctx);  // counts | huge-row counter
@@ -533,11 +540,25 @@ int64_t sort_reduce(Ctx& ctx, int64_t R, int64_t N_max, const Src& src, const Em
   {
     KernelScope ks(ctx.s, "k_sr_tiles");
     k_sr_tiles<GS, kUnique, kDistinct, Emit><<<(unsigned)tiles, kSrThreads, kSrSmem, ctx.s>>>(
-        items.p, res.rowptr.p, R, tiles, tile_row.p, status.p, (int32_t*)(status.p + tiles), res.total.p, emit);
+        items.p, res.rowptr.p, R, tiles, tile_row.p, status.p, (int32_t*)(status.p + tiles), res.total.p, emit,
+        extra_dev);
   }
   RAMA_LAUNCH_CHECK();
   ctx.launches++;
   if (!want) return -1;
+  if (extra_dev) {
+    const int32_t* hp = kUnique ? (const int32_t*)fetch(ctx, {{res.total.p, 8}, {extra_dev, 4}})
+                                : (const int32_t*)fetch(ctx, {{res.rowptr.p + R, 4}, {extra_dev, 4}});
+    int64_t cnt;
+    if (kUnique) {
+      memcpy(&cnt, hp, 8);
+      *extra_out = hp[2];
+    } else {
+      cnt = hp[0];
+      *extra_out = hp[1];
+    }
+    return cnt;
+  }
   if (!kUnique) return read_scalar(ctx, res.rowptr.p + R);  // every item is an output
   return read_scalar(ctx, res.total.p);
 }
