@@ -67,6 +67,11 @@ struct Ctx {
   int64_t* pinned = nullptr;  // kPinSlots int64 slots: 0-62 read-back data, 63 the sequence, kPinTagged.. tagged words
   int64_t* pinned_dev = nullptr;  // the same block, mapped into the device
   uint32_t seq = 0;           // last read-back sequence number published
+  // piggyback: 8 device bytes the next fetch() brings back as well (the
+  // round's lower bound rides on the contraction's first read-back)
+  const void* piggy = nullptr;
+  bool piggy_done = false;
+  uint64_t piggy_val = 0;
   cudaEvent_t ev = nullptr;   // asynchronous read-backs (recycled with `pinned`)
   int launches = 0;           // kernels launched through this context
 

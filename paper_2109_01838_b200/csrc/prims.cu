@@ -149,6 +149,14 @@ void* fetch(Ctx& ctx, std::initializer_list<FetchPart> parts, int at) {
     words += a.words[a.n];
     a.n++;
   }
+  int piggy_at = -1;  // word offset of the piggyback value
+  if (ctx.piggy && a.n < 4) {
+    a.src[a.n] = (const uint32_t*)ctx.piggy;
+    a.words[a.n] = 2;
+    piggy_at = words;
+    words += 2;
+    a.n++;
+  }
   RAMA_REQUIRE(at % 4 == 0 && at + 4 * words <= 63 * 8, "fetch: range exceeds the pinned block");
   const uint32_t s = ++ctx.seq;
   k_fetch<<<1, 32, 0, ctx.s>>>(a, (volatile unsigned long long*)(ctx.pinned_dev + kPinTagged), s);
@@ -169,6 +177,11 @@ void* fetch(Ctx& ctx, std::initializer_list<FetchPart> parts, int at) {
     if (i < words) out[i] = (uint32_t)w;
   }
   *(volatile uint32_t*)(ctx.pinned + 63) = s;  // the sequence survives recycling of the block
+  if (piggy_at >= 0) {
+    memcpy(&ctx.piggy_val, out + piggy_at, 8);
+    ctx.piggy_done = true;
+    ctx.piggy = nullptr;
+  }
   std::atomic_thread_fence(std::memory_order_acquire);
   HostStats& hs = host_stats();
   hs.sync_ms += host_ms_since(t0);

@@ -150,7 +150,10 @@ void solve(Ctx& ctx, const GraphView& g, const SolveConfig& cfg, int32_t* labels
       mark(2);
       Graph rep = reparametrized_graph(ctx, st, cl.p);
       mark(3);
+      ctx.piggy = d_lb.p;  // the bound returns with the contraction's first read-back
+      ctx.piggy_done = false;
       contraction_step(ctx, rep.view(), 3, cfg.switch_fraction, step);
+      ctx.piggy = nullptr;
       mark(4);
       if (phase_prof)
         fprintf(stderr, "[rama] round %d n %lld m %lld T %lld: separate %.2f triangulate %.2f mp+lb %.2f "
@@ -161,7 +164,12 @@ void solve(Ctx& ctx, const GraphView& g, const SolveConfig& cfg, int32_t* labels
     }
     // round end: the LB comes back (the wait also closes the round's timing)
     if (dual) {
-      lb_r = read_scalar(ctx, d_lb.p);
+      if (ctx.piggy_done) {
+        memcpy(&lb_r, &ctx.piggy_val, 8);
+        ctx.piggy_done = false;
+      } else {
+        lb_r = read_scalar(ctx, d_lb.p);
+      }
       if (rnd == 1) lb = lb_r;
     } else {
       ctx.sync();

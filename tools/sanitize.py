@@ -47,3 +47,8 @@ n, u, v, c = instances.grid_coo(400, 900, 0, seed=1)  # ~720k edges: several 4 M
 g = P.WeightedGraph(n, u, v, c)
 print("host", P.solve_host(n, np.ascontiguousarray(g.edges_u, np.int32), np.ascontiguousarray(g.edges_v, np.int32),
                            np.ascontiguousarray(g.costs), P.SolverConfig(mode="P"))[1])
+# round-2 late: forests of small trees (per-tree conflict loop) and of larger trees
+for shift in (1.0, 0.8):
+    n, u, v, c = instances.grid_coo(60, 80, 2, seed=3)
+    g = P.WeightedGraph(n, u, v, c - shift)
+    print("forest", shift, len(P.select_spanning_forest_no_conflicts(g)))
