@@ -1458,8 +1458,10 @@ static void separate_tables(Ctx& ctx, const GraphView& g, int L, CycleRows& out,
     if (trace_print()) fprintf(stderr, "[rama] k_sep_src groups=%lld\n", (long long)ng);
     // algorithmic bytes: the positive CSR once, the miss list and its
     // edges' endpoints, the cycle rows written
+    // (the miss count is on the device: profiled runs read it for the bytes)
+    const double n2_alg = prof_enabled() ? (double)read_scalar(ctx, n2c.p) : 0.0;
     KernelScope ks(ctx.s, "k_sep_src",
-                   4.0 * (double)(g.n + 1) + 4.0 * (double)csr.arcs + (16.0 + 4.0 * L) * (double)n2);
+                   4.0 * (double)(g.n + 1) + 4.0 * (double)csr.arcs + (16.0 + 4.0 * L) * n2_alg);
     k_sep_src<SrcTier1, kSrcThreads1, 12, false><<<(unsigned)blocks, kSrcThreads1, 0, ctx.s>>>(
         gstart.p, gsrc.p, (const int32_t*)nullptr, -1, (const int32_t*)nullptr, ngc.p, n2c.p, Q2.p, qb.p, csr.ptr.p,
         csr.adj.p, L, out.len.p, out.nodes.p, G15.p, cnt.p, (int32_t*)nullptr, (int32_t*)nullptr, force ? 1 : 0,

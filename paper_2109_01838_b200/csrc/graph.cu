@@ -232,6 +232,89 @@ __global__ void k_joined_mass(const int32_t* __restrict__ u, const int32_t* __re
   GRID_STRIDE(i, m) jc[i] = (f[u[i]] == f[v[i]]) ? c[i] : 0.0;
 }
 
+// ---- contraction by a device-wide radix sort (long rows) -----------------
+// When the contracted rows are long (the cleanup's quotient of the original
+// graph: 9.9 M edges into ~290 k clusters on C2), the row tiles of the
+// sort-reduce spend their time on long in-row rankings and on waiting for
+// each other's look-back.  This path sorts (min, max) target pairs packed in
+// 2 * bits(R) key bits with the source index as the value by CUB's stable
+// LSD onesweep passes -- equal pairs keep the canonical source order, i.e.
+// exactly the reduceat order of contraction.py:142-163 -- then marks the
+// heads of equal keys, compacts them, and sums each group in numpy's
+// pairwise order from the gathered costs.
+__global__ void k_crx_keys(const int32_t* __restrict__ u, const int32_t* __restrict__ v,
+                           const int32_t* __restrict__ f, int64_t m, int bits, uint64_t* __restrict__ key,
+                           int32_t* __restrict__ val) {
+  const uint64_t sentinel = (1ull << (2 * bits)) - 1ull;  // self-loops sort last
+  GRID_STRIDE(i, m) {
+    const int32_t a = __ldg(f + u[i]), b = __ldg(f + v[i]);
+    key[i] = a == b ? sentinel
+                    : ((uint64_t)(uint32_t)(a < b ? a : b) << bits) | (uint64_t)(uint32_t)(a < b ? b : a);
+    val[i] = (int32_t)i;
+  }
+}
+
+__global__ void k_crx_heads(const uint64_t* __restrict__ key, int64_t m, int bits, uint8_t* __restrict__ head,
+                            int32_t* __restrict__ nvalid) {
+  const uint64_t sentinel = (1ull << (2 * bits)) - 1ull;
+  GRID_STRIDE(p, m) {
+    const uint64_t k = key[p];
+    const bool ok = k != sentinel;
+    head[p] = ok && (p == 0 || key[p - 1] != k);
+    if (ok && (p + 1 == m || key[p + 1] == sentinel)) *nvalid = (int32_t)(p + 1);
+  }
+}
+
+struct GatherPay {  // costs of a run of sorted positions through the source index
+  const double* c;
+  const int32_t* idx;
+  __device__ __forceinline__ double operator[](int64_t i) const { return c[idx[i]]; }
+  __device__ __forceinline__ GatherPay operator+(int64_t k) const { return GatherPay{c, idx + k}; }
+};
+
+__global__ void k_crx_emit(const int32_t* __restrict__ H, int64_t M, const int32_t* __restrict__ nvalid,
+                           const uint64_t* __restrict__ key, const int32_t* __restrict__ val,
+                           const double* __restrict__ c, int bits, int32_t* __restrict__ ou, int32_t* __restrict__ ov,
+                           double* __restrict__ oc) {
+  const int64_t end = *nvalid;
+  GRID_STRIDE(gi, M) {
+    const int64_t p = H[gi], e = gi + 1 < M ? H[gi + 1] : end;
+    const uint64_t k = key[p];
+    ou[gi] = (int32_t)(k >> bits);
+    ov[gi] = (int32_t)(k & ((1ull << bits) - 1ull));
+    const GatherPay pays{c, val + p};
+    const int64_t len = e - p;
+    oc[gi] = len == 1 ? pays[0] : len == 2 ? __dadd_rn(pays[0], pays[1]) : seg_sum(pays, len);
+  }
+}
+
+static Graph contract_radix(Ctx& ctx, const GraphView& g, const int32_t* map, int64_t n_targets,
+                            const int32_t* nt_dev) {
+  const int64_t m = g.m;
+  int bits = 1;
+  while ((1ll << bits) <= n_targets) bits++;  // ids <= n_targets - 1 < 2^bits - 1
+  Buf<uint64_t> k1(m, ctx), k2(m, ctx);
+  Buf<int32_t> v1(m, ctx), v2(m, ctx);
+  RAMA_KERNEL(ctx, k_crx_keys, m, g.u, g.v, map, m, bits, k1.p, v1.p);
+  radix_sort_pairs(ctx, k1.p, v1.p, k2.p, v2.p, m, 0, 2 * bits);
+  k1.release();
+  v1.release();
+  Buf<uint8_t> head(m, ctx);
+  Buf<int32_t> nvalid(1, ctx);
+  nvalid.zero();
+  RAMA_KERNEL(ctx, k_crx_heads, m, k2.p, m, bits, head.p, nvalid.p);
+  Buf<int32_t> H;
+  const int64_t M = compact_indices(ctx, head.p, m, H);
+  Graph out;
+  out.n = nt_dev ? (int64_t)read_scalar(ctx, nt_dev) : n_targets;  // (forced radix on a round contraction)
+  out.m = M;
+  out.u.alloc(M > 0 ? M : 1, ctx.s);
+  out.v.alloc(M > 0 ? M : 1, ctx.s);
+  out.c.alloc(M > 0 ? M : 1, ctx.s);
+  RAMA_KERNEL(ctx, k_crx_emit, M, H.p, M, nvalid.p, k2.p, v2.p, g.c, bits, out.u.p, out.v.p, out.c.p);
+  return out;
+}
+
 Graph contract(Ctx& ctx, const GraphView& g, const int32_t* map, int64_t n_targets, double* joined,
                const int32_t* nt_dev) {
   // algorithmic bytes: 24 m_in + 16 m_out
@@ -248,7 +331,15 @@ Graph contract(Ctx& ctx, const GraphView& g, const int32_t* map, int64_t n_targe
     RAMA_KERNEL(ctx, k_joined_mass, m, g.u, g.v, g.c, m, map, jc.p);
     *joined = device_sum(ctx, jc.p, m);
   }
-  Graph out = sort_reduce_graph(ctx, n_targets, m, ContractSrc{g.u, g.v, g.c, map, m}, nt_dev);
+  // long rows on average (few targets per edge: the cleanup's quotient) take
+  // the radix path; RAMA_CONTRACT_RADIX=0/1 forces either (A/B, tests)
+  static const int force_radix = [] {
+    const char* e = getenv("RAMA_CONTRACT_RADIX");
+    return e ? atoi(e) : -1;
+  }();
+  const bool radix = force_radix == 1 || (force_radix < 0 && !nt_dev && m >= 16 * n_targets);
+  Graph out = radix ? contract_radix(ctx, g, map, n_targets, nt_dev)
+                    : sort_reduce_graph(ctx, n_targets, m, ContractSrc{g.u, g.v, g.c, map, m}, nt_dev);
   prof.add_bytes(16.0 * (double)out.m);
   return out;
 }

@@ -284,6 +284,25 @@ def test_agreement_matches_reference_and_oracle():
             assert P.check_edge_triangle_agreement(st, eps) == O.check_edge_triangle_agreement(ost, eps)
 
 
+def test_contract_into_few_clusters_radix_path():
+    """m >= 16 targets per edge (the cleanup's quotient of the original
+    graph): the contraction takes the device-wide radix path (graph.cu
+    contract_radix); edges, reduceat-order sums and self-loop removal equal
+    the oracle bit for bit, including duplicates and a single cluster."""
+    rng = np.random.default_rng(11)
+    cases = [instances.grid8_coo(60, 80, strides=(2, 3), seed=2), instances.random_coo(3000, 0.01, seed=3)]
+    for n, u, v, c in cases:
+        g, og = _both(n, u, v, c)
+        for nt in (1, 7, 50, max(1, g.num_edges // 40)):
+            fmap = np.sort(rng.integers(0, nt, n))
+            fmap = np.unique(fmap, return_inverse=True)[1]  # canonical-ish ids, all targets used
+            k = int(fmap.max()) + 1
+            og2, ojoined = O.contract_graph(og, fmap, k)
+            g2, joined = P.contract_graph(g, P.ContractionMapping(np.asarray(fmap, np.int64), k))
+            assert np.array_equal(g2.edges_u, og2.edges_u) and np.array_equal(g2.edges_v, og2.edges_v), (n, nt)
+            assert np.array_equal(g2.costs, og2.costs), (n, nt)
+
+
 def test_hub_rows_sort_paths_match_oracle():
     """Rows far beyond the shared-memory tiles (a hub with 9k neighbours, a
     second with 2.5k, plus duplicates): canonicalisation and contraction take
