@@ -513,9 +513,10 @@ __global__ void k_mark_removed(const int32_t* __restrict__ qe, const uint8_t* __
 // (contraction.py:231-284) runs as written, per tree: a repulsive edge only
 // meets removals inside its own tree, so each tree's queries in ascending
 // (u, v) order are independent of every other tree's.  A thread holds its
-// tree (<= 32 nodes, <= 31 edges) in registers / local memory, finds the
-// unique path of each query by relaxation sweeps over the not-yet-removed
-// edges and cuts the path's cheapest edge (ties: smallest (u, v)).  This
+// tree (<= 32 nodes, <= 31 edges) in registers / local memory, roots it
+// once, walks each query's unique path up to the meeting node (a removed
+// edge on it: already separated, as the reference's BFS finds) and cuts
+// the path's cheapest edge (ties: smallest (u, v)).  This
 // replaces the Euler tour, the lifting tables and the dependency passes of
 // the general path (~40 launches and ~6 read-backs per forest round).
 constexpr int kSmallTree = 32;
@@ -566,33 +567,47 @@ __global__ void k_tree_resolve(const int32_t* __restrict__ rptr, const uint64_t*
       fid[ne] = i;
       ne++;
     }
-    uint32_t rem = 0;  // removed tree edges
-    for (; p < e; p++) {
-      const int32_t ed = Q[(int32_t)(uint32_t)key[p]];
-      const int sa = tree_slot(node, nn, u[ed], false), sb = tree_slot(node, nn, v[ed], false);
-      if (sa < 0 || sb < 0) continue;
-      uint32_t vis = 1u << sa;
-      int8_t pe[kSmallTree];  // tree edge that reached each node
+    // root the tree at its first node once: parent edge and depth per node
+    int8_t pe[kSmallTree], dep[kSmallTree];
+    {
+      uint32_t vis = 1u;
+      dep[0] = 0;
+      pe[0] = -1;
       bool grew = true;
-      while (!((vis >> sb) & 1u) && grew) {
+      while (grew) {
         grew = false;
         for (int k = 0; k < ne; k++) {
-          if ((rem >> k) & 1u) continue;
           const bool ia = (vis >> ea[k]) & 1u, ib = (vis >> eb[k]) & 1u;
           if (ia != ib) {
-            const int y = ia ? eb[k] : ea[k];
+            const int y = ia ? eb[k] : ea[k], x = ia ? ea[k] : eb[k];
             vis |= 1u << y;
             pe[y] = (int8_t)k;
+            dep[y] = (int8_t)(dep[x] + 1);
             grew = true;
           }
         }
       }
-      if (!((vis >> sb) & 1u)) continue;  // already separated
+    }
+    uint32_t rem = 0;  // removed tree edges
+    for (; p < e; p++) {
+      const int32_t ed = Q[(int32_t)(uint32_t)key[p]];
+      int x = tree_slot(node, nn, u[ed], false), y = tree_slot(node, nn, v[ed], false);
+      if (x < 0 || y < 0) continue;
+      // the unique tree path: climb from the deeper end until the ends meet;
+      // a removed edge on it means the ends are already separated
+      uint32_t path = 0;
+      while (x != y) {
+        int& w = dep[x] >= dep[y] ? x : y;
+        const int k = pe[w];
+        path |= 1u << k;
+        w = ea[k] == w ? eb[k] : ea[k];
+      }
+      if (!path || (path & rem)) continue;
       int best = -1;
       double bc = 0.0;
       int32_t bu = 0, bv = 0;
-      for (int x = sb; x != sa;) {
-        const int k = pe[x];
+      for (uint32_t bits = path; bits; bits &= bits - 1) {
+        const int k = __ffs(bits) - 1;
         const int32_t fe = P[Fi[fid[k]]];
         const double ck = c[fe];
         const int32_t uk = u[fe], vk = v[fe];
@@ -602,7 +617,6 @@ __global__ void k_tree_resolve(const int32_t* __restrict__ rptr, const uint64_t*
           bu = uk;
           bv = vk;
         }
-        x = ea[k] == x ? eb[k] : ea[k];
       }
       rem |= 1u << best;
       removed[fid[best]] = 1;
