@@ -831,8 +831,9 @@ void row_ptr_from_sorted(Ctx& ctx, const int32_t* u, int64_t m, int64_t n, int32
 // row < 0 are dropped (contraction's merged edges).  Plain atomics beat
 // warp aggregation with __match_any_sync here (C2: 1.23 -> 0.92 ms).
 __global__ void k_bucket_count(const int32_t* __restrict__ row, int64_t N, int32_t* __restrict__ cnt,
-                               int32_t* __restrict__ off) {
+                               int32_t* __restrict__ off, int32_t* __restrict__ zero2) {
   const int lane = threadIdx.x & 31;
+  if (zero2 && blockIdx.x == 0 && threadIdx.x < 2) zero2[threadIdx.x] = 0;  // the rank pass's list counters
   for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x - lane; i0 < N;
        i0 += (int64_t)gridDim.x * blockDim.x) {  // warp-uniform trip count
     const int64_t i = i0 + lane;
@@ -1050,8 +1051,12 @@ void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint6
   if (want_row) out.row.alloc(N > 0 ? N : 1, ctx.s);
   Buf<int32_t> cnt(R > 0 ? R : 1, ctx), off(N > 0 ? N : 1, ctx);
   cnt.zero();
+  Buf<int32_t> lists(2 * sort_rows + 2, ctx);  // big list | huge list | counters (zeroed by the count pass)
+  int32_t* big_list = lists.p;
+  int32_t* huge_list = lists.p + sort_rows;
+  int32_t* counters = lists.p + 2 * sort_rows;
   prof_set_bytes(8.0 * (double)N);
-  RAMA_KERNEL(ctx, k_bucket_count, N, row, N, cnt.p, off.p);
+  RAMA_KERNEL(ctx, k_bucket_count, N, row, N, cnt.p, off.p, counters);
   exclusive_scan(ctx, cnt.p, out.row_ptr.p, R, false);  // row_ptr[R] = kept items (row >= 0)
   if (R == 0 || N == 0) {
     out.total = 0;
@@ -1065,11 +1070,6 @@ void bucket_sort(Ctx& ctx, int64_t R, int64_t N, const int32_t* row, const uint6
   RAMA_KERNEL(ctx, k_bucket_scatter, N, row, key, off.p, N, out.row_ptr.p, items.p);
   off.release();
   cnt.release();
-  Buf<int32_t> lists(2 * sort_rows + 2, ctx);  // big list | huge list | counters
-  int32_t* big_list = lists.p;
-  int32_t* huge_list = lists.p + sort_rows;
-  int32_t* counters = lists.p + 2 * sort_rows;
-  RAMA_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(int32_t), ctx.s));
   prof_set_bytes(16.0 * (double)N + 12.0 * (double)N + (want_row ? 4.0 * (double)N : 0.0));
   RAMA_KERNEL(ctx, k_rank_rows, N, items.p, out.row_ptr.p, out.row_ptr.p + R, sort_rows, out.key.p, out.src.p,
               want_row ? out.row.p : (int32_t*)nullptr, big_list, huge_list, counters);

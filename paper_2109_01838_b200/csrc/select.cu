@@ -73,9 +73,12 @@ __global__ void k_match_vote(const int32_t* __restrict__ P, const int32_t* __res
   }
 }
 
+// (clear: the other vote buffer, zeroed here for the next round instead of
+// by a memset)
 __global__ void k_match_pair(int64_t n, const ulonglong2* __restrict__ vote, uint8_t* __restrict__ matched,
-                             int32_t* __restrict__ partner) {
+                             int32_t* __restrict__ partner, ulonglong2* __restrict__ clear) {
   GRID_STRIDE(x, n) {
+    if (clear) clear[x] = make_ulonglong2(0ULL, 0ULL);
     ulonglong2 vx = vote[x];
     if (vx.y == 0ULL) continue;
     int32_t t = (int32_t)(0xffffffffULL - vx.x);
@@ -117,10 +120,14 @@ int64_t select_matching(Ctx& ctx, const GraphView& g, int rounds, Buf<int32_t>& 
   Buf<ulonglong2> vote(n, ctx);
   Buf<int32_t> partner(n, ctx);
   partner.fill_bytes(0xff);
+  // votes alternate between two buffers; each pair pass clears the other
+  Buf<ulonglong2> vote1(rounds > 1 ? n : 1, ctx);
+  vote.zero();
   for (int r = 0; r < rounds; r++) {
-    vote.zero();
-    RAMA_KERNEL(ctx, k_match_vote, m, P.p, npd.p, g.u, g.v, g.c, matched.p, vote.p);
-    RAMA_KERNEL(ctx, k_match_pair, n, n, vote.p, matched.p, partner.p);
+    ulonglong2* cur = (r & 1) ? vote1.p : vote.p;
+    ulonglong2* nxt = r + 1 < rounds ? ((r & 1) ? vote.p : vote1.p) : nullptr;
+    RAMA_KERNEL(ctx, k_match_vote, m, P.p, npd.p, g.u, g.v, g.c, matched.p, cur);
+    RAMA_KERNEL(ctx, k_match_pair, n, n, cur, matched.p, partner.p, nxt);
   }
   Buf<uint8_t> lf(n, ctx);
   RAMA_KERNEL(ctx, k_flag_lower, n, partner.p, n, lf.p);

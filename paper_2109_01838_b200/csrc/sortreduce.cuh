@@ -223,7 +223,11 @@ static __global__ void k_sr_huge(const int32_t* __restrict__ rowptr, int64_t R, 
 // none), for t in [0, tiles]: row r owns the windows (rowptr[r-1], rowptr[r]]
 // (one parallel pass instead of two binary searches per tile)
 static __global__ void k_sr_tilemap(const int32_t* __restrict__ rowptr, int64_t R, int64_t tiles,
-                                    int32_t* __restrict__ tile_row) {
+                                    int32_t* __restrict__ tile_row, uint64_t* __restrict__ status,
+                                    int64_t* __restrict__ total) {
+  // the tiles' look-back words and the output counter start at zero (no memsets)
+  GRID_STRIDE(t, tiles + 1) status[t] = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *total = 0;
   GRID_STRIDE(r, R + 1) {
     const int64_t prev = r == 0 ? -1 : (int64_t)rowptr[r - 1];
     const int64_t cur = r == R ? (int64_t)tiles * kSrTile : (int64_t)rowptr[r];
@@ -469,8 +473,8 @@ int64_t sort_reduce(Ctx& ctx, int64_t R, int64_t N_max, const Src& src, const Em
   // it is also the number of rows in use (R bounds it; rows beyond are empty)
   res.rowptr.alloc(R + 1, ctx.s);
   res.total.alloc(1, ctx.s);
-  RAMA_CUDA(cudaMemsetAsync(res.total.p, 0, sizeof(int64_t), ctx.s));
   if (R == 0 || N_max == 0) {
+    RAMA_CUDA(cudaMemsetAsync(res.total.p, 0, sizeof(int64_t), ctx.s));
     RAMA_CUDA(cudaMemsetAsync(res.rowptr.p, 0, sizeof(int32_t) * (R + 1), ctx.s));
     if (want && extra_dev) *extra_out = read_scalar(ctx, extra_dev);
     return want ? 0 : -1;
@@ -518,11 +522,12 @@ int64_t sort_reduce(Ctx& ctx, int64_t R, int64_t N_max, const Src& src, const Em
   if (nh > 0) sr_sort_huge(ctx, res.rowptr.p, hlist.p, nh, items.p);
   const int64_t tiles = (N_max + kSrTile - 1) / kSrTile;
   Buf<uint64_t> status(tiles + 1, ctx);
-  RAMA_CUDA(cudaMemsetAsync(status.p, 0, sizeof(uint64_t) * (tiles + 1), ctx.s));
   Buf<int32_t> tile_row(tiles + 1, ctx);
   {
     KernelScope ks(ctx.s, "k_sr_tilemap", 4.0 * (double)R);
-    k_sr_tilemap<<<capped_grid(R + 1), kBlock, 0, ctx.s>>>(res.rowptr.p, R, tiles, tile_row.p);
+    k_sr_tilemap<<<capped_grid(std::max<int64_t>(R, tiles) + 1), kBlock, 0, ctx.s>>>(res.rowptr.p, R, tiles,
+                                                                                    tile_row.p, status.p,
+                                                                                    res.total.p);
   }
   RAMA_LAUNCH_CHECK();
   ctx.launches++;
