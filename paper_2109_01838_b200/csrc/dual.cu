@@ -149,13 +149,13 @@ struct PosCSR {
 static void positive_csr(Ctx& ctx, const GraphView& g, const Buf<int32_t>& P, int64_t np, PosCSR& out) {
   int64_t na = 2 * np;
   if (np > 0) {  // short rows: count, scatter, sort each row in registers
-    Buf<int32_t> cnt(g.n, ctx), off(na, ctx), flag(1, ctx);
+    Buf<int32_t> cnt(g.n + 1, ctx), off(na, ctx);  // counts | long-row flag: one memset
     cnt.zero();
-    flag.zero();
-    RAMA_KERNEL(ctx, k_pcsr_count, np, P.p, np, g.u, g.v, cnt.p, off.p, flag.p);
+    int32_t* flag = cnt.p + g.n;
+    RAMA_KERNEL(ctx, k_pcsr_count, np, P.p, np, g.u, g.v, cnt.p, off.p, flag);
     out.ptr.alloc(g.n + 1, ctx.s);
     exclusive_scan(ctx, cnt.p, out.ptr.p, g.n, false);
-    if (read_scalar(ctx, flag.p) == 0) {
+    if (read_scalar(ctx, flag) == 0) {
       out.adj.alloc(na, ctx.s);
       RAMA_KERNEL(ctx, k_pcsr_scatter, np, P.p, np, g.u, g.v, out.ptr.p, off.p, out.adj.p);
       RAMA_KERNEL(ctx, k_rowsort_i32, g.n, out.ptr.p, g.n, out.adj.p);
@@ -1658,8 +1658,11 @@ __global__ void k_tri_out_handles(const int32_t* __restrict__ heads, int64_t T, 
                                   const uint64_t* __restrict__ key, const int32_t* __restrict__ rptr,
                                   const int32_t* __restrict__ gv, const int32_t* __restrict__ crptr,
                                   const int32_t* __restrict__ cv, int64_t m, int32_t* __restrict__ tn,
-                                  int32_t* __restrict__ te) {
+                                  int32_t* __restrict__ te, double* __restrict__ lam) {
   GRID_STRIDE(t, T) {
+    lam[3 * t] = 0.0;  // the multipliers start at zero (no memset)
+    lam[3 * t + 1] = 0.0;
+    lam[3 * t + 2] = 0.0;
     const int32_t p = heads[t];
     const uint64_t k = key[p];
     const int32_t i = row[p], j = (int32_t)(k >> 32), l = (int32_t)(uint32_t)k;
@@ -1705,18 +1708,18 @@ __global__ void k_slot_scatter(const int32_t* __restrict__ te, int64_t S, const 
 
 void build_slot_lists(Ctx& ctx, DualState& st) {
   int64_t S = 3 * st.T;
-  st.coverage.alloc(st.m_aug > 0 ? st.m_aug : 1, ctx.s);
+  st.coverage.alloc(st.m_aug + 1, ctx.s);  // coverage | long-row flag: one memset
   st.slots.alloc(S > 0 ? S : 1, ctx.s);
   st.long_e.release();
   st.n_long.release();
   st.coverage.zero();
   {
-    Buf<int32_t> off(S > 0 ? S : 1, ctx), flag(1, ctx);
-    flag.zero();
-    RAMA_KERNEL(ctx, k_slot_count, S, st.tri_edges.p, S, st.coverage.p, off.p, flag.p);
+    Buf<int32_t> off(S > 0 ? S : 1, ctx);
+    int32_t* flag = st.coverage.p + st.m_aug;
+    RAMA_KERNEL(ctx, k_slot_count, S, st.tri_edges.p, S, st.coverage.p, off.p, flag);
     st.slot_ptr.alloc(st.m_aug + 1, ctx.s);
     exclusive_scan(ctx, st.coverage.p, st.slot_ptr.p, st.m_aug, false);
-    if (read_scalar(ctx, flag.p) == 0) {
+    if (read_scalar(ctx, flag) == 0) {
       RAMA_KERNEL(ctx, k_slot_scatter, S, st.tri_edges.p, S, st.slot_ptr.p, off.p, st.slots.p);
       RAMA_KERNEL(ctx, k_rowsort_i32, st.m_aug, st.slot_ptr.p, st.m_aug, st.slots.p);
       return;
@@ -1786,18 +1789,18 @@ void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& 
   row_ptr_from_sorted(ctx, st.eu.p + m, C, n, st.chord_ptr.p);
 
   // triplets: handles
+  st.lam.alloc(T > 0 ? 3 * T : 1, ctx.s);
   if (T > 0) {
     st.tri_nodes.alloc(3 * T, ctx.s);
     st.tri_edges.alloc(3 * T, ctx.s);
     RAMA_KERNEL(ctx, k_tri_out_handles, T, ht.p, T, bs.row.p, bs.key.p, rptr_p, g.v, st.chord_ptr.p, st.ev.p + m, m,
-                st.tri_nodes.p, st.tri_edges.p);
+                st.tri_nodes.p, st.tri_edges.p, st.lam.p);
   } else {
     st.tri_nodes.alloc(1, ctx.s);
     st.tri_edges.alloc(1, ctx.s);
+    st.lam.zero();
   }
   st.T = T;
-  st.lam.alloc(T > 0 ? 3 * T : 1, ctx.s);
-  st.lam.zero();
   build_slot_lists(ctx, st);
   // algorithmic bytes: cycle rows read (4 + 4 L), the
   // originals' (u, v) read for the handles (8 m), augmented edges written
