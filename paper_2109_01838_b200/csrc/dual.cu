@@ -1602,6 +1602,27 @@ struct TripletHead {
   }
 };
 
+// kind of each sorted item: 1 first of a run of equal triplets, 2 first of
+// a run of equal chords that is not an edge of g, 0 otherwise (one thread
+// per item, so the graph-row searches overlap at full occupancy)
+__global__ void k_tri_kinds(const int32_t* __restrict__ row, const uint64_t* __restrict__ key, int64_t N,
+                            const int32_t* __restrict__ rptr, const int32_t* __restrict__ gv,
+                            uint8_t* __restrict__ kind) {
+  GRID_STRIDE(p, N) {
+    const uint64_t k = key[p];
+    const int32_t r = row[p];
+    uint8_t out = 0;
+    if (p == 0 || row[p - 1] != r || key[p - 1] != k)
+      out = !(k & kChordTag) ? 1 : (find_in_row(rptr, gv, r, (int32_t)(uint32_t)k) < 0 ? 2 : 0);
+    kind[p] = out;
+  }
+}
+struct KindIs {
+  const uint8_t* kind;
+  uint8_t want;
+  __device__ __forceinline__ bool operator()(int32_t p) const { return kind[p] == want; }
+};
+
 __global__ void k_chord_new(const int32_t* __restrict__ heads, int64_t nh, const int32_t* __restrict__ row,
                             const uint64_t* __restrict__ key, const int32_t* __restrict__ rptr,
                             const int32_t* __restrict__ gv, uint8_t* __restrict__ is_new) {
@@ -1773,8 +1794,9 @@ void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& 
   Buf<int32_t> hc, ht;
   if (N > 0) {
     bucket_sort(ctx, n, N, irow.p, ikey.p, bs, true);
-    partition2(ctx, bs.total, NewChordHeadTagged{bs.row.p, bs.key.p, rptr_p, g.v}, TripletHead{bs.row.p, bs.key.p},
-               hc, ht, C, T);
+    Buf<uint8_t> kind(bs.total > 0 ? bs.total : 1, ctx);
+    RAMA_KERNEL(ctx, k_tri_kinds, bs.total, bs.row.p, bs.key.p, bs.total, rptr_p, g.v, kind.p);
+    partition2(ctx, bs.total, KindIs{kind.p, 2}, KindIs{kind.p, 1}, hc, ht, C, T);
   }
   irow.release();
   ikey.release();
