@@ -1690,9 +1690,29 @@ __global__ void k_tri_out_handles(const int32_t* __restrict__ heads, int64_t T, 
     tn[3 * t] = i;
     tn[3 * t + 1] = j;
     tn[3 * t + 2] = l;
-    te[3 * t] = edge_handle(rptr, gv, crptr, cv, m, i, j);
-    te[3 * t + 1] = edge_handle(rptr, gv, crptr, cv, m, i, l);
-    te[3 * t + 2] = edge_handle(rptr, gv, crptr, cv, m, j, l);
+    // the three edges' searches in the graph's rows run interleaved (ILP);
+    // an edge not in g is a chord (present by construction)
+    const int32_t ra[3] = {i, i, j}, rb[3] = {j, l, l};
+    int32_t lo[3], hi[3], end[3];
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+      lo[q] = rptr[ra[q]];
+      end[q] = hi[q] = rptr[ra[q] + 1];
+    }
+    while (lo[0] < hi[0] || lo[1] < hi[1] || lo[2] < hi[2]) {
+#pragma unroll
+      for (int q = 0; q < 3; q++) {
+        if (lo[q] < hi[q]) {
+          const int32_t mid = (lo[q] + hi[q]) >> 1;
+          if (gv[mid] < rb[q]) lo[q] = mid + 1;
+          else hi[q] = mid;
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 3; q++)
+      te[3 * t + q] = lo[q] < end[q] && gv[lo[q]] == rb[q] ? lo[q]
+                                                          : (int32_t)(m + find_in_row(crptr, cv, ra[q], rb[q]));
   }
 }
 

@@ -563,14 +563,18 @@ __global__ void k_tree_resolve(const int32_t* __restrict__ rptr, const uint64_t*
     if (e - b < 2 || (key[e - 1] >> 32) == 0) continue;  // no edge or no query
     int32_t node[kSmallTree];
     int8_t ea[kSmallTree], eb[kSmallTree];
-    int32_t fid[kSmallTree];
+    int32_t fid[kSmallTree], fu[kSmallTree], fv[kSmallTree];
+    double fc[kSmallTree];
     int nn = 0, ne = 0;
     int32_t p = b;
     for (; p < e && (key[p] >> 32) == 0; p++) {
       const int32_t i = (int32_t)(uint32_t)key[p];
       const int32_t ed = P[Fi[i]];
-      ea[ne] = (int8_t)tree_slot(node, nn, u[ed], true);
-      eb[ne] = (int8_t)tree_slot(node, nn, v[ed], true);
+      fu[ne] = u[ed];
+      fv[ne] = v[ed];
+      fc[ne] = c[ed];
+      ea[ne] = (int8_t)tree_slot(node, nn, fu[ne], true);
+      eb[ne] = (int8_t)tree_slot(node, nn, fv[ne], true);
       fid[ne] = i;
       ne++;
     }
@@ -615,9 +619,8 @@ __global__ void k_tree_resolve(const int32_t* __restrict__ rptr, const uint64_t*
       int32_t bu = 0, bv = 0;
       for (uint32_t bits = path; bits; bits &= bits - 1) {
         const int k = __ffs(bits) - 1;
-        const int32_t fe = P[Fi[fid[k]]];
-        const double ck = c[fe];
-        const int32_t uk = u[fe], vk = v[fe];
+        const double ck = fc[k];
+        const int32_t uk = fu[k], vk = fv[k];
         if (best < 0 || ck < bc || (ck == bc && (uk < bu || (uk == bu && vk < bv)))) {
           best = k;
           bc = ck;
