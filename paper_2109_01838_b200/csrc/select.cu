@@ -649,6 +649,61 @@ __global__ void k_gather_pairs(const int32_t* __restrict__ idx, int64_t k, const
   }
 }
 
+// All Boruvka iterations in one cooperative launch (reset, vote, hook,
+// flatten with grid barriers; stop when no edge crosses components) instead
+// of 2 memsets, 3 launches and a read-back per iteration.  any2: two
+// alternating "an edge crossed" flags (zero on entry); iters: iterations run.
+__global__ void __launch_bounds__(kBlock) k_boruvka_coop(const int32_t* __restrict__ P, int64_t np,
+                                                         const int32_t* __restrict__ u, const int32_t* __restrict__ v,
+                                                         const int32_t* __restrict__ rank,
+                                                         const int32_t* __restrict__ order, int32_t* comp,
+                                                         uint32_t* best, uint8_t* __restrict__ in_forest, int64_t n,
+                                                         int32_t* any2, int32_t* iters) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, GT = (int64_t)gridDim.x * blockDim.x;
+  for (int it = 0;; it++) {
+    for (int64_t x = gtid; x < n; x += GT) best[x] = 0xffffffffu;
+    if (gtid == 0) any2[(it + 1) & 1] = 0;  // the next iteration's flag (this one's was cleared before)
+    grid.sync();
+    bool crossed = false;
+    for (int64_t i = gtid; i < np; i += GT) {
+      const int32_t e = P[i];
+      const int32_t a = sf_find(comp, u[e]), b = sf_find(comp, v[e]);
+      if (a == b) continue;
+      const uint32_t r = (uint32_t)rank[i];
+      atomicMin(best + a, r);
+      atomicMin(best + b, r);
+      crossed = true;
+    }
+    if (__any_sync(0xffffffffu, crossed) && (threadIdx.x & 31) == 0) any2[it & 1] = 1;
+    grid.sync();
+    if (__ldcg(any2 + (it & 1)) == 0) {  // uniform: read after the barrier
+      if (gtid == 0) *iters = it + 1;
+      break;
+    }
+    for (int64_t x = gtid; x < n; x += GT) {
+      const uint32_t r = __ldcg(best + x);
+      if (r == 0xffffffffu) continue;
+      const int32_t pi = order[r];
+      in_forest[pi] = 1;
+      const int32_t e = P[pi];
+      sf_union(comp, u[e], v[e]);
+    }
+    grid.sync();
+    for (int64_t x = gtid; x < n; x += GT) {
+      int32_t r = (int32_t)x;
+      while (true) {
+        const int32_t p = __ldcg(comp + r);
+        if (p == r) break;
+        r = p;
+      }
+      comp[x] = r;
+    }
+    grid.sync();
+  }
+}
+
 int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_t>& sv) {
   int64_t n = g.n, m = g.m;
   // algorithmic bytes: the graph read once, the selected pairs written
@@ -685,14 +740,28 @@ int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_
   Buf<uint8_t> in_forest(np, ctx);
   in_forest.zero();
   iota(ctx, comp.p, n);
-  while (true) {
-    best.fill_bytes(0xff);
-    any.zero();
-    RAMA_KERNEL(ctx, k_bv_vote, np, P.p, np, g.u, g.v, rank.p, comp.p, best.p, any.p);
-    bv_iters++;
-    if (read_scalar(ctx, any.p) == 0) break;
-    RAMA_KERNEL(ctx, k_bv_hook, n, n, best.p, order.p, P.p, g.u, g.v, comp.p, in_forest.p);
-    RAMA_KERNEL(ctx, k_flatten, n, comp.p, n);
+  static const bool bv_launches = getenv("RAMA_BORUVKA_LAUNCHES") != nullptr;  // A/B: one launch set per iteration
+  if (bv_launches) {
+    while (true) {
+      best.fill_bytes(0xff);
+      any.zero();
+      RAMA_KERNEL(ctx, k_bv_vote, np, P.p, np, g.u, g.v, rank.p, comp.p, best.p, any.p);
+      bv_iters++;
+      if (read_scalar(ctx, any.p) == 0) break;
+      RAMA_KERNEL(ctx, k_bv_hook, n, n, best.p, order.p, P.p, g.u, g.v, comp.p, in_forest.p);
+      RAMA_KERNEL(ctx, k_flatten, n, comp.p, n);
+    }
+  } else {
+    Buf<int32_t> flags(3, ctx);  // any2 | iterations
+    flags.zero();
+    const int32_t *pP = P.p, *pu = g.u, *pv = g.v, *prank = rank.p, *porder = order.p;
+    int32_t *pcomp = comp.p, *pany = flags.p, *piters = flags.p + 2;
+    uint32_t* pbest = best.p;
+    uint8_t* pin = in_forest.p;
+    int64_t np_ = np, n_ = n;
+    void* args[] = {&pP, &np_, &pu, &pv, &prank, &porder, &pcomp, &pbest, &pin, &n_, &pany, &piters};
+    launch_coop(ctx, (const void*)k_boruvka_coop, "k_boruvka_coop", args, std::max<int64_t>(n, np));
+    if (phase_prof) bv_iters = read_scalar(ctx, piters);
   }
   RAMA_KERNEL(ctx, k_flatten, n, comp.p, n);
 
