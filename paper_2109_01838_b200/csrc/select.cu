@@ -520,10 +520,10 @@ __global__ void k_mark_removed(const int32_t* __restrict__ qe, const uint8_t* __
 // (contraction.py:231-284) runs as written, per tree: a repulsive edge only
 // meets removals inside its own tree, so each tree's queries in ascending
 // (u, v) order are independent of every other tree's.  A thread holds its
-// tree (<= 32 nodes, <= 31 edges) in registers / local memory, roots it
-// once, walks each query's unique path up to the meeting node (a removed
-// edge on it: already separated, as the reference's BFS finds) and cuts
-// the path's cheapest edge (ties: smallest (u, v)).  This
+// tree (<= 32 nodes, <= 31 edges) in local memory, roots it once, walks
+// each query's unique path up to the meeting node (a removed edge on it:
+// already separated, as the reference's BFS finds) and cuts the path's
+// cheapest edge (ties: smallest (u, v)).  This
 // replaces the Euler tour, the lifting tables and the dependency passes of
 // the general path (~40 launches and ~6 read-backs per forest round).
 constexpr int kSmallTree = 32;
@@ -558,9 +558,17 @@ __global__ void k_tree_resolve(const int32_t* __restrict__ rptr, const uint64_t*
                                const int32_t* __restrict__ Q, const int32_t* __restrict__ u,
                                const int32_t* __restrict__ v, const double* __restrict__ c,
                                uint8_t* __restrict__ removed) {
-  GRID_STRIDE(r, R) {
+  // one warp per tree: every lane builds the same rooted tree (broadcast
+  // loads), the lanes take 32 queries at a time and find their paths and
+  // cheapest edges in parallel -- both depend on the tree alone -- then the
+  // warp applies them in query order: a query whose path meets an edge
+  // already cut is separated, otherwise its cheapest edge is cut
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t W = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp0; r < R; r += W) {
     const int32_t b = rptr[r], e = rptr[r + 1];
-    if (e - b < 2 || (key[e - 1] >> 32) == 0) continue;  // no edge or no query
+    if (e - b < 2 || (key[e - 1] >> 32) == 0) continue;  // no edge or no query (warp-uniform)
     int32_t node[kSmallTree];
     int8_t ea[kSmallTree], eb[kSmallTree];
     int32_t fid[kSmallTree], fu[kSmallTree], fv[kSmallTree];
@@ -599,37 +607,43 @@ __global__ void k_tree_resolve(const int32_t* __restrict__ rptr, const uint64_t*
         }
       }
     }
-    uint32_t rem = 0;  // removed tree edges
-    for (; p < e; p++) {
-      const int32_t ed = Q[(int32_t)(uint32_t)key[p]];
-      int x = tree_slot(node, nn, u[ed], false), y = tree_slot(node, nn, v[ed], false);
-      if (x < 0 || y < 0) continue;
-      // the unique tree path: climb from the deeper end until the ends meet;
-      // a removed edge on it means the ends are already separated
+    uint32_t rem = 0;  // removed tree edges (identical in every lane)
+    for (int32_t p0 = p; p0 < e; p0 += 32) {
       uint32_t path = 0;
-      while (x != y) {
-        int& w = dep[x] >= dep[y] ? x : y;
-        const int k = pe[w];
-        path |= 1u << k;
-        w = ea[k] == w ? eb[k] : ea[k];
-      }
-      if (!path || (path & rem)) continue;
       int best = -1;
-      double bc = 0.0;
-      int32_t bu = 0, bv = 0;
-      for (uint32_t bits = path; bits; bits &= bits - 1) {
-        const int k = __ffs(bits) - 1;
-        const double ck = fc[k];
-        const int32_t uk = fu[k], vk = fv[k];
-        if (best < 0 || ck < bc || (ck == bc && (uk < bu || (uk == bu && vk < bv)))) {
-          best = k;
-          bc = ck;
-          bu = uk;
-          bv = vk;
+      if (p0 + lane < e) {
+        const int32_t ed = Q[(int32_t)(uint32_t)key[p0 + lane]];
+        int x = tree_slot(node, nn, u[ed], false), y = tree_slot(node, nn, v[ed], false);
+        // the unique tree path: climb from the deeper end until the ends meet
+        while (x >= 0 && y >= 0 && x != y) {
+          int& w = dep[x] >= dep[y] ? x : y;
+          const int k = pe[w];
+          path |= 1u << k;
+          w = ea[k] == w ? eb[k] : ea[k];
+        }
+        double bc = 0.0;
+        int32_t bu = 0, bv = 0;
+        for (uint32_t bits = path; bits; bits &= bits - 1) {
+          const int k = __ffs(bits) - 1;
+          const double ck = fc[k];
+          const int32_t uk = fu[k], vk = fv[k];
+          if (best < 0 || ck < bc || (ck == bc && (uk < bu || (uk == bu && vk < bv)))) {
+            best = k;
+            bc = ck;
+            bu = uk;
+            bv = vk;
+          }
         }
       }
-      rem |= 1u << best;
-      removed[fid[best]] = 1;
+      const int cnt = min(32, e - p0);
+      for (int j = 0; j < cnt; j++) {  // in query order
+        const uint32_t pj = __shfl_sync(0xffffffffu, path, j);
+        const int bj = __shfl_sync(0xffffffffu, best, j);
+        if (pj && !(pj & rem)) {
+          rem |= 1u << bj;
+          if (lane == 0) removed[fid[bj]] = 1;
+        }
+      }
     }
   }
 }
@@ -803,7 +817,8 @@ int64_t select_forest(Ctx& ctx, const GraphView& g, Buf<int32_t>& su, Buf<int32_
       RAMA_KERNEL(ctx, k_tree_items, ni, Fi.p, kf, Q.p, nq, P.p, g.u, loc.p, comp_loc.p, irow.p, ikey.p);
       BucketSorted ts;
       bucket_sort(ctx, nf, ni, irow.p, ikey.p, ts, false);
-      RAMA_KERNEL(ctx, k_tree_resolve, nf, ts.row_ptr.p, ts.key.p, nf, Fi.p, P.p, Q.p, g.u, g.v, g.c, removed.p);
+      RAMA_KERNEL(ctx, k_tree_resolve, 32 * nf, ts.row_ptr.p, ts.key.p, nf, Fi.p, P.p, Q.p, g.u, g.v, g.c,
+                  removed.p);  // a warp per tree
       mark(4);
       if (phase_prof)
         fprintf(stderr, "[rama]   forest n %lld m+ %lld kf %lld conflicts %lld trees <= %lld nodes: rank sort %.2f "
