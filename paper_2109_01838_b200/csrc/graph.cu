@@ -242,15 +242,21 @@ __global__ void k_joined_mass(const int32_t* __restrict__ u, const int32_t* __re
 // exactly the reduceat order of contraction.py:142-163 -- then marks the
 // heads of equal keys, compacts them, and sums each group in numpy's
 // pairwise order from the gathered costs.
-__global__ void k_crx_keys(const int32_t* __restrict__ u, const int32_t* __restrict__ v,
-                           const int32_t* __restrict__ f, int64_t m, int bits, uint64_t* __restrict__ key,
-                           int32_t* __restrict__ val) {
-  const uint64_t sentinel = (1ull << (2 * bits)) - 1ull;  // self-loops sort last
-  GRID_STRIDE(i, m) {
+// self-loops (both ends in one target) are dropped before the sort: a flag
+// per edge, a stable compaction, then (key, source index) of the kept edges
+__global__ void k_crx_flags(const int32_t* __restrict__ u, const int32_t* __restrict__ v,
+                            const int32_t* __restrict__ f, int64_t m, uint8_t* __restrict__ cross) {
+  GRID_STRIDE(i, m) cross[i] = __ldg(f + u[i]) != __ldg(f + v[i]);
+}
+
+__global__ void k_crx_keys_of(const int32_t* __restrict__ E, int64_t N, const int32_t* __restrict__ u,
+                              const int32_t* __restrict__ v, const int32_t* __restrict__ f, int bits,
+                              uint64_t* __restrict__ key, int32_t* __restrict__ val) {
+  GRID_STRIDE(t, N) {
+    const int32_t i = E[t];
     const int32_t a = __ldg(f + u[i]), b = __ldg(f + v[i]);
-    key[i] = a == b ? sentinel
-                    : ((uint64_t)(uint32_t)(a < b ? a : b) << bits) | (uint64_t)(uint32_t)(a < b ? b : a);
-    val[i] = (int32_t)i;
+    key[t] = ((uint64_t)(uint32_t)(a < b ? a : b) << bits) | (uint64_t)(uint32_t)(a < b ? b : a);
+    val[t] = i;
   }
 }
 
@@ -293,18 +299,26 @@ static Graph contract_radix(Ctx& ctx, const GraphView& g, const int32_t* map, in
   const int64_t m = g.m;
   int bits = 1;
   while ((1ll << bits) <= n_targets) bits++;  // ids <= n_targets - 1 < 2^bits - 1
-  Buf<uint64_t> k1(m, ctx), k2(m, ctx);
-  Buf<int32_t> v1(m, ctx), v2(m, ctx);
-  RAMA_KERNEL(ctx, k_crx_keys, m, g.u, g.v, map, m, bits, k1.p, v1.p);
-  radix_sort_pairs(ctx, k1.p, v1.p, k2.p, v2.p, m, 0, 2 * bits);
+  int64_t N = m;  // edges into the sort
+  Buf<int32_t> E;
+  {
+    Buf<uint8_t> cross(m, ctx);
+    RAMA_KERNEL(ctx, k_crx_flags, m, g.u, g.v, map, m, cross.p);
+    N = compact_indices(ctx, cross.p, m, E);  // ascending: the source order is kept
+  }
+  Buf<uint64_t> k1(N > 0 ? N : 1, ctx), k2(N > 0 ? N : 1, ctx);
+  Buf<int32_t> v1(N > 0 ? N : 1, ctx), v2(N > 0 ? N : 1, ctx);
+  RAMA_KERNEL(ctx, k_crx_keys_of, N, E.p, N, g.u, g.v, map, bits, k1.p, v1.p);
+  E.release();
+  radix_sort_pairs(ctx, k1.p, v1.p, k2.p, v2.p, N, 0, 2 * bits);
   k1.release();
   v1.release();
-  Buf<uint8_t> head(m, ctx);
+  Buf<uint8_t> head(N > 0 ? N : 1, ctx);
   Buf<int32_t> nvalid(1, ctx);
   nvalid.zero();
-  RAMA_KERNEL(ctx, k_crx_heads, m, k2.p, m, bits, head.p, nvalid.p);
+  RAMA_KERNEL(ctx, k_crx_heads, N, k2.p, N, bits, head.p, nvalid.p);
   Buf<int32_t> H;
-  const int64_t M = compact_indices(ctx, head.p, m, H);
+  const int64_t M = compact_indices(ctx, head.p, N, H);
   Graph out;
   out.n = nt_dev ? (int64_t)read_scalar(ctx, nt_dev) : n_targets;  // (forced radix on a round contraction)
   out.m = M;
