@@ -2184,15 +2184,48 @@ void message_passing(Ctx& ctx, DualState& st, int iters) {
   }
 }
 
+// merge position of originals [0, m) and chords [m, m_aug) (both sorted):
+// the count of the other list's keys below (a, b) is that list's row start
+// plus a search inside its (short) row a
+__device__ __forceinline__ int32_t row_lower(const int32_t* ptr, const int32_t* col, int32_t a, int32_t b) {
+  int32_t lo = ptr[a], hi = ptr[a + 1];
+  while (lo < hi) {
+    int32_t mid = (lo + hi) >> 1;
+    if (col[mid] < b) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// the reparametrized graph written directly by the bound's edge pass: c^lambda
+// of augmented edge e goes to its merged canonical position (k_merge_scatter)
+struct MergeOut {
+  int32_t* ou = nullptr;
+  int32_t* ov = nullptr;
+  double* oc = nullptr;
+  const int32_t* eu = nullptr;
+  const int32_t* ev = nullptr;
+  const int32_t* optr = nullptr;
+  const int32_t* cptr = nullptr;
+  int64_t m = 0;  // originals [0, m), chords after
+  __device__ __forceinline__ void put(int64_t i, double x) const {
+    const int32_t a = eu[i], b = ev[i];
+    const int64_t pos = i < m ? i + row_lower(cptr, ev + m, a, b) : (i - m) + row_lower(optr, ev, a, b);
+    ou[pos] = a;
+    ov[pos] = b;
+    oc[pos] = x;
+  }
+};
+
 __global__ void k_reparam(int64_t m, const double* __restrict__ base, const int32_t* __restrict__ ptr,
                           const int32_t* __restrict__ slots, const double* __restrict__ lam,
-                          double* __restrict__ cl, double* __restrict__ negpart, int32_t long_cov) {
+                          double* __restrict__ cl, double* __restrict__ negpart, int32_t long_cov, MergeOut mo) {
   GRID_STRIDE(e, m) {
     if (ptr != nullptr && ptr[e + 1] - ptr[e] > long_cov) continue;  // k_reparam_long
     int32_t cov;
     double acc = (ptr != nullptr) ? edge_sum(ptr, slots, lam, e, &cov) : 0.0;
     double x = __dadd_rn(base[e], acc);
     if (cl) cl[e] = x;
+    if (mo.ou) mo.put(e, x);
     if (negpart) negpart[e] = mn2(x, 0.0);
   }
 }
@@ -2200,7 +2233,7 @@ __global__ void k_reparam(int64_t m, const double* __restrict__ base, const int3
 __global__ void k_reparam_long(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
                                const double* __restrict__ base, const int32_t* __restrict__ ptr,
                                const int32_t* __restrict__ slots, const double* __restrict__ lam,
-                               double* __restrict__ cl, double* __restrict__ negpart) {
+                               double* __restrict__ cl, double* __restrict__ negpart, MergeOut mo) {
   const int32_t nl = *count;
   const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t W = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -2210,19 +2243,20 @@ __global__ void k_reparam_long(const int32_t* __restrict__ list, const int32_t* 
     const double x = __dadd_rn(base[e], warp_edge_sum(ptr, slots, lam, e, cov));
     if ((threadIdx.x & 31) == 0) {
       if (cl) cl[e] = x;
+      if (mo.ou) mo.put(e, x);
       if (negpart) negpart[e] = mn2(x, 0.0);
     }
   }
 }
 
 // c^lambda (and its negative part): short slot lists a thread per edge, hub lists a warp per edge
-static void reparam_pass(Ctx& ctx, const DualState& st, double* cl, double* neg) {
+static void reparam_pass(Ctx& ctx, const DualState& st, double* cl, double* neg, const MergeOut& mo = MergeOut{}) {
   RAMA_KERNEL(ctx, k_reparam, st.m_aug, st.m_aug, st.base.p, st.T ? st.slot_ptr.p : (const int32_t*)nullptr,
-              st.slots.p, st.lam.p, cl, neg, st.n_long.p ? kLongCov : INT32_MAX);
+              st.slots.p, st.lam.p, cl, neg, st.n_long.p ? kLongCov : INT32_MAX, mo);
   if (st.T && st.n_long.p) {
     KernelScope ks(ctx.s, "k_reparam_long", 0.0);
     k_reparam_long<<<(unsigned)num_sms() * 8, kBlock, 0, ctx.s>>>(st.long_e.p, st.n_long.p, st.base.p,
-                                                                  st.slot_ptr.p, st.slots.p, st.lam.p, cl, neg);
+                                                                  st.slot_ptr.p, st.slots.p, st.lam.p, cl, neg, mo);
     RAMA_LAUNCH_CHECK();
     ctx.launches++;
   }
@@ -2253,10 +2287,10 @@ __global__ void k_lb_total(const double* __restrict__ sn, const double* __restri
   *out = total;
 }
 
-void lower_bound_to(Ctx& ctx, const DualState& st, double* cl_out, double* out) {
-  ProfScope prof(ctx.s, kFamBound, 36.0 * (double)st.T + 20.0 * (double)st.m_aug);
+static void lower_bound_to_impl(Ctx& ctx, const DualState& st, double* cl_out, double* out, const MergeOut& mo) {
   Buf<double> neg(st.m_aug > 0 ? st.m_aug : 1, ctx), tm(st.T > 0 ? st.T : 1, ctx), sums(2, ctx);
-  lower_bound_terms(ctx, st, cl_out, neg.p, tm.p);
+  reparam_pass(ctx, st, cl_out, neg.p, mo);
+  RAMA_KERNEL(ctx, k_tri_min, st.T, st.T, st.lam.p, tm.p);
   if (st.m_aug > 0) device_sum_to(ctx, neg.p, st.m_aug, sums.p);
   if (st.T > 0) device_sum_to(ctx, tm.p, st.T, sums.p + 1);
   {
@@ -2265,6 +2299,38 @@ void lower_bound_to(Ctx& ctx, const DualState& st, double* cl_out, double* out) 
   }
   RAMA_LAUNCH_CHECK();
   ctx.launches++;
+}
+
+void lower_bound_to(Ctx& ctx, const DualState& st, double* cl_out, double* out) {
+  ProfScope prof(ctx.s, kFamBound, 36.0 * (double)st.T + 20.0 * (double)st.m_aug);
+  lower_bound_to_impl(ctx, st, cl_out, out, MergeOut{});
+}
+
+Graph bound_and_reparametrized(Ctx& ctx, const DualState& st, double* lb_out) {
+  if (st.m_aug == 0 || !st.chords_sorted || !st.orig_ptr.p || !st.chord_ptr.p) {
+    Buf<double> cl(st.m_aug > 0 ? st.m_aug : 1, ctx);
+    lower_bound_to(ctx, st, cl.p, lb_out);
+    return reparametrized_graph(ctx, st, cl.p);
+  }
+  // bound terms + the merged canonical graph in the same edge pass
+  ProfScope prof(ctx.s, kFamBound, 36.0 * (double)st.T + 20.0 * (double)st.m_aug + 32.0 * (double)st.m_aug);
+  Graph g;
+  g.n = st.n;
+  g.m = st.m_aug;
+  g.u.alloc(st.m_aug, ctx.s);
+  g.v.alloc(st.m_aug, ctx.s);
+  g.c.alloc(st.m_aug, ctx.s);
+  MergeOut mo;
+  mo.ou = g.u.p;
+  mo.ov = g.v.p;
+  mo.oc = g.c.p;
+  mo.eu = st.eu.p;
+  mo.ev = st.ev.p;
+  mo.optr = st.orig_ptr.p;
+  mo.cptr = st.chord_ptr.p;
+  mo.m = st.m_orig;
+  lower_bound_to_impl(ctx, st, nullptr, lb_out, mo);
+  return g;
 }
 
 double lower_bound(Ctx& ctx, const DualState& st, double* cl_out) {
@@ -2384,18 +2450,6 @@ bool check_edge_triangle_agreement(Ctx& ctx, const DualState& st, double eps) {
 }
 
 // --------------------------------------------------- reparametrized graph
-
-// merge position of originals [0, m) and chords [m, m_aug) (both sorted):
-// the count of the other list's keys below (a, b) is that list's row start
-// plus a search inside its (short) row a
-__device__ __forceinline__ int32_t row_lower(const int32_t* ptr, const int32_t* col, int32_t a, int32_t b) {
-  int32_t lo = ptr[a], hi = ptr[a + 1];
-  while (lo < hi) {
-    int32_t mid = (lo + hi) >> 1;
-    if (col[mid] < b) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
 
 __global__ void k_merge_scatter(int64_t m, int64_t C, const int32_t* __restrict__ eu, const int32_t* __restrict__ ev,
                                 const double* __restrict__ cl, const int32_t* __restrict__ optr,

@@ -132,6 +132,9 @@ void lower_bound_to(Ctx& ctx, const DualState& st, double* cl_out, double* out);
 // a12 reparametrized_graph (dual.py:408-411): canonical merge of originals
 // and chords carrying c^lambda
 Graph reparametrized_graph(Ctx& ctx, const DualState& st, const double* cl = nullptr);
+// lower_bound_to + reparametrized_graph with one pass over the augmented
+// edges (c^lambda goes straight to the merged graph)
+Graph bound_and_reparametrized(Ctx& ctx, const DualState& st, double* lb_out);
 // edge -> slot CSR + coverage for an existing tri_edges array
 void build_slot_lists(Ctx& ctx, DualState& st);
 

@@ -144,11 +144,11 @@ void solve(Ctx& ctx, const GraphView& g, const SolveConfig& cfg, int32_t* labels
       triangulate(ctx, cur.view(), cyc, st);
       mark(1);
       message_passing(ctx, st, cfg.mp_iterations);
-      Buf<double> cl(st.m_aug > 0 ? st.m_aug : 1, ctx);
-      lower_bound_to(ctx, st, cl.p, d_lb.p);  // c^lambda computed once for the bound and the graph
+      // c^lambda computed once: the bound's terms and the reparametrized
+      // graph (written at its merged canonical positions) in one edge pass
+      Graph rep = bound_and_reparametrized(ctx, st, d_lb.p);
       T = st.T;
       mark(2);
-      Graph rep = reparametrized_graph(ctx, st, cl.p);
       mark(3);
       ctx.piggy = d_lb.p;  // the bound returns with the contraction's first read-back
       ctx.piggy_done = false;
