@@ -1777,7 +1777,7 @@ void build_slot_lists(Ctx& ctx, DualState& st) {
   if (bs.big_rows > 0) compact_if_dev(ctx, st.m_aug, LongCov{st.slot_ptr.p}, st.long_e, st.n_long);
 }
 
-void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& st) {
+void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& st, Graph* steal) {
   ProfScope prof(ctx.s, kFamTriangulate);
   int64_t rows = cyc.rows, m = g.m, n = g.n;
   st.n = n;
@@ -1804,12 +1804,23 @@ void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& 
   row_ptr_from_sorted(ctx, g.u, m, n, rptr_p);
   int64_t C = 0, T = 0;
   Buf<uint64_t> ckeys(1, ctx);
-  st.eu.alloc(m + craw > 0 ? m + craw : 1, ctx.s);
-  st.ev.alloc(m + craw > 0 ? m + craw : 1, ctx.s);
-  st.base.alloc(m + craw > 0 ? m + craw : 1, ctx.s);
-  copy_d2d(ctx, st.eu.p, g.u, m);
-  copy_d2d(ctx, st.ev.p, g.v, m);
-  copy_d2d(ctx, st.base.p, g.c, m);
+  const size_t cap = (size_t)(m + craw > 0 ? m + craw : 1);
+  if (steal && steal->u.p == g.u && steal->v.p == g.v && steal->c.p == g.c && steal->u.n >= cap &&
+      steal->v.n >= cap && steal->c.n >= cap) {
+    // the caller's graph has room for the chords after its edges (a
+    // contraction's output is sized by its input): take its buffers
+    // instead of copying the m edges (g's pointers stay valid: same memory)
+    st.eu = std::move(steal->u);
+    st.ev = std::move(steal->v);
+    st.base = std::move(steal->c);
+  } else {
+    st.eu.alloc(cap, ctx.s);
+    st.ev.alloc(cap, ctx.s);
+    st.base.alloc(cap, ctx.s);
+    copy_d2d(ctx, st.eu.p, g.u, m);
+    copy_d2d(ctx, st.ev.p, g.v, m);
+    copy_d2d(ctx, st.base.p, g.c, m);
+  }
   BucketSorted bs;
   Buf<int32_t> hc, ht;
   if (N > 0) {

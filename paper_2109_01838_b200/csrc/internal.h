@@ -109,7 +109,9 @@ struct DualState {
   Buf<int32_t> n_long;
 };
 // a6/a7 _triangulate_arrays (dual.py:216-290)
-void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& st);
+// steal: g's owner, whose buffers DualState may take over when they have
+// room for the chords (no copy of the m edges; the owner is left empty)
+void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& st, Graph* steal = nullptr);
 // extend_separation (dual.py:414-474): returns the number of triplets added
 int64_t extend_separation(Ctx& ctx, DualState& st, int L);
 // a8 reparametrized_edge_costs (dual.py:309-316)

@@ -118,7 +118,10 @@ void solve(Ctx& ctx, const GraphView& g, const SolveConfig& cfg, int32_t* labels
 
   const bool dual = (cfg.mode == 1 || cfg.mode == 2);
   iota(ctx, labels, n0);  // f_total
-  Graph cur = copy_graph(ctx, g);
+  // round 1 reads the caller's graph in place (nothing writes it); later
+  // rounds own their contracted graph, whose buffers the triangulation takes
+  Graph cur_own;
+  GraphView cur = g;
   double lb = nan;
   Buf<double> d_lb(1, ctx);
   for (int rnd = 1; rnd <= cfg.max_rounds; rnd++) {
@@ -138,10 +141,10 @@ void solve(Ctx& ctx, const GraphView& g, const SolveConfig& cfg, int32_t* labels
         tp = clk::now();
       };
       CycleRows cyc;
-      separate(ctx, cur.view(), cfg.max_cycle_length, cyc);
+      separate(ctx, cur, cfg.max_cycle_length, cyc);
       mark(0);
       DualState st;
-      triangulate(ctx, cur.view(), cyc, st);
+      triangulate(ctx, cur, cyc, st, rnd > 1 ? &cur_own : nullptr);
       mark(1);
       message_passing(ctx, st, cfg.mp_iterations);
       // c^lambda computed once: the bound's terms and the reparametrized
@@ -160,7 +163,7 @@ void solve(Ctx& ctx, const GraphView& g, const SolveConfig& cfg, int32_t* labels
                 "reparam %.2f contraction %.2f ms%s\n", rnd, (long long)cur.n, (long long)cur.m, (long long)st.T,
                 ph[0], ph[1], ph[2], ph[3], ph[4], step.used_forest ? " (forest)" : "");
     } else {
-      contraction_step(ctx, cur.view(), 3, cfg.switch_fraction, step);
+      contraction_step(ctx, cur, 3, cfg.switch_fraction, step);
     }
     // round end: the LB comes back (the wait also closes the round's timing)
     if (dual) {
@@ -179,7 +182,8 @@ void solve(Ctx& ctx, const GraphView& g, const SolveConfig& cfg, int32_t* labels
                    nodes_before - step.num_targets, ms_since(t0)});
     if (step.identity) break;
     compose(ctx, labels, n0, step.map.p);
-    cur = std::move(step.next);
+    cur_own = std::move(step.next);
+    cur = cur_own.view();
     if (cur.n <= 1) break;
   }
   if (dual) {
