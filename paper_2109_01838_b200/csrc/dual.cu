@@ -271,8 +271,13 @@ __global__ void k_gather_i32(const int32_t* __restrict__ src, const int32_t* __r
 __global__ void k_sep3(const int32_t* __restrict__ Q, int64_t nq, const int32_t* __restrict__ NQ,
                        const int32_t* __restrict__ u, const int32_t* __restrict__ v, const int32_t* __restrict__ ptr,
                        const int32_t* __restrict__ adj, int L, int32_t* __restrict__ out_len,
-                       int32_t* __restrict__ out_nodes, uint8_t* __restrict__ miss) {
+                       int32_t* __restrict__ out_nodes, uint8_t* __restrict__ miss,
+                       uint8_t* __restrict__ zero_flags, int32_t* __restrict__ zero_cnt) {
+  // (zero_flags[nq], zero_cnt[4]: the later passes' flags and list counters,
+  // cleared here instead of by memsets)
+  if (zero_cnt && blockIdx.x == 0 && threadIdx.x < 4) zero_cnt[threadIdx.x] = 0;
   GRID_STRIDE(i, nq) {
+    if (zero_flags) zero_flags[i] = 0;
     int32_t q = Q ? Q[i] : (int32_t)i;
     int32_t e = NQ[q];
     int32_t a = u[e], b = v[e];
@@ -1395,10 +1400,7 @@ void separate(Ctx& ctx, const GraphView& g, int L, CycleRows& out) {
   // searches the capped 5-cycle passes truncate are flagged and rerun
   // exactly; the exact pass scans the flags itself (no compaction, no read-back)
   Buf<uint8_t> capped;
-  if (L >= 5) {
-    capped.alloc(nq, ctx.s);
-    capped.zero();
-  }
+  if (L >= 5) capped.alloc(nq, ctx.s);  // zeroed by k_sep3
   separate_tables(ctx, g, L, out, csr, NQ, nq, capped.p);
   if (capped.p) {
     KernelScope ks(ctx.s, "k_sep5_ordered", 0.0);
@@ -1427,8 +1429,9 @@ static void separate_tables(Ctx& ctx, const GraphView& g, int L, CycleRows& out,
                             const Buf<int32_t>& NQ, int64_t nq, uint8_t* capped) {
   // triangles: thread per edge, sorted-row intersection
   Buf<uint8_t> miss(nq, ctx);
+  Buf<int32_t> cnt(4, ctx);  // G15 | G2 | fall-back | misses (zeroed by k_sep3)
   RAMA_KERNEL(ctx, k_sep3, nq, (const int32_t*)nullptr, nq, NQ.p, g.u, g.v, csr.ptr.p, csr.adj.p, L, out.len.p,
-              out.nodes.p, L >= 4 ? miss.p : (uint8_t*)nullptr);
+              out.nodes.p, L >= 4 ? miss.p : (uint8_t*)nullptr, capped, cnt.p);
   if (L < 4) return;
   // the edges without a triangle and their sources' group starts stay on
   // the device (counts n2c / ngc): grids are sized by nq, no read-back
@@ -1444,8 +1447,6 @@ static void separate_tables(Ctx& ctx, const GraphView& g, int L, CycleRows& out,
   const int64_t n2 = nq, ng = nq;  // upper bounds of both counts (grid sizes, list capacities)
   // overflow lists, appended on the device: tier 1 -> 1.5 -> 2 sources, then
   // the fall-back edges and the 4-cycle misses of the row-intersection pass
-  Buf<int32_t> cnt(4, ctx);  // G15 | G2 | fall-back | misses
-  cnt.zero();
   Buf<int32_t> G15(ng, ctx), G2(ng, ctx), FB(n2, ctx), M4(n2, ctx);
   static const int64_t cap = [] {  // RAMA_SEP_BLOCKS overrides the grid cap (tests)
     const char* e = getenv("RAMA_SEP_BLOCKS");
