@@ -1513,18 +1513,20 @@ static void separate_tables(Ctx& ctx, const GraphView& g, int L, CycleRows& out,
 
 // --------------------------------------------------------- triangulation
 
-__global__ void k_fan_counts(const int32_t* __restrict__ len, int64_t rows, int32_t* __restrict__ nt,
-                             int32_t* __restrict__ nc) {
-  GRID_STRIDE(r, rows) {
-    int32_t l = len[r];
-    nt[r] = l >= 3 ? l - 2 : 0;
-    nc[r] = l >= 4 ? l - 3 : 0;
+// per cycle row: triplets (high word) and chords (low word) of its fan, one
+// 64-bit value so one scan gives both offsets (neither sum reaches 2^32);
+// entry `rows` is 0, so the scan's last entry is both totals
+__global__ void k_fan_counts(const int32_t* __restrict__ len, int64_t rows, uint64_t* __restrict__ cnt) {
+  GRID_STRIDE(r, rows + 1) {
+    const int32_t l = r < rows ? len[r] : 0;
+    const uint64_t nt = l >= 3 ? (uint64_t)(l - 2) : 0, nc = l >= 4 ? (uint64_t)(l - 3) : 0;
+    cnt[r] = (nt << 32) | nc;
   }
 }
 
 // _fan_arrays (dual.py:228-252): triplets {v0, v_j, v_j+1} and chords (v0, v_j)
 __global__ void k_fan_emit(const int32_t* __restrict__ len, const int32_t* __restrict__ nodes, int64_t rows, int L,
-                           const int32_t* __restrict__ toff, const int32_t* __restrict__ coff,
+                           const uint64_t* __restrict__ off,
                            int32_t* __restrict__ trow, uint64_t* __restrict__ tkey, int32_t* __restrict__ crow,
                            uint64_t* __restrict__ ckey, uint64_t ctag) {
   GRID_STRIDE(r, rows) {
@@ -1532,7 +1534,8 @@ __global__ void k_fan_emit(const int32_t* __restrict__ len, const int32_t* __res
     if (l < 3) continue;
     const int32_t* row = nodes + r * (int64_t)L;
     int32_t v0 = row[0];
-    int32_t t = toff[r];
+    const uint64_t o = off[r];
+    int32_t t = (int32_t)(o >> 32);
     for (int j = 1; j < l - 1; j++) {
       int32_t a = v0, b = row[j], c = row[j + 1], s;
       if (a > b) { s = a; a = b; b = s; }
@@ -1542,7 +1545,7 @@ __global__ void k_fan_emit(const int32_t* __restrict__ len, const int32_t* __res
       tkey[t] = ((uint64_t)(uint32_t)b << 32) | (uint64_t)(uint32_t)c;
       t++;
     }
-    int32_t h = coff[r];
+    int32_t h = (int32_t)(uint32_t)o;
     for (int j = 2; j < l - 1; j++) {
       int32_t a = v0 < row[j] ? v0 : row[j];
       int32_t b = v0 < row[j] ? row[j] : v0;
@@ -1783,13 +1786,16 @@ void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& 
   int64_t rows = cyc.rows, m = g.m, n = g.n;
   st.n = n;
   st.m_orig = m;
-  Buf<int32_t> nt(rows > 0 ? rows : 1, ctx), nc(rows > 0 ? rows : 1, ctx);
-  Buf<int32_t> toff(rows + 1, ctx), coff(rows + 1, ctx);
-  RAMA_KERNEL(ctx, k_fan_counts, rows, cyc.len.p, rows, nt.p, nc.p);
-  exclusive_scan(ctx, nt.p, toff.p, rows, false);
-  exclusive_scan(ctx, nc.p, coff.p, rows, false);
+  Buf<uint64_t> fcnt(rows + 1, ctx), foff(rows + 1, ctx);
+  RAMA_KERNEL(ctx, k_fan_counts, rows + 1, cyc.len.p, rows, fcnt.p);
+  exclusive_scan64(ctx, (const int64_t*)fcnt.p, (int64_t*)foff.p, rows + 1);
   int64_t traw = 0, craw = 0;
-  read_pair(ctx, toff.p + rows, coff.p + rows, traw, craw);
+  {
+    uint64_t tot;
+    memcpy(&tot, fetch(ctx, {{foff.p + rows, 8}}), 8);
+    traw = (int64_t)(tot >> 32);
+    craw = (int64_t)(uint32_t)tot;
+  }
   // triplets and chords in one list, sorted once (chords tagged after each
   // row's triplets); one partition then keeps the first triplet of each run
   // and the first chord of each run that is not an edge of g, both in
@@ -1797,7 +1803,7 @@ void triangulate(Ctx& ctx, const GraphView& g, const CycleRows& cyc, DualState& 
   const int64_t N = traw + craw;
   Buf<int32_t> irow(N > 0 ? N : 1, ctx);
   Buf<uint64_t> ikey(N > 0 ? N : 1, ctx);
-  RAMA_KERNEL(ctx, k_fan_emit, rows, cyc.len.p, cyc.nodes.p, rows, cyc.L, toff.p, coff.p, irow.p, ikey.p,
+  RAMA_KERNEL(ctx, k_fan_emit, rows, cyc.len.p, cyc.nodes.p, rows, cyc.L, foff.p, irow.p, ikey.p,
               irow.p + traw, ikey.p + traw, kChordTag);
 
   st.orig_ptr.alloc(n + 1, ctx.s);
@@ -1960,14 +1966,15 @@ int64_t extend_separation(Ctx& ctx, DualState& st, int L) {
   separate(ctx, rep.view(), L, cyc);
   const int64_t rows = cyc.rows;
   if (rows == 0) return 0;
-  Buf<int32_t> nt(rows, ctx), nc(rows, ctx), toff(rows + 1, ctx), coff(rows + 1, ctx);
-  RAMA_KERNEL(ctx, k_fan_counts, rows, cyc.len.p, rows, nt.p, nc.p);
-  int64_t traw = exclusive_scan(ctx, nt.p, toff.p, rows, true);
+  Buf<uint64_t> fcnt(rows + 1, ctx), foff(rows + 1, ctx);
+  RAMA_KERNEL(ctx, k_fan_counts, rows + 1, cyc.len.p, rows, fcnt.p);
+  exclusive_scan64(ctx, (const int64_t*)fcnt.p, (int64_t*)foff.p, rows + 1);
+  const uint64_t tot = read_scalar(ctx, foff.p + rows);
+  const int64_t traw = (int64_t)(tot >> 32), craw = (int64_t)(uint32_t)tot;
   if (traw == 0) return 0;  // no cycle: nothing changes (dual.py:428-429)
-  int64_t craw = exclusive_scan(ctx, nc.p, coff.p, rows, true);
   Buf<int32_t> trow(traw, ctx), crow(craw > 0 ? craw : 1, ctx);
   Buf<uint64_t> tkey(traw, ctx), ckey(craw > 0 ? craw : 1, ctx);
-  RAMA_KERNEL(ctx, k_fan_emit, rows, cyc.len.p, cyc.nodes.p, rows, cyc.L, toff.p, coff.p, trow.p, tkey.p, crow.p,
+  RAMA_KERNEL(ctx, k_fan_emit, rows, cyc.len.p, cyc.nodes.p, rows, cyc.L, foff.p, trow.p, tkey.p, crow.p,
               ckey.p, 0ull);
   // new chords (sorted, unique, not yet augmented edges) join at base 0
   int64_t C = 0;
