@@ -93,6 +93,7 @@ __global__ void k_match_pair(int64_t n, const ulonglong2* __restrict__ vote, uin
     int32_t t = (int32_t)(0xffffffffULL - vx.x);
     if ((int32_t)x < t && vote[t].x == 0xffffffffULL - (uint32_t)x) {
       partner[x] = t;
+      partner[t] = (int32_t)x;  // (the pair's root is x: components straight from the partners)
       matched[x] = 1;
       matched[t] = 1;
     }
@@ -112,12 +113,9 @@ __global__ void k_flag_lower(const int32_t* __restrict__ partner, int64_t n, uin
   GRID_STRIDE(x, n) f[x] = partner[x] > (int32_t)x;
 }
 
-int64_t select_matching(Ctx& ctx, const GraphView& g, int rounds, Buf<int32_t>& su, Buf<int32_t>& sv) {
-  ProfScope prof(ctx.s, kFamMatching);
-  int64_t n = g.n, m = g.m;
-  su.alloc(1, ctx.s);
-  sv.alloc(1, ctx.s);
-  if (n == 0 || m == 0) return 0;
+// the handshake rounds: partner[x] = x's mate (both ends) or -1
+static void matching_rounds(Ctx& ctx, const GraphView& g, int rounds, ProfScope& prof, Buf<int32_t>& partner) {
+  const int64_t n = g.n, m = g.m;
   Buf<int32_t> P, npd;
   compact_if_dev(ctx, m, PosCost{g.c}, P, npd);
   // algorithmic bytes: costs scanned once (8 m), then SURVEY.md 8(d)'s
@@ -126,7 +124,7 @@ int64_t select_matching(Ctx& ctx, const GraphView& g, int rounds, Buf<int32_t>& 
   prof.add_bytes(8.0 * (double)m + (double)rounds * (34.0 * 0.5 * (double)m + 17.0 * (double)n));
   Buf<uint8_t> matched(n, ctx);
   Buf<ulonglong2> vote(n, ctx);
-  Buf<int32_t> partner(n, ctx);
+  partner.alloc(n, ctx.s);
   RAMA_KERNEL(ctx, k_match_init, n, n, matched.p, partner.p, vote.p);  // one pass instead of three memsets
   // votes alternate between two buffers; each pair pass clears the other
   Buf<ulonglong2> vote1(rounds > 1 ? n : 1, ctx);
@@ -136,6 +134,16 @@ int64_t select_matching(Ctx& ctx, const GraphView& g, int rounds, Buf<int32_t>& 
     RAMA_KERNEL(ctx, k_match_vote, m, P.p, npd.p, g.u, g.v, g.c, matched.p, cur);
     RAMA_KERNEL(ctx, k_match_pair, n, n, cur, matched.p, partner.p, nxt);
   }
+}
+
+int64_t select_matching(Ctx& ctx, const GraphView& g, int rounds, Buf<int32_t>& su, Buf<int32_t>& sv) {
+  ProfScope prof(ctx.s, kFamMatching);
+  int64_t n = g.n, m = g.m;
+  su.alloc(1, ctx.s);
+  sv.alloc(1, ctx.s);
+  if (n == 0 || m == 0) return 0;
+  Buf<int32_t> partner;
+  matching_rounds(ctx, g, rounds, prof, partner);
   Buf<uint8_t> lf(n, ctx);
   RAMA_KERNEL(ctx, k_flag_lower, n, partner.p, n, lf.p);
   Buf<int32_t> idx;
@@ -144,6 +152,42 @@ int64_t select_matching(Ctx& ctx, const GraphView& g, int rounds, Buf<int32_t>& 
   sv.alloc(k > 0 ? k : 1, ctx.s);
   RAMA_KERNEL(ctx, k_match_out, k, idx.p, k, partner.p, su.p, sv.p);
   return k;
+}
+
+// The matching's contraction mapping without the pair list and the
+// union-find: a pair's smaller node is its component's root (the smallest
+// member, as components() roots it), so flags, one scan and one gather give
+// the same canonical labels (contraction.py:101-111).  Returns the pairs;
+// *nt = the number of targets.
+__global__ void k_pair_roots(const int32_t* __restrict__ partner, int64_t n, int32_t* __restrict__ flag) {
+  GRID_STRIDE(x, n) {
+    const int32_t p = partner[x];
+    flag[x] = !(p >= 0 && p < (int32_t)x);
+  }
+}
+__global__ void k_pair_label(const int32_t* __restrict__ partner, const int32_t* __restrict__ rank, int64_t n,
+                             int32_t* __restrict__ map) {
+  GRID_STRIDE(x, n) {
+    const int32_t p = partner[x];
+    map[x] = rank[p >= 0 && p < (int32_t)x ? p : (int32_t)x];
+  }
+}
+
+int64_t select_matching_map(Ctx& ctx, const GraphView& g, int rounds, int32_t* map, int64_t* nt) {
+  int64_t n = g.n, m = g.m;
+  *nt = n;
+  if (n == 0 || m == 0) return 0;
+  Buf<int32_t> partner;
+  {
+    ProfScope prof(ctx.s, kFamMatching);
+    matching_rounds(ctx, g, rounds, prof, partner);
+  }
+  ProfScope prof(ctx.s, kFamComponents, 12.0 * (double)n);
+  Buf<int32_t> flag(n, ctx), rank(n + 1, ctx);
+  RAMA_KERNEL(ctx, k_pair_roots, n, partner.p, n, flag.p);
+  *nt = exclusive_scan(ctx, flag.p, rank.p, n, true);
+  RAMA_KERNEL(ctx, k_pair_label, n, partner.p, rank.p, n, map);
+  return n - *nt;
 }
 
 // ----------------------------------------------------------------- max edge
@@ -946,16 +990,24 @@ void contraction_step(Ctx& ctx, const GraphView& g, int policy, double switch_fr
       copy_d2d(ctx, sv.p, g.v + e, 1);
       k = 1;
     }
-  } else if (policy == 1) {
-    k = select_matching(ctx, g, 5, su, sv);
   } else if (policy == 2) {
     k = select_forest(ctx, g, su, sv);
     out.used_forest = true;
-  } else {
-    k = select_matching(ctx, g, 5, su, sv);
-    if ((double)k < switch_fraction * (double)g.n) {
+  } else {  // matching (1), auto (3): the matching's mapping comes straight from the partners
+    out.map.alloc(g.n > 0 ? g.n : 1, ctx.s);
+    int64_t nt = g.n;
+    k = select_matching_map(ctx, g, 5, out.map.p, &nt);
+    if (policy == 3 && (double)k < switch_fraction * (double)g.n) {
       k = select_forest(ctx, g, su, sv);
       out.used_forest = true;
+    } else {
+      out.num_selected = k;
+      out.joined = 0.0;
+      out.identity = k == 0;
+      out.num_targets = nt;
+      if (k == 0) return;
+      out.next = contract(ctx, g, out.map.p, nt, want_joined ? &out.joined : nullptr);
+      return;
     }
   }
   out.num_selected = k;
