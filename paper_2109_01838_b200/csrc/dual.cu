@@ -1569,42 +1569,9 @@ __device__ __forceinline__ int32_t find_in_row(const int32_t* __restrict__ rptr,
   return -1;
 }
 
-// unique chords that are not already edges of g, as one selection predicate
-// over the sorted chord list (run head, and no edge (row, key) in g)
-struct NewChordHead {
-  const int32_t* row;
-  const uint64_t* key;
-  const int32_t* rptr;
-  const int32_t* gv;
-  __device__ __forceinline__ bool operator()(int32_t p) const {
-    if (!(p == 0 || row[p] != row[p - 1] || key[p] != key[p - 1])) return false;
-    return find_in_row(rptr, gv, row[p], (int32_t)key[p]) < 0;
-  }
-};
-
 // triangulate's combined sort: chords carry kChordTag in the key (after the
 // row's triplets), triplets (b << 32 | c) with b < 2^31
 constexpr uint64_t kChordTag = 1ull << 63;
-struct NewChordHeadTagged {
-  const int32_t* row;
-  const uint64_t* key;
-  const int32_t* rptr;
-  const int32_t* gv;
-  __device__ __forceinline__ bool operator()(int32_t p) const {
-    const uint64_t k = key[p];
-    if (!(k & kChordTag)) return false;
-    if (!(p == 0 || row[p] != row[p - 1] || k != key[p - 1])) return false;
-    return find_in_row(rptr, gv, row[p], (int32_t)(uint32_t)k) < 0;
-  }
-};
-struct TripletHead {
-  const int32_t* row;
-  const uint64_t* key;
-  __device__ __forceinline__ bool operator()(int32_t p) const {
-    const uint64_t k = key[p];
-    return !(k & kChordTag) && (p == 0 || row[p] != row[p - 1] || k != key[p - 1]);
-  }
-};
 
 // kind of each sorted item: 1 first of a run of equal triplets, 2 first of
 // a run of equal chords that is not an edge of g, 0 otherwise (one thread
@@ -1627,6 +1594,7 @@ struct KindIs {
   __device__ __forceinline__ bool operator()(int32_t p) const { return kind[p] == want; }
 };
 
+// unique chords that are not already edges of g (extend_separation)
 __global__ void k_chord_new(const int32_t* __restrict__ heads, int64_t nh, const int32_t* __restrict__ row,
                             const uint64_t* __restrict__ key, const int32_t* __restrict__ rptr,
                             const int32_t* __restrict__ gv, uint8_t* __restrict__ is_new) {
